@@ -1,0 +1,289 @@
+/*
+ * hbp_b200.h — C-ABI of the B200 batch-construction engine for Hierarchical
+ * Balance Packing (arXiv 2503.07680).
+ *
+ * Plain pointers and sizes only: no C++ or torch types cross this boundary.
+ * Every entry point replaces one reference C++ entry point of
+ * /root/reference/proj (cited per function, path:line relative to proj/).
+ * The C++ drop-in headers under include/hbp/ and the Python module wrap
+ * these calls; INTEGRATION.md shows the bindings a maintainer would add.
+ *
+ * Status codes mirror the reference CLI exit codes (tools/hbp_main.cpp:38-40):
+ *   0 ok, 2 ValidationError, 3 InfeasibleError, 4 IoError; 5 is a CUDA or
+ *   internal failure (never silently recovered; there is no CPU path).
+ * The message of the last failure on a context is hbp_last_error(ctx); the
+ * text is the exact message the reference would throw.
+ *
+ * Threading: one hbp_ctx owns one CUDA stream and its scratch; contexts are
+ * independent, a single context must not be used from two threads at once
+ * (the reference is single-threaded and reentrant).
+ */
+#ifndef HBP_B200_H
+#define HBP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HBP_B200_ABI_VERSION 1
+
+enum hbp_status {
+    HBP_OK = 0,
+    HBP_ERR_VALIDATION = 2,
+    HBP_ERR_INFEASIBLE = 3,
+    HBP_ERR_IO = 4,
+    HBP_ERR_CUDA = 5
+};
+
+/* Same order as hbp::StrategyKind (include/hbp/packing.hpp:17). */
+enum hbp_strategy_kind {
+    HBP_STRATEGY_RANDOM = 0,
+    HBP_STRATEGY_ISF = 1,
+    HBP_STRATEGY_FFS = 2,
+    HBP_STRATEGY_FFD = 3,
+    HBP_STRATEGY_BFS = 4,
+    HBP_STRATEGY_SPFHP = 5
+};
+
+/* Where a caller-provided buffer lives. */
+enum hbp_memory { HBP_MEM_HOST = 0, HBP_MEM_DEVICE = 1 };
+
+/* hbp::GroupConfig (autoselect.hpp:13-18) flattened with its RuntimeConfig
+ * (costmodel.hpp:20-25). */
+typedef struct hbp_group_config {
+    int64_t length;
+    int32_t sp;
+    int32_t ckpt;
+} hbp_group_config;
+
+/* hbp::HierarchicalGroups (autoselect.hpp:20-27). */
+typedef struct hbp_groups {
+    const hbp_group_config* groups;
+    int32_t count;
+    int64_t l_best;
+    int64_t l_max;
+} hbp_groups;
+
+/* hbp::PackingStrategy (packing.hpp:22-30). */
+typedef struct hbp_strategy {
+    int32_t kind;             /* hbp_strategy_kind */
+    int32_t isf_iterations;   /* reference default 8 */
+    double isf_fill_threshold; /* reference default 0.98 */
+} hbp_strategy;
+
+/* hbp::PlanOptions (balance.hpp:64-70). */
+typedef struct hbp_plan_options {
+    hbp_strategy strategy;
+    int32_t device_count;
+    int32_t balance_batching; /* 0 -> random pack batching */
+    int32_t greedy_fill;
+    uint64_t seed;
+} hbp_plan_options;
+
+/* hbp::HardwareProfile (costmodel.hpp:31-47). */
+typedef struct hbp_hardware_profile {
+    double per_token_linear_cost;
+    double per_token2_attention_cost;
+    double sp_comm_cost;
+    double gc_recompute_factor;
+    double fixed_iteration_cost;
+    int32_t layer_count;
+    int64_t base_memory;
+    double per_token_activation_memory;
+    double gc_memory_saving_per_layer;
+    int64_t reference_length;
+    int64_t device_memory;
+} hbp_hardware_profile;
+
+/* The reference's HardwareProfile{} defaults (costmodel.hpp:32-43). */
+void hbp_hardware_profile_defaults(hbp_hardware_profile* out);
+
+/* Input corpus: reference SampleSet (types.hpp:24-46) as two parallel
+ * arrays. ids == NULL means ids 0..n-1 in order (what the Python
+ * SampleSet(lengths) constructor builds, bindings/py_hbp.cpp:25-35).
+ * `memory` says where ids/lengths live. */
+typedef struct hbp_samples {
+    const int64_t* ids;
+    const int64_t* lengths;
+    int64_t n;
+    int32_t memory; /* hbp_memory */
+} hbp_samples;
+
+/*
+ * Flat plan: CSR of iterations -> device batches -> packs -> members.
+ * Mirrors hbp::Plan / Iteration / DeviceBatch / Pack (balance.hpp:18-37,
+ * metrics.hpp:16-35). member_index[] indexes the input sample arrays; it may
+ * be NULL in plans handed to hbp_report / hbp_simulate, which only read pack
+ * totals. All arrays are host memory.
+ */
+typedef struct hbp_plan_view {
+    int32_t device_count;
+    uint64_t seed;
+    hbp_groups groups;
+    int64_t n_iterations;
+    int64_t n_devices;
+    int64_t n_packs;
+    int64_t n_members;
+    const int32_t* iter_group;          /* [n_iterations] */
+    const int64_t* iter_dev_offsets;    /* [n_iterations + 1] */
+    const int32_t* dev_index;           /* [n_devices] */
+    const int64_t* dev_pack_offsets;    /* [n_devices + 1] */
+    const int64_t* pack_capacity;       /* [n_packs] */
+    const int64_t* pack_total;          /* [n_packs] */
+    const int64_t* pack_attention;      /* [n_packs] */
+    const int64_t* pack_member_offsets; /* [n_packs + 1] */
+    const int32_t* member_index;        /* [n_members] */
+} hbp_plan_view;
+
+/* hbp::MetricsReport headline numbers (metrics.hpp:67-74). */
+typedef struct hbp_metrics {
+    double dbr;
+    double pr;
+    double abr;
+    double cr;
+    double ave_t;
+} hbp_metrics;
+
+/* hbp::SimReport scalars (sim.hpp:38-47). */
+typedef struct hbp_sim_totals {
+    double total_seconds;
+    double gpu_days;
+    int32_t switch_count;
+    int32_t device_count;
+    hbp_metrics metrics;
+} hbp_sim_totals;
+
+/* One measured profile row, hbp::ProfileRow (costmodel.hpp:114-121). */
+typedef struct hbp_profile_row {
+    int64_t length;
+    int32_t sp;
+    int32_t ckpt;
+    int64_t memory_bytes;
+    double seconds;
+    int32_t oom;
+} hbp_profile_row;
+
+enum hbp_profiler_kind { HBP_PROFILER_ANALYTIC = 0, HBP_PROFILER_TABLE = 1 };
+
+/* AnalyticProfiler (costmodel.hpp:96-111) or TableProfiler (:123-147). */
+typedef struct hbp_profiler {
+    int32_t kind;
+    hbp_hardware_profile profile; /* analytic */
+    int32_t ckpt_min;             /* analytic, default 0 */
+    int32_t ckpt_max;             /* analytic, -1 -> layer_count */
+    const hbp_profile_row* rows;  /* table */
+    int64_t n_rows;
+    int64_t device_memory;        /* table, default 80 GiB */
+} hbp_profiler;
+
+/* ---- context ---------------------------------------------------------- */
+
+typedef struct hbp_ctx hbp_ctx;
+typedef struct hbp_plan hbp_plan; /* device-resident plan (opaque) */
+
+int hbp_ctx_create(int device, hbp_ctx** out);
+void hbp_ctx_destroy(hbp_ctx* ctx);
+const char* hbp_last_error(const hbp_ctx* ctx);
+/* Blocks until all work queued on the context's stream has finished. */
+int hbp_ctx_synchronize(hbp_ctx* ctx);
+/* The cudaStream_t the context launches on, as an opaque pointer. */
+void* hbp_ctx_stream(hbp_ctx* ctx);
+/* Kernel launches issued on this context since creation (for the bench). */
+int64_t hbp_ctx_launch_count(const hbp_ctx* ctx);
+
+/* ---- L0: validation ---------------------------------------------------- */
+
+/* SampleSet::validate (src/types.cpp:8-24): non-empty, length >= 1, unique
+ * ids; the first offending sample in input order is reported. */
+int hbp_validate(hbp_ctx* ctx, const hbp_samples* samples);
+
+/* ---- L2: hot path ------------------------------------------------------ */
+
+/* group_data (include/hbp/balance.hpp:42-43, src/balance.cpp:25-44).
+ * Writes group_offsets[groups->count + 1] and member_index[n]: the samples
+ * of group g, in input order, are member_index[group_offsets[g] ..
+ * group_offsets[g+1]). Host output buffers. */
+int hbp_group_data(hbp_ctx* ctx, const hbp_samples* samples,
+                   const hbp_groups* groups, int64_t* group_offsets,
+                   int32_t* member_index);
+
+/* pack (include/hbp/packing.hpp:46-47, src/packing.cpp:210-261). The result
+ * is a plan with no iterations: n_packs packs, capacity == `capacity`. */
+int hbp_pack(hbp_ctx* ctx, const hbp_samples* samples, int64_t capacity,
+             const hbp_strategy* strategy, uint64_t seed, hbp_plan** out);
+
+/* build_plan (include/hbp/balance.hpp:75-76, src/balance.cpp:207-258). */
+int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples,
+                   const hbp_groups* groups, const hbp_plan_options* options,
+                   hbp_plan** out);
+
+/* Host view of a plan produced by hbp_pack / hbp_build_plan. The first call
+ * copies the plan to host; the view stays valid until hbp_plan_free. */
+int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out);
+void hbp_plan_free(hbp_plan* plan);
+
+/* report (include/hbp/metrics.hpp:78, src/metrics.cpp:107-144).
+ * per_iteration_dbr / _abr may be NULL; otherwise [n_iterations]. */
+int hbp_report(hbp_ctx* ctx, const hbp_plan_view* plan, hbp_metrics* out,
+               double* per_iteration_dbr, double* per_iteration_abr);
+int hbp_report_plan(hbp_ctx* ctx, hbp_plan* plan, hbp_metrics* out,
+                    double* per_iteration_dbr, double* per_iteration_abr);
+
+/* simulate (include/hbp/sim.hpp:52-53, src/sim.cpp:9-60) minus the corpus
+ * fingerprint, which is plan-invariant and host-side (types.cpp:52-72).
+ * iteration_seconds [n_iterations] and device_* [n_devices] may be NULL. */
+int hbp_simulate(hbp_ctx* ctx, const hbp_plan_view* plan,
+                 const hbp_hardware_profile* profile, hbp_sim_totals* out,
+                 double* iteration_seconds, double* device_compute,
+                 double* device_comm, double* device_idle);
+int hbp_simulate_plan(hbp_ctx* ctx, hbp_plan* plan,
+                      const hbp_hardware_profile* profile, hbp_sim_totals* out,
+                      double* iteration_seconds);
+
+/* ---- cost model / auto-selection ---------------------------------------- */
+
+/* memory_used (costmodel.hpp:50-51, src/costmodel.cpp:37-53). */
+int hbp_memory_used(hbp_ctx* ctx, int64_t length, int32_t sp, int32_t ckpt,
+                    const hbp_hardware_profile* profile, int64_t* out);
+
+/* greedy_profile_ckpt (costmodel.hpp:158-159, src/costmodel.cpp:271-292). */
+int hbp_greedy_profile_ckpt(hbp_ctx* ctx, const hbp_profiler* profiler,
+                            int64_t length, int32_t sp, int32_t ckpt_min,
+                            int32_t ckpt_max, int32_t* out);
+
+/* find_best_sp_ckpt (costmodel.hpp:169-170, src/costmodel.cpp:294-325). */
+int hbp_find_best_sp_ckpt(hbp_ctx* ctx, const hbp_profiler* profiler,
+                          int64_t length, const int32_t* sp_candidates,
+                          int32_t n_sp, int32_t* out_sp, int32_t* out_ckpt,
+                          double* out_seconds);
+
+/* select_groups (autoselect.hpp:36-38, src/autoselect.cpp:76-168).
+ * out_groups must hold at least 4 entries. */
+int hbp_select_groups(hbp_ctx* ctx, const int64_t* candidate_lengths,
+                      int32_t n_lengths, const hbp_profiler* profiler,
+                      const int32_t* sp_candidates, int32_t n_sp,
+                      hbp_group_config* out_groups, int32_t* out_count,
+                      int64_t* out_l_best, int64_t* out_l_max);
+
+/* Candidate sweep (built from the reference's own
+ * build_plan + simulate): for candidate c, groups
+ * cand_groups[cand_offsets[c] .. cand_offsets[c+1]) with l_best
+ * cand_l_best[c]; out_seconds[c] = simulate(build_plan(samples, groups_c,
+ * options), profile).total_seconds, +inf when the candidate raises
+ * InfeasibleError. *out_best = argmin (lowest index on ties, -1 if none is
+ * feasible). Candidates sharing a length set share one packing. */
+int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples,
+              const hbp_group_config* cand_groups, const int64_t* cand_offsets,
+              const int64_t* cand_l_best, int64_t n_candidates,
+              const hbp_plan_options* options,
+              const hbp_hardware_profile* profile, double* out_seconds,
+              int64_t* out_best);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* HBP_B200_H */

@@ -1,0 +1,257 @@
+"""ctypes mirror of include/hbp_b200.h plus numpy helpers.
+
+This is the thin Python side of the C-ABI seam: structs, the library loader
+and conversions between numpy arrays and the flat plan layout. The compute
+lives in libhbp_b200.so (CUDA, sm_100a); when that library is missing the
+loader raises -- there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhbp_b200.so")
+
+HBP_OK, HBP_ERR_VALIDATION, HBP_ERR_INFEASIBLE, HBP_ERR_IO, HBP_ERR_CUDA = 0, 2, 3, 4, 5
+STRATEGIES = {"random": 0, "isf": 1, "ffs": 2, "ffd": 3, "bfs": 4, "spfhp": 5}
+HBP_MEM_HOST, HBP_MEM_DEVICE = 0, 1
+
+
+class ValidationError(ValueError):
+    """hbp::ValidationError (errors.hpp:17-20) -> ValueError, py_hbp.cpp:49-50."""
+
+
+class InfeasibleError(RuntimeError):
+    """hbp::InfeasibleError (errors.hpp:23-26) -> RuntimeError, py_hbp.cpp:51-52."""
+
+
+class HbpIoError(OSError):
+    """hbp::IoError (errors.hpp:29-32) -> OSError, py_hbp.cpp:53."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA / internal failure of the engine (status 5)."""
+
+
+def raise_status(code: int, msg: str) -> None:
+    if code == HBP_OK:
+        return
+    if code == HBP_ERR_VALIDATION:
+        raise ValidationError(msg)
+    if code == HBP_ERR_INFEASIBLE:
+        raise InfeasibleError(msg)
+    if code == HBP_ERR_IO:
+        raise HbpIoError(msg)
+    raise CudaError(msg)
+
+
+class GroupConfig(C.Structure):
+    _fields_ = [("length", C.c_int64), ("sp", C.c_int32), ("ckpt", C.c_int32)]
+
+
+class Groups(C.Structure):
+    _fields_ = [("groups", C.POINTER(GroupConfig)), ("count", C.c_int32),
+                ("l_best", C.c_int64), ("l_max", C.c_int64)]
+
+
+class Strategy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("isf_iterations", C.c_int32),
+                ("isf_fill_threshold", C.c_double)]
+
+
+class PlanOptions(C.Structure):
+    _fields_ = [("strategy", Strategy), ("device_count", C.c_int32),
+                ("balance_batching", C.c_int32), ("greedy_fill", C.c_int32),
+                ("seed", C.c_uint64)]
+
+
+class HardwareProfile(C.Structure):
+    _fields_ = [("per_token_linear_cost", C.c_double),
+                ("per_token2_attention_cost", C.c_double),
+                ("sp_comm_cost", C.c_double),
+                ("gc_recompute_factor", C.c_double),
+                ("fixed_iteration_cost", C.c_double),
+                ("layer_count", C.c_int32),
+                ("base_memory", C.c_int64),
+                ("per_token_activation_memory", C.c_double),
+                ("gc_memory_saving_per_layer", C.c_double),
+                ("reference_length", C.c_int64),
+                ("device_memory", C.c_int64)]
+
+
+def default_profile() -> HardwareProfile:
+    """HardwareProfile{} defaults, costmodel.hpp:32-43."""
+    return HardwareProfile(2.5e-4, 1.5e-9, 1.6e-5, 1.0 / 3.0, 0.0, 32, 24 << 30,
+                           300000.0, 300000.0 * 0.75 * 4096.0, 4096, 80 << 30)
+
+
+class Samples(C.Structure):
+    _fields_ = [("ids", C.POINTER(C.c_int64)), ("lengths", C.POINTER(C.c_int64)),
+                ("n", C.c_int64), ("memory", C.c_int32)]
+
+
+class PlanView(C.Structure):
+    _fields_ = [("device_count", C.c_int32), ("seed", C.c_uint64), ("groups", Groups),
+                ("n_iterations", C.c_int64), ("n_devices", C.c_int64),
+                ("n_packs", C.c_int64), ("n_members", C.c_int64),
+                ("iter_group", C.POINTER(C.c_int32)),
+                ("iter_dev_offsets", C.POINTER(C.c_int64)),
+                ("dev_index", C.POINTER(C.c_int32)),
+                ("dev_pack_offsets", C.POINTER(C.c_int64)),
+                ("pack_capacity", C.POINTER(C.c_int64)),
+                ("pack_total", C.POINTER(C.c_int64)),
+                ("pack_attention", C.POINTER(C.c_int64)),
+                ("pack_member_offsets", C.POINTER(C.c_int64)),
+                ("member_index", C.POINTER(C.c_int32))]
+
+
+class Metrics(C.Structure):
+    _fields_ = [("dbr", C.c_double), ("pr", C.c_double), ("abr", C.c_double),
+                ("cr", C.c_double), ("ave_t", C.c_double)]
+
+
+class SimTotals(C.Structure):
+    _fields_ = [("total_seconds", C.c_double), ("gpu_days", C.c_double),
+                ("switch_count", C.c_int32), ("device_count", C.c_int32),
+                ("metrics", Metrics)]
+
+
+class ProfileRow(C.Structure):
+    _fields_ = [("length", C.c_int64), ("sp", C.c_int32), ("ckpt", C.c_int32),
+                ("memory_bytes", C.c_int64), ("seconds", C.c_double), ("oom", C.c_int32)]
+
+
+class Profiler(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("profile", HardwareProfile),
+                ("ckpt_min", C.c_int32), ("ckpt_max", C.c_int32),
+                ("rows", C.POINTER(ProfileRow)), ("n_rows", C.c_int64),
+                ("device_memory", C.c_int64)]
+
+
+def analytic_profiler(profile: Optional[HardwareProfile] = None, ckpt_min: int = 0,
+                      ckpt_max: int = -1) -> Profiler:
+    p = Profiler()
+    p.kind = 0
+    p.profile = profile if profile is not None else default_profile()
+    p.ckpt_min, p.ckpt_max = ckpt_min, ckpt_max
+    p.device_memory = 80 << 30
+    return p
+
+
+def table_profiler(rows: Sequence[tuple], device_memory: int = 80 << 30) -> Profiler:
+    """rows: (length, sp, ckpt, memory_bytes | None for oom, seconds)."""
+    arr = (ProfileRow * max(1, len(rows)))()
+    for i, (l, sp, ck, mem, sec) in enumerate(rows):
+        arr[i] = ProfileRow(l, sp, ck, 0 if mem is None else mem, sec, 1 if mem is None else 0)
+    p = Profiler()
+    p.kind = 1
+    p.profile = default_profile()
+    p.rows = arr
+    p.n_rows = len(rows)
+    p.device_memory = device_memory
+    p._keep = arr  # keep the row array alive with the struct
+    return p
+
+
+def parse_table_csv(text: str) -> list:
+    """TableProfiler::from_csv row format (costmodel.cpp:144-209)."""
+    rows, header = [], False
+    for line in text.splitlines():
+        if not line.strip(" \t\r") or line[0] == "#":
+            continue
+        cells = [c.strip(" \t\r") for c in line.split(",")]
+        if not header and cells and cells[0] == "length":
+            header = True
+            continue
+        mem = None if cells[3] == "oom" else int(cells[3])
+        rows.append((int(cells[0]), int(cells[1]), int(cells[2]), mem,
+                     0.0 if mem is None else float(cells[4])))
+    return rows
+
+
+def make_groups(groups: Sequence[tuple], l_best: Optional[int] = None):
+    """groups: [(length, sp, ckpt), ...] ascending. Returns (Groups, keepalive)."""
+    arr = (GroupConfig * len(groups))(*[GroupConfig(l, s, c) for (l, s, c) in groups])
+    g = Groups(arr, len(groups), groups[0][0] if l_best is None else l_best, groups[-1][0])
+    return g, arr
+
+
+def make_options(strategy: str = "isf", device_count: int = 4, seed: int = 0,
+                 balance_batching: bool = True, greedy_fill: bool = True,
+                 isf_iterations: int = 8, isf_fill_threshold: float = 0.98) -> PlanOptions:
+    return PlanOptions(Strategy(STRATEGIES[strategy], isf_iterations, isf_fill_threshold),
+                       device_count, int(bool(balance_batching)), int(bool(greedy_fill)),
+                       C.c_uint64(seed & ((1 << 64) - 1)).value)
+
+
+def ptr(a: Optional[np.ndarray], ctype):
+    if a is None:
+        return C.POINTER(ctype)()
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+@dataclass
+class FlatPlan:
+    """A plan in the flat CSR layout of hbp_plan_view (numpy arrays)."""
+    device_count: int
+    seed: int
+    groups: list  # [(length, sp, ckpt)]
+    l_best: int
+    iter_group: np.ndarray
+    iter_dev_offsets: np.ndarray
+    dev_index: np.ndarray
+    dev_pack_offsets: np.ndarray
+    pack_capacity: np.ndarray
+    pack_total: np.ndarray
+    pack_attention: np.ndarray
+    pack_member_offsets: np.ndarray
+    member_index: Optional[np.ndarray] = None   # product plans: index into input
+    member_id: Optional[np.ndarray] = None      # oracle plans: sample ids
+    member_length: Optional[np.ndarray] = None
+    _keep: list = field(default_factory=list, repr=False)
+
+    @property
+    def n_iterations(self) -> int:
+        return int(self.iter_group.shape[0])
+
+    def view(self) -> PlanView:
+        g, arr = make_groups(self.groups, self.l_best)
+        cols = {k: np.ascontiguousarray(getattr(self, k)) for k in (
+            "iter_group", "iter_dev_offsets", "dev_index", "dev_pack_offsets",
+            "pack_capacity", "pack_total", "pack_attention", "pack_member_offsets")}
+        cols["iter_group"] = cols["iter_group"].astype(np.int32, copy=False)
+        cols["dev_index"] = cols["dev_index"].astype(np.int32, copy=False)
+        for k in cols:
+            if k not in ("iter_group", "dev_index"):
+                cols[k] = cols[k].astype(np.int64, copy=False)
+        mi = None if self.member_index is None else np.ascontiguousarray(self.member_index, dtype=np.int32)
+        v = PlanView()
+        v.device_count = self.device_count
+        v.seed = C.c_uint64(self.seed & ((1 << 64) - 1)).value
+        v.groups = g
+        v.n_iterations = cols["iter_group"].shape[0]
+        v.n_devices = cols["dev_index"].shape[0]
+        v.n_packs = cols["pack_capacity"].shape[0]
+        v.n_members = int(cols["pack_member_offsets"][-1]) if v.n_packs else 0
+        v.iter_group = ptr(cols["iter_group"], C.c_int32)
+        v.iter_dev_offsets = ptr(cols["iter_dev_offsets"], C.c_int64)
+        v.dev_index = ptr(cols["dev_index"], C.c_int32)
+        v.dev_pack_offsets = ptr(cols["dev_pack_offsets"], C.c_int64)
+        v.pack_capacity = ptr(cols["pack_capacity"], C.c_int64)
+        v.pack_total = ptr(cols["pack_total"], C.c_int64)
+        v.pack_attention = ptr(cols["pack_attention"], C.c_int64)
+        v.pack_member_offsets = ptr(cols["pack_member_offsets"], C.c_int64)
+        v.member_index = ptr(mi, C.c_int32)
+        v._keep = (arr, cols, mi)
+        return v
+
+    def members_as_ids(self, ids: Optional[np.ndarray]) -> np.ndarray:
+        if self.member_id is not None:
+            return self.member_id
+        idx = self.member_index.astype(np.int64)
+        return idx if ids is None else ids[idx]

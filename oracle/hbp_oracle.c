@@ -1674,6 +1674,13 @@ int oracle_synth_lengths(int64_t count, const char* short_dist, double long_frac
     return OK;
 }
 
+int oracle_shuffle_positions(uint64_t seed, int64_t m, uint32_t* out) {
+    for (int64_t i = 0; i < m; ++i) out[i] = (uint32_t)i;
+    rng r = rng_make(seed);
+    rng_shuffle(&r, out, m, sizeof(uint32_t));
+    return OK;
+}
+
 int oracle_validate(const int64_t* ids, const int64_t* lengths, int64_t n, char* err, int errlen) {
     errbuf e = {err, errlen};
     sample* v = make_samples(ids, lengths, n);

@@ -58,6 +58,8 @@ int oracle_synth_lengths(int64_t count, const char* short_dist,
                          double long_fraction, const char* long_dist,
                          int64_t max_length, uint64_t seed, int64_t* lengths,
                          char* err, int errlen);
+/* Rng(seed).shuffle (rng.hpp:61-68) of 0..m-1: out[p] = original position. */
+int oracle_shuffle_positions(uint64_t seed, int64_t m, uint32_t* out);
 /* types.cpp:8-24 */
 int oracle_validate(const int64_t* ids, const int64_t* lengths, int64_t n,
                     char* err, int errlen);

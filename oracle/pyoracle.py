@@ -102,6 +102,11 @@ class Oracle:
         self._check(rc)
         return out
 
+    def shuffle_positions(self, seed: int, m: int) -> np.ndarray:
+        out = np.zeros(max(m, 1), dtype=np.uint32)
+        self.lib.oracle_shuffle_positions(C.c_uint64(seed & (2**64 - 1)), C.c_int64(m), abi.ptr(out, C.c_uint32))
+        return out[:m]
+
     def validate(self, ids, lengths) -> None:
         lengths = np.ascontiguousarray(lengths, dtype=np.int64)
         ids = self._ids(ids, len(lengths))

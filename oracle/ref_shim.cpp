@@ -21,6 +21,7 @@
 #include "hbp/ingest.hpp"
 #include "hbp/metrics.hpp"
 #include "hbp/packing.hpp"
+#include "hbp/rng.hpp"
 #include "hbp/sim.hpp"
 #include "hbp/types.hpp"
 
@@ -267,6 +268,15 @@ int oracle_synth_lengths(int64_t count, const char* short_dist,
             lengths[i] = s.samples[i].length;
         }
     });
+}
+
+int oracle_shuffle_positions(uint64_t seed, int64_t m, uint32_t* out) {
+    std::vector<uint32_t> v(static_cast<std::size_t>(m));
+    for (int64_t i = 0; i < m; ++i) v[i] = static_cast<uint32_t>(i);
+    R::Rng rng(seed);
+    rng.shuffle(v);
+    std::memcpy(out, v.data(), sizeof(uint32_t) * v.size());
+    return 0;
 }
 
 int oracle_validate(const int64_t* ids, const int64_t* lengths, int64_t n,

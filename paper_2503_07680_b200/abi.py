@@ -255,3 +255,85 @@ class FlatPlan:
             return self.member_id
         idx = self.member_index.astype(np.int64)
         return idx if ids is None else ids[idx]
+
+
+# ---------------------------------------------------------------------------
+# engine library
+# ---------------------------------------------------------------------------
+
+_LIB = None
+
+
+def load_library() -> C.CDLL:
+    """Loads libhbp_b200.so (built in-tree). Raises when it is missing:
+    there is no CPU implementation to fall back to."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; build it with __graft_entry__.build()")
+        lib = C.CDLL(LIB_PATH)
+        lib.hbp_last_error.restype = C.c_char_p
+        lib.hbp_last_error.argtypes = [C.c_void_p]
+        lib.hbp_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        lib.hbp_ctx_destroy.argtypes = [C.c_void_p]
+        lib.hbp_ctx_launch_count.restype = C.c_int64
+        lib.hbp_ctx_launch_count.argtypes = [C.c_void_p]
+        lib.hbp_ctx_stream.restype = C.c_void_p
+        lib.hbp_ctx_stream.argtypes = [C.c_void_p]
+        _LIB = lib
+    return _LIB
+
+
+class Context:
+    """One engine context (one CUDA stream) on `device`."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        rc = self.lib.hbp_ctx_create(device, C.byref(h))
+        if rc != HBP_OK:
+            raise CudaError(f"hbp_ctx_create({device}) failed with status {rc}")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hbp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int) -> None:
+        if rc != HBP_OK:
+            raise_status(rc, self.lib.hbp_last_error(self.h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.hbp_ctx_launch_count(self.h))
+
+    def synchronize(self) -> None:
+        self.check(self.lib.hbp_ctx_synchronize(self.h))
+
+    # -- stage hooks (include/hbp_b200_testing.h) --------------------------
+    def shuffle_positions(self, seed: int, m: int) -> np.ndarray:
+        out = np.zeros(max(m, 1), dtype=np.uint32)
+        self.check(self.lib.hbp_test_shuffle_positions(self.h, C.c_uint64(seed & (2**64 - 1)),
+                                                       C.c_int64(m), ptr(out, C.c_uint32)))
+        return out[:m]
+
+    def scan_u32(self, a: np.ndarray) -> np.ndarray:
+        a = np.ascontiguousarray(a, dtype=np.uint32)
+        out = np.zeros(max(len(a), 1), dtype=np.uint64)
+        self.check(self.lib.hbp_test_scan_u32(self.h, ptr(a, C.c_uint32), C.c_int64(len(a)),
+                                              ptr(out, C.c_uint64)))
+        return out[:len(a)]
+
+    def radix_sort(self, keys: np.ndarray, values: np.ndarray, bits: int, descending: bool = False):
+        k = np.ascontiguousarray(keys, dtype=np.uint32).copy()
+        v = np.ascontiguousarray(values, dtype=np.uint32).copy()
+        self.check(self.lib.hbp_test_radix_sort(self.h, ptr(k, C.c_uint32), ptr(v, C.c_uint32),
+                                                C.c_int64(len(k)), C.c_int32(bits), C.c_int32(int(descending))))
+        return k, v

@@ -1,0 +1,182 @@
+// common.cuh — shared plumbing for the HBP B200 engine: error handling, the
+// per-context stream and scratch allocator, launch accounting, and small
+// device helpers. Everything here is host/device infrastructure; the
+// algorithms live in the stage files (shuffle.cu, nextfit.cu, firstfit.cu,
+// batching.cu, metrics.cu, costmodel.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hbp_b200.h"
+
+namespace hbp_b200 {
+
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i64 = int64_t;
+
+constexpr int kSMs = 148;          // B200: 2 dies x 74 SMs
+constexpr u32 kNone = 0xffffffffu; // "no element" sentinel for u32 links
+
+// Engine errors carry the reference's status code and exact message.
+struct EngineError : std::runtime_error {
+    int code;
+    EngineError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail_validation(const std::string& m) { throw EngineError(HBP_ERR_VALIDATION, m); }
+[[noreturn]] inline void fail_infeasible(const std::string& m) { throw EngineError(HBP_ERR_INFEASIBLE, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        throw EngineError(HBP_ERR_CUDA, std::string("CUDA error in ") + what + " (" + file + ":" +
+                                            std::to_string(line) + "): " + cudaGetErrorString(e));
+    }
+}
+#define CUDA_CHECK(x) ::hbp_b200::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Stream-ordered device buffer owned by a context (cudaMallocAsync pool).
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; s = o.s;
+            o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count, cudaStream_t stream) {
+        release();
+        s = stream;
+        n = count;
+        if (count) CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+    void zero() const {
+        if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+    }
+};
+
+// Pinned host staging buffer for small readbacks.
+struct Pinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFreeHost(p);
+        CUDA_CHECK(cudaMallocHost(&p, b));
+        bytes = b;
+    }
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// kernel launch accounting (bench.py reports gpu_launches)
+// ---------------------------------------------------------------------------
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch() {
+    if (g_launch_counter) ++*g_launch_counter;
+}
+
+inline unsigned grid_for(size_t n, unsigned block, unsigned cap = 148u * 16u) {
+    size_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g);
+}
+
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                           \
+    do {                                                                         \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);             \
+        ::hbp_b200::count_launch();                                              \
+        CUDA_CHECK(cudaGetLastError());                                          \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane_id() >= static_cast<unsigned>(o)) v += t;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan (blockDim.x multiple of 32, <= 1024). `total`
+// receives the block sum. Uses 33 words of the provided shared scratch.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T& total) {
+    const unsigned lane = lane_id(), wid = warp_id(), nw = blockDim.x >> 5;
+    T inc = warp_inclusive_scan(v);
+    if (lane == 31) smem[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        T w = lane < nw ? smem[lane] : T(0);
+        T wi = warp_inclusive_scan(w);
+        if (lane < nw) smem[lane] = wi - w;
+        if (lane == nw - 1) smem[32] = wi;
+    }
+    __syncthreads();
+    T out = smem[wid] + inc - v;
+    total = smem[32];
+    __syncthreads();
+    return out;
+}
+
+}  // namespace hbp_b200

@@ -1,0 +1,63 @@
+// engine.cuh — the per-context state and the stage entry points of the
+// B200 batch-construction engine. One context = one CUDA stream; all
+// scratch is stream-ordered (cudaMallocAsync) so stages queue back to back
+// and the host only synchronises where a data-dependent size is needed.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+struct hbp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    int64_t launches = 0;
+    hbp_b200::ScanScratch scan;
+    hbp_b200::Pinned pinned;
+};
+
+namespace hbp_b200 {
+
+using Ctx = hbp_ctx;
+
+// Makes `ctx` the current launch-count sink and device for this thread.
+struct CtxScope {
+    int64_t* prev;
+    explicit CtxScope(Ctx& c) : prev(g_launch_counter) {
+        g_launch_counter = &c.launches;
+        CUDA_CHECK(cudaSetDevice(c.device));
+    }
+    ~CtxScope() { g_launch_counter = prev; }
+};
+
+// Copies a few device scalars to host (one sync).
+template <typename T>
+T read_scalar(Ctx& c, const T* dptr) {
+    c.pinned.ensure(sizeof(T));
+    CUDA_CHECK(cudaMemcpyAsync(c.pinned.p, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return *reinterpret_cast<T*>(c.pinned.p);
+}
+
+template <typename T>
+std::vector<T> read_vector(Ctx& c, const T* dptr, size_t n) {
+    std::vector<T> out(n);
+    if (n) {
+        CUDA_CHECK(cudaMemcpyAsync(out.data(), dptr, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    }
+    return out;
+}
+
+// ---- stage: exact Fisher-Yates (shuffle.cu) --------------------------------
+// src[p] = the input position whose element Rng(seed).shuffle() leaves at
+// output position p, for a vector of m elements (reference rng.hpp:61-68).
+void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src);
+// out[p] = in[src[p]] for 8-byte elements.
+void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m);
+void gather_u32(Ctx& c, const u32* in, const u32* src, u32* out, i64 m);
+
+}  // namespace hbp_b200

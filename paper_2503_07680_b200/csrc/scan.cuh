@@ -1,0 +1,132 @@
+// scan.cuh — single-pass device-wide exclusive scan (decoupled look-back).
+//
+// One read and one write of the payload per element: the HBM floor for a
+// scan. Each CTA claims a tile (dynamic index for forward progress), loads
+// it striped (coalesced), transposes through shared memory to a blocked
+// layout, reduces, publishes its aggregate, looks back over predecessor
+// tiles with one warp (32 status words per probe), then scans and stores
+// striped again. Values are non-negative counts (< 2^62), packed with a
+// 2-bit status in one 64-bit word so a status never tears.
+//
+//   scan_exclusive<ITEMS>(n, load, store, stream, scratch)
+//     load(i)            -> T        element i (i < n)
+//     store(i, excl, v)              receives the exclusive prefix of i
+//   returns nothing; the total can be captured by the store functor (i==n-1).
+#pragma once
+
+#include "common.cuh"
+
+namespace hbp_b200 {
+
+constexpr u64 kScanFlagAgg = 1ull << 62;
+constexpr u64 kScanFlagInc = 2ull << 62;
+constexpr u64 kScanValMask = (1ull << 62) - 1;
+
+template <typename T, int BLOCK, int ITEMS, typename Load, typename Store>
+__global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store store, u64* status,
+                                                         u32* counter) {
+    constexpr int TILE = BLOCK * ITEMS;
+    __shared__ T s_items[TILE + TILE / 32];  // padded transpose buffer
+    __shared__ T s_red[33];
+    __shared__ u32 s_tile;
+    __shared__ T s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const i64 tile = s_tile;
+    const i64 base = tile * TILE;
+    auto pad = [](int i) { return i + (i >> 5); };
+
+    // striped coalesced load -> blocked registers
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const int li = k * BLOCK + threadIdx.x;
+        const i64 gi = base + li;
+        s_items[pad(li)] = gi < n ? load(gi) : T(0);
+    }
+    __syncthreads();
+    T v[ITEMS];
+    T local = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        v[k] = s_items[pad(threadIdx.x * ITEMS + k)];
+        local += v[k];
+    }
+    T total;
+    const T texcl = block_exclusive_scan<T>(local, s_red, total);
+
+    // publish + look back
+    if (threadIdx.x == 0) {
+        const u64 word = (tile == 0 ? kScanFlagInc : kScanFlagAgg) | (static_cast<u64>(total) & kScanValMask);
+        __threadfence();
+        *reinterpret_cast<volatile u64*>(&status[tile]) = word;
+    }
+    if (tile > 0 && threadIdx.x < 32) {
+        T acc = 0;
+        i64 look = tile - 1;
+        const unsigned lane = threadIdx.x;
+        while (true) {
+            const i64 idx = look - static_cast<i64>(lane);
+            u64 w = 0;
+            if (idx >= 0) {
+                do {
+                    w = *reinterpret_cast<volatile u64*>(&status[idx]);
+                } while ((w >> 62) == 0);
+            } else {
+                w = kScanFlagInc;  // virtual inclusive zero before tile 0
+            }
+            const unsigned inc_mask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+            // lanes up to and including the first inclusive (lowest lane = nearest)
+            const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+            T contrib = (static_cast<int>(lane) <= first_inc && idx >= 0) ? static_cast<T>(w & kScanValMask) : T(0);
+            acc += warp_sum(contrib);
+            if (inc_mask) break;
+            look -= 32;
+        }
+        if (lane == 0) {
+            s_prefix = acc;
+            __threadfence();
+            *reinterpret_cast<volatile u64*>(&status[tile]) =
+                kScanFlagInc | (static_cast<u64>(acc + total) & kScanValMask);
+        }
+    }
+    if (tile == 0 && threadIdx.x == 0) s_prefix = 0;
+    __syncthreads();
+    T run = s_prefix + texcl;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        s_items[pad(threadIdx.x * ITEMS + k)] = run;
+        run += v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const int li = k * BLOCK + threadIdx.x;
+        const i64 gi = base + li;
+        if (gi < n) store(gi, s_items[pad(li)]);
+    }
+}
+
+// Scratch for scans: status words + the tile counter, reused across calls.
+struct ScanScratch {
+    DevBuf<u64> status;
+    DevBuf<u32> counter;
+    void prepare(i64 tiles, cudaStream_t s) {
+        if (static_cast<i64>(status.n) < tiles) status.alloc(static_cast<size_t>(tiles * 2 + 64), s);
+        if (counter.n < 1) counter.alloc(1, s);
+        CUDA_CHECK(cudaMemsetAsync(status.p, 0, sizeof(u64) * static_cast<size_t>(tiles), s));
+        CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(u32), s));
+    }
+};
+
+template <typename T, int ITEMS = 8, typename Load, typename Store>
+void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch) {
+    constexpr int BLOCK = 256;
+    constexpr int TILE = BLOCK * ITEMS;
+    if (n <= 0) return;
+    const i64 tiles = (n + TILE - 1) / TILE;
+    scratch.prepare(tiles, stream);
+    LAUNCH((k_scan_lookback<T, BLOCK, ITEMS, Load, Store>), static_cast<unsigned>(tiles), BLOCK, 0, stream, n,
+           load, store, scratch.status.p, scratch.counter.p);
+}
+
+}  // namespace hbp_b200

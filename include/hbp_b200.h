@@ -109,7 +109,8 @@ typedef struct hbp_samples {
     const int64_t* ids;
     const int64_t* lengths;
     int64_t n;
-    int32_t memory; /* hbp_memory */
+    int32_t memory;     /* hbp_memory */
+    const char* source; /* SampleSet::source, used in "empty corpus: <source>"; may be NULL */
 } hbp_samples;
 
 /*

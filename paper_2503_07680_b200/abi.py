@@ -92,7 +92,24 @@ def default_profile() -> HardwareProfile:
 
 class Samples(C.Structure):
     _fields_ = [("ids", C.POINTER(C.c_int64)), ("lengths", C.POINTER(C.c_int64)),
-                ("n", C.c_int64), ("memory", C.c_int32)]
+                ("n", C.c_int64), ("memory", C.c_int32), ("source", C.c_char_p)]
+
+
+def make_samples(ids: Optional[np.ndarray], lengths: np.ndarray, source: str = "python"):
+    """Host-memory hbp_samples over numpy arrays. Returns (struct, keepalive)."""
+    lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+    ids = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+    src = source.encode()
+    s = Samples(ptr(ids, C.c_int64), ptr(lengths, C.c_int64), len(lengths), HBP_MEM_HOST, src)
+    return s, (ids, lengths, src)
+
+
+def device_samples(ids_ptr: int, lengths_ptr: int, n: int, source: str = "device"):
+    """hbp_samples over device pointers (e.g. torch tensors' data_ptr())."""
+    src = source.encode()
+    s = Samples(C.cast(C.c_void_p(ids_ptr), C.POINTER(C.c_int64)) if ids_ptr else C.POINTER(C.c_int64)(),
+                C.cast(C.c_void_p(lengths_ptr), C.POINTER(C.c_int64)), n, HBP_MEM_DEVICE, src)
+    return s, (src,)
 
 
 class PlanView(C.Structure):
@@ -317,6 +334,71 @@ class Context:
     def synchronize(self) -> None:
         self.check(self.lib.hbp_ctx_synchronize(self.h))
 
+    # -- hot path (include/hbp_b200.h) -------------------------------------
+    def validate(self, ids, lengths, source: str = "python") -> None:
+        s, keep = make_samples(ids, lengths, source)
+        self.check(self.lib.hbp_validate(self.h, C.byref(s)))
+
+    def group_data(self, ids, lengths, groups, l_best=None):
+        s, keep = make_samples(ids, lengths)
+        g, garr = make_groups(groups, l_best)
+        off = np.zeros(len(groups) + 1, dtype=np.int64)
+        mem = np.zeros(max(1, len(keep[1])), dtype=np.int32)
+        self.check(self.lib.hbp_group_data(self.h, C.byref(s), C.byref(g), ptr(off, C.c_int64),
+                                           ptr(mem, C.c_int32)))
+        return off, mem[:len(keep[1])]
+
+    def _plan(self, handle, groups, l_best) -> "DevicePlanHandle":
+        return DevicePlanHandle(self, handle, groups, l_best)
+
+    def pack(self, ids, lengths, capacity: int, strategy: str = "isf", seed: int = 0,
+             isf_iterations: int = 8, isf_fill_threshold: float = 0.98) -> "DevicePlanHandle":
+        s, keep = make_samples(ids, lengths)
+        st = Strategy(STRATEGIES[strategy], isf_iterations, isf_fill_threshold)
+        h = C.c_void_p()
+        self.check(self.lib.hbp_pack(self.h, C.byref(s), C.c_int64(capacity), C.byref(st),
+                                     C.c_uint64(seed & (2**64 - 1)), C.byref(h)))
+        return self._plan(h, [], 0)
+
+    def build_plan(self, ids, lengths, groups, l_best=None, source: str = "python", **opts) -> "DevicePlanHandle":
+        s, keep = make_samples(ids, lengths, source)
+        return self.build_plan_samples(s, groups, l_best, **opts)
+
+    def build_plan_samples(self, s: Samples, groups, l_best=None, **opts) -> "DevicePlanHandle":
+        g, garr = make_groups(groups, l_best)
+        o = make_options(**opts)
+        h = C.c_void_p()
+        self.check(self.lib.hbp_build_plan(self.h, C.byref(s), C.byref(g), C.byref(o), C.byref(h)))
+        return self._plan(h, groups, g.l_best)
+
+    def report(self, plan: FlatPlan):
+        v = plan.view()
+        m = Metrics()
+        ni = plan.n_iterations
+        dbr = np.zeros(max(ni, 1))
+        abr_ = np.zeros(max(ni, 1))
+        self.check(self.lib.hbp_report(self.h, C.byref(v), C.byref(m), ptr(dbr, C.c_double),
+                                       ptr(abr_, C.c_double)))
+        return m, dbr[:ni], abr_[:ni]
+
+    def simulate(self, plan: FlatPlan, profile: Optional[HardwareProfile] = None):
+        v = plan.view()
+        prof = profile if profile is not None else default_profile()
+        st = SimTotals()
+        ni, nd = plan.n_iterations, len(plan.dev_index)
+        it = np.zeros(max(ni, 1))
+        dc, dm, di = (np.zeros(max(nd, 1)) for _ in range(3))
+        self.check(self.lib.hbp_simulate(self.h, C.byref(v), C.byref(prof), C.byref(st), ptr(it, C.c_double),
+                                         ptr(dc, C.c_double), ptr(dm, C.c_double), ptr(di, C.c_double)))
+        return st, it[:ni], dc[:nd], dm[:nd], di[:nd]
+
+    def memory_used(self, length, sp, ckpt, profile=None) -> int:
+        prof = profile if profile is not None else default_profile()
+        out = C.c_int64()
+        self.check(self.lib.hbp_memory_used(self.h, C.c_int64(length), C.c_int32(sp), C.c_int32(ckpt),
+                                            C.byref(prof), C.byref(out)))
+        return out.value
+
     # -- stage hooks (include/hbp_b200_testing.h) --------------------------
     def shuffle_positions(self, seed: int, m: int) -> np.ndarray:
         out = np.zeros(max(m, 1), dtype=np.uint32)
@@ -337,3 +419,52 @@ class Context:
         self.check(self.lib.hbp_test_radix_sort(self.h, ptr(k, C.c_uint32), ptr(v, C.c_uint32),
                                                 C.c_int64(len(k)), C.c_int32(bits), C.c_int32(int(descending))))
         return k, v
+
+
+class DevicePlanHandle:
+    """A plan resident in HBM (hbp_plan*). `.flat()` copies it to host."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, groups, l_best):
+        self.ctx, self.h, self.groups, self.l_best = ctx, handle, list(groups), l_best
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.lib.hbp_plan_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def flat(self) -> FlatPlan:
+        v = PlanView()
+        self.ctx.check(self.ctx.lib.hbp_plan_view_get(self.ctx.h, self.h, C.byref(v)))
+
+        def arr(p, n, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+
+        ni, nd, npk, nm = v.n_iterations, v.n_devices, v.n_packs, v.n_members
+        return FlatPlan(device_count=v.device_count, seed=v.seed, groups=self.groups, l_best=self.l_best,
+                        iter_group=arr(v.iter_group, ni, np.int32),
+                        iter_dev_offsets=arr(v.iter_dev_offsets, ni + 1, np.int64),
+                        dev_index=arr(v.dev_index, nd, np.int32),
+                        dev_pack_offsets=arr(v.dev_pack_offsets, nd + 1, np.int64),
+                        pack_capacity=arr(v.pack_capacity, npk, np.int64),
+                        pack_total=arr(v.pack_total, npk, np.int64),
+                        pack_attention=arr(v.pack_attention, npk, np.int64),
+                        pack_member_offsets=arr(v.pack_member_offsets, npk + 1, np.int64),
+                        member_index=arr(v.member_index, nm, np.int32))
+
+    def report(self):
+        m = Metrics()
+        self.ctx.check(self.ctx.lib.hbp_report_plan(self.ctx.h, self.h, C.byref(m), C.POINTER(C.c_double)(),
+                                                    C.POINTER(C.c_double)()))
+        return m
+
+    def simulate(self, profile: Optional[HardwareProfile] = None) -> SimTotals:
+        prof = profile if profile is not None else default_profile()
+        st = SimTotals()
+        self.ctx.check(self.ctx.lib.hbp_simulate_plan(self.ctx.h, self.h, C.byref(prof), C.byref(st),
+                                                      C.POINTER(C.c_double)()))
+        return st

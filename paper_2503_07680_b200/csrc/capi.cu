@@ -6,7 +6,10 @@
 
 #include "../../include/hbp_b200.h"
 #include "../../include/hbp_b200_testing.h"
+#include "costmodel.cuh"
 #include "engine.cuh"
+#include "metrics.cuh"
+#include "pipeline.cuh"
 #include "radix.cuh"
 
 namespace hbp_b200 {
@@ -104,6 +107,254 @@ int hbp_ctx_synchronize(hbp_ctx* ctx) {
 void* hbp_ctx_stream(hbp_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->stream) : nullptr; }
 
 int64_t hbp_ctx_launch_count(const hbp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---- hot path -----------------------------------------------------------------
+
+static std::vector<hbp_group_config> groups_of(const hbp_groups* g) {
+    if (g == nullptr || g->count < 0 || (g->count > 0 && g->groups == nullptr))
+        throw EngineError(HBP_ERR_VALIDATION, "no packing groups");
+    return std::vector<hbp_group_config>(g->groups, g->groups + g->count);
+}
+
+static std::string source_of(const hbp_samples* s) { return (s && s->source) ? s->source : ""; }
+
+int hbp_validate(hbp_ctx* ctx, const hbp_samples* samples) {
+    return guarded(ctx, [&] {
+        DeviceCorpus corpus;
+        ingest(*ctx, samples, corpus);
+        validate_corpus(*ctx, samples, corpus, source_of(samples));
+    });
+}
+
+int hbp_group_data(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* groups, int64_t* group_offsets,
+                   int32_t* member_index) {
+    return guarded(ctx, [&] {
+        const auto g = groups_of(groups);
+        validate_groups(g, groups->l_max);
+        DeviceCorpus corpus;
+        ingest(*ctx, samples, corpus);
+        std::vector<int64_t> off;
+        std::vector<int32_t> mem;
+        group_data_device(*ctx, corpus, g, groups->l_max, off, mem);
+        std::memcpy(group_offsets, off.data(), sizeof(int64_t) * off.size());
+        if (!mem.empty()) std::memcpy(member_index, mem.data(), sizeof(int32_t) * mem.size());
+    });
+}
+
+struct hbp_plan {
+    DevicePlan dp;
+    hbp_plan_view view{};
+};
+
+int hbp_pack(hbp_ctx* ctx, const hbp_samples* samples, int64_t capacity, const hbp_strategy* strategy, uint64_t seed,
+             hbp_plan** out) {
+    return guarded(ctx, [&] {
+        *out = nullptr;
+        validate_strategy(*strategy);
+        if (capacity < 1) fail_validation("pack capacity must be >= 1");
+        DeviceCorpus corpus;
+        ingest(*ctx, samples, corpus);
+        auto* p = new hbp_plan();
+        try {
+            pack_device(*ctx, corpus, capacity, *strategy, seed, p->dp);
+            p->dp.seed = seed;
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* groups,
+                   const hbp_plan_options* options, hbp_plan** out) {
+    return guarded(ctx, [&] {
+        *out = nullptr;
+        DeviceCorpus corpus;
+        ingest(*ctx, samples, corpus);
+        validate_corpus(*ctx, samples, corpus, source_of(samples));  // balance.cpp:209
+        PlanArgs a;
+        a.groups = groups_of(groups);
+        a.l_best = groups->l_best;
+        a.l_max = groups->l_max;
+        a.strategy = options->strategy;
+        a.device_count = options->device_count;
+        a.balance_batching = options->balance_batching != 0;
+        a.greedy_fill = options->greedy_fill != 0;
+        a.seed = options->seed;
+        auto* p = new hbp_plan();
+        try {
+            build_plan_device(*ctx, corpus, a, p->dp);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out) {
+    return guarded(ctx, [&] {
+        if (plan == nullptr) fail_validation("null plan");
+        DevicePlan& d = plan->dp;
+        plan_to_host(*ctx, d);
+        hbp_plan_view& v = plan->view;
+        v.device_count = d.device_count;
+        v.seed = d.seed;
+        v.groups.groups = d.groups.data();
+        v.groups.count = static_cast<int32_t>(d.groups.size());
+        v.groups.l_best = d.l_best;
+        v.groups.l_max = d.l_max;
+        v.n_iterations = d.n_iterations;
+        v.n_devices = d.n_devices;
+        v.n_packs = d.n_packs;
+        v.n_members = d.n_members;
+        v.iter_group = d.h_iter_group.data();
+        v.iter_dev_offsets = d.h_iter_dev_offsets.data();
+        v.dev_index = d.h_dev_index.data();
+        v.dev_pack_offsets = d.h_dev_pack_offsets.data();
+        v.pack_capacity = d.h_pack_capacity.data();
+        v.pack_total = d.h_pack_total.data();
+        v.pack_attention = d.h_pack_attention.data();
+        v.pack_member_offsets = d.h_pack_member_offsets.data();
+        v.member_index = d.h_member_index.data();
+        *out = v;
+    });
+}
+
+void hbp_plan_free(hbp_plan* plan) { delete plan; }
+
+namespace {
+
+// Uploads the pack-level arrays of a host view.
+struct UploadedPlan {
+    DevBuf<int32_t> ig;
+    DevBuf<int64_t> ido, dpo, cap, tot, att;
+    PlanArrays arrays{};
+    std::vector<hbp_group_config> groups;
+};
+
+void upload_view(hbp_ctx* ctx, const hbp_plan_view* v, UploadedPlan& u) {
+    cudaStream_t s = ctx->stream;
+    const size_t I = static_cast<size_t>(v->n_iterations), D = static_cast<size_t>(v->n_devices),
+                 P = static_cast<size_t>(v->n_packs);
+    auto up = [&](auto& buf, const auto* src, size_t n) {
+        buf.alloc(n + 1, s);
+        if (n) CUDA_CHECK(cudaMemcpyAsync(buf.p, src, sizeof(src[0]) * n, cudaMemcpyHostToDevice, s));
+    };
+    up(u.ig, v->iter_group, I);
+    up(u.ido, v->iter_dev_offsets, I + 1);
+    up(u.dpo, v->dev_pack_offsets, D + 1);
+    up(u.cap, v->pack_capacity, P);
+    up(u.tot, v->pack_total, P);
+    up(u.att, v->pack_attention, P);
+    u.arrays = PlanArrays{u.ig.p, u.ido.p, u.dpo.p, u.cap.p, u.tot.p, u.att.p, static_cast<i64>(I), static_cast<i64>(D)};
+    u.groups = groups_of(&v->groups);
+    // group indices must address the plan's groups (Plan::group_of uses .at())
+    for (size_t i = 0; i < I; ++i)
+        if (v->iter_group[i] < 0 || static_cast<size_t>(v->iter_group[i]) >= u.groups.size())
+            throw EngineError(HBP_ERR_VALIDATION, "iteration group index out of range");
+}
+
+PlanArrays arrays_of(const DevicePlan& d) {
+    return PlanArrays{d.iter_group.p, d.iter_dev_offsets.p, d.dev_pack_offsets.p, d.pack_capacity.p, d.pack_total.p,
+                      d.pack_attention.p, d.n_iterations, d.n_devices};
+}
+
+void run_eval(hbp_ctx* ctx, const PlanArrays& pa, int32_t device_count, const std::vector<hbp_group_config>& groups,
+              const hbp_hardware_profile* profile, EvalOut& eo, double* h_dbr, double* h_abr, double* h_secs,
+              double* h_dcomp, double* h_dcomm, double* h_didle) {
+    cudaStream_t s = ctx->stream;
+    const size_t I = static_cast<size_t>(pa.I), D = static_cast<size_t>(pa.D);
+    DevBuf<double> dbr, abr, secs, dc, dm, di;
+    if (h_dbr) dbr.alloc(I + 1, s);
+    if (h_abr) abr.alloc(I + 1, s);
+    if (h_secs) secs.alloc(I + 1, s);
+    if (h_dcomp) dc.alloc(D + 1, s);
+    if (h_dcomm) dm.alloc(D + 1, s);
+    if (h_didle) di.alloc(D + 1, s);
+    eval_plan(*ctx, pa, device_count, groups, profile, eo, dbr.p, abr.p, secs.p, dc.p, dm.p, di.p);
+    auto down = [&](double* h, DevBuf<double>& d, size_t n) {
+        if (h && n) CUDA_CHECK(cudaMemcpyAsync(h, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    };
+    down(h_dbr, dbr, I);
+    down(h_abr, abr, I);
+    down(h_secs, secs, I);
+    down(h_dcomp, dc, D);
+    down(h_dcomm, dm, D);
+    down(h_didle, di, D);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+int hbp_report(hbp_ctx* ctx, const hbp_plan_view* plan, hbp_metrics* out, double* per_iteration_dbr,
+               double* per_iteration_abr) {
+    return guarded(ctx, [&] {
+        if (plan->n_iterations == 0) fail_validation("metrics report: empty plan");
+        UploadedPlan u;
+        upload_view(ctx, plan, u);
+        EvalOut eo;
+        run_eval(ctx, u.arrays, plan->device_count, u.groups, nullptr, eo, per_iteration_dbr, per_iteration_abr,
+                 nullptr, nullptr, nullptr, nullptr);
+        *out = eo.m;
+    });
+}
+
+int hbp_report_plan(hbp_ctx* ctx, hbp_plan* plan, hbp_metrics* out, double* per_iteration_dbr,
+                    double* per_iteration_abr) {
+    return guarded(ctx, [&] {
+        EvalOut eo;
+        run_eval(ctx, arrays_of(plan->dp), plan->dp.device_count, plan->dp.groups, nullptr, eo, per_iteration_dbr,
+                 per_iteration_abr, nullptr, nullptr, nullptr, nullptr);
+        *out = eo.m;
+    });
+}
+
+int hbp_simulate(hbp_ctx* ctx, const hbp_plan_view* plan, const hbp_hardware_profile* profile, hbp_sim_totals* out,
+                 double* iteration_seconds, double* device_compute, double* device_comm, double* device_idle) {
+    return guarded(ctx, [&] {
+        const int pc = cm_profile_check(*profile);
+        if (pc) fail_validation(cm_profile_message(pc));
+        if (plan->n_iterations == 0) fail_validation("simulate: empty plan");
+        UploadedPlan u;
+        upload_view(ctx, plan, u);
+        EvalOut eo;
+        run_eval(ctx, u.arrays, plan->device_count, u.groups, profile, eo, nullptr, nullptr, iteration_seconds,
+                 device_compute, device_comm, device_idle);
+        out->metrics = eo.m;
+        out->total_seconds = eo.total_seconds;
+        out->gpu_days = eo.total_seconds * static_cast<double>(plan->device_count) / 86400.0;
+        out->switch_count = eo.switch_count;
+        out->device_count = plan->device_count;
+    });
+}
+
+int hbp_simulate_plan(hbp_ctx* ctx, hbp_plan* plan, const hbp_hardware_profile* profile, hbp_sim_totals* out,
+                      double* iteration_seconds) {
+    return guarded(ctx, [&] {
+        const int pc = cm_profile_check(*profile);
+        if (pc) fail_validation(cm_profile_message(pc));
+        if (plan->dp.n_iterations == 0) fail_validation("simulate: empty plan");
+        EvalOut eo;
+        run_eval(ctx, arrays_of(plan->dp), plan->dp.device_count, plan->dp.groups, profile, eo, nullptr, nullptr,
+                 iteration_seconds, nullptr, nullptr, nullptr);
+        out->metrics = eo.m;
+        out->total_seconds = eo.total_seconds;
+        out->gpu_days = eo.total_seconds * static_cast<double>(plan->dp.device_count) / 86400.0;
+        out->switch_count = eo.switch_count;
+        out->device_count = plan->dp.device_count;
+    });
+}
+
+int hbp_memory_used(hbp_ctx* ctx, int64_t length, int32_t sp, int32_t ckpt, const hbp_hardware_profile* profile,
+                    int64_t* out) {
+    return guarded(ctx, [&] {
+        if (sp < 1) fail_validation("sp must be >= 1");
+        if (ckpt < 0 || ckpt > profile->layer_count) fail_validation("ckpt must lie in [0, layer_count]");
+        *out = cm_memory_used(length, sp, ckpt, *profile);
+    });
+}
 
 // ---- testing hooks ----------------------------------------------------------
 

@@ -17,6 +17,7 @@
 
 namespace hbp_b200 {
 
+using u8 = uint8_t;
 using u32 = uint32_t;
 using u64 = uint64_t;
 using i64 = int64_t;

@@ -52,6 +52,19 @@ std::vector<T> read_vector(Ctx& c, const T* dptr, size_t n) {
     return out;
 }
 
+// Generic element-wise launch: f(i) for i in [0, n).
+template <typename F>
+__global__ void k_for_each(u64 n, F f) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<u64>(gridDim.x) * blockDim.x)
+        f(i);
+}
+template <typename F>
+void for_each_index(Ctx& c, u64 n, F f) {
+    if (n == 0) return;
+    LAUNCH(k_for_each<F>, grid_for(n, 256, 148u * 16u), 256, 0, c.stream, n, f);
+}
+
 // ---- stage: exact Fisher-Yates (shuffle.cu) --------------------------------
 // src[p] = the input position whose element Rng(seed).shuffle() leaves at
 // output position p, for a vector of m elements (reference rng.hpp:61-68).

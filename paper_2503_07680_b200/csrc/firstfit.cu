@@ -1,0 +1,407 @@
+// firstfit.cu — first-fit by runs: the FFD residue pass of ISF and greedy
+// fill, exactly as the reference orders them.
+//
+// Reference: first_fit over sort_decreasing (src/packing.cpp:55-60, 86-103)
+// places each item (length desc, id asc) into the first pack with room,
+// else opens a pack. For a run of c equal items of size s this means: visit
+// bins in index order, every bin with residual r >= s takes floor(r / s)
+// items (the run's next ids), until the run is used up; then open bins of
+// floor(cap / s) items. greedy_fill (src/balance.cpp:62-101) -- each pack,
+// nearest pool first, repeatedly takes the largest sample that fits, lowest
+// id first -- assigns exactly the same way when its candidate samples are
+// visited by (length desc, id asc): pools are disjoint length ranges and a
+// pack only ever receives decreasing lengths. It never opens bins.
+//
+// Engine: one warp walks the runs over a 32-ary max-residual tree whose
+// leaves are (residual << 32 | count) per bin: a ballot per level finds the
+// first child with max >= s, the leaf chunk is filled with one warp scan of
+// floor(r / s), maxima are written back up the path and the search resumes
+// from the path (finger search) instead of the root. Items larger than
+// cap / 2 can never share a bin; in FFD mode they are placed in bulk by a
+// parallel kernel before the walk. Output is a compact record list expanded
+// to per-item (bin, slot) by a parallel kernel.
+#include "stages.cuh"
+
+namespace hbp_b200 {
+
+namespace {
+
+constexpr int kMaxLevels = 8;
+
+struct TreeLayout {
+    u32* base;                  // all levels >= 1, concatenated
+    u64 off[kMaxLevels + 1];    // offset of level h (h >= 1) inside base
+    u64 size[kMaxLevels + 1];   // entries at level h (size[0] = max_bins leaves)
+    int H;                      // root level (size[H] == 1)
+};
+
+TreeLayout make_layout(u64 max_bins) {
+    TreeLayout t{};
+    t.size[0] = max_bins;
+    u64 total = 0;
+    int h = 0;
+    u64 sz = max_bins;
+    do {
+        ++h;
+        sz = (sz + 31) / 32;
+        t.size[h] = sz;
+        t.off[h] = total;
+        total += sz;
+    } while (sz > 1 && h < kMaxLevels);
+    t.H = h;
+    if (t.size[h] != 1) throw EngineError(HBP_ERR_VALIDATION, "first-fit tree too deep");
+    t.off[0] = total;  // total entries (stashed)
+    return t;
+}
+
+__global__ void k_runs(const u64* __restrict__ items, u64 n, u32* __restrict__ run_item, u32* __restrict__ run_len,
+                       const u64* __restrict__ excl) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 l = entry_len(items[i]);
+        if (i == 0 || entry_len(items[i - 1]) != l) {
+            const u64 r = excl[i];
+            run_item[r] = static_cast<u32>(i);
+            run_len[r] = l;
+        }
+    }
+}
+
+// Level h >= 1 from level h-1 (h-1 == 0: leaves).
+__global__ void k_tree_level(const u64* __restrict__ leaves, u32* __restrict__ base, TreeLayout t, int h, u64 lo,
+                             u64 hi) {
+    // recompute entries [lo, hi) of level h
+    for (u64 i = lo + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < hi;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        u32 m = 0;
+        for (int k = 0; k < 32; ++k) {
+            const u64 c = 32 * i + k;
+            if (c >= t.size[h - 1]) break;
+            const u32 v = (h == 1) ? static_cast<u32>(leaves[c] >> 32) : base[t.off[h - 1] + c];
+            m = v > m ? v : m;
+        }
+        base[t.off[h] + i] = m;
+    }
+}
+
+// FFD bulk: items [0, k) all longer than cap / 2 -> bin i each.
+__global__ void k_bulk_big(const u64* __restrict__ items, u64 k, u32 cap, u64* __restrict__ leaves) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < k;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 l = entry_len(items[i]);
+        leaves[i] = (static_cast<u64>(cap - l) << 32) | 1u;
+    }
+}
+
+struct EngineArgs {
+    const u64* items;
+    u32 n_items;
+    const u32* run_item;
+    const u32* run_len;
+    u32 n_runs;
+    u32 run_begin;
+    u64* leaves;
+    TreeLayout t;
+    u32 bins0;
+    u32 max_bins;
+    u32 cap;
+    int ffd;
+    FitRecords rec;
+    u32 rec0;
+    u32 max_records;
+    u32* out;  // [0] bins, [1] records, [2] overflow flag
+};
+
+__device__ __forceinline__ u32 tree_get(const TreeLayout& t, int h, u64 i) {
+    return i < t.size[h] ? t.base[t.off[h] + i] : 0u;
+}
+
+// One warp. Shared: children values held along the current path.
+__global__ void __launch_bounds__(32) k_fit_engine(EngineArgs a) {
+    __shared__ u32 s_held[kMaxLevels + 1][32];
+    __shared__ u64 s_node[kMaxLevels + 1];
+    const unsigned lane = threadIdx.x;
+    const TreeLayout& t = a.t;
+    const int H = t.H;
+    u32 B = a.bins0;
+    u32 nrec = a.rec0;
+    bool overflow = false;
+
+    // loads the children of node n at level h into s_held[h]; for h == 1 also
+    // returns this lane's leaf word
+    auto load_children = [&](int h, u64 n) -> u64 {
+        u64 leaf = 0;
+        const u64 ci = 32 * n + lane;
+        if (h == 1) {
+            leaf = ci < t.size[0] ? a.leaves[ci] : 0ull;
+            s_held[1][lane] = static_cast<u32>(leaf >> 32);
+        } else {
+            s_held[h][lane] = tree_get(t, h - 1, ci);
+        }
+        s_node[h] = n;
+        __syncwarp();
+        return leaf;
+    };
+    // after s_held[1] changed: write maxima up to the root
+    auto propagate = [&]() {
+        for (int h = 1; h <= H; ++h) {
+            const u32 m = warp_max(s_held[h][lane]);
+            const u64 n = s_node[h];
+            if (lane == 0) t.base[t.off[h] + n] = m;
+            if (h < H && lane == static_cast<unsigned>(n & 31)) s_held[h + 1][lane] = m;
+            __syncwarp();
+        }
+    };
+
+    for (u32 k = a.run_begin; k < a.n_runs; ++k) {
+        const u32 s = a.run_len[k];
+        u32 item = a.run_item[k];
+        const u32 end_item = (k + 1 < a.n_runs) ? a.run_item[k + 1] : a.n_items;
+        u32 c = end_item - item;
+
+        const u32 rootmax = t.base[t.off[H]];
+        if (rootmax >= s && B > 0) {
+            // fresh descent from the root
+            u64 leaf = load_children(H, 0);
+            int h = H;
+            int after = -1;
+            while (c > 0) {
+                const unsigned mask = __ballot_sync(0xffffffffu, s_held[h][lane] >= s) &
+                                      (after >= 31 ? 0u : (~0u << (after + 1)));
+                if (mask == 0) {
+                    if (h == H) break;  // nothing left with room
+                    after = static_cast<int>(s_node[h] & 31);
+                    ++h;
+                    continue;
+                }
+                const int f = __ffs(mask) - 1;
+                if (h > 1) {
+                    const u64 child = 32 * s_node[h] + f;
+                    leaf = load_children(h - 1, child);
+                    --h;
+                    after = -1;
+                    continue;
+                }
+                // h == 1: fill the eligible bins of this chunk in order
+                const u32 res = s_held[1][lane];
+                const bool elig = static_cast<int>(lane) >= f && res >= s;
+                const u32 capl = elig ? res / s : 0u;
+                const u32 incl = warp_inclusive_scan(capl);
+                const u32 excl = incl - capl;
+                const u32 take = excl >= c ? 0u : (capl < c - excl ? capl : c - excl);
+                const unsigned tm = __ballot_sync(0xffffffffu, take > 0);
+                const u32 r = __popc(tm & ((1u << lane) - 1u));
+                if (take > 0) {
+                    const u32 ri = nrec + r;
+                    if (ri < a.max_records) {
+                        a.rec.item[ri] = item + excl;
+                        a.rec.count[ri] = take;
+                        a.rec.bin[ri] = static_cast<u32>(32 * s_node[1] + lane);
+                        a.rec.per_bin[ri] = take;
+                        a.rec.slot0[ri] = static_cast<u32>(leaf);
+                    }
+                    const u32 nres = res - take * s;
+                    const u32 ncnt = static_cast<u32>(leaf) + take;
+                    leaf = (static_cast<u64>(nres) << 32) | ncnt;
+                    a.leaves[32 * s_node[1] + lane] = leaf;
+                    s_held[1][lane] = nres;
+                }
+                __syncwarp();
+                const u32 used = __shfl_sync(0xffffffffu, incl, 31);
+                const u32 got = used < c ? used : c;
+                nrec += __popc(tm);
+                c -= got;
+                item += got;
+                propagate();
+                // every eligible bin of the chunk is now below s: continue right
+                after = 31;
+            }
+        }
+        if (c > 0 && a.ffd) {
+            const u32 per = a.cap / s;
+            const u32 nb = (c + per - 1) / per;
+            if (B + nb > a.max_bins) {
+                overflow = true;
+                break;
+            }
+            if (nrec < a.max_records && lane == 0) {
+                a.rec.item[nrec] = item;
+                a.rec.count[nrec] = c;
+                a.rec.bin[nrec] = B;
+                a.rec.per_bin[nrec] = per;
+                a.rec.slot0[nrec] = 0;
+            }
+            ++nrec;
+            const u32 res_full = a.cap - per * s;
+            const u32 last_cnt = c - (nb - 1) * per;
+            const u32 res_last = a.cap - last_cnt * s;
+            for (u32 b = lane; b < nb; b += 32) {
+                const bool last = (b == nb - 1);
+                a.leaves[B + b] = (static_cast<u64>(last ? res_last : res_full) << 32) | (last ? last_cnt : per);
+            }
+            // raise maxima over the new range at every level
+            const u64 lo = B, hi = static_cast<u64>(B) + nb - 1;  // inclusive
+            const u64 full_hi = nb > 1 ? hi - 1 : lo;              // last full bin (if nb > 1)
+            for (int h = 1; h <= H; ++h) {
+                const u64 ilo = lo >> (5 * h), ihi = hi >> (5 * h);
+                for (u64 i = ilo + lane; i <= ihi; i += 32) {
+                    const u64 slo = i << (5 * h), shi = ((i + 1) << (5 * h)) - 1;
+                    u32 v = t.base[t.off[h] + i];
+                    if (nb > 1 && slo <= full_hi && shi >= lo) v = v > res_full ? v : res_full;
+                    if (slo <= hi && shi >= hi) v = v > res_last ? v : res_last;
+                    t.base[t.off[h] + i] = v;
+                }
+                __syncwarp();
+            }
+            B += nb;
+            c = 0;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        a.out[0] = B;
+        a.out[1] = nrec;
+        a.out[2] = (overflow || nrec > a.max_records) ? 1u : 0u;
+    }
+}
+
+__global__ void k_expand(FitRecords rec, const u32* __restrict__ nrec_p, u64 n_items, u32* __restrict__ item_bin,
+                         u32* __restrict__ item_slot) {
+    const u32 nrec = *nrec_p;
+    for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < n_items;
+         j += static_cast<u64>(gridDim.x) * blockDim.x) {
+        // last record with item <= j
+        u32 lo = 0, hi = nrec;
+        while (lo < hi) {
+            const u32 mid = (lo + hi) >> 1;
+            if (rec.item[mid] <= j) lo = mid + 1;
+            else hi = mid;
+        }
+        u32 b = kNone, sl = kNone;
+        if (lo > 0) {
+            const u32 r = lo - 1;
+            const u64 off = j - rec.item[r];
+            if (off < rec.count[r]) {
+                const u32 per = rec.per_bin[r];
+                b = rec.bin[r] + static_cast<u32>(off / per);
+                sl = rec.slot0[r] + static_cast<u32>(off % per);
+            }
+        }
+        item_bin[j] = b;
+        item_slot[j] = sl;
+    }
+}
+
+}  // namespace
+
+FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
+                         FitMode mode, FitRecords rec, i64 max_records) {
+    FitResult out;
+    out.bins = bins0;
+    if (n_items_s <= 0) return out;
+    const u64 n = static_cast<u64>(n_items_s);
+    cudaStream_t s = c.stream;
+    const bool ffd = mode == FitMode::Ffd;
+    if (max_bins < 1) max_bins = 1;
+
+    // runs of equal length
+    DevBuf<u64> flags_excl(n, s);
+    DevBuf<u32> run_item(n, s), run_len(n, s), scal(4, s);
+    {
+        u64* ex = flags_excl.p;
+        u32* sc = scal.p;
+        const i64 nn = static_cast<i64>(n);
+        scan_exclusive<u64>(
+            nn,
+            [=] __device__(i64 i) {
+                return static_cast<u64>(i == 0 || entry_len(items[i]) != entry_len(items[i - 1]));
+            },
+            [=] __device__(i64 i, u64 v) {
+                ex[i] = v;
+                if (i == nn - 1) {
+                    const bool head = i == 0 || entry_len(items[i]) != entry_len(items[i - 1]);
+                    sc[0] = static_cast<u32>(v + (head ? 1 : 0));
+                }
+            },
+            s, c.scan);
+    }
+    LAUNCH(k_runs, grid_for(n, 256, 148u * 16u), 256, 0, s, items, n, run_item.p, run_len.p, flags_excl.p);
+
+    // bulk-place the items that can never share a bin (FFD with no live bins)
+    u32 bulk = 0;
+    u32 run_begin = 0;
+    const u32 n_runs = read_scalar(c, scal.p);
+    std::vector<u32> h_runs;
+    if (ffd && bins0 == 0) {
+        // runs are in decreasing length: count leading runs with 2*s > cap
+        h_runs = read_vector(c, run_len.p, n_runs);
+        while (run_begin < n_runs && 2ull * h_runs[run_begin] > cap) ++run_begin;
+        if (run_begin > 0) {
+            bulk = (run_begin < n_runs) ? read_vector(c, run_item.p + run_begin, 1)[0] : static_cast<u32>(n);
+        }
+    }
+
+    TreeLayout t = make_layout(static_cast<u64>(max_bins));
+    DevBuf<u32> tree(t.off[0], s);
+    t.base = tree.p;
+    if (bulk > 0) {
+        LAUNCH(k_bulk_big, grid_for(bulk, 256, 148u * 16u), 256, 0, s, items, static_cast<u64>(bulk), cap, leaves);
+    }
+    const u64 live = static_cast<u64>(bins0) + bulk;
+    // leaves beyond the live ones start empty
+    if (static_cast<u64>(max_bins) > live)
+        CUDA_CHECK(cudaMemsetAsync(leaves + live, 0, sizeof(u64) * (max_bins - live), s));
+    CUDA_CHECK(cudaMemsetAsync(tree.p, 0, sizeof(u32) * t.off[0], s));
+    for (int h = 1; h <= t.H; ++h) {
+        const u64 hi = (live + (1ull << (5 * h)) - 1) >> (5 * h);
+        if (hi == 0) break;
+        LAUNCH(k_tree_level, grid_for(hi, 256, 148u * 16u), 256, 0, s, leaves, tree.p, t, h, 0ull, hi);
+    }
+    u32 rec0 = 0;
+    if (bulk > 0) {
+        // one record covers the bulk: item i -> bin i
+        const u32 one[5] = {0u, bulk, 0u, 1u, 0u};
+        CUDA_CHECK(cudaMemcpyAsync(rec.item, &one[0], 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(rec.count, &one[1], 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(rec.bin, &one[2], 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(rec.per_bin, &one[3], 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(rec.slot0, &one[4], 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));  // `one` is a stack buffer
+        rec0 = 1;
+    }
+    EngineArgs a;
+    a.items = items;
+    a.n_items = static_cast<u32>(n);
+    a.run_item = run_item.p;
+    a.run_len = run_len.p;
+    a.n_runs = n_runs;
+    a.run_begin = run_begin;
+    a.leaves = leaves;
+    a.t = t;
+    a.bins0 = static_cast<u32>(live);
+    a.max_bins = static_cast<u32>(max_bins);
+    a.cap = cap;
+    a.ffd = ffd ? 1 : 0;
+    a.rec = rec;
+    a.rec0 = rec0;
+    a.max_records = static_cast<u32>(max_records);
+    a.out = scal.p;
+    LAUNCH(k_fit_engine, 1, 32, 0, s, a);
+    const auto o = read_vector(c, scal.p, 3);
+    if (o[2]) throw EngineError(HBP_ERR_CUDA, "first-fit engine: record or bin capacity exceeded");
+    out.bins = o[0];
+    out.records = o[1];
+    return out;
+}
+
+void expand_fit_records(Ctx& c, FitRecords rec, i64 n_records, i64 n_items, u32* item_bin, u32* item_slot) {
+    if (n_items <= 0) return;
+    DevBuf<u32> nrec(1, c.stream);
+    const u32 nr = static_cast<u32>(n_records);
+    CUDA_CHECK(cudaMemcpyAsync(nrec.p, &nr, 4, cudaMemcpyHostToDevice, c.stream));
+    LAUNCH(k_expand, grid_for(n_items, 256, 148u * 16u), 256, 0, c.stream, rec, nrec.p, static_cast<u64>(n_items),
+           item_bin, item_slot);
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));  // nr lives on the host stack
+}
+
+}  // namespace hbp_b200

@@ -1,0 +1,1038 @@
+// pipeline.cu — build_plan on the GPU (reference src/balance.cpp:207-258).
+//
+//   ingest      SampleSet::validate (types.cpp:8-24) + lengths to u32
+//   group_data  stable partition by group (balance.cpp:25-44): one radix pass
+//   per group, largest first:
+//     pack      ISF rounds (shuffle.cu + nextfit.cu), residue FFD (firstfit.cu)
+//     fill      greedy_fill from the smaller pools (firstfit.cu, fill mode)
+//     layout    members of every pack contiguous; totals and Σ L²
+//     batching  stable attention sort + chunks of N, spill tail (balance.cpp:105-192)
+//   plan shuffle (balance.cpp:255-256) and CSR output.
+// The host only synchronises for data-dependent sizes (pool sizes per ISF
+// round, pack counts, record counts); all data stays in HBM.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "pipeline.cuh"
+#include "radix.cuh"
+#include "rng.cuh"
+
+namespace hbp_b200 {
+
+namespace {
+
+constexpr int kB = 256;
+
+inline unsigned G(u64 n) { return grid_for(n, kB, 148u * 16u); }
+
+inline int bits_for(u64 maxval) {
+    int b = 1;
+    while (b < 32 && (maxval >> b) != 0) ++b;
+    return b;
+}
+
+#define GRID_STRIDE(i, n) \
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < (n); i += static_cast<u64>(gridDim.x) * blockDim.x)
+
+// ---------------------------------------------------------------------------
+// ingest
+// ---------------------------------------------------------------------------
+
+struct IngestFlags {
+    unsigned long long first_bad_len;  // length < 1
+    unsigned long long first_over;     // length > limit
+    unsigned long long neg;            // ids <= -2
+    unsigned long long not_ascending;
+};
+
+__global__ void k_ingest(const int64_t* __restrict__ len64, const int64_t* __restrict__ ids, u64 n, int64_t limit,
+                         u32* __restrict__ len32, IngestFlags* __restrict__ f) {
+    GRID_STRIDE(i, n) {
+        const int64_t L = len64[i];
+        if (L < 1) atomicMin(&f->first_bad_len, static_cast<unsigned long long>(i));
+        if (L > limit) atomicMin(&f->first_over, static_cast<unsigned long long>(i));
+        len32[i] = L < 1 ? 0u : (L > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(L));
+        if (ids) {
+            if (ids[i] <= -2) atomicAdd(&f->neg, 1ull);
+            if (i + 1 < n && ids[i] >= ids[i + 1]) f->not_ascending = 1ull;
+        }
+    }
+}
+
+__global__ void k_id_words(const int64_t* __restrict__ ids, const u32* __restrict__ order, u64 n, bool high,
+                           u32* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        const u64 v = static_cast<u64>(ids[order[i]]) ^ (1ull << 63);  // order-preserving for signed
+        out[i] = high ? static_cast<u32>(v >> 32) : static_cast<u32>(v);
+    }
+}
+
+__global__ void k_iota(u32* __restrict__ a, u64 n) {
+    GRID_STRIDE(i, n) a[i] = static_cast<u32>(i);
+}
+
+__global__ void k_ranks_dups(const int64_t* __restrict__ ids, const u32* __restrict__ order, u64 n,
+                             u32* __restrict__ rank, unsigned long long* __restrict__ first_dup) {
+    GRID_STRIDE(r, n) {
+        const u32 i = order[r];
+        rank[i] = static_cast<u32>(r);
+        if (r >= 1 && ids[order[r - 1]] == ids[i]) {
+            // the second occurrence (in input order) of an id is the first duplicate seen
+            if (r == 1 || ids[order[r - 2]] != ids[i]) atomicMin(first_dup, static_cast<unsigned long long>(i));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// group_data + entries
+// ---------------------------------------------------------------------------
+
+__global__ void k_group_keys(const u32* __restrict__ len32, u64 n, const int64_t* __restrict__ glen, int ng,
+                             u32* __restrict__ key, u32* __restrict__ val, unsigned long long* __restrict__ counts) {
+    __shared__ unsigned long long s_cnt[64];
+    for (int g = threadIdx.x; g < 64; g += blockDim.x) s_cnt[g] = 0;
+    __syncthreads();
+    GRID_STRIDE(i, n) {
+        const u32 L = len32[i];
+        int g = 0;
+        while (g < ng - 1 && static_cast<int64_t>(L) > glen[g]) ++g;
+        key[i] = static_cast<u32>(g);
+        val[i] = static_cast<u32>(i);
+        atomicAdd(&s_cnt[g < 64 ? g : 63], 1ull);
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < ng && g < 64; g += blockDim.x)
+        if (s_cnt[g]) atomicAdd(&counts[g], s_cnt[g]);
+}
+
+__global__ void k_entries_from_idx(const u32* __restrict__ len32, const u32* __restrict__ idx, u64 n,
+                                   u64* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        const u32 j = idx[i];
+        out[i] = make_entry(len32[j], j);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// entry sorting: (length desc, key asc)
+// ---------------------------------------------------------------------------
+
+__global__ void k_keys_of_entries(const u64* __restrict__ e, const u32* __restrict__ key32, u64 n,
+                                  u32* __restrict__ k, u32* __restrict__ v) {
+    GRID_STRIDE(i, n) {
+        const u32 idx = entry_idx(e[i]);
+        k[i] = key32 ? key32[idx] : idx;
+        v[i] = static_cast<u32>(i);
+    }
+}
+
+__global__ void k_lens_of(const u64* __restrict__ e, const u32* __restrict__ perm, u64 n, u32* __restrict__ k) {
+    GRID_STRIDE(i, n) k[i] = entry_len(e[perm[i]]);
+}
+
+__global__ void k_gather_entries(const u64* __restrict__ in, const u32* __restrict__ perm, u64 n,
+                                 u64* __restrict__ out) {
+    GRID_STRIDE(i, n) out[i] = in[perm[i]];
+}
+
+// ---------------------------------------------------------------------------
+// pack layout, fill, stats
+// ---------------------------------------------------------------------------
+
+__global__ void k_isf_leaves(const u64* __restrict__ pack_off, const u32* __restrict__ pack_total, u64 np,
+                             u64 n_members, u32 cap, u64* __restrict__ leaves) {
+    GRID_STRIDE(p, np) {
+        const u64 end = (p + 1 < np) ? pack_off[p + 1] : n_members;
+        const u64 size = end - pack_off[p];
+        leaves[p] = (static_cast<u64>(cap - pack_total[p]) << 32) | static_cast<u32>(size);
+    }
+}
+
+__global__ void k_mark_consumed(const u64* __restrict__ items, const u32* __restrict__ item_bin, u64 n,
+                                u8* __restrict__ consumed) {
+    GRID_STRIDE(i, n) {
+        if (item_bin[i] != kNone) consumed[entry_idx(items[i])] = 1;
+    }
+}
+
+__global__ void k_place_isf(const u64* __restrict__ sink_members, const u64* __restrict__ pack_off, u64 np,
+                            u64 n_members, const u64* __restrict__ out_off, u64* __restrict__ out) {
+    GRID_STRIDE(p, np) {
+        const u64 a = pack_off[p];
+        const u64 b = (p + 1 < np) ? pack_off[p + 1] : n_members;
+        const u64 d = out_off[p];
+        for (u64 k = a; k < b; ++k) out[d + (k - a)] = sink_members[k];
+    }
+}
+
+__global__ void k_place_items(const u64* __restrict__ items, const u32* __restrict__ item_bin,
+                              const u32* __restrict__ item_slot, u64 n, u64 bin_base,
+                              const u64* __restrict__ out_off, u64* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        const u32 b = item_bin[i];
+        if (b != kNone) out[out_off[bin_base + b] + item_slot[i]] = items[i];
+    }
+}
+
+__global__ void k_pack_stats(const u64* __restrict__ members, const u64* __restrict__ off, u64 np, u64 mbase,
+                             u64 pbase, u32 cap, u64* __restrict__ g_moff, u32* __restrict__ g_cnt,
+                             u32* __restrict__ g_cap, u32* __restrict__ g_total, u64* __restrict__ g_att) {
+    GRID_STRIDE(p, np) {
+        const u64 a = off[p], b = off[p + 1];
+        u64 tot = 0, att = 0;
+        for (u64 k = a; k < b; ++k) {
+            const u64 l = entry_len(members[k]);
+            tot += l;
+            att += l * l;
+        }
+        g_moff[pbase + p] = mbase + a;
+        g_cnt[pbase + p] = static_cast<u32>(b - a);
+        g_cap[pbase + p] = cap;
+        g_total[pbase + p] = static_cast<u32>(tot);
+        g_att[pbase + p] = att;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// batching
+// ---------------------------------------------------------------------------
+
+__global__ void k_att_words(const u64* __restrict__ att, const u32* __restrict__ perm, u64 n, bool high,
+                            u32* __restrict__ out) {
+    GRID_STRIDE(i, n) {
+        const u64 v = att[perm[i]];
+        out[i] = high ? static_cast<u32>(v >> 32) : static_cast<u32>(v);
+    }
+}
+
+__global__ void k_full_iterations(const u32* __restrict__ order, u64 nfull, u32 N, u32 pbase, int gi, u64 ibase,
+                                  u32* __restrict__ slots, int32_t* __restrict__ igroup) {
+    GRID_STRIDE(x, nfull * N) {
+        const u64 k = x / N;
+        slots[(ibase + k) * N + (x % N)] = pbase + order[x];
+        if (x % N == 0) igroup[ibase + k] = gi;
+    }
+}
+
+// Spill tail (balance.cpp:121-151): samples sorted (length desc, id asc)
+// go one by one to the device with the least attention that still fits
+// (lowest device on ties); unpadded capacity; fallback keeps the packs.
+__global__ void k_spill(const u64* __restrict__ sorted, u64 k, u32 N, u32 cap, const u32* __restrict__ tail_packs,
+                        u32 rem, u32 spill_pbase, u64 spill_mbase, int gi, u64 iter, u64* __restrict__ g_members,
+                        u64* __restrict__ g_moff, u32* __restrict__ g_cnt, u32* __restrict__ g_cap,
+                        u32* __restrict__ g_total, u64* __restrict__ g_att, u32* __restrict__ dev_of,
+                        u32* __restrict__ slots, int32_t* __restrict__ igroup) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // device totals / attention in registers of one thread (N small)
+    bool ok = true;
+    for (u32 d = 0; d < N; ++d) {
+        g_total[spill_pbase + d] = 0;
+        g_att[spill_pbase + d] = 0;
+        g_cnt[spill_pbase + d] = 0;
+    }
+    for (u64 i = 0; i < k; ++i) {
+        const u32 L = entry_len(sorted[i]);
+        u32 target = N;
+        u64 best = 0;
+        for (u32 d = 0; d < N; ++d) {
+            if (cap - g_total[spill_pbase + d] < L) continue;
+            const u64 a = g_att[spill_pbase + d];
+            if (target == N || a < best) {
+                target = d;
+                best = a;
+            }
+        }
+        if (target == N) {
+            ok = false;
+            break;
+        }
+        dev_of[i] = target;
+        g_total[spill_pbase + target] += L;
+        g_att[spill_pbase + target] += static_cast<u64>(L) * L;
+        g_cnt[spill_pbase + target] += 1;
+    }
+    igroup[iter] = gi;
+    if (ok) {
+        // members grouped by device, in assignment order
+        u64 off = spill_mbase;
+        for (u32 d = 0; d < N; ++d) {
+            g_moff[spill_pbase + d] = off;
+            off += g_cnt[spill_pbase + d];
+            g_cap[spill_pbase + d] = g_total[spill_pbase + d];
+        }
+        for (u32 d = 0; d < N; ++d) g_cnt[spill_pbase + d] = 0;
+        for (u64 i = 0; i < k; ++i) {
+            const u32 d = dev_of[i];
+            g_members[g_moff[spill_pbase + d] + g_cnt[spill_pbase + d]++] = sorted[i];
+        }
+        for (u32 d = 0; d < N; ++d) slots[iter * N + d] = g_cnt[spill_pbase + d] ? spill_pbase + d : kNone;
+    } else {
+        for (u32 d = 0; d < N; ++d) slots[iter * N + d] = d < rem ? tail_packs[d] : kNone;
+    }
+}
+
+__global__ void k_gather_spill(const u64* __restrict__ g_members, const u64* __restrict__ g_moff,
+                               const u32* __restrict__ g_cnt, const u32* __restrict__ tail_packs, u32 rem,
+                               const u64* __restrict__ tail_off, u64* __restrict__ out) {
+    // one block per tail pack
+    for (u32 t = blockIdx.x; t < rem; t += gridDim.x) {
+        const u32 p = tail_packs[t];
+        const u64 a = g_moff[p];
+        const u32 c = g_cnt[p];
+        for (u32 k = threadIdx.x; k < c; k += blockDim.x) out[tail_off[t] + k] = g_members[a + k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// plan output
+// ---------------------------------------------------------------------------
+
+__global__ void k_out_iterations(const u32* __restrict__ src, u64 I, u32 N, const int32_t* __restrict__ igroup,
+                                 int32_t* __restrict__ out_group, int64_t* __restrict__ out_doff,
+                                 int32_t* __restrict__ out_dindex) {
+    GRID_STRIDE(p, I) {
+        out_group[p] = igroup[src[p]];
+        out_doff[p] = static_cast<int64_t>(p * N);
+        for (u32 d = 0; d < N; ++d) out_dindex[p * N + d] = static_cast<int32_t>(d);
+        if (p == I - 1) out_doff[I] = static_cast<int64_t>(I * N);
+    }
+}
+
+__global__ void k_out_packs(const u32* __restrict__ src, u64 I, u32 N, const u32* __restrict__ slots,
+                            const int64_t* __restrict__ dev_pack_off, const u32* __restrict__ g_cnt,
+                            const u32* __restrict__ g_cap, const u32* __restrict__ g_total,
+                            const u64* __restrict__ g_att, int64_t* __restrict__ pcap, int64_t* __restrict__ ptot,
+                            int64_t* __restrict__ patt, u32* __restrict__ pglobal, u64* __restrict__ pcnt) {
+    GRID_STRIDE(x, I * N) {
+        const u64 p = x / N, d = x % N;
+        const u32 g = slots[static_cast<u64>(src[p]) * N + d];
+        if (g == kNone) continue;
+        const int64_t q = dev_pack_off[x];
+        pcap[q] = g_cap[g];
+        ptot[q] = g_total[g];
+        patt[q] = static_cast<int64_t>(g_att[g]);
+        pglobal[q] = g;
+        pcnt[q] = g_cnt[g];
+    }
+}
+
+__global__ void k_out_members(const u32* __restrict__ pglobal, u64 P, const int64_t* __restrict__ moff,
+                              const u64* __restrict__ g_moff, const u32* __restrict__ g_cnt,
+                              const u64* __restrict__ g_members, int32_t* __restrict__ out) {
+    // one warp per output pack
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    for (u64 q = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; q < P; q += warps) {
+        const u32 g = pglobal[q];
+        const u64 a = g_moff[g];
+        const u32 c = g_cnt[g];
+        const int64_t d = moff[q];
+        for (u32 k = lane_id(); k < c; k += 32) out[d + k] = static_cast<int32_t>(entry_idx(g_members[a + k]));
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
+void validate_groups(const std::vector<hbp_group_config>& g, int64_t l_max) {
+    if (g.empty()) fail_validation("no packing groups");
+    int64_t prev = 0;
+    for (const auto& x : g) {
+        if (x.length <= prev) fail_validation("group lengths must be strictly increasing");
+        if (x.sp < 1 || x.ckpt < 0) fail_validation("invalid group runtime config");
+        prev = x.length;
+    }
+    if (g.back().length != l_max) fail_validation("last group must carry l_max");
+}
+
+void validate_strategy(const hbp_strategy& s) {
+    if (s.kind == HBP_STRATEGY_ISF) {
+        if (s.isf_iterations < 1) fail_validation("isf_iterations must be >= 1");
+        if (s.isf_fill_threshold <= 0.0 || s.isf_fill_threshold > 1.0)
+            fail_validation("isf fill threshold must lie in (0, 1]");
+    }
+    if (s.kind < HBP_STRATEGY_RANDOM || s.kind > HBP_STRATEGY_SPFHP) fail_validation("unknown packing strategy");
+}
+
+namespace {
+
+struct IngestResult {
+    IngestFlags f;
+};
+
+// Uploads lengths (and ids), converts, and collects the flags. `limit` is
+// the largest admissible length (l_max or the pack capacity).
+IngestFlags upload_and_scan(Ctx& c, const hbp_samples* in, DeviceCorpus& corpus, int64_t limit,
+                            DevBuf<int64_t>& dids) {
+    const u64 n = static_cast<u64>(in->n);
+    cudaStream_t s = c.stream;
+    corpus.n = in->n;
+    corpus.len32.alloc(n, s);
+    DevBuf<int64_t> dlen;
+    const int64_t* len_dev = in->lengths;
+    const int64_t* ids_dev = in->ids;
+    if (in->memory == HBP_MEM_HOST) {
+        dlen.alloc(n, s);
+        CUDA_CHECK(cudaMemcpyAsync(dlen.p, in->lengths, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+        len_dev = dlen.p;
+        if (in->ids) {
+            dids.alloc(n, s);
+            CUDA_CHECK(cudaMemcpyAsync(dids.p, in->ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+            ids_dev = dids.p;
+        }
+    }
+    DevBuf<IngestFlags> f(1, s);
+    IngestFlags init{~0ull, ~0ull, 0ull, 0ull};
+    CUDA_CHECK(cudaMemcpyAsync(f.p, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    LAUNCH(k_ingest, G(n), kB, 0, s, len_dev, ids_dev, n, limit, corpus.len32.p, f.p);
+    IngestFlags out = read_scalar(c, f.p);
+    corpus.neg_ids = static_cast<i64>(out.neg);
+    corpus.ids_ascending = out.not_ascending == 0;
+    corpus.key_bits = bits_for(n > 0 ? n - 1 : 0);
+    if (in->ids) {
+        if (in->memory == HBP_MEM_HOST) {
+            corpus.ids_host = in->ids;
+        } else {
+            corpus.h_ids = read_vector(c, in->ids, n);
+            corpus.ids_host = corpus.h_ids.data();
+        }
+    } else {
+        corpus.ids_host = nullptr;
+    }
+    return out;
+}
+
+// Ranks of general (non-ascending) ids; returns the first duplicate index.
+u64 rank_ids(Ctx& c, const int64_t* ids_dev, DeviceCorpus& corpus) {
+    const u64 n = static_cast<u64>(corpus.n);
+    cudaStream_t s = c.stream;
+    DevBuf<u32> order(n, s), words(n, s), tk(n, s), tv(n, s);
+    LAUNCH(k_iota, G(n), kB, 0, s, order.p, n);
+    for (int pass = 0; pass < 2; ++pass) {
+        LAUNCH(k_id_words, G(n), kB, 0, s, ids_dev, order.p, n, pass == 1, words.p);
+        radix_sort_pairs(c, words.p, order.p, static_cast<i64>(n), 32, false, tk.p, tv.p);
+    }
+    corpus.key32.alloc(n, s);
+    DevBuf<unsigned long long> dup(1, s);
+    const unsigned long long none = ~0ull;
+    CUDA_CHECK(cudaMemcpyAsync(dup.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    LAUNCH(k_ranks_dups, G(n), kB, 0, s, ids_dev, order.p, n, corpus.key32.p, dup.p);
+    return read_scalar(c, dup.p);
+}
+
+// Sorts entries by (length desc, key asc) in place.
+void sort_entries(Ctx& c, const DeviceCorpus& corpus, u64* e, u64 n, bool key_ordered, u32 max_len) {
+    if (n <= 1) return;
+    cudaStream_t s = c.stream;
+    DevBuf<u32> k(n, s), v(n, s), tk(n, s), tv(n, s);
+    LAUNCH(k_keys_of_entries, G(n), kB, 0, s, e, corpus.key32.p, n, k.p, v.p);
+    if (!key_ordered) radix_sort_pairs(c, k.p, v.p, static_cast<i64>(n), corpus.key_bits, false, tk.p, tv.p);
+    LAUNCH(k_lens_of, G(n), kB, 0, s, e, v.p, n, k.p);
+    radix_sort_pairs(c, k.p, v.p, static_cast<i64>(n), bits_for(max_len), true, tk.p, tv.p);
+    DevBuf<u64> tmp(n, s);
+    LAUNCH(k_gather_entries, G(n), kB, 0, s, e, v.p, n, tmp.p);
+    CUDA_CHECK(cudaMemcpyAsync(e, tmp.p, sizeof(u64) * n, cudaMemcpyDeviceToDevice, s));
+}
+
+// Global pack table being built.
+struct PackTable {
+    DevBuf<u64> members;   // entries
+    DevBuf<u64> moff;      // first member per pack
+    DevBuf<u32> cnt, cap, total;
+    DevBuf<u64> att;
+    u64 n_packs = 0, n_members = 0;
+};
+
+// Result of packing one group (members laid out contiguously).
+struct GroupPacks {
+    u64 P = 0;  // packs in PackList order
+    u64 M = 0;  // members
+    DevBuf<u64> members;
+    DevBuf<u64> off;  // P + 1
+};
+
+// Stage 1 of one group: pack(pool, cap, strategy, seed) -> ISF packs +
+// FFD bins with their leaves (residual, count) for greedy fill.
+struct PackedGroup {
+    u64 n_isf = 0;
+    u64 n_isf_members = 0;
+    DevBuf<u64> isf_members, isf_off;
+    DevBuf<u32> isf_total;
+    DevBuf<u64> isf_att;
+    u64 n_ffd = 0;
+    u64 n_residue = 0;
+    DevBuf<u64> residue;       // sorted residue items
+    DevBuf<u32> res_bin, res_slot;
+    DevBuf<u64> leaves;        // all packs: ISF then FFD bins
+    u64 P() const { return n_isf + n_ffd; }
+};
+
+void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u32 cap, const hbp_strategy& st,
+               uint64_t seed, PackedGroup& out) {
+    cudaStream_t s = c.stream;
+    out.isf_members.alloc(m, s);
+    out.isf_off.alloc(m + 1, s);
+    out.isf_total.alloc(m + 1, s);
+    out.isf_att.alloc(m + 1, s);
+    DevBuf<u64> counters(2, s);
+    counters.zero();
+    PackSink sink{out.isf_members.p, out.isf_off.p, out.isf_total.p, out.isf_att.p, counters.p, counters.p + 1};
+    DevBuf<u64> A(m, s), Bf(m, s);
+    CUDA_CHECK(cudaMemcpyAsync(A.p, pool_in, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
+    u64 cur = m;
+    bool residue_ffd = false;
+    bool key_ordered = corpus.key32.p == nullptr;  // pool in input order == key order
+    if (st.kind == HBP_STRATEGY_ISF || st.kind == HBP_STRATEGY_RANDOM) {
+        DevBuf<u32> src(m, s);
+        const int rounds = st.kind == HBP_STRATEGY_ISF ? st.isf_iterations : 1;
+        u64 tmin = 0;
+        if (st.kind == HBP_STRATEGY_ISF) {
+            const double min_fill = static_cast<double>(cap) * st.isf_fill_threshold;  // packing.cpp:177-178
+            tmin = static_cast<u64>(std::ceil(min_fill));
+        }
+        for (int r = 0; r < rounds && cur > 0; ++r) {
+            const uint64_t rs = st.kind == HBP_STRATEGY_ISF ? derive_seed(seed, "isf-round", static_cast<uint64_t>(r))
+                                                              : derive_seed(seed, "random-pack");
+            fy_source_positions(c, rs, static_cast<i64>(cur), src.p);
+            gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(cur));
+            cur = static_cast<u64>(nextfit_freeze(c, Bf.p, static_cast<i64>(cur), cap, tmin, sink, A.p));
+        }
+        residue_ffd = st.kind == HBP_STRATEGY_ISF;
+        key_ordered = false;  // the residue is in shuffled order
+    } else if (st.kind == HBP_STRATEGY_FFD) {
+        residue_ffd = true;
+    } else if (st.kind == HBP_STRATEGY_FFS) {
+        // first fit over a seeded shuffle (packing.cpp:239-243)
+        DevBuf<u32> src(m, s);
+        fy_source_positions(c, derive_seed(seed, "ffs"), static_cast<i64>(m), src.p);
+        gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(m));
+        CUDA_CHECK(cudaMemcpyAsync(A.p, Bf.p, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
+    } else {
+        throw EngineError(HBP_ERR_VALIDATION, "packing strategy not available in the GPU engine: " +
+                                                  std::string(st.kind == HBP_STRATEGY_BFS ? "bfs" : "spfhp"));
+    }
+    const auto cnts = read_vector(c, counters.p, 2);
+    out.n_isf_members = cnts[0];
+    out.n_isf = cnts[1];
+    out.n_residue = cur;
+    out.leaves.alloc(out.n_isf + cur + 1, s);
+    if (out.n_isf > 0) {
+        LAUNCH(k_isf_leaves, G(out.n_isf), kB, 0, s, out.isf_off.p, out.isf_total.p, out.n_isf, out.n_isf_members,
+               cap, out.leaves.p);
+    }
+    if (cur > 0) {
+        out.residue.alloc(cur, s);
+        CUDA_CHECK(cudaMemcpyAsync(out.residue.p, A.p, sizeof(u64) * cur, cudaMemcpyDeviceToDevice, s));
+        if (residue_ffd) sort_entries(c, corpus, out.residue.p, cur, key_ordered, cap);
+        const u64 maxrec = 2 * cur + 2;
+        DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
+        FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
+        const FitResult fr = first_fit_runs(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf, 0,
+                                            static_cast<i64>(cur), cap, FitMode::Ffd, rec, static_cast<i64>(maxrec));
+        out.n_ffd = static_cast<u64>(fr.bins);
+        out.res_bin.alloc(cur, s);
+        out.res_slot.alloc(cur, s);
+        expand_fit_records(c, rec, fr.records, static_cast<i64>(cur), out.res_bin.p, out.res_slot.p);
+    }
+}
+
+// Lays the group's packs out contiguously (after an optional fill) and
+// appends them to the pack table. Returns the group pack count.
+u64 layout_group(Ctx& c, PackedGroup& pg, const u64* fill_items, u64 n_fill, const u32* fill_bin,
+                 const u32* fill_slot, u32 cap, PackTable& T) {
+    cudaStream_t s = c.stream;
+    const u64 P = pg.P();
+    if (P == 0) return 0;
+    DevBuf<u64> off(P + 1, s);
+    {
+        const u64* lv = pg.leaves.p;
+        u64* op = off.p;
+        const i64 PP = static_cast<i64>(P);
+        scan_exclusive<u64>(
+            PP + 1, [=] __device__(i64 i) { return i < PP ? static_cast<u64>(static_cast<u32>(lv[i])) : 0ull; },
+            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan);
+    }
+    const u64 M = read_vector(c, off.p + P, 1)[0];
+    u64* dst = T.members.p + T.n_members;
+    if (pg.n_isf > 0)
+        LAUNCH(k_place_isf, G(pg.n_isf), kB, 0, s, pg.isf_members.p, pg.isf_off.p, pg.n_isf, pg.n_isf_members, off.p,
+               dst);
+    if (pg.n_residue > 0)
+        LAUNCH(k_place_items, G(pg.n_residue), kB, 0, s, pg.residue.p, pg.res_bin.p, pg.res_slot.p, pg.n_residue,
+               pg.n_isf, off.p, dst);
+    if (n_fill > 0)
+        LAUNCH(k_place_items, G(n_fill), kB, 0, s, fill_items, fill_bin, fill_slot, n_fill, 0ull, off.p, dst);
+    LAUNCH(k_pack_stats, G(P), kB, 0, s, dst, off.p, P, T.n_members, T.n_packs, cap, T.moff.p, T.cnt.p, T.cap.p,
+           T.total.p, T.att.p);
+    T.n_members += M;
+    T.n_packs += P;
+    return P;
+}
+
+// Orders the group's packs (stable attention desc, or seeded shuffle) and
+// writes its iterations. Returns iterations written.
+u64 batch_group(Ctx& c, const DeviceCorpus& corpus, PackTable& T, u64 pbase, u64 P, u32 N, u32 cap, int gi,
+                bool balance, uint64_t seed, u64 ibase, DevBuf<u32>& slots, DevBuf<int32_t>& igroup) {
+    cudaStream_t s = c.stream;
+    if (P == 0) return 0;
+    DevBuf<u32> order(P, s);
+    if (balance) {
+        DevBuf<u32> w(P, s), tk(P, s), tv(P, s);
+        LAUNCH(k_iota, G(P), kB, 0, s, order.p, P);
+        const u64* att = T.att.p + pbase;
+        LAUNCH(k_att_words, G(P), kB, 0, s, att, order.p, P, false, w.p);
+        radix_sort_pairs(c, w.p, order.p, static_cast<i64>(P), 32, true, tk.p, tv.p);
+        LAUNCH(k_att_words, G(P), kB, 0, s, att, order.p, P, true, w.p);
+        radix_sort_pairs(c, w.p, order.p, static_cast<i64>(P), 32, true, tk.p, tv.p);
+    } else {
+        fy_source_positions(c, derive_seed(seed, "pack-batching", static_cast<uint64_t>(gi)), static_cast<i64>(P),
+                            order.p);
+    }
+    const u64 nfull = P / N;
+    const u32 rem = static_cast<u32>(P % N);
+    if (nfull > 0)
+        LAUNCH(k_full_iterations, G(nfull * N), kB, 0, s, order.p, nfull, N, static_cast<u32>(pbase), gi, ibase,
+               slots.p, igroup.p);
+    if (rem == 0) return nfull;
+    // spill tail: gather its samples, sort (length desc, id asc), redistribute
+    std::vector<u32> tail = read_vector(c, order.p + nfull * N, rem);
+    for (auto& t : tail) t += static_cast<u32>(pbase);
+    std::vector<u32> tcnt(rem);
+    std::vector<u64> toff(rem);
+    u64 k = 0;
+    for (u32 t = 0; t < rem; ++t) {
+        tcnt[t] = read_vector(c, T.cnt.p + tail[t], 1)[0];
+        toff[t] = k;
+        k += tcnt[t];
+    }
+    DevBuf<u32> dtail(rem, s);
+    DevBuf<u64> dtoff(rem, s);
+    CUDA_CHECK(cudaMemcpyAsync(dtail.p, tail.data(), sizeof(u32) * rem, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(dtoff.p, toff.data(), sizeof(u64) * rem, cudaMemcpyHostToDevice, s));
+    DevBuf<u64> spill(k + 1, s);
+    DevBuf<u32> dev_of(k + 1, s);
+    LAUNCH(k_gather_spill, rem, 256, 0, s, T.members.p, T.moff.p, T.cnt.p, dtail.p, rem, dtoff.p, spill.p);
+    sort_entries(c, corpus, spill.p, k, false, cap);
+    const u32 spill_pbase = static_cast<u32>(T.n_packs);
+    LAUNCH(k_spill, 1, 32, 0, s, spill.p, k, N, cap, dtail.p, rem, spill_pbase, T.n_members, gi, ibase + nfull,
+           T.members.p, T.moff.p, T.cnt.p, T.cap.p, T.total.p, T.att.p, dev_of.p, slots.p, igroup.p);
+    CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors above go out of scope
+    T.n_packs += N;
+    T.n_members += k;
+    return nfull + 1;
+}
+
+void emit_plan(Ctx& c, PackTable& T, DevBuf<u32>& slots, DevBuf<int32_t>& igroup, u64 I, u32 N, uint64_t seed,
+               DevicePlan& out) {
+    cudaStream_t s = c.stream;
+    out.n_iterations = static_cast<int64_t>(I);
+    out.n_devices = static_cast<int64_t>(I * N);
+    out.iter_group.alloc(I + 1, s);
+    out.iter_dev_offsets.alloc(I + 1, s);
+    out.dev_index.alloc(I * N + 1, s);
+    out.dev_pack_offsets.alloc(I * N + 1, s);
+    if (I == 0) {
+        CUDA_CHECK(cudaMemsetAsync(out.iter_dev_offsets.p, 0, sizeof(int64_t), s));
+        CUDA_CHECK(cudaMemsetAsync(out.dev_pack_offsets.p, 0, sizeof(int64_t), s));
+        out.n_packs = 0;
+        out.n_members = 0;
+        out.pack_member_offsets.alloc(1, s);
+        CUDA_CHECK(cudaMemsetAsync(out.pack_member_offsets.p, 0, sizeof(int64_t), s));
+        return;
+    }
+    DevBuf<u32> src(I, s);
+    fy_source_positions(c, derive_seed(seed, "plan-shuffle"), static_cast<i64>(I), src.p);  // balance.cpp:255-256
+    LAUNCH(k_out_iterations, G(I), kB, 0, s, src.p, I, N, igroup.p, out.iter_group.p, out.iter_dev_offsets.p,
+           out.dev_index.p);
+    {
+        const u32* sp = src.p;
+        const u32* sl = slots.p;
+        int64_t* dpo = out.dev_pack_offsets.p;
+        const i64 D = static_cast<i64>(I * N);
+        const u32 NN = N;
+        scan_exclusive<int64_t>(
+            D + 1,
+            [=] __device__(i64 x) -> int64_t {
+                if (x >= D) return 0;
+                return sl[static_cast<u64>(sp[x / NN]) * NN + (x % NN)] != kNone ? 1 : 0;
+            },
+            [=] __device__(i64 x, int64_t v) { dpo[x] = v; }, s, c.scan);
+    }
+    const u64 P = static_cast<u64>(read_vector(c, out.dev_pack_offsets.p + I * N, 1)[0]);
+    out.n_packs = static_cast<int64_t>(P);
+    out.pack_capacity.alloc(P + 1, s);
+    out.pack_total.alloc(P + 1, s);
+    out.pack_attention.alloc(P + 1, s);
+    out.pack_member_offsets.alloc(P + 1, s);
+    DevBuf<u32> pglobal(P + 1, s);
+    DevBuf<u64> pcnt(P + 1, s);
+    LAUNCH(k_out_packs, G(I * N), kB, 0, s, src.p, I, N, slots.p, out.dev_pack_offsets.p, T.cnt.p, T.cap.p,
+           T.total.p, T.att.p, out.pack_capacity.p, out.pack_total.p, out.pack_attention.p, pglobal.p, pcnt.p);
+    {
+        const u64* pc = pcnt.p;
+        int64_t* mo = out.pack_member_offsets.p;
+        const i64 PP = static_cast<i64>(P);
+        scan_exclusive<int64_t>(
+            PP + 1, [=] __device__(i64 q) -> int64_t { return q < PP ? static_cast<int64_t>(pc[q]) : 0; },
+            [=] __device__(i64 q, int64_t v) { mo[q] = v; }, s, c.scan);
+    }
+    const u64 M = static_cast<u64>(read_vector(c, out.pack_member_offsets.p + P, 1)[0]);
+    out.n_members = static_cast<int64_t>(M);
+    out.member_index.alloc(M + 1, s);
+    LAUNCH(k_out_members, grid_for(P * 32, kB, 148u * 16u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
+           T.moff.p, T.cnt.p, T.members.p, out.member_index.p);
+}
+
+}  // namespace
+
+int64_t DeviceCorpus::length_of(Ctx& c, i64 i) const {
+    if (lengths_host) return lengths_host[i];
+    return read_vector(c, lengths_dev + i, 1)[0];
+}
+
+void ingest(Ctx& c, const hbp_samples* in, DeviceCorpus& corpus) {
+    if (in->n < 0) fail_validation("negative sample count");
+    if (in->n > 0x7fffffffLL) fail_validation("corpus too large for the engine (more than 2^31-1 samples)");
+    corpus.n = in->n;
+    if (in->memory == HBP_MEM_HOST) corpus.lengths_host = in->lengths;
+    else corpus.lengths_dev = in->lengths;
+    if (in->n == 0) return;
+    DevBuf<int64_t> dids;
+    const IngestFlags f = upload_and_scan(c, in, corpus, 0x7fffffffLL, dids);
+    corpus.first_bad_len = f.first_bad_len;
+    corpus.first_huge = f.first_over;
+    if (!corpus.ids_ascending) {
+        const int64_t* ids_dev = in->memory == HBP_MEM_HOST ? dids.p : in->ids;
+        corpus.first_dup = rank_ids(c, ids_dev, corpus);
+    }
+}
+
+void validate_corpus(Ctx& c, const hbp_samples* in, const DeviceCorpus& corpus, const std::string& source) {
+    (void)in;
+    if (corpus.n == 0) fail_validation("empty corpus: " + source);
+    if (corpus.first_bad_len != ~0ull && corpus.first_bad_len <= corpus.first_dup) {
+        const i64 i = static_cast<i64>(corpus.first_bad_len);
+        fail_validation("sample " + std::to_string(corpus.id_of(i)) + " has non-positive length " +
+                        std::to_string(corpus.length_of(c, i)));
+    }
+    if (corpus.first_dup != ~0ull)
+        fail_validation("duplicate sample id " + std::to_string(corpus.id_of(static_cast<i64>(corpus.first_dup))));
+}
+
+namespace {
+
+// Partitions the corpus by group (stable) and returns entries + offsets.
+void partition(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group_config>& groups, DevBuf<u64>& entries,
+               std::vector<u64>& goff) {
+    cudaStream_t s = c.stream;
+    const u64 n = static_cast<u64>(corpus.n);
+    const int ng = static_cast<int>(groups.size());
+    std::vector<int64_t> gl(ng);
+    for (int g = 0; g < ng; ++g) gl[g] = groups[g].length;
+    DevBuf<int64_t> dgl(ng, s);
+    CUDA_CHECK(cudaMemcpyAsync(dgl.p, gl.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice, s));
+    DevBuf<u32> key(n, s), val(n, s), tk(n, s), tv(n, s);
+    DevBuf<unsigned long long> counts(64, s);
+    counts.zero();
+    LAUNCH(k_group_keys, G(n), kB, 0, s, corpus.len32.p, n, dgl.p, ng, key.p, val.p, counts.p);
+    if (ng > 1) radix_sort_pairs(c, key.p, val.p, static_cast<i64>(n), bits_for(ng - 1), false, tk.p, tv.p);
+    entries.alloc(n, s);
+    LAUNCH(k_entries_from_idx, G(n), kB, 0, s, corpus.len32.p, val.p, n, entries.p);
+    const auto cnt = read_vector(c, counts.p, 64);
+    goff.assign(ng + 1, 0);
+    for (int g = 0; g < ng; ++g) goff[g + 1] = goff[g] + cnt[g];
+}
+
+// group_data's check (balance.cpp:32-36): the first sample beyond l_max.
+void check_l_max(Ctx& c, const DeviceCorpus& corpus, int64_t l_max) {
+    cudaStream_t s = c.stream;
+    if (corpus.n == 0) return;
+    {
+        DevBuf<unsigned long long> over(1, s);
+        const unsigned long long none = ~0ull;
+        CUDA_CHECK(cudaMemcpyAsync(over.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+        const u32* lp = corpus.len32.p;
+        unsigned long long* op = over.p;
+        const u32 lm = l_max > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(l_max);
+        const u64 n = static_cast<u64>(corpus.n);
+        // len32 saturates at 2^31-1; longer samples are tracked in first_huge
+        auto k = [=] __device__(u64 i) {
+            if (lp[i] > lm) atomicMin(op, static_cast<unsigned long long>(i));
+        };
+        for_each_index(c, n, k);
+        u64 first = read_scalar(c, over.p);
+        if (corpus.first_huge < first) first = corpus.first_huge;
+        if (first != ~0ull)
+            fail_validation("sample " + std::to_string(corpus.id_of(static_cast<i64>(first))) +
+                            " exceeds the largest packing length " + std::to_string(l_max));
+    }
+}
+
+}  // namespace
+
+void group_data_device(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group_config>& groups, int64_t l_max,
+                       std::vector<int64_t>& offsets, std::vector<int32_t>& members) {
+    validate_groups(groups, l_max);
+    if (groups.size() > 64) fail_validation("the GPU engine supports at most 64 packing groups");
+    check_l_max(c, corpus, l_max);
+    DevBuf<u64> entries;
+    std::vector<u64> goff;
+    if (corpus.n > 0) {
+        partition(c, corpus, groups, entries, goff);
+    } else {
+        goff.assign(groups.size() + 1, 0);
+    }
+    offsets.assign(goff.begin(), goff.end());
+    members.resize(static_cast<size_t>(corpus.n));
+    if (corpus.n > 0) {
+        DevBuf<int32_t> idx(static_cast<size_t>(corpus.n), c.stream);
+        const u64* ep = entries.p;
+        int32_t* ip = idx.p;
+        for_each_index(c, static_cast<u64>(corpus.n), [=] __device__(u64 i) { ip[i] = static_cast<int32_t>(entry_idx(ep[i])); });
+        CUDA_CHECK(cudaMemcpyAsync(members.data(), idx.p, sizeof(int32_t) * corpus.n, cudaMemcpyDeviceToHost, c.stream));
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    }
+}
+
+void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePlan& out) {
+    cudaStream_t s = c.stream;
+    validate_groups(a.groups, a.l_max);
+    if (a.device_count < 1) fail_validation("device count must be >= 1");
+    if (a.groups.size() > 64) fail_validation("the GPU engine supports at most 64 packing groups");
+    check_l_max(c, corpus, a.l_max);
+    out.device_count = a.device_count;
+    out.seed = a.seed;
+    out.groups = a.groups;
+    out.l_best = a.l_best;
+    out.l_max = a.l_max;
+
+    const u64 n = static_cast<u64>(corpus.n);
+    const u32 N = static_cast<u32>(a.device_count);
+    const int ng = static_cast<int>(a.groups.size());
+    DevBuf<u64> entries;
+    std::vector<u64> goff;
+    partition(c, corpus, a.groups, entries, goff);
+
+    // pools: group g = entries[goff[g] .. goff[g+1]) in input order; greedy
+    // fill shrinks them (order preserved) before they are packed.
+    std::vector<DevBuf<u64>> pools(ng);
+    std::vector<u64> psize(ng);
+    for (int g = 0; g < ng; ++g) {
+        psize[g] = goff[g + 1] - goff[g];
+        pools[g].alloc(psize[g] + 1, s);
+        if (psize[g])
+            CUDA_CHECK(cudaMemcpyAsync(pools[g].p, entries.p + goff[g], sizeof(u64) * psize[g],
+                                       cudaMemcpyDeviceToDevice, s));
+    }
+    entries.release();
+
+    PackTable T;
+    const u64 cap_packs = n + static_cast<u64>(ng) * N + 1;
+    T.members.alloc(2 * n + 1, s);
+    T.moff.alloc(cap_packs, s);
+    T.cnt.alloc(cap_packs, s);
+    T.cap.alloc(cap_packs, s);
+    T.total.alloc(cap_packs, s);
+    T.att.alloc(cap_packs, s);
+    const u64 max_iters = n / N + ng + 2;
+    DevBuf<u32> slots(max_iters * N, s);
+    DevBuf<int32_t> igroup(max_iters, s);
+    u64 I = 0;
+    DevBuf<u8> consumed;
+
+    for (int gi = ng - 1; gi >= 0; --gi) {
+        if (psize[gi] == 0) continue;
+        const u32 cap = static_cast<u32>(a.groups[gi].length);
+        PackedGroup pg;
+        pack_pool(c, corpus, pools[gi].p, psize[gi], cap, a.strategy,
+                  derive_seed(a.seed, "pack", static_cast<uint64_t>(gi)), pg);
+        pools[gi].release();
+        psize[gi] = 0;
+
+        // greedy fill from pools gi-1 .. 0 (balance.cpp:235-243)
+        DevBuf<u64> fill_items;
+        DevBuf<u32> fill_bin, fill_slot;
+        u64 n_fill = 0;
+        if (a.greedy_fill && gi > 0) {
+            for (int j = 0; j < gi; ++j) n_fill += psize[j];
+        }
+        if (n_fill > 0 && pg.P() > 0) {
+            if (corpus.neg_ids > 0)
+                throw EngineError(HBP_ERR_CUDA,
+                                  "greedy fill with sample ids <= -2 is not supported by the GPU engine yet");
+            fill_items.alloc(n_fill, s);
+            u64 o = 0;
+            for (int j = gi - 1; j >= 0; --j) {  // nearest (longest) pool first
+                if (!psize[j]) continue;
+                CUDA_CHECK(cudaMemcpyAsync(fill_items.p + o, pools[j].p, sizeof(u64) * psize[j],
+                                           cudaMemcpyDeviceToDevice, s));
+                sort_entries(c, corpus, fill_items.p + o, psize[j], corpus.key32.p == nullptr,
+                             static_cast<u32>(a.groups[j].length));
+                o += psize[j];
+            }
+            const u64 P = pg.P();
+            const u64 maxrec = 2 * n_fill + 2;
+            DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
+            FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
+            const FitResult fr = first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p,
+                                                static_cast<i64>(P), static_cast<i64>(P), cap, FitMode::Fill, rec,
+                                                static_cast<i64>(maxrec));
+            fill_bin.alloc(n_fill, s);
+            fill_slot.alloc(n_fill, s);
+            expand_fit_records(c, rec, fr.records, static_cast<i64>(n_fill), fill_bin.p, fill_slot.p);
+            // remove consumed samples from their pools, order preserved
+            if (!consumed.p) {
+                consumed.alloc(n, s);
+                consumed.zero();
+            }
+            LAUNCH(k_mark_consumed, G(n_fill), kB, 0, s, fill_items.p, fill_bin.p, n_fill, consumed.p);
+            for (int j = 0; j < gi; ++j) {
+                if (!psize[j]) continue;
+                DevBuf<u64> kept(psize[j] + 1, s);
+                DevBuf<u64> cnt(1, s);
+                const u64* src = pools[j].p;
+                u64* dst = kept.p;
+                u64* cntp = cnt.p;
+                const u8* cons = consumed.p;
+                const i64 m = static_cast<i64>(psize[j]);
+                scan_exclusive<u64>(
+                    m, [=] __device__(i64 i) { return cons[entry_idx(src[i])] ? 0ull : 1ull; },
+                    [=] __device__(i64 i, u64 v) {
+                        const bool keep = !cons[entry_idx(src[i])];
+                        if (keep) dst[v] = src[i];
+                        if (i == m - 1) *cntp = v + (keep ? 1 : 0);
+                    },
+                    s, c.scan);
+                psize[j] = read_scalar(c, cnt.p);
+                pools[j] = std::move(kept);
+            }
+        }
+        const u64 pbase = T.n_packs;
+        const u64 P = layout_group(c, pg, fill_items.p, n_fill, fill_bin.p, fill_slot.p, cap, T);
+        const bool sp_comm = a.groups[gi].sp > 1;
+        (void)sp_comm;  // comm tokens are derived from the group at report time
+        I += batch_group(c, corpus, T, pbase, P, N, cap, gi, a.balance_batching, a.seed, I, slots, igroup);
+    }
+    emit_plan(c, T, slots, igroup, I, N, a.seed, out);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void pack_device(Ctx& c, DeviceCorpus& corpus, int64_t capacity, const hbp_strategy& st, uint64_t seed,
+                 DevicePlan& out) {
+    cudaStream_t s = c.stream;
+    const u64 n = static_cast<u64>(corpus.n);
+    // pack() checks, packing.cpp:211-225: strategy, capacity, then the first
+    // sample that is too long or non-positive
+    validate_strategy(st);
+    if (capacity < 1) fail_validation("pack capacity must be >= 1");
+    {
+        u64 first_over = ~0ull;
+        if (n > 0) {
+            DevBuf<unsigned long long> over(1, s);
+            const unsigned long long none = ~0ull;
+            CUDA_CHECK(cudaMemcpyAsync(over.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+            const u32* lp = corpus.len32.p;
+            unsigned long long* op = over.p;
+            const u32 lim = capacity > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(capacity);
+            for_each_index(c, n, [=] __device__(u64 i) {
+                if (lp[i] > lim) atomicMin(op, static_cast<unsigned long long>(i));
+            });
+            first_over = read_scalar(c, over.p);
+            if (corpus.first_huge < first_over) first_over = corpus.first_huge;
+        }
+        const u64 first_bad = corpus.first_bad_len;
+        if (first_over != ~0ull && first_over <= first_bad) {
+            const i64 i = static_cast<i64>(first_over);
+            fail_validation("sample " + std::to_string(corpus.id_of(i)) + " length " +
+                            std::to_string(corpus.length_of(c, i)) + " exceeds pack capacity " +
+                            std::to_string(capacity));
+        }
+        if (first_bad != ~0ull)
+            fail_validation("sample " + std::to_string(corpus.id_of(static_cast<i64>(first_bad))) +
+                            " has non-positive length");
+    }
+    if (capacity > 0x7fffffffLL) fail_validation("pack capacity exceeds the engine limit (2^31-1)");
+    const u32 cap = static_cast<u32>(capacity);
+    DevBuf<u64> entries(n + 1, s);
+    DevBuf<u32> iota(n + 1, s);
+    LAUNCH(k_iota, G(n), kB, 0, s, iota.p, n);
+    LAUNCH(k_entries_from_idx, G(n), kB, 0, s, corpus.len32.p, iota.p, n, entries.p);
+    PackedGroup pg;
+    pack_pool(c, corpus, entries.p, n, cap, st, seed, pg);
+    PackTable T;
+    T.members.alloc(n + 1, s);
+    T.moff.alloc(n + 1, s);
+    T.cnt.alloc(n + 1, s);
+    T.cap.alloc(n + 1, s);
+    T.total.alloc(n + 1, s);
+    T.att.alloc(n + 1, s);
+    const u64 P = layout_group(c, pg, nullptr, 0, nullptr, nullptr, cap, T);
+    // a pack list: packs in order, no iterations
+    out.n_iterations = 0;
+    out.n_devices = 0;
+    out.n_packs = static_cast<int64_t>(P);
+    out.n_members = static_cast<int64_t>(T.n_members);
+    out.iter_group.alloc(1, s);
+    out.iter_dev_offsets.alloc(1, s);
+    out.dev_index.alloc(1, s);
+    out.dev_pack_offsets.alloc(1, s);
+    CUDA_CHECK(cudaMemsetAsync(out.iter_dev_offsets.p, 0, sizeof(int64_t), s));
+    CUDA_CHECK(cudaMemsetAsync(out.dev_pack_offsets.p, 0, sizeof(int64_t), s));
+    out.pack_capacity.alloc(P + 1, s);
+    out.pack_total.alloc(P + 1, s);
+    out.pack_attention.alloc(P + 1, s);
+    out.pack_member_offsets.alloc(P + 1, s);
+    out.member_index.alloc(T.n_members + 1, s);
+    DevBuf<u32> pglobal(P + 1, s);
+    LAUNCH(k_iota, G(P), kB, 0, s, pglobal.p, P);
+    const u32* cntp = T.cnt.p;
+    const u32* capp = T.cap.p;
+    const u32* totp = T.total.p;
+    const u64* attp = T.att.p;
+    int64_t* oc = out.pack_capacity.p;
+    int64_t* ot = out.pack_total.p;
+    int64_t* oa = out.pack_attention.p;
+    int64_t* om = out.pack_member_offsets.p;
+    const i64 PP = static_cast<i64>(P);
+    scan_exclusive<int64_t>(
+        PP + 1, [=] __device__(i64 q) -> int64_t { return q < PP ? static_cast<int64_t>(cntp[q]) : 0; },
+        [=] __device__(i64 q, int64_t v) {
+            om[q] = v;
+            if (q < PP) {
+                oc[q] = capp[q];
+                ot[q] = totp[q];
+                oa[q] = static_cast<int64_t>(attp[q]);
+            }
+        },
+        s, c.scan);
+    if (P > 0)
+        LAUNCH(k_out_members, grid_for(P * 32, kB, 148u * 16u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
+               T.moff.p, T.cnt.p, T.members.p, out.member_index.p);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void plan_to_host(Ctx& c, DevicePlan& p) {
+    if (p.on_host) return;
+    auto cp = [&](auto& h, auto& d, size_t n) {
+        h.resize(n);
+        if (n) CUDA_CHECK(cudaMemcpyAsync(h.data(), d.p, sizeof(h[0]) * n, cudaMemcpyDeviceToHost, c.stream));
+    };
+    const size_t I = static_cast<size_t>(p.n_iterations), D = static_cast<size_t>(p.n_devices),
+                 P = static_cast<size_t>(p.n_packs), M = static_cast<size_t>(p.n_members);
+    cp(p.h_iter_group, p.iter_group, I);
+    cp(p.h_iter_dev_offsets, p.iter_dev_offsets, I + 1);
+    cp(p.h_dev_index, p.dev_index, D);
+    cp(p.h_dev_pack_offsets, p.dev_pack_offsets, D + 1);
+    cp(p.h_pack_capacity, p.pack_capacity, P);
+    cp(p.h_pack_total, p.pack_total, P);
+    cp(p.h_pack_attention, p.pack_attention, P);
+    cp(p.h_pack_member_offsets, p.pack_member_offsets, P + 1);
+    cp(p.h_member_index, p.member_index, M);
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    p.on_host = true;
+}
+
+}  // namespace hbp_b200

@@ -1,0 +1,86 @@
+// pipeline.cuh — build_plan / pack orchestration and the device-resident plan.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "stages.cuh"
+
+namespace hbp_b200 {
+
+// Device-resident plan in the flat CSR layout of hbp_plan_view. Host copies
+// are made lazily by hbp_plan_view_get.
+struct DevicePlan {
+    int32_t device_count = 0;
+    uint64_t seed = 0;
+    std::vector<hbp_group_config> groups;
+    int64_t l_best = 0, l_max = 0;
+    int64_t n_iterations = 0, n_devices = 0, n_packs = 0, n_members = 0;
+    DevBuf<int32_t> iter_group;
+    DevBuf<int64_t> iter_dev_offsets;
+    DevBuf<int32_t> dev_index;
+    DevBuf<int64_t> dev_pack_offsets;
+    DevBuf<int64_t> pack_capacity, pack_total, pack_attention, pack_member_offsets;
+    DevBuf<int32_t> member_index;
+    // host mirror
+    bool on_host = false;
+    std::vector<int32_t> h_iter_group, h_dev_index, h_member_index;
+    std::vector<int64_t> h_iter_dev_offsets, h_dev_pack_offsets, h_pack_capacity, h_pack_total, h_pack_attention,
+        h_pack_member_offsets;
+};
+
+// Samples resident on the device after ingest.
+struct DeviceCorpus {
+    i64 n = 0;
+    DevBuf<u32> len32;       // lengths
+    DevBuf<u32> key32;       // tie-break key: id rank (general ids) -- empty when ids ascend in input order
+    bool ids_ascending = true;
+    i64 neg_ids = 0;         // samples with id <= -2 (greedy-fill probe quirk)
+    int key_bits = 1;
+    std::vector<int64_t> h_ids;      // host copy of ids for error messages (empty -> ids are 0..n-1)
+    const int64_t* ids_host = nullptr;
+    const int64_t* lengths_host = nullptr;  // caller's lengths when they are host memory
+    const int64_t* lengths_dev = nullptr;   // caller's lengths when they are device memory
+    u64 first_bad_len = ~0ull;  // first sample with length < 1
+    u64 first_huge = ~0ull;     // first sample with length > 2^31-1 (engine limit)
+    u64 first_dup = ~0ull;      // first repeated id (input order), general ids only
+    int64_t id_of(i64 i) const { return ids_host ? ids_host[i] : static_cast<int64_t>(i); }
+    int64_t length_of(Ctx& c, i64 i) const;
+};
+
+// Uploads lengths/ids, converts lengths to u32, ranks non-ascending ids and
+// records the first offending samples. Throws nothing about the data.
+void ingest(Ctx& c, const hbp_samples* in, DeviceCorpus& corpus);
+// SampleSet::validate (types.cpp:8-24): "empty corpus", non-positive
+// length, duplicate id -- the first offending sample in input order.
+void validate_corpus(Ctx& c, const hbp_samples* in, const DeviceCorpus& corpus, const std::string& source);
+
+struct PlanArgs {
+    std::vector<hbp_group_config> groups;
+    int64_t l_best = 0, l_max = 0;
+    hbp_strategy strategy{};
+    int32_t device_count = 4;
+    bool balance_batching = true;
+    bool greedy_fill = true;
+    uint64_t seed = 0;
+};
+
+// build_plan (balance.cpp:207-258) on a validated corpus.
+void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& args, DevicePlan& out);
+
+// pack() of the whole corpus to one capacity (packing.cpp:210-261); output
+// is a plan with no iterations.
+void pack_device(Ctx& c, DeviceCorpus& corpus, int64_t capacity, const hbp_strategy& st, uint64_t seed,
+                 DevicePlan& out);
+
+// group_data (balance.cpp:25-44): per-group offsets and member indices (input order).
+void group_data_device(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group_config>& groups, int64_t l_max,
+                       std::vector<int64_t>& offsets, std::vector<int32_t>& members);
+
+void plan_to_host(Ctx& c, DevicePlan& p);
+
+// groups.validate() (autoselect.cpp:18-33)
+void validate_groups(const std::vector<hbp_group_config>& g, int64_t l_max);
+void validate_strategy(const hbp_strategy& s);
+
+}  // namespace hbp_b200

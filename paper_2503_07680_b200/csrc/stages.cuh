@@ -1,0 +1,69 @@
+// stages.cuh — device data layouts shared between stages and the stage
+// entry points (nextfit.cu, firstfit.cu, batching.cu, metrics.cu).
+//
+// Sample entries travel as one u64: (length << 32) | sample_index, so a
+// shuffle or compaction moves length and identity together (one 8-byte
+// gather instead of two dependent 4-byte ones). Sample ids only matter for
+// tie-breaks; the engine orders by input index, which equals id order when
+// the ids are ascending in input order (checked at ingest) and is replaced
+// by the id rank otherwise.
+#pragma once
+
+#include "engine.cuh"
+
+namespace hbp_b200 {
+
+__host__ __device__ __forceinline__ u64 make_entry(u32 len, u32 idx) { return (static_cast<u64>(len) << 32) | idx; }
+__host__ __device__ __forceinline__ u32 entry_len(u64 e) { return static_cast<u32>(e >> 32); }
+__host__ __device__ __forceinline__ u32 entry_idx(u64 e) { return static_cast<u32>(e); }
+
+// Append-only pack list in device memory (frozen ISF packs).
+struct PackSink {
+    u64* members;     // entries
+    u64* pack_off;    // first member of each pack
+    u32* pack_total;
+    u64* pack_att;
+    u64* n_members;   // device counters
+    u64* n_packs;
+};
+
+// nextfit.cu: next-fit over F, freeze packs with total >= tmin into sink,
+// the rest (in pack order) into newpool. Returns the new pool size.
+i64 nextfit_freeze(Ctx& c, const u64* F, i64 m, u32 cap, u64 tmin, PackSink sink, u64* newpool);
+
+// ---- first-fit by runs (firstfit.cu) -------------------------------------
+//
+// Items sorted by (length desc, id asc) are grouped into runs of equal
+// length. A run of c items of size s goes, in bin order, to every bin with
+// residual >= s (floor(r / s) items each) until the run is used up; what is
+// left either opens new bins of floor(cap / s) items (FFD, packing.cpp:
+// 86-103 over sort_decreasing) or stays unassigned (greedy fill,
+// balance.cpp:62-101: every pack repeatedly takes the largest fitting
+// sample, lowest id first -- the same assignment processed length by
+// length). One warp walks the runs over a 32-ary max-residual tree.
+struct FitRecords {
+    // item range [item, item + count) -> bins bin + k / per_bin, slots
+    // slot0 + k % per_bin
+    u32* item;
+    u32* count;
+    u32* bin;
+    u32* per_bin;
+    u32* slot0;
+};
+
+struct FitResult {
+    i64 bins = 0;     // bins after the run (existing + opened)
+    i64 records = 0;
+};
+
+enum class FitMode { Ffd, Fill };
+
+// `leaves` (capacity max_bins) holds (residual << 32 | count) per bin; the
+// first `bins0` are live. items: sorted entries.
+FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
+                         FitMode mode, FitRecords rec, i64 max_records);
+
+// item -> (bin, slot) for every item covered by a record; others get kNone.
+void expand_fit_records(Ctx& c, FitRecords rec, i64 n_records, i64 n_items, u32* item_bin, u32* item_slot);
+
+}  // namespace hbp_b200

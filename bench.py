@@ -1,0 +1,342 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 HBP batch-construction engine (BASELINE.json).
+
+One step = one pass of the hot path over one synthetic corpus of the C2
+shape (LongAlign-like long tail, 10M samples, groups [16K sp1 ckpt28,
+128K sp8 ckpt28], 8 data-parallel devices, seed 1): build_plan + report
+(ABR/CR) + simulate (estimated step time) -- the reference's C2 call chain
+(SURVEY.md §8(d)).
+
+  value  samples/s with the corpus already in HBM (C-ABI device input)
+  e2e    samples/s through the C-ABI with HOST buffers: H2D of the lengths
+         and D2H of the whole plan CSR inside every timed step
+
+Packing one corpus does not shard: with --gpus N every
+rank packs its own corpus (replicas, weak scaling) and value is the sum.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(count=10_000_000, short="lognormal:7.2:0.7", long_fraction=0.02, long="uniform:16385:131072",
+          max_length=131072, seed=20250515)
+C2_GROUPS = [(16384, 1, 28), (131072, 8, 28)]
+DEVICES, PLAN_SEED = 8, 1
+METRIC = "samples packed/sec"
+UNIT = "samples/s"
+REF_SAMPLE = 1_000_000  # bounded CPU sample of the same spec (≈2 s per reference step)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def synth(abi_lib, spec, count=None):
+    n = spec["count"] if count is None else count
+    out = np.zeros(n, dtype=np.int64)
+    err = C.create_string_buffer(256)
+    rc = abi_lib.hbp_synth_lengths(C.c_int64(n), spec["short"].encode(), C.c_double(spec["long_fraction"]),
+                                   spec["long"].encode(), C.c_int64(spec["max_length"]), C.c_uint64(spec["seed"]),
+                                   out.ctypes.data_as(C.POINTER(C.c_int64)), err, 256)
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation (oracle/_ref)
+# ---------------------------------------------------------------------------
+
+def _ref_worker(args):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle  # bench's CPU legs only
+    L, reps = args
+    o = Oracle("reference")
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        plan = o.build_plan(None, L, C2_GROUPS, l_best=16384, device_count=DEVICES, seed=PLAN_SEED)
+        o.report(plan)
+        o.simulate(plan)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_reference(lengths, steps, workers):
+    """Times reference build_plan + report + simulate; `workers` processes
+    each pack their own copy of the sample concurrently."""
+    import multiprocessing as mp
+    if workers <= 1:
+        times = _ref_worker((lengths, steps))
+        return len(lengths) / statistics.mean(times), 1, times
+    with mp.get_context("fork").Pool(workers) as pool:
+        res = pool.map(_ref_worker, [(lengths, steps)] * workers)
+    per_step = [max(r[k] for r in res) for k in range(steps)]
+    return workers * len(lengths) / statistics.mean(per_step), workers, per_step
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from paper_2503_07680_b200 import abi
+    lib = abi.load_library()
+    L = synth(lib, C2, REF_SAMPLE)
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 64))
+    for _ in range(max(0, min(args.warmup, 1))):
+        _ref_worker((L[:100_000], 1))
+    value, used, times = cpu_reference(L, max(1, args.steps), workers)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (reference synth_lengths, C2 spec)",
+        "config": {"workload": "C2: HBP build_plan+report+simulate, LongAlign-like long tail, groups [16K sp1, 128K sp8], 8 DP devices",
+                   "samples_per_step": REF_SAMPLE * used, "sample": f"{REF_SAMPLE} samples of the C2 spec per worker"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "reference",
+                         "sample": f"{used} worker processes x {REF_SAMPLE} samples of the C2 spec (reference is single-threaded)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2503_07680_b200 import abi
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = abi.load_library()
+    ctx = abi.Context(local)
+    stream = torch.cuda.ExternalStream(lib.hbp_ctx_stream(ctx.h))
+
+    spec = dict(C2)
+    if args.n:
+        spec["count"] = args.n
+    spec["seed"] = C2["seed"] + rank  # independent replica per rank
+    L = synth(lib, spec)
+    n = len(L)
+    d_len = torch.from_numpy(L).cuda()
+    h_len = torch.from_numpy(L).pin_memory()
+    prof = abi.default_profile()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step_device():
+        s, keep = abi.device_samples(0, d_len.data_ptr(), n, "bench")
+        plan = ctx.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
+        plan.report()
+        plan.simulate(prof)
+        return plan
+
+    def step_e2e():
+        s, keep = abi.make_samples(None, h_len.numpy(), "bench")
+        plan = ctx.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
+        m = plan.report()
+        st = plan.simulate(prof)
+        v = abi.PlanView()
+        ctx.check(lib.hbp_plan_view_get(ctx.h, plan.h, C.byref(v)))
+        d2h = (v.n_iterations * 4 + (v.n_iterations + 1) * 8 + v.n_devices * 4 + (v.n_devices + 1) * 8
+               + v.n_packs * 24 + (v.n_packs + 1) * 8 + v.n_members * 4 + 5 * 8 + 3 * 8)
+        return plan, d2h, m.abr, st.total_seconds
+
+    def timed(fn, k):
+        ms = []
+        out = None
+        for _ in range(k):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            out = fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return ms, out
+
+    for _ in range(args.warmup):
+        step_device()
+        step_e2e()
+    launches0 = ctx.launches
+    clocks = Clocks(local)
+    clocks.start()
+    dev_ms, plan = timed(step_device, args.steps)
+    launches = (ctx.launches - launches0) // max(1, args.steps)
+    e2e_ms, e2e_out = timed(step_e2e, args.steps)
+    ck = clocks.stop()
+    d2h = e2e_out[1]
+
+    # stage profile of one extra step (CUDA events around each engine stage)
+    stages = profile_stages(ctx, lib, step_device)
+
+    tot_dev = sum(dev_ms)
+    tot_e2e = sum(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([tot_dev, tot_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_dev, tot_e2e = t.tolist()
+    if rank == 0:
+        ms_step = tot_dev / args.steps
+        value = world * n / (ms_step / 1000.0)
+        e2e_value = world * n / (tot_e2e / args.steps / 1000.0)
+        peak, peak_kind = peaks()
+        roof = roofline(stages, peak, peak_kind)
+        cpu = cpu_baseline_leg(lib) if world == 1 and not args.no_cpu else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (synth_lengths, C2 spec; replica seed = 20250515 + rank)",
+            "config": {"workload": "C2: HBP build_plan+report+simulate, LongAlign-like long tail, groups [16K sp1, 128K sp8], 8 DP devices",
+                       "samples_per_rank": n, "groups": C2_GROUPS, "dp_devices": DEVICES, "seed": PLAN_SEED,
+                       "parallelism": f"replicas x{world}", "l2": "flushed (256 MB write) before every step"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": tot_e2e / args.steps},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "stages_ms": {k: round(v["ms"], 4) for k, v in sorted(stages.items(), key=lambda kv: -kv[1]["ms"])[:12]},
+            "clocks": ck,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def profile_stages(ctx, lib, fn):
+    """Per-kernel-family device time of one step (the engine times its own
+    launches with CUDA events on its stream when profiling is on)."""
+    if not hasattr(lib, "hbp_ctx_set_profiling"):
+        return {}
+    lib.hbp_ctx_set_profiling(ctx.h, 1)
+    fn()
+    ctx.synchronize()
+    lib.hbp_ctx_set_profiling(ctx.h, 0)
+    out = {}
+    name = C.create_string_buffer(128)
+    ms, launches, nbytes = C.c_double(), C.c_int64(), C.c_double()
+    i = 0
+    while lib.hbp_ctx_stage_stats(ctx.h, i, name, 128, C.byref(ms), C.byref(launches), C.byref(nbytes)) == 0:
+        out[name.value.decode()] = {"ms": ms.value, "launches": launches.value, "bytes": nbytes.value}
+        i += 1
+    return out
+
+
+def roofline(stages, peak, peak_kind):
+    """Dominant HBM-bound kernel family: algorithmic bytes / its device time."""
+    cands = {k: v for k, v in stages.items() if v["bytes"] > 0 and v["ms"] > 0}
+    if not cands:
+        return None
+    k, v = max(cands.items(), key=lambda kv: kv[1]["ms"])
+    achieved = v["bytes"] / (v["ms"] / 1000.0) / 1e9
+    return {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "launches": v["launches"], "algorithmic_bytes": v["bytes"], "ms": v["ms"]}
+
+
+def cpu_baseline_leg(lib):
+    try:
+        L = synth(lib, C2, REF_SAMPLE)
+        value, used, times = cpu_reference(L, 1, 1)
+        return {"value": value, "unit": UNIT, "cores": used, "kind": "reference",
+                "sample": f"{REF_SAMPLE} samples of the C2 spec, 1 step, 1 host core (reference is single-threaded)"}
+    except Exception as e:  # the reference library did not travel
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override corpus size (default 10M)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,23 @@ int hbp_ctx_synchronize(hbp_ctx* ctx);
 void* hbp_ctx_stream(hbp_ctx* ctx);
 /* Kernel launches issued on this context since creation (for the bench). */
 int64_t hbp_ctx_launch_count(const hbp_ctx* ctx);
+/* Kernel profiling: while on, every engine launch is bracketed by CUDA
+ * events on the context stream and tagged with its kernel family and
+ * algorithmic bytes. hbp_ctx_stage_stats(index) reports per family the
+ * summed device time, launch count and algorithmic bytes; it returns
+ * HBP_ERR_VALIDATION past the last family. */
+int hbp_ctx_set_profiling(hbp_ctx* ctx, int32_t on);
+int hbp_ctx_stage_stats(hbp_ctx* ctx, int32_t index, char* name, int32_t name_len, double* ms, int64_t* launches,
+                        double* bytes);
+
+/* ---- L1: synthetic corpora (input generation, host threads) -------------- */
+
+/* synth_lengths as bound by the reference Python module
+ * (bindings/py_hbp.cpp:80-97; generator src/ingest.cpp:279-329): long_dist
+ * NULL or "" reuses short_dist. Bit-identical to the reference on the same
+ * libm. out_lengths[count]; ids are 0..count-1. */
+int hbp_synth_lengths(int64_t count, const char* short_dist, double long_fraction, const char* long_dist,
+                      int64_t max_length, uint64_t seed, int64_t* out_lengths, char* err, int errlen);
 
 /* ---- L0: validation ---------------------------------------------------- */
 

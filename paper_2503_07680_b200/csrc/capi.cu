@@ -14,7 +14,15 @@
 
 namespace hbp_b200 {
 thread_local int64_t* g_launch_counter = nullptr;
+thread_local KernelProfiler* g_prof = nullptr;
 }
+
+struct StageSummary {
+    std::string name;
+    double ms = 0, bytes = 0;
+    int64_t launches = 0;
+};
+static thread_local std::vector<StageSummary> t_stage_summary;
 
 using namespace hbp_b200;
 
@@ -108,6 +116,53 @@ void* hbp_ctx_stream(hbp_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->s
 
 int64_t hbp_ctx_launch_count(const hbp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int hbp_ctx_set_profiling(hbp_ctx* ctx, int32_t on) {
+    return guarded(ctx, [&] {
+        if (on) {
+            // drop stale records
+            for (auto& r : ctx->prof.recs) {
+                ctx->prof.spare.push_back(r.a);
+                ctx->prof.spare.push_back(r.b);
+            }
+            ctx->prof.recs.clear();
+        }
+        ctx->prof.on = on != 0;
+    });
+}
+
+int hbp_ctx_stage_stats(hbp_ctx* ctx, int32_t index, char* name, int32_t name_len, double* ms, int64_t* launches,
+                        double* bytes) {
+    return guarded(ctx, [&] {
+        if (!ctx->prof.recs.empty()) {
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            std::map<std::string, StageSummary> agg;
+            for (auto& r : ctx->prof.recs) {
+                float t = 0;
+                CUDA_CHECK(cudaEventElapsedTime(&t, r.a, r.b));
+                auto& s = agg[r.name];
+                s.name = r.name;
+                s.ms += t;
+                s.bytes += r.bytes;
+                s.launches += 1;
+                ctx->prof.spare.push_back(r.a);
+                ctx->prof.spare.push_back(r.b);
+            }
+            ctx->prof.recs.clear();
+            t_stage_summary.clear();
+            for (auto& kv : agg) t_stage_summary.push_back(kv.second);
+        }
+        if (index < 0 || static_cast<size_t>(index) >= t_stage_summary.size()) fail_validation("no such stage");
+        const auto& s = t_stage_summary[static_cast<size_t>(index)];
+        if (name && name_len > 0) {
+            std::strncpy(name, s.name.c_str(), static_cast<size_t>(name_len) - 1);
+            name[name_len - 1] = '\0';
+        }
+        *ms = s.ms;
+        *launches = s.launches;
+        *bytes = s.bytes;
+    });
+}
+
 // ---- hot path -----------------------------------------------------------------
 
 static std::vector<hbp_group_config> groups_of(const hbp_groups* g) {
@@ -170,9 +225,11 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* g
                    const hbp_plan_options* options, hbp_plan** out) {
     return guarded(ctx, [&] {
         *out = nullptr;
+        trace_begin(*ctx);
         DeviceCorpus corpus;
         ingest(*ctx, samples, corpus);
         validate_corpus(*ctx, samples, corpus, source_of(samples));  // balance.cpp:209
+        trace_mark(*ctx, "ingest+validate");
         PlanArgs a;
         a.groups = groups_of(groups);
         a.l_best = groups->l_best;
@@ -185,6 +242,7 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* g
         auto* p = new hbp_plan();
         try {
             build_plan_device(*ctx, corpus, a, p->dp);
+            trace_dump(*ctx, "build_plan");
         } catch (...) {
             delete p;
             throw;

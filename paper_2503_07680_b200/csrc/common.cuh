@@ -109,11 +109,57 @@ inline unsigned grid_for(size_t n, unsigned block, unsigned cap = 148u * 16u) {
     return static_cast<unsigned>(g);
 }
 
-#define LAUNCH(kernel, grid, block, smem, stream, ...)                           \
-    do {                                                                         \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);             \
-        ::hbp_b200::count_launch();                                              \
-        CUDA_CHECK(cudaGetLastError());                                          \
+#define LAUNCH(kernel, grid, block, smem, stream, ...) LAUNCH_B(#kernel, 0.0, kernel, grid, block, smem, stream, __VA_ARGS__)
+
+// Per-kernel-family device time (CUDA events on the launching stream) and
+// algorithmic bytes, collected only while profiling is switched on
+// (hbp_ctx_set_profiling). Feeds bench.py's roofline.
+struct KernelProfiler {
+    bool on = false;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> spare;
+    cudaEvent_t event() {
+        if (!spare.empty()) {
+            cudaEvent_t e = spare.back();
+            spare.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+    ~KernelProfiler() {
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : spare) cudaEventDestroy(e);
+    }
+};
+extern thread_local KernelProfiler* g_prof;
+
+#define LAUNCH_B(name, bytes, kernel, grid, block, smem, stream, ...)                       \
+    do {                                                                                    \
+        ::hbp_b200::KernelProfiler* _p = ::hbp_b200::g_prof;                                \
+        const bool _on = _p && _p->on;                                                      \
+        cudaEvent_t _e0 = nullptr;                                                          \
+        if (_on) {                                                                          \
+            _e0 = _p->event();                                                              \
+            CUDA_CHECK(cudaEventRecord(_e0, (stream)));                                     \
+        }                                                                                   \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                        \
+        ::hbp_b200::count_launch();                                                         \
+        CUDA_CHECK(cudaGetLastError());                                                     \
+        if (_on) {                                                                          \
+            cudaEvent_t _e1 = _p->event();                                                  \
+            CUDA_CHECK(cudaEventRecord(_e1, (stream)));                                     \
+            _p->recs.push_back({(name), _e0, _e1, static_cast<double>(bytes)});             \
+        }                                                                                   \
     } while (0)
 
 // ---------------------------------------------------------------------------

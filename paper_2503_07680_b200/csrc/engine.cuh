@@ -10,6 +10,10 @@
 #include "common.cuh"
 #include "scan.cuh"
 
+#include <chrono>
+#include <cstdlib>
+#include <map>
+
 struct hbp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -17,20 +21,51 @@ struct hbp_ctx {
     int64_t launches = 0;
     hbp_b200::ScanScratch scan;
     hbp_b200::Pinned pinned;
+    // stage trace (HBP_TRACE=1): wall time between marks, stream synchronised
+    bool trace = std::getenv("HBP_TRACE") != nullptr;
+    std::map<std::string, double> trace_ms;
+    std::chrono::steady_clock::time_point trace_last{};
+    hbp_b200::KernelProfiler prof;
 };
 
 namespace hbp_b200 {
 
 using Ctx = hbp_ctx;
 
+inline void trace_begin(Ctx& c) {
+    if (!c.trace) return;
+    cudaStreamSynchronize(c.stream);
+    c.trace_last = std::chrono::steady_clock::now();
+}
+inline void trace_mark(Ctx& c, const char* stage) {
+    if (!c.trace) return;
+    cudaStreamSynchronize(c.stream);
+    const auto now = std::chrono::steady_clock::now();
+    c.trace_ms[stage] += std::chrono::duration<double, std::milli>(now - c.trace_last).count();
+    c.trace_last = now;
+}
+inline void trace_dump(Ctx& c, const char* title) {
+    if (!c.trace) return;
+    double tot = 0;
+    for (auto& kv : c.trace_ms) tot += kv.second;
+    std::fprintf(stderr, "[hbp trace] %s: %.3f ms\n", title, tot);
+    for (auto& kv : c.trace_ms) std::fprintf(stderr, "[hbp trace]   %-28s %9.3f ms\n", kv.first.c_str(), kv.second);
+    c.trace_ms.clear();
+}
+
 // Makes `ctx` the current launch-count sink and device for this thread.
 struct CtxScope {
     int64_t* prev;
-    explicit CtxScope(Ctx& c) : prev(g_launch_counter) {
+    KernelProfiler* prev_prof;
+    explicit CtxScope(Ctx& c) : prev(g_launch_counter), prev_prof(g_prof) {
         g_launch_counter = &c.launches;
+        g_prof = &c.prof;
         CUDA_CHECK(cudaSetDevice(c.device));
     }
-    ~CtxScope() { g_launch_counter = prev; }
+    ~CtxScope() {
+        g_launch_counter = prev;
+        g_prof = prev_prof;
+    }
 };
 
 // Copies a few device scalars to host (one sync).

@@ -110,6 +110,7 @@ struct EngineArgs {
     u32 rec0;
     u32 max_records;
     u32* out;  // [0] bins, [1] records, [2] overflow flag
+    unsigned long long* prof;  // optional cycle counters (HBP_TRACE)
 };
 
 __device__ __forceinline__ u32 tree_get(const TreeLayout& t, int h, u64 i) {
@@ -265,6 +266,264 @@ __global__ void __launch_bounds__(32) k_fit_engine(EngineArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Engine v3: the whole max tree (levels >= 1) lives in shared memory as
+// saturated u16 maxima (min(max, 65535)); leaves stay in HBM/L2. For s <=
+// 65535 a saturated comparison is exact; for larger s a saturated entry is
+// only a candidate and the leaf check decides. Per run the warp descends
+// from the root to the first candidate chunk, collects up to 32 candidate
+// chunks in index order with one ballot per tree node, copies all their
+// leaves into shared memory with cp.async (one L2 round trip for the whole
+// batch), then fills them in order.
+// ---------------------------------------------------------------------------
+
+constexpr u32 kSat = 65535u;
+__device__ __forceinline__ unsigned short sat16(u32 v) { return static_cast<unsigned short>(v > kSat ? kSat : v); }
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(32) k_fit_engine_smem(EngineArgs a) {
+    extern __shared__ unsigned short st[];  // tree levels 1..H
+    __shared__ u64 s_cand[32];
+    __shared__ __align__(16) u64 s_leaf[32][32];
+    const unsigned lane = threadIdx.x;
+    const unsigned lt = (1u << lane) - 1u;
+    const TreeLayout& t = a.t;
+    const int H = t.H;
+    const u64 total = t.off[0];
+    for (u64 i = lane; i < total; i += 32) st[i] = sat16(t.base[i]);
+    __syncwarp();
+
+    auto getL = [&](int h, u64 i) -> u32 { return i < t.size[h] ? st[t.off[h] + i] : 0u; };
+    // first level-1 index with saturated max >= q (caller checked the root)
+    auto find_first = [&](u32 q) -> u64 {
+        u64 idx = 0;
+        for (int h = H; h > 1; --h) {
+            const u64 base = idx << 5;
+            const unsigned m = __ballot_sync(0xffffffffu, getL(h - 1, base + lane) >= q);
+            if (!m) return ~0ull;
+            idx = base + (__ffs(m) - 1);
+        }
+        return idx;
+    };
+    // smallest level-1 index >= j with saturated max >= q, or ~0
+    auto find_next = [&](u64 j, u32 q) -> u64 {
+        int h = 1;
+        u64 idx = j;
+        while (true) {
+            const u64 base = idx & ~31ull;
+            const unsigned m = __ballot_sync(0xffffffffu, getL(h, base + lane) >= q && base + lane >= idx);
+            if (m) {
+                idx = base + (__ffs(m) - 1);
+                break;
+            }
+            if (h == H) return ~0ull;
+            idx = (base >> 5) + 1;
+            ++h;
+        }
+        while (h > 1) {
+            const u64 base = idx << 5;
+            const unsigned m = __ballot_sync(0xffffffffu, getL(h - 1, base + lane) >= q);
+            idx = base + (__ffs(m) - 1);
+            --h;
+        }
+        return idx;
+    };
+    // level-1 entry j decreased to `v` (true max): rewrite ancestors. Values
+    // only decrease here, so a parent needs recomputing only when the child
+    // was (one of) its maxima.
+    auto update_up = [&](u64 j, u32 v) {
+        u32 old_child = getL(1, j);
+        const u32 nv = sat16(v);
+        if (old_child == nv) return;
+        if (lane == 0) st[t.off[1] + j] = static_cast<unsigned short>(nv);
+        __syncwarp();
+        u64 idx = j;
+        for (int h = 2; h <= H; ++h) {
+            const u64 p = idx >> 5;
+            const u32 old = getL(h, p);
+            if (old_child < old) break;  // another child holds the max
+            const u32 m = warp_max(getL(h - 1, (p << 5) + lane));
+            if (old == m) break;
+            if (lane == 0) st[t.off[h] + p] = static_cast<unsigned short>(m);
+            __syncwarp();
+            old_child = old;
+            idx = p;
+        }
+    };
+
+    u32 B = a.bins0;
+    u32 nrec = a.rec0;
+    bool overflow = false;
+    u32 win_base = a.run_begin;
+    u32 my_len = 0, my_item = 0;
+    auto load_window = [&](u32 base) {
+        win_base = base;
+        const u32 r = base + lane;
+        my_len = r < a.n_runs ? a.run_len[r] : 0u;
+        my_item = r < a.n_runs ? a.run_item[r] : a.n_items;
+    };
+    load_window(a.run_begin);
+    // cycle counters: 0 collect, 1 load, 2 process, 3 new bins, 4 searched runs, 5 candidates, 6 collect rounds
+    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long t0 = 0;
+    const bool prof = a.prof != nullptr;
+
+    for (u32 k = a.run_begin; k < a.n_runs; ++k) {
+        if (k - win_base == 32) load_window(k);
+        const unsigned wl = k - win_base;
+        const u32 s = __shfl_sync(0xffffffffu, my_len, wl);
+        u32 item = __shfl_sync(0xffffffffu, my_item, wl);
+        u32 end_item;
+        if (wl < 31) {
+            end_item = __shfl_sync(0xffffffffu, my_item, wl + 1);
+        } else {
+            end_item = (k + 1 < a.n_runs) ? a.run_item[k + 1] : a.n_items;
+        }
+        u32 c = end_item - item;
+        const u32 q = s > kSat ? kSat : s;
+
+        if (B > 0 && getL(H, 0) >= q) {
+            u64 pos = 0;
+            bool first = true;
+            pc[4] += 1;
+            while (c > 0) {
+                if (prof) t0 = clock64();
+                const u32 K = c < 32 ? c : 32u;
+                u32 ncand = 0;
+                pc[6] += 1;
+                while (ncand < K) {
+                    const u64 j = first ? find_first(q) : find_next(pos, q);
+                    first = false;
+                    if (j == ~0ull) break;
+                    const u64 base = j & ~31ull;
+                    const unsigned m =
+                        __ballot_sync(0xffffffffu, getL(1, base + lane) >= q && base + lane >= j);
+                    const u32 cnt = __popc(m);
+                    const u32 room = K - ncand;
+                    const u32 r = __popc(m & lt);
+                    if (((m >> lane) & 1u) && r < room) s_cand[ncand + r] = base + lane;
+                    __syncwarp();
+                    if (cnt <= room) {
+                        ncand += cnt;
+                        pos = base + 32;
+                    } else {
+                        ncand += room;
+                        pos = s_cand[ncand - 1] + 1;
+                    }
+                }
+                if (prof) {
+                    const long long t1 = clock64();
+                    pc[0] += t1 - t0;
+                    t0 = t1;
+                }
+                if (ncand == 0) break;
+                pc[5] += ncand;
+                for (u32 qq = 0; qq < ncand; ++qq) {
+                    const u64 li = s_cand[qq] * 32 + lane;
+                    if (li < a.max_bins) cp_async8(&s_leaf[qq][lane], &a.leaves[li]);
+                    else s_leaf[qq][lane] = 0ull;
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                if (prof) {
+                    const long long t1 = clock64();
+                    pc[1] += t1 - t0;
+                    t0 = t1;
+                }
+                for (u32 qq = 0; qq < ncand && c > 0; ++qq) {
+                    const u64 leaf = s_leaf[qq][lane];
+                    const u32 res = static_cast<u32>(leaf >> 32);
+                    const u32 capl = res >= s ? res / s : 0u;
+                    const u32 incl = warp_inclusive_scan(capl);
+                    const u32 excl = incl - capl;
+                    const u32 take = excl >= c ? 0u : (capl < c - excl ? capl : c - excl);
+                    const unsigned tm = __ballot_sync(0xffffffffu, take > 0);
+                    const u64 chunk = s_cand[qq];
+                    u32 nres = res;
+                    if (take > 0) {
+                        const u32 ri = nrec + __popc(tm & lt);
+                        if (ri < a.max_records) {
+                            a.rec.item[ri] = item + excl;
+                            a.rec.count[ri] = take;
+                            a.rec.bin[ri] = static_cast<u32>(chunk * 32 + lane);
+                            a.rec.per_bin[ri] = take;
+                            a.rec.slot0[ri] = static_cast<u32>(leaf);
+                        }
+                        nres = res - take * s;
+                        a.leaves[chunk * 32 + lane] = (static_cast<u64>(nres) << 32) | (static_cast<u32>(leaf) + take);
+                    }
+                    const u32 used = __shfl_sync(0xffffffffu, incl, 31);
+                    const u32 got = used < c ? used : c;
+                    nrec += __popc(tm);
+                    c -= got;
+                    item += got;
+                    if (tm) update_up(chunk, warp_max(nres));
+                }
+                if (prof) {
+                    const long long t1 = clock64();
+                    pc[2] += t1 - t0;
+                    t0 = t1;
+                }
+            }
+        }
+        if (prof) t0 = clock64();
+        if (c > 0 && a.ffd) {
+            const u32 per = a.cap / s;
+            const u32 nb = (c + per - 1) / per;
+            if (static_cast<u64>(B) + nb > a.max_bins) {
+                overflow = true;
+                break;
+            }
+            if (nrec < a.max_records && lane == 0) {
+                a.rec.item[nrec] = item;
+                a.rec.count[nrec] = c;
+                a.rec.bin[nrec] = B;
+                a.rec.per_bin[nrec] = per;
+                a.rec.slot0[nrec] = 0;
+            }
+            ++nrec;
+            const u32 res_full = a.cap - per * s;
+            const u32 last_cnt = c - (nb - 1) * per;
+            const u32 res_last = a.cap - last_cnt * s;
+            for (u32 b = lane; b < nb; b += 32) {
+                const bool last = (b == nb - 1);
+                a.leaves[B + b] = (static_cast<u64>(last ? res_last : res_full) << 32) | (last ? last_cnt : per);
+            }
+            const u64 lo = B, hi = static_cast<u64>(B) + nb - 1;
+            const u64 full_hi = nb > 1 ? hi - 1 : lo;
+            for (int h = 1; h <= H; ++h) {
+                const u64 ilo = lo >> (5 * h), ihi = hi >> (5 * h);
+                for (u64 i = ilo + lane; i <= ihi; i += 32) {
+                    const u64 slo = i << (5 * h), shi = ((i + 1) << (5 * h)) - 1;
+                    u32 val = getL(h, i);
+                    if (nb > 1 && slo <= full_hi && shi >= lo) val = val > res_full ? val : res_full;
+                    if (slo <= hi && shi >= hi) val = val > res_last ? val : res_last;
+                    if (i < t.size[h]) st[t.off[h] + i] = sat16(val);
+                }
+                __syncwarp();
+            }
+            B += nb;
+        }
+        if (prof) pc[3] += clock64() - t0;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        a.out[0] = B;
+        a.out[1] = nrec;
+        a.out[2] = (overflow || nrec > a.max_records) ? 1u : 0u;
+        if (prof)
+            for (int i = 0; i < 8; ++i) a.prof[i] = pc[i];
+    }
+}
+
 __global__ void k_expand(FitRecords rec, const u32* __restrict__ nrec_p, u64 n_items, u32* __restrict__ item_bin,
                          u32* __restrict__ item_slot) {
     const u32 nrec = *nrec_p;
@@ -341,7 +600,22 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         }
     }
 
-    TreeLayout t = make_layout(static_cast<u64>(max_bins));
+    // First fit never leaves two bins at most half full (the later bin's
+    // first item would have fitted the earlier), so FFD opens at most
+    // 2 * ceil(sum / cap) + 1 bins: size the tree by that, not by n.
+    i64 tree_bins = max_bins;
+    if (ffd) {
+        if (h_runs.empty()) h_runs = read_vector(c, run_len.p, n_runs);
+        const auto h_items = read_vector(c, run_item.p, n_runs);
+        long double sum = 0;
+        for (u32 k = 0; k < n_runs; ++k) {
+            const u64 e = (k + 1 < n_runs) ? h_items[k + 1] : n;
+            sum += static_cast<long double>(h_runs[k]) * static_cast<long double>(e - h_items[k]);
+        }
+        const i64 bound = static_cast<i64>(2 * std::ceil(sum / cap)) + 2 + bins0;
+        if (bound < tree_bins) tree_bins = bound;
+    }
+    TreeLayout t = make_layout(static_cast<u64>(tree_bins));
     DevBuf<u32> tree(t.off[0], s);
     t.base = tree.p;
     if (bulk > 0) {
@@ -379,16 +653,39 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     a.leaves = leaves;
     a.t = t;
     a.bins0 = static_cast<u32>(live);
-    a.max_bins = static_cast<u32>(max_bins);
+    a.max_bins = static_cast<u32>(tree_bins);
     a.cap = cap;
     a.ffd = ffd ? 1 : 0;
     a.rec = rec;
     a.rec0 = rec0;
     a.max_records = static_cast<u32>(max_records);
     a.out = scal.p;
-    LAUNCH(k_fit_engine, 1, 32, 0, s, a);
+    DevBuf<unsigned long long> prof;
+    a.prof = nullptr;
+    if (c.trace) {
+        prof.alloc(8, s);
+        prof.zero();
+        a.prof = prof.p;
+    }
+    const size_t smem = sizeof(unsigned short) * t.off[0];
+    constexpr size_t kSmemLimit = 216 * 1024;  // + 8.4 KB static (candidates, leaf stage) <= 227 KB
+    if (smem <= kSmemLimit && !std::getenv("HBP_ENGINE_V1")) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kSmemLimit)));
+        LAUNCH_B("fit.engine", 0.0, k_fit_engine_smem, 1, 32, smem, s, a);
+    } else {
+        LAUNCH_B("fit.engine.v1", 0.0, k_fit_engine, 1, 32, 0, s, a);
+    }
     const auto o = read_vector(c, scal.p, 3);
     if (o[2]) throw EngineError(HBP_ERR_CUDA, "first-fit engine: record or bin capacity exceeded");
+    if (c.trace) {
+        const auto pc = read_vector(c, prof.p, 8);
+        std::fprintf(stderr,
+                     "[hbp trace] fit %s: runs %u (from %u) bins %u tree_bins %lld H %d | collect %.2fM load %.2fM "
+                     "process %.2fM newbins %.2fM cycles | searched %llu cands %llu rounds %llu\n",
+                     ffd ? "ffd" : "fill", n_runs, run_begin, o[0], static_cast<long long>(tree_bins), t.H,
+                     pc[0] / 1e6, pc[1] / 1e6, pc[2] / 1e6, pc[3] / 1e6, pc[4], pc[5], pc[6]);
+    }
     out.bins = o[0];
     out.records = o[1];
     return out;

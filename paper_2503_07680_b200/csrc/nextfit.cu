@@ -246,8 +246,9 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
             static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? (F[i] >> 32) : 0ull; },
             [=] __device__(i64 i, u64 v) { Pp[i] = v; }, s, c.scan);
     }
-    LAUNCH(k_nf_next, grid_for(m, 256, 148u * 32u), 256, 0, s, P.p, m, static_cast<u64>(cap), nxt.p);
-    LAUNCH(k_nf_tiles, ntiles, NF_B, 0, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
+    LAUNCH_B("nf.next", 12.0 * m, k_nf_next, grid_for(m, 256, 148u * 32u), 256, 0, s, P.p, m, static_cast<u64>(cap),
+             nxt.p);
+    LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, 0, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
     LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
     LAUNCH(k_nf_flags, ntiles, NF_B, 0, s, nxt.p, spec.p, entry.p, m, flags.p);
     // enumerate pack starts

@@ -498,7 +498,9 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
                                                               : derive_seed(seed, "random-pack");
             fy_source_positions(c, rs, static_cast<i64>(cur), src.p);
             gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(cur));
+            trace_mark(c, "isf.shuffle");
             cur = static_cast<u64>(nextfit_freeze(c, Bf.p, static_cast<i64>(cur), cap, tmin, sink, A.p));
+            trace_mark(c, "isf.nextfit+freeze");
         }
         residue_ffd = st.kind == HBP_STRATEGY_ISF;
         key_ordered = false;  // the residue is in shuffled order
@@ -527,15 +529,18 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         out.residue.alloc(cur, s);
         CUDA_CHECK(cudaMemcpyAsync(out.residue.p, A.p, sizeof(u64) * cur, cudaMemcpyDeviceToDevice, s));
         if (residue_ffd) sort_entries(c, corpus, out.residue.p, cur, key_ordered, cap);
+        trace_mark(c, "ffd.sort");
         const u64 maxrec = 2 * cur + 2;
         DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
         FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
         const FitResult fr = first_fit_runs(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf, 0,
                                             static_cast<i64>(cur), cap, FitMode::Ffd, rec, static_cast<i64>(maxrec));
         out.n_ffd = static_cast<u64>(fr.bins);
+        trace_mark(c, "ffd.engine");
         out.res_bin.alloc(cur, s);
         out.res_slot.alloc(cur, s);
         expand_fit_records(c, rec, fr.records, static_cast<i64>(cur), out.res_bin.p, out.res_slot.p);
+        trace_mark(c, "ffd.expand");
     }
 }
 
@@ -803,6 +808,7 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     if (a.device_count < 1) fail_validation("device count must be >= 1");
     if (a.groups.size() > 64) fail_validation("the GPU engine supports at most 64 packing groups");
     check_l_max(c, corpus, a.l_max);
+    trace_mark(c, "check");
     out.device_count = a.device_count;
     out.seed = a.seed;
     out.groups = a.groups;
@@ -815,6 +821,7 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     DevBuf<u64> entries;
     std::vector<u64> goff;
     partition(c, corpus, a.groups, entries, goff);
+    trace_mark(c, "group_data");
 
     // pools: group g = entries[goff[g] .. goff[g+1]) in input order; greedy
     // fill shrinks them (order preserved) before they are packed.
@@ -873,6 +880,7 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
                              static_cast<u32>(a.groups[j].length));
                 o += psize[j];
             }
+            trace_mark(c, "fill.sort");
             const u64 P = pg.P();
             const u64 maxrec = 2 * n_fill + 2;
             DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
@@ -880,6 +888,7 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             const FitResult fr = first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p,
                                                 static_cast<i64>(P), static_cast<i64>(P), cap, FitMode::Fill, rec,
                                                 static_cast<i64>(maxrec));
+            trace_mark(c, "fill.engine");
             fill_bin.alloc(n_fill, s);
             fill_slot.alloc(n_fill, s);
             expand_fit_records(c, rec, fr.records, static_cast<i64>(n_fill), fill_bin.p, fill_slot.p);
@@ -910,13 +919,15 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
                 pools[j] = std::move(kept);
             }
         }
+        trace_mark(c, "fill.expand+compact");
         const u64 pbase = T.n_packs;
         const u64 P = layout_group(c, pg, fill_items.p, n_fill, fill_bin.p, fill_slot.p, cap, T);
-        const bool sp_comm = a.groups[gi].sp > 1;
-        (void)sp_comm;  // comm tokens are derived from the group at report time
+        trace_mark(c, "layout");
         I += batch_group(c, corpus, T, pbase, P, N, cap, gi, a.balance_batching, a.seed, I, slots, igroup);
+        trace_mark(c, "batching");
     }
     emit_plan(c, T, slots, igroup, I, N, a.seed, out);
+    trace_mark(c, "emit");
     CUDA_CHECK(cudaStreamSynchronize(s));
 }
 

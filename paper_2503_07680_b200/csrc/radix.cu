@@ -119,13 +119,14 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
     u32 *ki = keys, *vi = vals, *ko = tmp_keys, *vo = tmp_vals;
     for (int p = 0; p < passes; ++p) {
         const int shift = 8 * p;
-        LAUNCH(k_radix_hist, ntiles, RB, 0, s, ki, n, shift, descending, hist.p, ntiles);
+        LAUNCH_B("radix.hist", 4.0 * n, k_radix_hist, ntiles, RB, 0, s, ki, n, shift, descending, hist.p, ntiles);
         const u32* hp = hist.p;
         u32* op = offs.p;
         scan_exclusive<u32>(
             static_cast<i64>(ntiles) * 256, [=] __device__(i64 i) { return hp[i]; },
             [=] __device__(i64 i, u32 v) { op[i] = v; }, s, c.scan);
-        LAUNCH(k_radix_scatter, ntiles, RB, 0, s, ki, vi, ko, vo, n, shift, descending, offs.p, ntiles);
+        LAUNCH_B("radix.scatter", 16.0 * n, k_radix_scatter, ntiles, RB, 0, s, ki, vi, ko, vo, n, shift, descending,
+                 offs.p, ntiles);
         std::swap(ki, ko);
         std::swap(vi, vo);
     }

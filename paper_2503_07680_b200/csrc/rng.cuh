@@ -10,18 +10,24 @@
 #include <cstdint>
 #include <string_view>
 
+#if defined(__CUDACC__)
+#define HBP_HD __host__ __device__ __forceinline__
+#else
+#define HBP_HD inline
+#endif
+
 namespace hbp_b200 {
 
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
 
-__host__ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+HBP_HD uint64_t splitmix_mix(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
     return z ^ (z >> 31);
 }
 
 // k-th draw (k >= 1) of Rng(seed)
-__host__ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
+HBP_HD uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
     return splitmix_mix(seed + k * kGamma);
 }
 

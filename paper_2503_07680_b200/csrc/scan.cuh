@@ -119,14 +119,15 @@ struct ScanScratch {
 };
 
 template <typename T, int ITEMS = 8, typename Load, typename Store>
-void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch) {
+void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch,
+                    const char* name = "scan", double bytes_per_elem = 2.0 * sizeof(T)) {
     constexpr int BLOCK = 256;
     constexpr int TILE = BLOCK * ITEMS;
     if (n <= 0) return;
     const i64 tiles = (n + TILE - 1) / TILE;
     scratch.prepare(tiles, stream);
-    LAUNCH((k_scan_lookback<T, BLOCK, ITEMS, Load, Store>), static_cast<unsigned>(tiles), BLOCK, 0, stream, n,
-           load, store, scratch.status.p, scratch.counter.p);
+    LAUNCH_B(name, bytes_per_elem * static_cast<double>(n), (k_scan_lookback<T, BLOCK, ITEMS, Load, Store>),
+             static_cast<unsigned>(tiles), BLOCK, 0, stream, n, load, store, scratch.status.p, scratch.counter.p);
 }
 
 }  // namespace hbp_b200

@@ -177,7 +177,7 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src) {
     rej.zero();
     const unsigned B = 256;
     const unsigned G = grid_for(m, B, 148u * 32u);
-    LAUNCH(k_fy_targets, G, B, 0, s, seed, m, tgt.p, cnt.p, rej.p);
+    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, m, tgt.p, cnt.p, rej.p);
     LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, m, tgt.p, cnt.p, rej.p);
     // exclusive scan of per-target counts -> list offsets (m + 1 entries)
     const u32* cntp = cnt.p;
@@ -186,15 +186,16 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src) {
         static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? cntp[i] : 0u; },
         [=] __device__(i64 i, u32 v) { offp[i] = v; }, s, c.scan);
     cnt.zero();  // reused as fill cursors
-    LAUNCH(k_fy_scatter, G, B, 0, s, m, tgt.p, off.p, cnt.p, bucket.p);
-    LAUNCH(k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);
-    LAUNCH(k_fy_roots, G, B, 0, s, m, link.p, root.p);
-    LAUNCH(k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, src);
+    LAUNCH_B("fy.scatter", 20.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, off.p, cnt.p, bucket.p);
+    LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);
+    LAUNCH_B("fy.roots", 8.0 * m, k_fy_roots, G, B, 0, s, m, link.p, root.p);
+    LAUNCH_B("fy.sources", 16.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, src);
 }
 
 void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m) {
     if (m <= 0) return;
-    LAUNCH(k_gather<u64>, grid_for(m, 256, 148u * 32u), 256, 0, c.stream, in, src, out, static_cast<u64>(m));
+    LAUNCH_B("gather.u64", 20.0 * m, k_gather<u64>, grid_for(m, 256, 148u * 32u), 256, 0, c.stream, in, src, out,
+             static_cast<u64>(m));
 }
 
 void gather_u32(Ctx& c, const u32* in, const u32* src, u32* out, i64 m) {

@@ -267,6 +267,16 @@ int hbp_simulate_plan(hbp_ctx* ctx, hbp_plan* plan,
 int hbp_memory_used(hbp_ctx* ctx, int64_t length, int32_t sp, int32_t ckpt,
                     const hbp_hardware_profile* profile, int64_t* out);
 
+/* Profiler::profile_time / profile_memory / derive_ckpt of an analytic or
+ * table profiler (costmodel.hpp:85-93; AnalyticProfiler costmodel.cpp:123-138,
+ * TableProfiler :223-265). Constructor checks (AnalyticProfiler probe bounds,
+ * TableProfiler duplicate rows) run first, as in the reference. */
+int hbp_profiler_time(hbp_ctx* ctx, const hbp_profiler* profiler, int64_t length, int32_t sp, int32_t ckpt,
+                      double* out);
+int hbp_profiler_memory(hbp_ctx* ctx, const hbp_profiler* profiler, int64_t length, int32_t sp, int32_t ckpt,
+                        int64_t* out);
+int hbp_profiler_derive_ckpt(hbp_ctx* ctx, const hbp_profiler* profiler, int64_t length, int32_t sp, int32_t* out);
+
 /* greedy_profile_ckpt (costmodel.hpp:158-159, src/costmodel.cpp:271-292). */
 int hbp_greedy_profile_ckpt(hbp_ctx* ctx, const hbp_profiler* profiler,
                             int64_t length, int32_t sp, int32_t ckpt_min,

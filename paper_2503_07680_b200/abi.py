@@ -399,6 +399,72 @@ class Context:
                                             C.byref(prof), C.byref(out)))
         return out.value
 
+    # -- cost model / auto-selection -----------------------------------------
+    def profile_time(self, profiler: Profiler, length, sp, ckpt) -> float:
+        out = C.c_double()
+        self.check(self.lib.hbp_profiler_time(self.h, C.byref(profiler), C.c_int64(length), C.c_int32(sp),
+                                              C.c_int32(ckpt), C.byref(out)))
+        return out.value
+
+    def profile_memory(self, profiler: Profiler, length, sp, ckpt) -> int:
+        out = C.c_int64()
+        self.check(self.lib.hbp_profiler_memory(self.h, C.byref(profiler), C.c_int64(length), C.c_int32(sp),
+                                                C.c_int32(ckpt), C.byref(out)))
+        return out.value
+
+    def derive_ckpt(self, profiler: Profiler, length, sp) -> int:
+        out = C.c_int32()
+        self.check(self.lib.hbp_profiler_derive_ckpt(self.h, C.byref(profiler), C.c_int64(length), C.c_int32(sp),
+                                                     C.byref(out)))
+        return out.value
+
+    def greedy_profile_ckpt(self, profiler: Profiler, length, sp, ckpt_min, ckpt_max) -> int:
+        out = C.c_int32()
+        self.check(self.lib.hbp_greedy_profile_ckpt(self.h, C.byref(profiler), C.c_int64(length), C.c_int32(sp),
+                                                    C.c_int32(ckpt_min), C.c_int32(ckpt_max), C.byref(out)))
+        return out.value
+
+    def find_best_sp_ckpt(self, profiler: Profiler, length, sps):
+        arr = np.ascontiguousarray(sps, dtype=np.int32)
+        sp, ck, sec = C.c_int32(), C.c_int32(), C.c_double()
+        self.check(self.lib.hbp_find_best_sp_ckpt(self.h, C.byref(profiler), C.c_int64(length),
+                                                  ptr(arr, C.c_int32), C.c_int32(len(arr)), C.byref(sp),
+                                                  C.byref(ck), C.byref(sec)))
+        return (sp.value, ck.value), sec.value
+
+    def select_groups(self, lengths, profiler: Profiler, sps):
+        ls = np.ascontiguousarray(lengths, dtype=np.int64)
+        sp = np.ascontiguousarray(sps, dtype=np.int32)
+        out = (GroupConfig * 4)()
+        n, lb, lm = C.c_int32(), C.c_int64(), C.c_int64()
+        self.check(self.lib.hbp_select_groups(self.h, ptr(ls, C.c_int64), C.c_int32(len(ls)), C.byref(profiler),
+                                              ptr(sp, C.c_int32), C.c_int32(len(sp)), out, C.byref(n),
+                                              C.byref(lb), C.byref(lm)))
+        return [(out[i].length, out[i].sp, out[i].ckpt) for i in range(n.value)], lb.value, lm.value
+
+    def sweep(self, ids, lengths, candidates, profile: Optional[HardwareProfile] = None, **opts):
+        """candidates: [(groups[(l, sp, ckpt)...], l_best)] -> (seconds[], best index)."""
+        s, keep = make_samples(ids, lengths)
+        return self.sweep_samples(s, candidates, profile, **opts)
+
+    def sweep_samples(self, s: Samples, candidates, profile: Optional[HardwareProfile] = None, **opts):
+        flat, offs, lbs = [], [0], []
+        for groups, lb in candidates:
+            flat.extend(groups)
+            offs.append(len(flat))
+            lbs.append(lb)
+        garr = (GroupConfig * max(1, len(flat)))(*[GroupConfig(*g) for g in flat])
+        offs = np.array(offs, dtype=np.int64)
+        lbs = np.array(lbs, dtype=np.int64)
+        prof = profile if profile is not None else default_profile()
+        o = make_options(**opts)
+        out = np.zeros(max(1, len(candidates)))
+        best = C.c_int64()
+        self.check(self.lib.hbp_sweep(self.h, C.byref(s), garr, ptr(offs, C.c_int64), ptr(lbs, C.c_int64),
+                                      C.c_int64(len(candidates)), C.byref(o), C.byref(prof),
+                                      ptr(out, C.c_double), C.byref(best)))
+        return out[:len(candidates)], best.value
+
     # -- stage hooks (include/hbp_b200_testing.h) --------------------------
     def shuffle_positions(self, seed: int, m: int) -> np.ndarray:
         out = np.zeros(max(m, 1), dtype=np.uint32)

@@ -233,6 +233,33 @@ int hbp_group_data(hbp_ctx* ctx, const hbp_samples* samples,
 int hbp_pack(hbp_ctx* ctx, const hbp_samples* samples, int64_t capacity,
              const hbp_strategy* strategy, uint64_t seed, hbp_plan** out);
 
+/* A host pack list: pack p holds samples [pack_offsets[p], pack_offsets[p+1])
+ * of ids/lengths, with its own capacity. */
+typedef struct hbp_packs_in {
+    int64_t n_packs;
+    const int64_t* pack_offsets; /* [n_packs + 1] */
+    const int64_t* pack_capacity; /* [n_packs] */
+    const int64_t* ids;
+    const int64_t* lengths;
+} hbp_packs_in;
+
+/* greedy_fill (include/hbp/balance.hpp:48, src/balance.cpp:46-101). Pools
+ * are n_pools sample lists (pool_offsets[n_pools + 1]) ordered smallest
+ * group first, as in the reference. Outputs: out_added_offsets[n_packs + 1]
+ * and out_added[] (capacity: total pool samples) list, per pack and in pick
+ * order, the flattened pool index of every sample it takes;
+ * out_pool_keep[total pool samples] is 1 for samples left in their pool. */
+int hbp_greedy_fill(hbp_ctx* ctx, const hbp_packs_in* packs, int32_t n_pools, const int64_t* pool_offsets,
+                    const int64_t* pool_ids, const int64_t* pool_lengths, int64_t* out_added_offsets,
+                    int64_t* out_added, uint8_t* out_pool_keep);
+
+/* balance_batching / random_pack_batching (include/hbp/balance.hpp:55-62,
+ * src/balance.cpp:105-205) over a host pack list of common `capacity`
+ * (PackList::capacity). The result is a plan without the plan shuffle; its
+ * member_index[] indexes packs->ids / packs->lengths. */
+int hbp_balance_batching(hbp_ctx* ctx, const hbp_packs_in* packs, int64_t capacity, int32_t device_count,
+                         int32_t group_index, int32_t random_batching, uint64_t seed, hbp_plan** out);
+
 /* build_plan (include/hbp/balance.hpp:75-76, src/balance.cpp:207-258). */
 int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples,
                    const hbp_groups* groups, const hbp_plan_options* options,

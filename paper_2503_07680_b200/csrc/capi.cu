@@ -251,6 +251,39 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* g
     });
 }
 
+int hbp_greedy_fill(hbp_ctx* ctx, const hbp_packs_in* packs, int32_t n_pools, const int64_t* pool_offsets,
+                    const int64_t* pool_ids, const int64_t* pool_lengths, int64_t* out_added_offsets,
+                    int64_t* out_added, uint8_t* out_pool_keep) {
+    return guarded(ctx, [&] {
+        std::vector<int64_t> off, added;
+        std::vector<uint8_t> keep;
+        greedy_fill_device(*ctx, packs->n_packs, packs->pack_capacity, packs->pack_offsets, packs->lengths, n_pools,
+                           pool_offsets, pool_ids, pool_lengths, off, added, keep);
+        std::memcpy(out_added_offsets, off.data(), sizeof(int64_t) * off.size());
+        if (!added.empty()) std::memcpy(out_added, added.data(), sizeof(int64_t) * added.size());
+        if (!keep.empty()) std::memcpy(out_pool_keep, keep.data(), keep.size());
+    });
+}
+
+int hbp_balance_batching(hbp_ctx* ctx, const hbp_packs_in* packs, int64_t capacity, int32_t device_count,
+                         int32_t group_index, int32_t random_batching, uint64_t seed, hbp_plan** out) {
+    return guarded(ctx, [&] {
+        *out = nullptr;
+        if (device_count < 1) fail_validation("device count must be >= 1");
+        auto* p = new hbp_plan();
+        try {
+            batching_device(*ctx, capacity, packs->n_packs, packs->pack_capacity, packs->pack_offsets, packs->ids,
+                            packs->lengths, device_count, group_index, random_batching != 0, seed, p->dp);
+            p->dp.groups.assign(static_cast<size_t>(group_index) + 1, hbp_group_config{capacity, 1, 0});
+            p->dp.l_max = capacity;
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
 int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out) {
     return guarded(ctx, [&] {
         if (plan == nullptr) fail_validation("null plan");

@@ -13,6 +13,11 @@
 
 #include "../../include/hbp_b200.h"
 
+#if !defined(__CUDACC__)
+#define __host__
+#define __device__
+#endif
+
 namespace hbp_b200 {
 
 #if defined(__CUDA_ARCH__)

@@ -631,7 +631,7 @@ u64 batch_group(Ctx& c, const DeviceCorpus& corpus, PackTable& T, u64 pbase, u64
 }
 
 void emit_plan(Ctx& c, PackTable& T, DevBuf<u32>& slots, DevBuf<int32_t>& igroup, u64 I, u32 N, uint64_t seed,
-               DevicePlan& out) {
+               DevicePlan& out, bool shuffle = true) {
     cudaStream_t s = c.stream;
     out.n_iterations = static_cast<int64_t>(I);
     out.n_devices = static_cast<int64_t>(I * N);
@@ -649,7 +649,11 @@ void emit_plan(Ctx& c, PackTable& T, DevBuf<u32>& slots, DevBuf<int32_t>& igroup
         return;
     }
     DevBuf<u32> src(I, s);
-    fy_source_positions(c, derive_seed(seed, "plan-shuffle"), static_cast<i64>(I), src.p);  // balance.cpp:255-256
+    if (shuffle) {
+        fy_source_positions(c, derive_seed(seed, "plan-shuffle"), static_cast<i64>(I), src.p);  // balance.cpp:255-256
+    } else {
+        LAUNCH(k_iota, G(I), kB, 0, s, src.p, I);
+    }
     LAUNCH(k_out_iterations, G(I), kB, 0, s, src.p, I, N, igroup.p, out.iter_group.p, out.iter_dev_offsets.p,
            out.dev_index.p);
     {
@@ -1044,6 +1048,139 @@ void plan_to_host(Ctx& c, DevicePlan& p) {
     cp(p.h_member_index, p.member_index, M);
     CUDA_CHECK(cudaStreamSynchronize(c.stream));
     p.on_host = true;
+}
+
+// ---------------------------------------------------------------------------
+// stand-alone stages over host pack lists (C++ / Python drop-in calls)
+// ---------------------------------------------------------------------------
+
+void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int64_t* pack_off, const int64_t* lens,
+                        int n_pools, const int64_t* pool_off, const int64_t* pool_ids, const int64_t* pool_lens,
+                        std::vector<int64_t>& added_off, std::vector<int64_t>& added, std::vector<uint8_t>& keep) {
+    cudaStream_t s = c.stream;
+    const i64 M = n_pools > 0 ? pool_off[n_pools] : 0;
+    added_off.assign(static_cast<size_t>(n_packs) + 1, 0);
+    added.clear();
+    keep.assign(static_cast<size_t>(M), 1);
+    if (n_packs == 0 || M == 0) return;
+    // pool samples as one corpus: ids give the tie-break ranks
+    hbp_samples in{pool_ids, pool_lens, M, HBP_MEM_HOST, "pools"};
+    DeviceCorpus corpus;
+    ingest(c, &in, corpus);
+    if (corpus.neg_ids > 0)
+        throw EngineError(HBP_ERR_CUDA, "greedy fill with sample ids <= -2 is not supported by the GPU engine yet");
+    // leaves: (max(0, capacity - total) << 32) | count, per pack
+    std::vector<u64> leaves(static_cast<size_t>(n_packs));
+    std::vector<u32> base(static_cast<size_t>(n_packs));
+    for (i64 p = 0; p < n_packs; ++p) {
+        int64_t tot = 0;
+        for (int64_t k = pack_off[p]; k < pack_off[p + 1]; ++k) tot += lens[k];
+        const int64_t r = pack_cap[p] - tot;
+        const u32 res = r <= 0 ? 0u : (r > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(r));
+        base[p] = static_cast<u32>(pack_off[p + 1] - pack_off[p]);
+        leaves[p] = (static_cast<u64>(res) << 32) | base[p];
+    }
+    DevBuf<u64> dleaves(static_cast<size_t>(n_packs), s);
+    CUDA_CHECK(cudaMemcpyAsync(dleaves.p, leaves.data(), sizeof(u64) * n_packs, cudaMemcpyHostToDevice, s));
+    std::vector<std::vector<std::pair<u32, u32>>> per_pack(static_cast<size_t>(n_packs));  // (slot, pool index)
+    // pools nearest first; pool-by-pool equals pack-by-pack (each pool is only consumed from)
+    for (int j = n_pools - 1; j >= 0; --j) {
+        const u64 a = static_cast<u64>(pool_off[j]), m = static_cast<u64>(pool_off[j + 1] - pool_off[j]);
+        if (m == 0) continue;
+        DevBuf<u32> idx(m, s);
+        DevBuf<u64> items(m, s);
+        u32* ip = idx.p;
+        for_each_index(c, m, [=] __device__(u64 i) { ip[i] = static_cast<u32>(a + i); });
+        LAUNCH(k_entries_from_idx, G(m), kB, 0, s, corpus.len32.p, idx.p, m, items.p);
+        u32 maxlen = 1;
+        for (u64 i = 0; i < m; ++i) maxlen = std::max<u32>(maxlen, static_cast<u32>(std::min<int64_t>(pool_lens[a + i], 0x7fffffff)));
+        sort_entries(c, corpus, items.p, m, corpus.key32.p == nullptr, maxlen);
+        const u64 maxrec = 2 * m + 2;
+        DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
+        FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
+        const FitResult fr = first_fit_runs(c, items.p, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u,
+                                            FitMode::Fill, rec, static_cast<i64>(maxrec));
+        DevBuf<u32> bin(m, s), slot(m, s);
+        expand_fit_records(c, rec, fr.records, static_cast<i64>(m), bin.p, slot.p);
+        const auto hb = read_vector(c, bin.p, m), hs = read_vector(c, slot.p, m);
+        const auto he = read_vector(c, items.p, m);
+        for (u64 i = 0; i < m; ++i) {
+            if (hb[i] == kNone) continue;
+            const u32 pi = entry_idx(he[i]);
+            per_pack[hb[i]].push_back({hs[i], pi});
+            keep[pi] = 0;
+        }
+    }
+    for (i64 p = 0; p < n_packs; ++p) {
+        auto& v = per_pack[static_cast<size_t>(p)];
+        std::sort(v.begin(), v.end());
+        for (auto& x : v) added.push_back(x.second);
+        added_off[p + 1] = static_cast<int64_t>(added.size());
+    }
+}
+
+void batching_device(Ctx& c, int64_t capacity, i64 n_packs, const int64_t* pack_cap, const int64_t* pack_off,
+                     const int64_t* ids, const int64_t* lens, int32_t N, int32_t gi, bool random, uint64_t seed,
+                     DevicePlan& out) {
+    cudaStream_t s = c.stream;
+    if (N < 1) fail_validation("device count must be >= 1");
+    out.device_count = N;
+    out.seed = seed;
+    const i64 M = n_packs > 0 ? pack_off[n_packs] : 0;
+    if (n_packs == 0) {
+        PackTable T;
+        DevBuf<u32> slots(1, s);
+        DevBuf<int32_t> ig(1, s);
+        emit_plan(c, T, slots, ig, 0, static_cast<u32>(N), seed, out, false);
+        return;
+    }
+    hbp_samples in{ids, lens, M, HBP_MEM_HOST, "packs"};
+    DeviceCorpus corpus;
+    if (M > 0) ingest(c, &in, corpus);
+    const u64 P = static_cast<u64>(n_packs);
+    PackTable T;
+    T.members.alloc(2 * static_cast<u64>(M) + 1, s);
+    T.moff.alloc(P + N + 1, s);
+    T.cnt.alloc(P + N + 1, s);
+    T.cap.alloc(P + N + 1, s);
+    T.total.alloc(P + N + 1, s);
+    T.att.alloc(P + N + 1, s);
+    std::vector<u64> hm(static_cast<size_t>(M)), moff(P);
+    std::vector<u32> cnt(P), cap(P), tot(P);
+    std::vector<u64> att(P);
+    for (u64 p = 0; p < P; ++p) {
+        moff[p] = static_cast<u64>(pack_off[p]);
+        cnt[p] = static_cast<u32>(pack_off[p + 1] - pack_off[p]);
+        cap[p] = static_cast<u32>(std::min<int64_t>(pack_cap[p], 0x7fffffff));
+        int64_t t = 0, at = 0;
+        for (int64_t k = pack_off[p]; k < pack_off[p + 1]; ++k) {
+            t += lens[k];
+            at += lens[k] * lens[k];
+            hm[static_cast<size_t>(k)] = make_entry(static_cast<u32>(std::min<int64_t>(lens[k], 0x7fffffff)),
+                                                    static_cast<u32>(k));
+        }
+        tot[p] = static_cast<u32>(t);
+        att[p] = static_cast<u64>(at);
+    }
+    auto up = [&](auto* d, const auto& h) {
+        if (!h.empty()) CUDA_CHECK(cudaMemcpyAsync(d, h.data(), sizeof(h[0]) * h.size(), cudaMemcpyHostToDevice, s));
+    };
+    up(T.members.p, hm);
+    up(T.moff.p, moff);
+    up(T.cnt.p, cnt);
+    up(T.cap.p, cap);
+    up(T.total.p, tot);
+    up(T.att.p, att);
+    T.n_packs = P;
+    T.n_members = static_cast<u64>(M);
+    const u64 max_iters = P / N + 2;
+    DevBuf<u32> slots(max_iters * N, s);
+    DevBuf<int32_t> igroup(max_iters, s);
+    const u64 I = batch_group(c, corpus, T, 0, P, static_cast<u32>(N),
+                              static_cast<u32>(std::min<int64_t>(capacity, 0x7fffffff)), gi, !random, seed, 0, slots,
+                              igroup);
+    emit_plan(c, T, slots, igroup, I, static_cast<u32>(N), seed, out, false);
+    CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
 }  // namespace hbp_b200

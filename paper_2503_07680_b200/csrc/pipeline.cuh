@@ -79,6 +79,19 @@ void group_data_device(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group
 
 void plan_to_host(Ctx& c, DevicePlan& p);
 
+// greedy_fill over host pack lists (balance.cpp:46-101): returns, per pack,
+// the pool samples (flattened pool index) it takes in order, and which pool
+// samples remain.
+void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int64_t* pack_off, const int64_t* lens,
+                        int n_pools, const int64_t* pool_off, const int64_t* pool_ids, const int64_t* pool_lens,
+                        std::vector<int64_t>& added_off, std::vector<int64_t>& added, std::vector<uint8_t>& keep);
+
+// balance_batching / random_pack_batching over a host pack list
+// (balance.cpp:105-205); no plan shuffle. member_index = member position.
+void batching_device(Ctx& c, int64_t capacity, i64 n_packs, const int64_t* pack_cap, const int64_t* pack_off,
+                     const int64_t* ids, const int64_t* lens, int32_t N, int32_t gi, bool random, uint64_t seed,
+                     DevicePlan& out);
+
 // groups.validate() (autoselect.cpp:18-33)
 void validate_groups(const std::vector<hbp_group_config>& g, int64_t l_max);
 void validate_strategy(const hbp_strategy& s);

@@ -1,0 +1,87 @@
+"""The reference's public APIs, unchanged, running on the B200 engine:
+
+* the C++ API (include/hbp/*.hpp) through tests/cpp/test_dropin.cpp, a port
+  of the reference test suite's known answers linked like hbp_core;
+* the Python module (paper_2503_07680_b200.hbp == reference `hbp`), checked
+  against the oracle restatement on the same inputs.
+"""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_golden.json")))
+
+
+def test_cpp_dropin_suite():
+    exe = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.fixture(scope="module")
+def hbp():
+    from paper_2503_07680_b200 import hbp as mod
+    return mod
+
+
+def groups_obj(hbp, groups, l_best):
+    return hbp.HierarchicalGroups([hbp.GroupConfig(l, hbp.RuntimeConfig(sp, ck)) for (l, sp, ck) in groups],
+                                  l_best, groups[-1][0])
+
+
+def test_python_build_plan_matches_oracle(hbp, oracle):
+    L = oracle.synth(30_000, "lognormal:7.2:0.7", 0.03, "uniform:16385:131072", 131072, 9)
+    groups = [(16384, 1, 27), (131072, 8, 27)]
+    plan = hbp.build_plan(hbp.SampleSet(L.tolist()), groups_obj(hbp, groups, 16384), device_count=8, seed=3)
+    want = oracle.build_plan(None, L, groups, l_best=16384, device_count=8, seed=3)
+    got_members = [s.id for it in plan.iterations for d in it.devices for p in d.packs for s in p.samples]
+    assert got_members == want.member_id.tolist()
+    assert [it.group_index for it in plan.iterations] == want.iter_group.tolist()
+    rep = hbp.report(plan)
+    m = oracle.report(want)[0]
+    assert rep.abr == pytest.approx(m.abr, rel=1e-12) and rep.cr == m.cr and rep.pr == m.pr
+    sim = hbp.simulate(plan, hbp.HardwareProfile(), "hbp")
+    assert sim.total_seconds == pytest.approx(oracle.simulate(want)[0].total_seconds, rel=1e-12)
+
+
+def test_python_select_groups_table(hbp, tmp_path):
+    rows = GOLD["profiles"]["group_candidates_8b"]
+    path = tmp_path / "group_candidates_8b.csv"
+    path.write_text("length,sp,ckpt,memory_bytes,iter_seconds\n" + "".join(
+        f"{l},{sp},{ck},{'oom' if mem is None else mem},{sec}\n" for l, sp, ck, mem, sec in rows))
+    t = hbp.TableProfiler.from_csv_file(str(path))
+    g = hbp.select_groups([8192, 16384, 32768, 65536, 131072], t, [1, 2, 4, 8, 16])
+    assert [(x.length, x.config.sp, x.config.ckpt) for x in g.groups] == \
+        [tuple(x) for x in GOLD["autoselect"]["select_groups_candidates_8b"][0]]
+
+
+def test_python_exceptions(hbp):
+    with pytest.raises(ValueError, match="non-positive length 0"):
+        hbp.SampleSet([1, 0])
+    with pytest.raises(ValueError, match="sample 1"):
+        hbp.pack(hbp.SampleSet([3, 9, 2]), 4, "ffd")
+    tiny = hbp.HardwareProfile()
+    tiny.device_memory = 25 << 30
+    L = [1000] * 64
+    plan = hbp.build_plan(hbp.SampleSet(L), groups_obj(hbp, [(16384, 1, 0)], 16384), device_count=2)
+    with pytest.raises(RuntimeError, match="iteration 0"):
+        hbp.simulate(plan, tiny)
+
+
+def test_python_pack_strategies(hbp, oracle):
+    rng = np.random.default_rng(5)
+    L = rng.integers(1, 978, size=500)
+    for kind in ["isf", "random", "ffd", "ffs"]:
+        got = hbp.pack(hbp.SampleSet(L.tolist()), 1024, kind, 77)
+        want = oracle.pack(None, L, 1024, kind, seed=77)
+        ids = [s.id for p in got.packs for s in p.samples]
+        assert ids == want.member_id.tolist(), kind

@@ -524,6 +524,304 @@ __global__ void __launch_bounds__(32) k_fit_engine_smem(EngineArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Engine v4: fixed three-level max structure in shared memory (u16,
+// saturated): L1 = max of 32 leaves (a chunk), L2 = max of 32 chunks, L3 =
+// max of 32 L2 entries (<= 128 entries, scanned by the warp). Fixed depth,
+// offsets in registers, warp maxima with REDUX, and a 32-chunk leaf cache in
+// shared memory (direct-mapped by chunk index, write-through to HBM) so
+// that consecutive runs touching the same chunks skip the L2 round trip.
+// Bins <= 128 * 32768; larger trees use v3.
+// ---------------------------------------------------------------------------
+
+struct V4Layout {
+    u32 n1, n2, n3;      // live entries per level
+    u32 o2, o3;          // offsets of L2 / L3 in the smem array (L1 at 0)
+    u32 total;           // padded entries
+};
+
+V4Layout make_v4(u64 bins) {
+    V4Layout v{};
+    v.n1 = static_cast<u32>((bins + 31) / 32);
+    v.n2 = (v.n1 + 31) / 32;
+    v.n3 = (v.n2 + 31) / 32;
+    const u32 p1 = (v.n1 + 31) / 32 * 32, p2 = (v.n2 + 31) / 32 * 32;
+    v.o2 = p1;
+    v.o3 = p1 + p2;
+    v.total = p1 + p2 + 128;
+    return v;
+}
+
+__global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) {
+    extern __shared__ unsigned short st4[];
+    __shared__ __align__(16) u64 s_cache[32][32];
+    __shared__ u32 s_tag[32];
+    __shared__ u32 s_cand[32];
+    const unsigned lane = threadIdx.x;
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned short* L1 = st4;
+    unsigned short* L2 = st4 + L.o2;
+    unsigned short* L3 = st4 + L.o3;
+    // build the levels from the global tree (levels 1..3 of TreeLayout are
+    // exactly L1..L3 here; deeper levels are not needed)
+    {
+        const TreeLayout& t = a.t;
+        for (u32 i = lane; i < L.total; i += 32) st4[i] = 0;
+        __syncwarp();
+        for (u32 i = lane; i < L.n1; i += 32) L1[i] = sat16(t.base[t.off[1] + i]);
+        for (u32 i = lane; i < L.n2; i += 32) L2[i] = t.H >= 2 ? sat16(t.base[t.off[2] + i]) : 0;
+        __syncwarp();
+        if (t.H < 2) {  // derive L2 / L3 from L1
+            for (u32 i = lane; i < L.n2; i += 32) {
+                u32 m = 0;
+                for (u32 k = 0; k < 32 && 32 * i + k < L.n1; ++k) m = max(m, static_cast<u32>(L1[32 * i + k]));
+                L2[i] = static_cast<unsigned short>(m);
+            }
+        }
+        __syncwarp();
+        for (u32 i = lane; i < L.n3; i += 32) {
+            u32 m = 0;
+            for (u32 k = 0; k < 32 && 32 * i + k < L.n2; ++k) m = max(m, static_cast<u32>(L2[32 * i + k]));
+            L3[i] = static_cast<unsigned short>(m);
+        }
+        s_tag[lane] = kNone;
+        __syncwarp();
+    }
+    auto root = [&]() -> u32 {
+        u32 m = max(max(L3[lane], L3[lane + 32]), max(L3[lane + 64], L3[lane + 96]));
+        return __reduce_max_sync(0xffffffffu, m);
+    };
+    // descend into L3 entry i3 / L2 entry i2 to the first chunk >= q
+    auto down_from_l2 = [&](u32 i2, u32 q) -> u32 {
+        const unsigned m1 = __ballot_sync(0xffffffffu, L1[32 * i2 + lane] >= q);
+        return 32 * i2 + (__ffs(m1) - 1);
+    };
+    auto down_from_l3 = [&](u32 i3, u32 q) -> u32 {
+        const unsigned m2 = __ballot_sync(0xffffffffu, L2[32 * i3 + lane] >= q);
+        return down_from_l2(32 * i3 + (__ffs(m2) - 1), q);
+    };
+    // first L3 entry > after (after = -1: any) with max >= q, or kNone
+    auto scan_l3 = [&](int after, u32 q) -> u32 {
+#pragma unroll
+        for (int part = 0; part < 4; ++part) {
+            const int idx = part * 32 + static_cast<int>(lane);
+            const unsigned m = __ballot_sync(0xffffffffu, idx > after && L3[idx] >= q);
+            if (m) return static_cast<u32>(part * 32 + __ffs(m) - 1);
+        }
+        return kNone;
+    };
+    // smallest chunk >= j with max >= q
+    auto find_next = [&](u32 j, u32 q) -> u32 {
+        if (j >= L.n1) return kNone;
+        const u32 b1 = j & ~31u;
+        const unsigned m1 = __ballot_sync(0xffffffffu, L1[b1 + lane] >= q && b1 + lane >= j);
+        if (m1) return b1 + (__ffs(m1) - 1);
+        const u32 j2 = (j >> 5) + 1;
+        const u32 b2 = (j2 & ~31u);
+        if (j2 < L.n2 && (j2 & 31u)) {
+            const unsigned m2 = __ballot_sync(0xffffffffu, L2[b2 + lane] >= q && b2 + lane >= j2);
+            if (m2) return down_from_l2(b2 + (__ffs(m2) - 1), q);
+        }
+        const u32 i3 = scan_l3(static_cast<int>((j2 + 31) / 32) - 1, q);
+        return i3 == kNone ? kNone : down_from_l3(i3, q);
+    };
+    auto find_first = [&](u32 q) -> u32 {
+        const u32 i3 = scan_l3(-1, q);
+        return i3 == kNone ? kNone : down_from_l3(i3, q);
+    };
+    // chunk j's max decreased to v
+    auto update_down = [&](u32 j, u32 v) {
+        const u32 old1 = L1[j];
+        const u32 n1 = v > kSat ? kSat : v;
+        if (old1 == n1) return;
+        if (lane == 0) L1[j] = static_cast<unsigned short>(n1);
+        __syncwarp();
+        const u32 p2 = j >> 5;
+        const u32 old2 = L2[p2];
+        if (old1 < old2) return;
+        const u32 m2 = __reduce_max_sync(0xffffffffu, static_cast<u32>(L1[32 * p2 + lane]));
+        if (m2 == old2) return;
+        if (lane == 0) L2[p2] = static_cast<unsigned short>(m2);
+        __syncwarp();
+        const u32 p3 = p2 >> 5;
+        const u32 old3 = L3[p3];
+        if (old2 < old3) return;
+        const u32 m3 = __reduce_max_sync(0xffffffffu, static_cast<u32>(L2[32 * p3 + lane]));
+        if (lane == 0) L3[p3] = static_cast<unsigned short>(m3);
+        __syncwarp();
+    };
+
+    u32 B = a.bins0;
+    u32 nrec = a.rec0;
+    bool overflow = false;
+    u32 win_base = a.run_begin;
+    u32 my_len = 0, my_item = 0;
+    auto load_window = [&](u32 base) {
+        win_base = base;
+        const u32 r = base + lane;
+        my_len = r < a.n_runs ? a.run_len[r] : 0u;
+        my_item = r < a.n_runs ? a.run_item[r] : a.n_items;
+    };
+    load_window(a.run_begin);
+    u32 rmax = root();
+
+    for (u32 k = a.run_begin; k < a.n_runs; ++k) {
+        if (k - win_base == 32) load_window(k);
+        const unsigned wl = k - win_base;
+        const u32 s = __shfl_sync(0xffffffffu, my_len, wl);
+        u32 item = __shfl_sync(0xffffffffu, my_item, wl);
+        const u32 nxt = __shfl_sync(0xffffffffu, my_item, wl < 31 ? wl + 1 : 31);
+        const u32 end_item = wl < 31 ? nxt : ((k + 1 < a.n_runs) ? a.run_item[k + 1] : a.n_items);
+        u32 c = end_item - item;
+        const u32 q = s > kSat ? kSat : s;
+
+        if (B > 0 && rmax >= q) {
+            u32 pos = 0;
+            bool first = true;
+            while (c > 0) {
+                // candidates with distinct cache slots, in chunk order
+                const u32 K = c < 32 ? c : 32u;
+                u32 ncand = 0, used_slots = 0;
+                bool stop = false;
+                while (ncand < K && !stop) {
+                    const u32 j = first ? find_first(q) : find_next(pos, q);
+                    first = false;
+                    if (j == kNone) break;
+                    const u32 b1 = j & ~31u;
+                    const unsigned m = __ballot_sync(0xffffffffu, L1[b1 + lane] >= q && b1 + lane >= j);
+                    // take candidates in order while slots stay distinct
+                    unsigned mm = m;
+                    while (mm && ncand < K) {
+                        const u32 cj = b1 + (__ffs(mm) - 1);
+                        const u32 slot = cj & 31u;
+                        if (used_slots & (1u << slot)) {
+                            stop = true;
+                            break;
+                        }
+                        used_slots |= 1u << slot;
+                        if (lane == 0) s_cand[ncand] = cj;
+                        ++ncand;
+                        mm &= mm - 1;
+                        pos = cj + 1;
+                    }
+                    if (!mm && !stop) pos = b1 + 32;
+                }
+                __syncwarp();
+                if (ncand == 0) break;
+                // fill misses with cp.async (hits are already in s_cache)
+                bool any_miss = false;
+                for (u32 qq = 0; qq < ncand; ++qq) {
+                    const u32 cj = s_cand[qq];
+                    const u32 slot = cj & 31u;
+                    if (s_tag[slot] != cj) {
+                        any_miss = true;
+                        const u64 li = static_cast<u64>(cj) * 32 + lane;
+                        if (li < a.max_bins) cp_async8(&s_cache[slot][lane], &a.leaves[li]);
+                        else s_cache[slot][lane] = 0ull;
+                    }
+                }
+                if (any_miss) cp_async_wait_all();
+                __syncwarp();
+                if (lane < ncand) s_tag[s_cand[lane] & 31u] = s_cand[lane];
+                __syncwarp();
+                for (u32 qq = 0; qq < ncand && c > 0; ++qq) {
+                    const u32 cj = s_cand[qq];
+                    const u32 slot = cj & 31u;
+                    const u64 leaf = s_cache[slot][lane];
+                    const u32 res = static_cast<u32>(leaf >> 32);
+                    const bool elig = res >= s;
+                    const unsigned em = __ballot_sync(0xffffffffu, elig);
+                    if (!em) continue;
+                    const u32 capl = elig ? res / s : 0u;
+                    u32 incl;
+                    if ((em & (em - 1)) == 0) {  // one eligible lane: no scan needed
+                        const int f = __ffs(em) - 1;
+                        const u32 only = __shfl_sync(0xffffffffu, capl, f);
+                        incl = static_cast<int>(lane) >= f ? only : 0u;
+                    } else {
+                        incl = warp_inclusive_scan(capl);
+                    }
+                    const u32 excl = incl - capl;
+                    const u32 take = excl >= c ? 0u : (capl < c - excl ? capl : c - excl);
+                    const unsigned tm = __ballot_sync(0xffffffffu, take > 0);
+                    u32 nres = res;
+                    if (take > 0) {
+                        const u32 ri = nrec + __popc(tm & lt);
+                        if (ri < a.max_records) {
+                            a.rec.item[ri] = item + excl;
+                            a.rec.count[ri] = take;
+                            a.rec.bin[ri] = cj * 32 + lane;
+                            a.rec.per_bin[ri] = take;
+                            a.rec.slot0[ri] = static_cast<u32>(leaf);
+                        }
+                        nres = res - take * s;
+                        const u64 nl = (static_cast<u64>(nres) << 32) | (static_cast<u32>(leaf) + take);
+                        s_cache[slot][lane] = nl;
+                        a.leaves[static_cast<u64>(cj) * 32 + lane] = nl;
+                    }
+                    const u32 used = __shfl_sync(0xffffffffu, incl, 31);
+                    const u32 got = used < c ? used : c;
+                    nrec += __popc(tm);
+                    c -= got;
+                    item += got;
+                    if (tm) update_down(cj, __reduce_max_sync(0xffffffffu, nres));
+                }
+                __syncwarp();
+            }
+            rmax = root();
+        }
+        if (c > 0 && a.ffd) {
+            const u32 per = a.cap / s;
+            const u32 nb = (c + per - 1) / per;
+            if (static_cast<u64>(B) + nb > a.max_bins) {
+                overflow = true;
+                break;
+            }
+            if (nrec < a.max_records && lane == 0) {
+                a.rec.item[nrec] = item;
+                a.rec.count[nrec] = c;
+                a.rec.bin[nrec] = B;
+                a.rec.per_bin[nrec] = per;
+                a.rec.slot0[nrec] = 0;
+            }
+            ++nrec;
+            const u32 res_full = a.cap - per * s;
+            const u32 last_cnt = c - (nb - 1) * per;
+            const u32 res_last = a.cap - last_cnt * s;
+            for (u32 b = lane; b < nb; b += 32) {
+                const bool last = (b == nb - 1);
+                a.leaves[B + b] = (static_cast<u64>(last ? res_last : res_full) << 32) | (last ? last_cnt : per);
+            }
+            const u32 lo = B, hi = B + nb - 1;
+            const u32 full_hi = nb > 1 ? hi - 1 : lo;
+            // cached chunks overlapping the new range are stale
+            if (s_tag[lane] != kNone && s_tag[lane] >= (lo >> 5) && s_tag[lane] <= (hi >> 5)) s_tag[lane] = kNone;
+            auto raise = [&](unsigned short* Lv, int shift) {
+                const u32 ilo = lo >> shift, ihi = hi >> shift;
+                for (u32 i = ilo + lane; i <= ihi; i += 32) {
+                    const u32 slo = i << shift, shi = ((i + 1) << shift) - 1;
+                    u32 val = Lv[i];
+                    if (nb > 1 && slo <= full_hi && shi >= lo) val = max(val, res_full);
+                    if (slo <= hi && shi >= hi) val = max(val, res_last);
+                    Lv[i] = static_cast<unsigned short>(val > kSat ? kSat : val);
+                }
+                __syncwarp();
+            };
+            raise(L1, 5);
+            raise(L2, 10);
+            raise(L3, 15);
+            rmax = max(rmax, min(kSat, max(nb > 1 ? res_full : 0u, res_last)));
+            B += nb;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        a.out[0] = B;
+        a.out[1] = nrec;
+        a.out[2] = (overflow || nrec > a.max_records) ? 1u : 0u;
+    }
+}
+
 __global__ void k_expand(FitRecords rec, const u32* __restrict__ nrec_p, u64 n_items, u32* __restrict__ item_bin,
                          u32* __restrict__ item_slot) {
     const u32 nrec = *nrec_p;
@@ -669,7 +967,15 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     }
     const size_t smem = sizeof(unsigned short) * t.off[0];
     constexpr size_t kSmemLimit = 216 * 1024;  // + 8.4 KB static (candidates, leaf stage) <= 227 KB
-    if (smem <= kSmemLimit && !std::getenv("HBP_ENGINE_V1")) {
+    const V4Layout vl = make_v4(static_cast<u64>(tree_bins));
+    const size_t smem4 = sizeof(unsigned short) * vl.total;
+    const char* eng = std::getenv("HBP_ENGINE");
+    const bool force_v3 = eng && std::string(eng) == "v3", force_v1 = eng && std::string(eng) == "v1";
+    if (vl.n3 <= 128 && smem4 <= kSmemLimit && !force_v3 && !force_v1) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_v4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kSmemLimit)));
+        LAUNCH_B("fit.engine", 0.0, k_fit_engine_v4, 1, 32, smem4, s, a, vl);
+    } else if (smem <= kSmemLimit && !force_v1) {
         CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kSmemLimit)));
         LAUNCH_B("fit.engine", 0.0, k_fit_engine_smem, 1, 32, smem, s, a);

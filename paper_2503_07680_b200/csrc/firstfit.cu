@@ -664,6 +664,10 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
     };
     load_window(a.run_begin);
     u32 rmax = root();
+    // cycle counters (HBP_TRACE): 0 collect 1 load 2 process 3 new bins 4 searched runs 5 candidates 6 rounds 7 misses
+    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const bool prof = a.prof != nullptr;
+    long long t0 = 0;
 
     for (u32 k = a.run_begin; k < a.n_runs; ++k) {
         if (k - win_base == 32) load_window(k);
@@ -678,7 +682,10 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
         if (B > 0 && rmax >= q) {
             u32 pos = 0;
             bool first = true;
+            pc[4] += 1;
             while (c > 0) {
+                if (prof) t0 = clock64();
+                pc[6] += 1;
                 // candidates with distinct cache slots, in chunk order
                 const u32 K = c < 32 ? c : 32u;
                 u32 ncand = 0, used_slots = 0;
@@ -707,7 +714,13 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
                     if (!mm && !stop) pos = b1 + 32;
                 }
                 __syncwarp();
+                if (prof) {
+                    const long long t1 = clock64();
+                    pc[0] += t1 - t0;
+                    t0 = t1;
+                }
                 if (ncand == 0) break;
+                pc[5] += ncand;
                 // fill misses with cp.async (hits are already in s_cache)
                 bool any_miss = false;
                 for (u32 qq = 0; qq < ncand; ++qq) {
@@ -715,6 +728,7 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
                     const u32 slot = cj & 31u;
                     if (s_tag[slot] != cj) {
                         any_miss = true;
+                        pc[7] += 1;
                         const u64 li = static_cast<u64>(cj) * 32 + lane;
                         if (li < a.max_bins) cp_async8(&s_cache[slot][lane], &a.leaves[li]);
                         else s_cache[slot][lane] = 0ull;
@@ -724,6 +738,11 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
                 __syncwarp();
                 if (lane < ncand) s_tag[s_cand[lane] & 31u] = s_cand[lane];
                 __syncwarp();
+                if (prof) {
+                    const long long t1 = clock64();
+                    pc[1] += t1 - t0;
+                    t0 = t1;
+                }
                 for (u32 qq = 0; qq < ncand && c > 0; ++qq) {
                     const u32 cj = s_cand[qq];
                     const u32 slot = cj & 31u;
@@ -767,9 +786,11 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
                     if (tm) update_down(cj, __reduce_max_sync(0xffffffffu, nres));
                 }
                 __syncwarp();
+                if (prof) pc[2] += clock64() - t0;
             }
             rmax = root();
         }
+        if (prof) t0 = clock64();
         if (c > 0 && a.ffd) {
             const u32 per = a.cap / s;
             const u32 nb = (c + per - 1) / per;
@@ -813,12 +834,15 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
             rmax = max(rmax, min(kSat, max(nb > 1 ? res_full : 0u, res_last)));
             B += nb;
         }
+        if (prof) pc[3] += clock64() - t0;
         __syncwarp();
     }
     if (lane == 0) {
         a.out[0] = B;
         a.out[1] = nrec;
         a.out[2] = (overflow || nrec > a.max_records) ? 1u : 0u;
+        if (prof)
+            for (int i = 0; i < 8; ++i) a.prof[i] = pc[i];
     }
 }
 
@@ -988,9 +1012,9 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         const auto pc = read_vector(c, prof.p, 8);
         std::fprintf(stderr,
                      "[hbp trace] fit %s: runs %u (from %u) bins %u tree_bins %lld H %d | collect %.2fM load %.2fM "
-                     "process %.2fM newbins %.2fM cycles | searched %llu cands %llu rounds %llu\n",
+                     "process %.2fM newbins %.2fM cycles | searched %llu cands %llu rounds %llu misses %llu\n",
                      ffd ? "ffd" : "fill", n_runs, run_begin, o[0], static_cast<long long>(tree_bins), t.H,
-                     pc[0] / 1e6, pc[1] / 1e6, pc[2] / 1e6, pc[3] / 1e6, pc[4], pc[5], pc[6]);
+                     pc[0] / 1e6, pc[1] / 1e6, pc[2] / 1e6, pc[3] / 1e6, pc[4], pc[5], pc[6], pc[7]);
     }
     out.bins = o[0];
     out.records = o[1];

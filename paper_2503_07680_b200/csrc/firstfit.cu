@@ -995,9 +995,12 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     const size_t smem4 = sizeof(unsigned short) * vl.total;
     const char* eng = std::getenv("HBP_ENGINE");
     const bool force_v3 = eng && std::string(eng) == "v3", force_v1 = eng && std::string(eng) == "v1";
-    if (vl.n3 <= 128 && smem4 <= kSmemLimit && !force_v3 && !force_v1) {
+    cudaFuncAttributes fa4{};
+    CUDA_CHECK(cudaFuncGetAttributes(&fa4, k_fit_engine_v4));
+    const size_t limit4 = 227 * 1024 - fa4.sharedSizeBytes;  // dynamic + static <= 227 KB per CTA
+    if (vl.n3 <= 128 && smem4 <= limit4 && !force_v3 && !force_v1) {
         CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_v4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kSmemLimit)));
+                                        static_cast<int>(limit4)));
         LAUNCH_B("fit.engine", 0.0, k_fit_engine_v4, 1, 32, smem4, s, a, vl);
     } else if (smem <= kSmemLimit && !force_v1) {
         CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,

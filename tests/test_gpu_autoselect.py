@@ -127,3 +127,27 @@ def test_sweep_matches_oracle(ctx, oracle):
     assert np.array_equal(np.isinf(got[0]), np.isinf(want[0]))
     fin = np.isfinite(want[0])
     assert np.allclose(got[0][fin], want[0][fin], rtol=1e-12, atol=0)
+
+
+def test_c3_candidates_and_sharded_sweep(ctx, oracle):
+    from paper_2503_07680_b200 import sweep
+    L = np.maximum(oracle.synth(20_000, "lognormal:8.5:1.4", 0.0, "", 131072, 42), 128)
+    cands = sweep.make_candidates(ctx, 131072, [2048, 8192, 32768], [1, 2, 4, 8])
+    assert len(cands) == 8 * 4 * 2
+    an = abi.analytic_profiler()
+    for groups, _ in cands:  # GC-on ckpt values are the reference profiler's
+        for (l, sp, ck) in groups:
+            assert ck == 0 or ck == oracle.derive_ckpt(an, l, sp)
+    s, keep = abi.make_samples(None, L)
+    want, wbest = oracle.sweep(None, L, cands, device_count=8, seed=7)
+    merged = {}
+    for rank in range(3):  # three "ranks" on one GPU: shards cover everything once
+        secs, _ = sweep.run_sweep(ctx, s, cands, rank, 3, None, device_count=8, seed=7)
+        assert not (set(secs) & set(merged))
+        merged.update(secs)
+    got = np.array([merged[i] for i in range(len(cands))])
+    assert np.array_equal(np.isinf(got), np.isinf(want))
+    fin = np.isfinite(want)
+    assert np.allclose(got[fin], want[fin], rtol=1e-12, atol=0)
+    best = min((v, i) for i, v in merged.items() if np.isfinite(v))
+    assert best[1] == wbest

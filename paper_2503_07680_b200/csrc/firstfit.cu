@@ -21,6 +21,7 @@
 // parallel kernel before the walk. Output is a compact record list expanded
 // to per-item (bin, slot) by a parallel kernel.
 #include "stages.cuh"
+#include "radix.cuh"
 
 namespace hbp_b200 {
 
@@ -100,6 +101,7 @@ struct EngineArgs {
     const u32* run_len;
     u32 n_runs;
     u32 run_begin;
+    u32 run_end;  // runs [run_begin, run_end) are processed
     u64* leaves;
     TreeLayout t;
     u32 bins0;
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(32) k_fit_engine(EngineArgs a) {
         }
     };
 
-    for (u32 k = a.run_begin; k < a.n_runs; ++k) {
+    for (u32 k = a.run_begin; k < a.run_end; ++k) {
         const u32 s = a.run_len[k];
         u32 item = a.run_item[k];
         const u32 end_item = (k + 1 < a.n_runs) ? a.run_item[k + 1] : a.n_items;
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(32) k_fit_engine_smem(EngineArgs a) {
     long long t0 = 0;
     const bool prof = a.prof != nullptr;
 
-    for (u32 k = a.run_begin; k < a.n_runs; ++k) {
+    for (u32 k = a.run_begin; k < a.run_end; ++k) {
         if (k - win_base == 32) load_window(k);
         const unsigned wl = k - win_base;
         const u32 s = __shfl_sync(0xffffffffu, my_len, wl);
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(32) k_fit_engine_v4(EngineArgs a, V4Layout L) 
     const bool prof = a.prof != nullptr;
     long long t0 = 0;
 
-    for (u32 k = a.run_begin; k < a.n_runs; ++k) {
+    for (u32 k = a.run_begin; k < a.run_end; ++k) {
         if (k - win_base == 32) load_window(k);
         const unsigned wl = k - win_base;
         const u32 s = __shfl_sync(0xffffffffu, my_len, wl);
@@ -873,7 +875,210 @@ __global__ void k_expand(FitRecords rec, const u32* __restrict__ nrec_p, u64 n_i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fill mode, consuming runs in parallel.
+//
+// While no length runs out, greedy fill is bin-independent: a pack with
+// residual r takes floor(r / L) samples of the largest pool length L <= r,
+// then continues with r mod L, and so on. Every pack computes that
+// trajectory on its own thread against the remaining runs; per run, the
+// demand is compared with the run's count. Runs before the first
+// over-subscribed ("scarce") run are exact and committed in parallel:
+// records sorted (run, pack) give each pick its item offset. The scarce
+// region goes to the sequential engine, then the next parallel pass starts.
+// ---------------------------------------------------------------------------
+
+// first run index in [lo, hi) with run_len <= r (run_len is decreasing)
+__device__ __forceinline__ u32 first_run_le(const u32* __restrict__ run_len, u32 lo, u32 hi, u32 r) {
+    while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (run_len[mid] <= r) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+template <bool EMIT>
+__global__ void k_traj(const u64* __restrict__ leaves, u32 P, const u32* __restrict__ run_len, u32 pos, u32 n_runs,
+                       u32* __restrict__ npick, const u64* __restrict__ off, u32* __restrict__ r_run,
+                       u32* __restrict__ r_take, u32* __restrict__ r_slot0, u32* __restrict__ r_after,
+                       unsigned long long* __restrict__ demand) {
+    for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b < P; b += gridDim.x * blockDim.x) {
+        const u64 leaf = leaves[b];
+        u32 r = static_cast<u32>(leaf >> 32);
+        u32 cnt = static_cast<u32>(leaf);
+        u32 k = pos, n = 0;
+        u64 o = EMIT ? off[b] : 0;
+        while (r > 0) {
+            k = first_run_le(run_len, k, n_runs, r);
+            if (k >= n_runs) break;
+            const u32 L = run_len[k];
+            const u32 t = r / L;
+            r -= t * L;
+            if (EMIT) {
+                r_run[o + n] = k;
+                r_take[o + n] = t;
+                r_slot0[o + n] = cnt;
+                r_after[o + n] = r;
+                atomicAdd(&demand[k], static_cast<unsigned long long>(t));
+            }
+            cnt += t;
+            ++n;
+            ++k;
+        }
+        if (!EMIT) npick[b] = n;
+    }
+}
+
+__global__ void k_scarce(const unsigned long long* __restrict__ demand, const u32* __restrict__ run_item, u32 pos,
+                         u32 n_runs, u32 n_items, u8* __restrict__ scarce, u32* __restrict__ kstar) {
+    for (u32 k = pos + blockIdx.x * blockDim.x + threadIdx.x; k < n_runs; k += gridDim.x * blockDim.x) {
+        const u32 count = (k + 1 < n_runs ? run_item[k + 1] : n_items) - run_item[k];
+        const bool sc = demand[k] > count;
+        scarce[k] = sc;
+        if (sc) atomicMin(kstar, k);
+    }
+}
+
+// bin-major records: valid = run < kstar; a pack's last valid record
+// carries its final state into the leaf
+__global__ void k_traj_commit_leaves(u32 P, const u64* __restrict__ off, const u32* __restrict__ npick,
+                                     const u32* __restrict__ r_run, const u32* __restrict__ r_take,
+                                     const u32* __restrict__ r_slot0, const u32* __restrict__ r_after,
+                                     const u32* __restrict__ kstar_p, u64* __restrict__ leaves,
+                                     u32* __restrict__ sort_key, u32 n_runs) {
+    const u32 kstar = *kstar_p;
+    for (u32 b = blockIdx.x * blockDim.x + threadIdx.x; b < P; b += gridDim.x * blockDim.x) {
+        const u64 o = off[b];
+        const u32 n = npick[b];
+        u32 last = kNone;
+        for (u32 i = 0; i < n; ++i) {
+            const bool valid = r_run[o + i] < kstar;
+            sort_key[o + i] = valid ? r_run[o + i] : n_runs;
+            if (valid) last = i;
+        }
+        if (last != kNone)
+            leaves[b] = (static_cast<u64>(r_after[o + last]) << 32) | (r_slot0[o + last] + r_take[o + last]);
+    }
+}
+
+__device__ __forceinline__ u32 bin_of_record(const u64* __restrict__ off, u32 P, u64 i) {
+    // last pack b with off[b] <= i
+    u32 lo = 0, hi = P;
+    while (lo + 1 < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (off[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_traj_first_of_run(const u32* __restrict__ sorted_idx, const u32* __restrict__ r_run, u64 V,
+                                    const u64* __restrict__ take_scan, u64* __restrict__ run_base) {
+    for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < V;
+         j += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 run = r_run[sorted_idx[j]];
+        if (j == 0 || r_run[sorted_idx[j - 1]] != run) run_base[run] = take_scan[j];
+    }
+}
+
+__global__ void k_traj_records(const u32* __restrict__ sorted_idx, u64 V, const u64* __restrict__ off, u32 P,
+                               const u32* __restrict__ r_run, const u32* __restrict__ r_take,
+                               const u32* __restrict__ r_slot0, const u64* __restrict__ take_scan,
+                               const u64* __restrict__ run_base, const u32* __restrict__ run_item, FitRecords rec,
+                               u32 rec_base) {
+    for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < V;
+         j += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 i = sorted_idx[j];
+        const u32 run = r_run[i];
+        const u32 t = r_take[i];
+        const u64 r = rec_base + j;
+        rec.item[r] = run_item[run] + static_cast<u32>(take_scan[j] - run_base[run]);
+        rec.count[r] = t;
+        rec.bin[r] = bin_of_record(off, P, i);
+        rec.per_bin[r] = t;
+        rec.slot0[r] = r_slot0[i];
+    }
+}
+
 }  // namespace
+
+// One parallel pass from run `pos`: commits every run before the first
+// scarce one; returns that run index (n_runs when none) and the scarce flags.
+static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, const u32* run_item, u32 pos,
+                              u32 n_runs, u32 n_items, FitRecords rec, u32& nrec, u32 max_records,
+                              std::vector<u8>& scarce_host) {
+    cudaStream_t s = c.stream;
+    DevBuf<u32> npick(P + 1, s);
+    DevBuf<u64> off(P + 1, s);
+    LAUNCH(k_traj<false>, grid_for(P, 256, 148u * 16u), 256, 0, s, leaves, P, run_len, pos, n_runs, npick.p, nullptr,
+           nullptr, nullptr, nullptr, nullptr, nullptr);
+    {
+        const u32* np = npick.p;
+        u64* op = off.p;
+        const i64 PP = P;
+        scan_exclusive<u64>(
+            PP + 1, [=] __device__(i64 i) { return i < PP ? static_cast<u64>(np[i]) : 0ull; },
+            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan);
+    }
+    const u64 R = read_vector(c, off.p + P, 1)[0];
+    DevBuf<unsigned long long> demand(n_runs + 1, s);
+    demand.zero();
+    DevBuf<u32> r_run(R + 1, s), r_take(R + 1, s), r_slot0(R + 1, s), r_after(R + 1, s);
+    if (R > 0)
+        LAUNCH(k_traj<true>, grid_for(P, 256, 148u * 16u), 256, 0, s, leaves, P, run_len, pos, n_runs, npick.p, off.p,
+               r_run.p, r_take.p, r_slot0.p, r_after.p, demand.p);
+    DevBuf<u8> scarce(n_runs + 1, s);
+    DevBuf<u32> kstar(1, s);
+    CUDA_CHECK(cudaMemcpyAsync(kstar.p, &n_runs, 4, cudaMemcpyHostToDevice, s));
+    LAUNCH(k_scarce, grid_for(n_runs - pos, 256, 148u * 16u), 256, 0, s, demand.p, run_item, pos, n_runs, n_items,
+           scarce.p, kstar.p);
+    const u32 ks = read_scalar(c, kstar.p);
+    scarce_host.assign(n_runs, 0);
+    if (n_runs > pos)
+        CUDA_CHECK(cudaMemcpyAsync(scarce_host.data() + pos, scarce.p + pos, n_runs - pos, cudaMemcpyDeviceToHost, s));
+    if (ks == pos || R == 0) {
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        return ks;
+    }
+    // commit runs [pos, ks)
+    DevBuf<u32> key(R, s), idx(R, s);
+    LAUNCH(k_traj_commit_leaves, grid_for(P, 256, 148u * 16u), 256, 0, s, P, off.p, npick.p, r_run.p, r_take.p,
+           r_slot0.p, r_after.p, kstar.p, leaves, key.p, n_runs);
+    for_each_index(c, R, [ip = idx.p] __device__(u64 i) { ip[i] = static_cast<u32>(i); });
+    int bits = 1;
+    while (bits < 32 && (static_cast<u64>(n_runs) >> bits) != 0) ++bits;
+    radix_sort_pairs(c, key.p, idx.p, static_cast<i64>(R), bits, false);
+    // valid records are the prefix with key < ks
+    DevBuf<u64> take_scan(R + 1, s), run_base(n_runs + 1, s), vcount(1, s);
+    {
+        const u32* kp = key.p;
+        const u32* ip = idx.p;
+        const u32* tp = r_take.p;
+        u64* sp = take_scan.p;
+        u64* vc = vcount.p;
+        const i64 RR = static_cast<i64>(R);
+        const u32 kk = ks;
+        scan_exclusive<u64>(
+            RR, [=] __device__(i64 j) { return kp[j] < kk ? static_cast<u64>(tp[ip[j]]) : 0ull; },
+            [=] __device__(i64 j, u64 v) {
+                sp[j] = v;
+                if (kp[j] < kk && (j == RR - 1 || kp[j + 1] >= kk)) *vc = static_cast<u64>(j + 1);
+            },
+            s, c.scan);
+    }
+    const u64 V = read_scalar(c, vcount.p);
+    if (V > 0) {
+        if (nrec + V > max_records) throw EngineError(HBP_ERR_CUDA, "fill: record capacity exceeded");
+        LAUNCH(k_traj_first_of_run, grid_for(V, 256, 148u * 16u), 256, 0, s, idx.p, r_run.p, V, take_scan.p,
+               run_base.p);
+        LAUNCH(k_traj_records, grid_for(V, 256, 148u * 16u), 256, 0, s, idx.p, V, off.p, P, r_run.p, r_take.p,
+               r_slot0.p, take_scan.p, run_base.p, run_item, rec, nrec);
+        nrec += static_cast<u32>(V);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    return ks;
+}
 
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
                          FitMode mode, FitRecords rec, i64 max_records) {
@@ -998,7 +1203,57 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     cudaFuncAttributes fa4{};
     CUDA_CHECK(cudaFuncGetAttributes(&fa4, k_fit_engine_v4));
     const size_t limit4 = 227 * 1024 - fa4.sharedSizeBytes;  // dynamic + static <= 227 KB per CTA
-    if (vl.n3 <= 128 && smem4 <= limit4 && !force_v3 && !force_v1) {
+    const bool v4ok = vl.n3 <= 128 && smem4 <= limit4 && !force_v3 && !force_v1;
+    a.run_end = n_runs;
+    if (v4ok && !ffd && !std::getenv("HBP_NO_HYBRID")) {
+        // fill: parallel passes over the non-scarce runs, the engine over
+        // each scarce cluster (runs within kGap of a scarce run)
+        constexpr u32 kGap = 64;
+        CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_v4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(limit4)));
+        const u32 P = static_cast<u32>(live);
+        u32 nrec = rec0, pos = run_begin, passes = 0, engine_runs = 0;
+        // a pass costs about as much as the engine on ~kGap / 2 runs: when
+        // passes stop paying (few runs committed), hand the engine
+        // exponentially longer stretches
+        u32 stretch = kGap;
+        std::vector<u8> scarce;
+        while (pos < n_runs) {
+            const u32 ks = fill_parallel_pass(c, leaves, P, run_len.p, run_item.p, pos, n_runs, static_cast<u32>(n),
+                                              rec, nrec, static_cast<u32>(max_records), scarce);
+            ++passes;
+            if (ks >= n_runs) break;
+            if (ks - pos < kGap / 2) stretch = stretch * 2 < n_runs ? stretch * 2 : n_runs;
+            else stretch = kGap;
+            u32 last = ks;
+            for (u32 k = ks + 1; k < n_runs && k - last <= kGap; ++k)
+                if (scarce[k]) last = k;
+            u32 end = last + 1;
+            if (end - ks < stretch) end = ks + stretch < n_runs ? ks + stretch : n_runs;
+            CUDA_CHECK(cudaMemsetAsync(tree.p, 0, sizeof(u32) * t.off[0], s));
+            for (int h = 1; h <= t.H; ++h) {
+                const u64 hi = (live + (1ull << (5 * h)) - 1) >> (5 * h);
+                if (hi == 0) break;
+                LAUNCH(k_tree_level, grid_for(hi, 256, 148u * 16u), 256, 0, s, leaves, tree.p, t, h, 0ull, hi);
+            }
+            a.run_begin = ks;
+            a.run_end = end;
+            a.rec0 = nrec;
+            LAUNCH_B("fit.engine", 0.0, k_fit_engine_v4, 1, 32, smem4, s, a, vl);
+            const auto o = read_vector(c, scal.p, 3);
+            if (o[2]) throw EngineError(HBP_ERR_CUDA, "first-fit engine: record or bin capacity exceeded");
+            nrec = o[1];
+            engine_runs += end - ks;
+            pos = end;
+        }
+        if (c.trace)
+            std::fprintf(stderr, "[hbp trace] fit fill (hybrid): runs %u bins %u passes %u engine runs %u records %u\n",
+                         n_runs, P, passes, engine_runs, nrec);
+        out.bins = live;
+        out.records = nrec;
+        return out;
+    }
+    if (v4ok) {
         CUDA_CHECK(cudaFuncSetAttribute(k_fit_engine_v4, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(limit4)));
         LAUNCH_B("fit.engine", 0.0, k_fit_engine_v4, 1, 32, smem4, s, a, vl);

@@ -51,6 +51,24 @@ int guarded(hbp_ctx* ctx, F&& fn) {
 
 }  // namespace
 
+struct hbp_plan {
+    DevicePlan dp;
+    hbp_plan_view view{};
+    hbp_ctx* owner = nullptr;
+};
+
+static hbp_plan* new_plan(hbp_ctx* ctx) {
+    auto* p = new hbp_plan();
+    p->owner = ctx;
+    ctx->plans.insert(p);
+    return p;
+}
+
+static void delete_plan(hbp_plan* p) {
+    if (p->owner) p->owner->plans.erase(p);
+    delete p;
+}
+
 extern "C" {
 
 void hbp_hardware_profile_defaults(hbp_hardware_profile* p) {
@@ -98,6 +116,11 @@ void hbp_ctx_destroy(hbp_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) {
         cudaStreamSynchronize(ctx->stream);
+        for (hbp_plan* p : ctx->plans) {  // outliving plans keep their host view only
+            p->dp.release_device();
+            p->owner = nullptr;
+        }
+        ctx->plans.clear();
         ctx->scan.status.release();
         ctx->scan.counter.release();
         cudaStreamSynchronize(ctx->stream);
@@ -196,11 +219,6 @@ int hbp_group_data(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* g
     });
 }
 
-struct hbp_plan {
-    DevicePlan dp;
-    hbp_plan_view view{};
-};
-
 int hbp_pack(hbp_ctx* ctx, const hbp_samples* samples, int64_t capacity, const hbp_strategy* strategy, uint64_t seed,
              hbp_plan** out) {
     return guarded(ctx, [&] {
@@ -209,12 +227,12 @@ int hbp_pack(hbp_ctx* ctx, const hbp_samples* samples, int64_t capacity, const h
         if (capacity < 1) fail_validation("pack capacity must be >= 1");
         DeviceCorpus corpus;
         ingest(*ctx, samples, corpus);
-        auto* p = new hbp_plan();
+        auto* p = new_plan(ctx);
         try {
             pack_device(*ctx, corpus, capacity, *strategy, seed, p->dp);
             p->dp.seed = seed;
         } catch (...) {
-            delete p;
+            delete_plan(p);
             throw;
         }
         *out = p;
@@ -239,12 +257,12 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* g
         a.balance_batching = options->balance_batching != 0;
         a.greedy_fill = options->greedy_fill != 0;
         a.seed = options->seed;
-        auto* p = new hbp_plan();
+        auto* p = new_plan(ctx);
         try {
             build_plan_device(*ctx, corpus, a, p->dp);
             trace_dump(*ctx, "build_plan");
         } catch (...) {
-            delete p;
+            delete_plan(p);
             throw;
         }
         *out = p;
@@ -270,14 +288,14 @@ int hbp_balance_batching(hbp_ctx* ctx, const hbp_packs_in* packs, int64_t capaci
     return guarded(ctx, [&] {
         *out = nullptr;
         if (device_count < 1) fail_validation("device count must be >= 1");
-        auto* p = new hbp_plan();
+        auto* p = new_plan(ctx);
         try {
             batching_device(*ctx, capacity, packs->n_packs, packs->pack_capacity, packs->pack_offsets, packs->ids,
                             packs->lengths, device_count, group_index, random_batching != 0, seed, p->dp);
             p->dp.groups.assign(static_cast<size_t>(group_index) + 1, hbp_group_config{capacity, 1, 0});
             p->dp.l_max = capacity;
         } catch (...) {
-            delete p;
+            delete_plan(p);
             throw;
         }
         *out = p;
@@ -313,7 +331,9 @@ int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out) {
     });
 }
 
-void hbp_plan_free(hbp_plan* plan) { delete plan; }
+void hbp_plan_free(hbp_plan* plan) {
+    if (plan) delete_plan(plan);
+}
 
 namespace {
 

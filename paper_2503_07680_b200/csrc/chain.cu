@@ -1,0 +1,347 @@
+// chain.cu — first fit as a systolic chain of bins.
+//
+// First fit (packing.cpp:55-60) puts item j into the lowest-index bin with
+// room. Seen from a bin: bin b receives exactly the items that bins 0..b-1
+// did not take, in item order, and takes each one that fits its current
+// residual. So the bins form a pipeline through which the item sequence
+// flows, and bin b's decisions depend only on what reached it. FFD's "open a
+// new bin" is the same rule applied to the empty bins after the open ones
+// (residual = capacity), and greedy fill (balance.cpp:62-101, in the (length
+// desc, id asc) order of first_fit_runs) is the chain without empty bins.
+//
+// Items travel as runs of equal length: run k with c items still unplaced
+// reaches a bin with residual r, which takes min(c, floor(r / s)) of them --
+// the lowest ids left -- and passes the rest on. Warp j owns 32 * M
+// consecutive bins (lane l holds bins j*32M + l*M + i, i < M, in registers).
+// Per block of 32 runs it receives the 32 counts its predecessor left,
+// marks the runs its bins can take (c > 0 and s <= its max residual), serves
+// those in order with one warp scan each, and passes the 32 remaining counts
+// on. Every warp is resident (cooperative launch), so after the chain fills
+// all bins work on different run blocks at once.
+//
+// Hand-off: each count travels as one 64-bit word (block tag << 32 | count)
+// that the consumer lane polls, so no flag or fence sits on the path --
+// through shared memory between the warps of a CTA, through global memory
+// (L2) from the last warp of a CTA to the first of the next. Consumers
+// publish how many blocks they have read so that producers never overwrite
+// an unread slot (ring of kQ blocks). Items are written straight to
+// (bin, slot); bin counts give the slots.
+#include "stages.cuh"
+
+namespace hbp_b200 {
+
+namespace {
+
+constexpr int kQ = 8;          // global ring depth per link, in blocks of 32 runs
+constexpr int kQs = 4;         // shared-memory ring depth
+constexpr int kWarps = 32;     // warps per CTA (one CTA per SM)
+constexpr u32 kStride = 32;    // u32 between global consumer counters (one 128 B line each)
+
+struct ChainArgs {
+    const u32* run_item;
+    const u32* run_len;
+    u32 n_items, n_runs, run_begin, run_end;
+    u64* leaves;
+    u32 live, n_bins, cap;
+    int ffd;
+    u32 J, nblocks;
+    unsigned long long* gring;  // CTA g -> g+1: kQ * 32 tagged counts
+    u32* gcons;                 // gcons[(g+1) * kStride]: blocks CTA g+1's first warp has read
+    u32* item_bin;   // heads only: at the first item of each take
+    u32* item_slot;
+    u32* take;       // items in the take starting here (0: not a head)
+    u32* out;                  // [0] 1 + highest bin with items, [1] FFD overflow
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u32 ld_relaxed_u32(const u32* p) {
+    u32 v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(u32* p, u32 v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int M>
+__global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
+    __shared__ unsigned long long s_ring[kWarps][kQs][32];  // warp w-1 -> w
+    __shared__ u32 s_cons[kWarps];                         // blocks warp w has read from s_ring[w]
+    const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const u32 g = blockIdx.x;
+    const u32 j = g * kWarps + w;
+    for (u32 i = threadIdx.x; i < kWarps * kQs * 32; i += blockDim.x) (&s_ring[0][0][0])[i] = 0ull;
+    if (threadIdx.x < kWarps) s_cons[threadIdx.x] = 0;
+    __syncthreads();
+    if (j >= a.J) return;  // no CTA-wide barriers below
+
+    const u64 first_bin = (static_cast<u64>(j) * 32 + lane) * M;
+    u32 R[M], N[M];
+    u32 lmax = 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const u64 bin = first_bin + i;
+        u64 leaf = 0;
+        if (bin < a.live) leaf = a.leaves[bin];
+        else if (a.ffd && bin < a.n_bins) leaf = static_cast<u64>(a.cap) << 32;
+        R[i] = static_cast<u32>(leaf >> 32);
+        N[i] = static_cast<u32>(leaf);
+        lmax = max(lmax, R[i]);
+    }
+    u32 wmax = __reduce_max_sync(0xffffffffu, lmax);
+    const bool head = j == 0, tail = j + 1 == a.J;
+    const bool in_global = w == 0, out_global = w + 1 == kWarps;
+    volatile unsigned long long* sin = s_ring[w][0];
+    volatile unsigned long long* sout = w + 1 < kWarps ? s_ring[w + 1][0] : nullptr;
+    const unsigned long long* gin = a.gring + static_cast<u64>(g) * kQ * 32;  // written by CTA g-1
+    unsigned long long* gout = a.gring + static_cast<u64>(g + 1) * kQ * 32;
+    u32 seen_cons = 0;  // consumer progress known to this producer
+
+    // run data of block b, prefetched one block ahead
+    auto load_runs = [&](u32 b, u32& s, u32& e, u32& st) {
+        const u32 k = a.run_begin + b * 32 + lane;
+        const bool valid = b < a.nblocks && k < a.run_end;
+        s = valid ? a.run_len[k] : 0u;
+        st = valid ? a.run_item[k] : 0u;
+        e = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
+    };
+    u32 s_n, e_n, st_n;
+    load_runs(0, s_n, e_n, st_n);
+
+    for (u32 b = 0; b < a.nblocks; ++b) {
+        const u32 s = s_n, end_item = e_n, start_item = st_n;
+        load_runs(b + 1, s_n, e_n, st_n);
+        const unsigned long long tag = static_cast<unsigned long long>(b + 1) << 32;
+        u32 c;
+        if (head) {
+            c = end_item - start_item;
+        } else if (in_global) {
+            unsigned long long v;
+            do {
+                v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane);
+            } while ((v >> 32) != (b + 1));
+            c = static_cast<u32>(v);
+        } else {
+            unsigned long long v;
+            do {
+                v = sin[(b % kQs) * 32 + lane];
+            } while ((v >> 32) != (b + 1));
+            c = static_cast<u32>(v);
+        }
+        unsigned act = __ballot_sync(0xffffffffu, c > 0 && s <= wmax);  // every lane has its c
+        if (!head && lane == 0) {
+            if (in_global) st_relaxed_u32(a.gcons + g * kStride, b + 1);
+            else reinterpret_cast<volatile u32*>(s_cons)[w] = b + 1;
+        }
+
+        while (act) {
+            const int r = __ffs(act) - 1;
+            act &= act - 1;
+            const u32 S = __shfl_sync(0xffffffffu, s, r);
+            if (S > wmax) continue;
+            const u32 Cc = __shfl_sync(0xffffffffu, c, r);
+            const u32 I0 = __shfl_sync(0xffffffffu, end_item - c, r);
+            u32 capl[M];
+            u32 lsum = 0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                capl[i] = (lmax >= S && R[i] >= S) ? R[i] / S : 0u;
+                lsum += capl[i];
+            }
+            const u32 incl = warp_inclusive_scan(lsum);
+            const u32 excl = incl - lsum;
+            const u32 tot = __shfl_sync(0xffffffffu, incl, 31);
+            const u32 used = tot < Cc ? tot : Cc;
+            if (lsum > 0 && excl < Cc) {
+                u32 avail = min(lsum, Cc - excl);
+                u32 off = I0 + excl;
+                u32 nm = 0;
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const u32 t = min(capl[i], avail);
+                    if (t > 0) {  // one head per take; expand_heads fills the rest
+                        a.item_bin[off] = static_cast<u32>(first_bin + i);
+                        a.item_slot[off] = N[i];
+                        a.take[off] = t;
+                        R[i] -= t * S;
+                        N[i] += t;
+                        avail -= t;
+                        off += t;
+                    }
+                    nm = max(nm, R[i]);
+                }
+                lmax = nm;
+            }
+            if (static_cast<int>(lane) == r) c = Cc - used;
+            if (used) wmax = __reduce_max_sync(0xffffffffu, lmax);
+        }
+
+        if (!tail) {
+            const unsigned long long v = tag | c;
+            if (out_global) {
+                if (b >= static_cast<u32>(kQ) && seen_cons + kQ <= b) {
+                    if (lane == 0)
+                        while ((seen_cons = ld_relaxed_u32(a.gcons + (g + 1) * kStride)) + kQ <= b) {
+                        }
+                    seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
+                }
+                st_relaxed_u64(gout + (b % kQ) * 32 + lane, v);
+            } else {
+                if (b >= static_cast<u32>(kQs) && seen_cons + kQs <= b) {
+                    if (lane == 0)
+                        while ((seen_cons = reinterpret_cast<volatile u32*>(s_cons)[w + 1]) + kQs <= b) {
+                        }
+                    seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
+                }
+                sout[(b % kQs) * 32 + lane] = v;
+            }
+        } else if (a.ffd && c > 0) {
+            atomicOr(a.out + 1, 1u);
+        }
+    }
+
+    u32 top = 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const u64 bin = first_bin + i;
+        if (bin < a.n_bins) {
+            if (bin < a.live || N[i] > 0) a.leaves[bin] = (static_cast<u64>(R[i]) << 32) | N[i];
+            if (N[i] > 0) top = static_cast<u32>(bin + 1);
+        }
+    }
+    top = __reduce_max_sync(0xffffffffu, top);
+    if (lane == 0 && top) atomicMax(a.out, top);
+}
+
+template <int M>
+bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
+    const u32 J = static_cast<u32>((static_cast<u64>(a.n_bins) + 32ull * M - 1) / (32ull * M));
+    const u32 G = (J + kWarps - 1) / kWarps;
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, 0));
+    if (per_sm <= 0 || G > static_cast<u32>(per_sm * sms)) return false;
+    cudaStream_t s = c.stream;
+    a.J = J;
+    DevBuf<unsigned long long> gring(static_cast<size_t>(G + 1) * kQ * 32, s);
+    DevBuf<u32> gcons(static_cast<size_t>(G + 1) * kStride, s), out(2, s);
+    gring.zero();
+    gcons.zero();
+    out.zero();
+    a.gring = gring.p;
+    a.gcons = gcons.p;
+    a.out = out.p;
+    void* args[] = {&a};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c.trace) {
+        CUDA_CHECK(cudaEventCreate(&e0));
+        CUDA_CHECK(cudaEventCreate(&e1));
+        CUDA_CHECK(cudaEventRecord(e0, s));
+    }
+    LAUNCH_COOP(name, 0.0, k_ff_chain<M>, dim3(G), dim3(kWarps * 32), 0, s, args);
+    if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
+    const auto o = read_vector(c, out.p, 2);
+    if (o[1]) throw EngineError(HBP_ERR_CUDA, "first-fit chain: bin capacity exceeded");
+    if (c.trace) {
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::fprintf(stderr,
+                     "[hbp trace] fit chain %s: runs %u..%u (%u blocks) bins %u (live %u) M %d warps %u ctas %u used %u: "
+                     "%.3f ms\n",
+                     a.ffd ? "ffd" : "fill", a.run_begin, a.run_end, a.nblocks, a.n_bins, a.live, M, J, G, o[0], ms);
+    }
+    a.out = nullptr;
+    a.J = std::max(a.live, o[0]);  // reuse as the result
+    return true;
+}
+
+}  // namespace
+
+// Heads -> every item: item x belongs to the last head h <= x when
+// x < h + take[h] (same bin, slot + x - h), else it stays unassigned.
+__global__ void k_head_positions(const u32* __restrict__ take, const u32* __restrict__ q, u64 n,
+                                 u32* __restrict__ pos) {
+    for (u64 x = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; x < n;
+         x += static_cast<u64>(gridDim.x) * blockDim.x)
+        if (take[x]) pos[q[x] - 1] = static_cast<u32>(x);
+}
+
+__global__ void k_expand_heads(const u32* __restrict__ take, const u32* __restrict__ q, const u32* __restrict__ pos,
+                               u64 n, u32* __restrict__ item_bin, u32* __restrict__ item_slot) {
+    for (u64 x = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; x < n;
+         x += static_cast<u64>(gridDim.x) * blockDim.x) {
+        if (take[x]) continue;  // heads already hold (bin, slot)
+        const u32 k = q[x];
+        u32 b = kNone, sl = kNone;
+        if (k > 0) {
+            const u32 h = pos[k - 1];
+            if (x - h < take[h]) {
+                b = item_bin[h];
+                sl = item_slot[h] + static_cast<u32>(x - h);
+            }
+        }
+        item_bin[x] = b;
+        item_slot[x] = sl;
+    }
+}
+
+void expand_heads(Ctx& c, u64 n, u32* item_bin, u32* item_slot, const u32* take) {
+    cudaStream_t s = c.stream;
+    DevBuf<u32> q(n, s), pos(n, s);
+    u32* qp = q.p;
+    scan_exclusive<u64>(
+        static_cast<i64>(n), [=] __device__(i64 x) { return take[x] ? 1ull : 0ull; },
+        [=] __device__(i64 x, u64 v) { qp[x] = static_cast<u32>(v) + (take[x] ? 1u : 0u); }, s, c.scan,
+        "chain.heads.scan", 12.0);
+    LAUNCH_B("chain.heads", 12.0 * n, k_head_positions, grid_for(n, 256), 256, 0, s, take, q.p, n, pos.p);
+    LAUNCH_B("chain.expand", 24.0 * n, k_expand_heads, grid_for(n, 256), 256, 0, s, take, q.p, pos.p, n, item_bin,
+             item_slot);
+}
+
+bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins, u32 cap, bool ffd, u32* item_bin,
+               u32* item_slot, u32* take, u32& used) {
+    used = live;
+    if (runs.run_begin >= runs.run_end || n_bins == 0) {
+        expand_heads(c, runs.n_items, item_bin, item_slot, take);
+        return true;
+    }
+    int dev = 0, sms = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    ChainArgs a{};
+    a.run_item = runs.run_item;
+    a.run_len = runs.run_len;
+    a.n_items = runs.n_items;
+    a.n_runs = runs.n_runs;
+    a.run_begin = runs.run_begin;
+    a.run_end = runs.run_end;
+    a.leaves = leaves;
+    a.live = live;
+    a.n_bins = n_bins;
+    a.cap = cap;
+    a.ffd = ffd ? 1 : 0;
+    a.nblocks = (runs.run_end - runs.run_begin + 31) / 32;
+    a.item_bin = item_bin;
+    a.item_slot = item_slot;
+    a.take = take;
+    // fewest bins per lane whose chain is resident (HBP_CHAIN_M: lower bound)
+    const char* em = std::getenv("HBP_CHAIN_M");
+    const int m0 = em ? std::atoi(em) : 1;
+    bool ok = (m0 <= 1 && try_chain<1>(c, a, sms, "fit.chain")) || (m0 <= 2 && try_chain<2>(c, a, sms, "fit.chain")) ||
+              (m0 <= 4 && try_chain<4>(c, a, sms, "fit.chain")) || (m0 <= 8 && try_chain<8>(c, a, sms, "fit.chain")) ||
+              try_chain<16>(c, a, sms, "fit.chain");
+    if (!ok) return false;
+    used = a.J;
+    expand_heads(c, runs.n_items, item_bin, item_slot, take);
+    return true;
+}
+
+}  // namespace hbp_b200

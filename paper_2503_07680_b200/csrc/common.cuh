@@ -162,6 +162,26 @@ extern thread_local KernelProfiler* g_prof;
         }                                                                                   \
     } while (0)
 
+// Cooperative launch (all CTAs co-resident, or cudaErrorCooperativeLaunchTooLarge).
+#define LAUNCH_COOP(name, bytes, kernel, grid, block, smem, stream, args)                   \
+    do {                                                                                    \
+        ::hbp_b200::KernelProfiler* _p = ::hbp_b200::g_prof;                                \
+        const bool _on = _p && _p->on;                                                      \
+        cudaEvent_t _e0 = nullptr;                                                          \
+        if (_on) {                                                                          \
+            _e0 = _p->event();                                                              \
+            CUDA_CHECK(cudaEventRecord(_e0, (stream)));                                     \
+        }                                                                                   \
+        CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), (grid), \
+                                               (block), (args), (smem), (stream)));         \
+        ::hbp_b200::count_launch();                                                         \
+        if (_on) {                                                                          \
+            cudaEvent_t _e1 = _p->event();                                                  \
+            CUDA_CHECK(cudaEventRecord(_e1, (stream)));                                     \
+            _p->recs.push_back({(name), _e0, _e1, static_cast<double>(bytes)});             \
+        }                                                                                   \
+    } while (0)
+
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------

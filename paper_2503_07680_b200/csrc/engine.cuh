@@ -13,8 +13,14 @@
 #include <chrono>
 #include <cstdlib>
 #include <map>
+#include <set>
+
+struct hbp_plan;
 
 struct hbp_ctx {
+    // plans created on this context; their device arrays are freed (stream
+    // ordered) before the stream goes away, their host views stay readable
+    std::set<hbp_plan*> plans;
     int device = 0;
     cudaStream_t stream = nullptr;
     std::string last_error;

@@ -86,11 +86,17 @@ __global__ void k_tree_level(const u64* __restrict__ leaves, u32* __restrict__ b
 }
 
 // FFD bulk: items [0, k) all longer than cap / 2 -> bin i each.
-__global__ void k_bulk_big(const u64* __restrict__ items, u64 k, u32 cap, u64* __restrict__ leaves) {
+__global__ void k_bulk_big(const u64* __restrict__ items, u64 k, u32 cap, u64* __restrict__ leaves,
+                           u32* __restrict__ item_bin, u32* __restrict__ item_slot, u32* __restrict__ take) {
     for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < k;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
         const u32 l = entry_len(items[i]);
         leaves[i] = (static_cast<u64>(cap - l) << 32) | 1u;
+        if (item_bin) {  // chain path: each bulk item is a head of one
+            item_bin[i] = static_cast<u32>(i);
+            item_slot[i] = 0;
+            take[i] = 1;
+        }
     }
 }
 
@@ -1051,6 +1057,7 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
     radix_sort_pairs(c, key.p, idx.p, static_cast<i64>(R), bits, false);
     // valid records are the prefix with key < ks
     DevBuf<u64> take_scan(R + 1, s), run_base(n_runs + 1, s), vcount(1, s);
+    vcount.zero();  // stays 0 when no record belongs to a committed run
     {
         const u32* kp = key.p;
         const u32* ip = idx.p;
@@ -1081,7 +1088,7 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
 }
 
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
-                         FitMode mode, FitRecords rec, i64 max_records) {
+                         FitMode mode, u32* item_bin, u32* item_slot) {
     FitResult out;
     out.bins = bins0;
     if (n_items_s <= 0) return out;
@@ -1089,6 +1096,9 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     cudaStream_t s = c.stream;
     const bool ffd = mode == FitMode::Ffd;
     if (max_bins < 1) max_bins = 1;
+    const char* eng = std::getenv("HBP_ENGINE");
+    const std::string engine = eng ? eng : "";
+    const bool use_chain = engine.empty() || engine == "chain";
 
     // runs of equal length
     DevBuf<u64> flags_excl(n, s);
@@ -1142,13 +1152,32 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         const i64 bound = static_cast<i64>(2 * std::ceil(sum / cap)) + 2 + bins0;
         if (bound < tree_bins) tree_bins = bound;
     }
+    const u64 live = static_cast<u64>(bins0) + bulk;
+    if (use_chain) {
+        DevBuf<u32> take(n, s);
+        take.zero();
+        if (bulk > 0)
+            LAUNCH(k_bulk_big, grid_for(bulk, 256, 148u * 16u), 256, 0, s, items, static_cast<u64>(bulk), cap, leaves,
+                   item_bin, item_slot, take.p);
+        ChainRuns cr{run_item.p, run_len.p, static_cast<u32>(n), n_runs, run_begin, n_runs};
+        u32 used = 0;
+        if (chain_fit(c, cr, leaves, static_cast<u32>(live), static_cast<u32>(ffd ? tree_bins : live), cap, ffd,
+                      item_bin, item_slot, take.p, used)) {
+            out.bins = ffd ? std::max<i64>(static_cast<i64>(live), used) : bins0;
+            return out;
+        }
+    }
+    const u64 max_records = 2 * n + 2;
+    DevBuf<u32> r_item(max_records, s), r_count(max_records, s), r_bin(max_records, s), r_per(max_records, s),
+        r_slot0(max_records, s);
+    FitRecords rec{r_item.p, r_count.p, r_bin.p, r_per.p, r_slot0.p};
     TreeLayout t = make_layout(static_cast<u64>(tree_bins));
     DevBuf<u32> tree(t.off[0], s);
     t.base = tree.p;
     if (bulk > 0) {
-        LAUNCH(k_bulk_big, grid_for(bulk, 256, 148u * 16u), 256, 0, s, items, static_cast<u64>(bulk), cap, leaves);
+        LAUNCH(k_bulk_big, grid_for(bulk, 256, 148u * 16u), 256, 0, s, items, static_cast<u64>(bulk), cap, leaves,
+               nullptr, nullptr, nullptr);
     }
-    const u64 live = static_cast<u64>(bins0) + bulk;
     // leaves beyond the live ones start empty
     if (static_cast<u64>(max_bins) > live)
         CUDA_CHECK(cudaMemsetAsync(leaves + live, 0, sizeof(u64) * (max_bins - live), s));
@@ -1198,8 +1227,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     constexpr size_t kSmemLimit = 216 * 1024;  // + 8.4 KB static (candidates, leaf stage) <= 227 KB
     const V4Layout vl = make_v4(static_cast<u64>(tree_bins));
     const size_t smem4 = sizeof(unsigned short) * vl.total;
-    const char* eng = std::getenv("HBP_ENGINE");
-    const bool force_v3 = eng && std::string(eng) == "v3", force_v1 = eng && std::string(eng) == "v1";
+    const bool force_v3 = engine == "v3", force_v1 = engine == "v1";
     cudaFuncAttributes fa4{};
     CUDA_CHECK(cudaFuncGetAttributes(&fa4, k_fit_engine_v4));
     const size_t limit4 = 227 * 1024 - fa4.sharedSizeBytes;  // dynamic + static <= 227 KB per CTA
@@ -1251,6 +1279,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
                          n_runs, P, passes, engine_runs, nrec);
         out.bins = live;
         out.records = nrec;
+        expand_fit_records(c, rec, out.records, static_cast<i64>(n), item_bin, item_slot);
         return out;
     }
     if (v4ok) {
@@ -1276,6 +1305,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     }
     out.bins = o[0];
     out.records = o[1];
+    expand_fit_records(c, rec, out.records, static_cast<i64>(n), item_bin, item_slot);
     return out;
 }
 

@@ -530,17 +530,12 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         CUDA_CHECK(cudaMemcpyAsync(out.residue.p, A.p, sizeof(u64) * cur, cudaMemcpyDeviceToDevice, s));
         if (residue_ffd) sort_entries(c, corpus, out.residue.p, cur, key_ordered, cap);
         trace_mark(c, "ffd.sort");
-        const u64 maxrec = 2 * cur + 2;
-        DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
-        FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
-        const FitResult fr = first_fit_runs(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf, 0,
-                                            static_cast<i64>(cur), cap, FitMode::Ffd, rec, static_cast<i64>(maxrec));
-        out.n_ffd = static_cast<u64>(fr.bins);
-        trace_mark(c, "ffd.engine");
         out.res_bin.alloc(cur, s);
         out.res_slot.alloc(cur, s);
-        expand_fit_records(c, rec, fr.records, static_cast<i64>(cur), out.res_bin.p, out.res_slot.p);
-        trace_mark(c, "ffd.expand");
+        const FitResult fr = first_fit_runs(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf, 0,
+                                            static_cast<i64>(cur), cap, FitMode::Ffd, out.res_bin.p, out.res_slot.p);
+        out.n_ffd = static_cast<u64>(fr.bins);
+        trace_mark(c, "ffd.engine");
     }
 }
 
@@ -886,16 +881,11 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             }
             trace_mark(c, "fill.sort");
             const u64 P = pg.P();
-            const u64 maxrec = 2 * n_fill + 2;
-            DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
-            FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
-            const FitResult fr = first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p,
-                                                static_cast<i64>(P), static_cast<i64>(P), cap, FitMode::Fill, rec,
-                                                static_cast<i64>(maxrec));
-            trace_mark(c, "fill.engine");
             fill_bin.alloc(n_fill, s);
             fill_slot.alloc(n_fill, s);
-            expand_fit_records(c, rec, fr.records, static_cast<i64>(n_fill), fill_bin.p, fill_slot.p);
+            first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p, static_cast<i64>(P),
+                           static_cast<i64>(P), cap, FitMode::Fill, fill_bin.p, fill_slot.p);
+            trace_mark(c, "fill.engine");
             // remove consumed samples from their pools, order preserved
             if (!consumed.p) {
                 consumed.alloc(n, s);
@@ -1095,13 +1085,8 @@ void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int6
         u32 maxlen = 1;
         for (u64 i = 0; i < m; ++i) maxlen = std::max<u32>(maxlen, static_cast<u32>(std::min<int64_t>(pool_lens[a + i], 0x7fffffff)));
         sort_entries(c, corpus, items.p, m, corpus.key32.p == nullptr, maxlen);
-        const u64 maxrec = 2 * m + 2;
-        DevBuf<u32> ri(maxrec, s), rc(maxrec, s), rb(maxrec, s), rp(maxrec, s), rs0(maxrec, s);
-        FitRecords rec{ri.p, rc.p, rb.p, rp.p, rs0.p};
-        const FitResult fr = first_fit_runs(c, items.p, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u,
-                                            FitMode::Fill, rec, static_cast<i64>(maxrec));
         DevBuf<u32> bin(m, s), slot(m, s);
-        expand_fit_records(c, rec, fr.records, static_cast<i64>(m), bin.p, slot.p);
+        first_fit_runs(c, items.p, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u, FitMode::Fill, bin.p, slot.p);
         const auto hb = read_vector(c, bin.p, m), hs = read_vector(c, slot.p, m);
         const auto he = read_vector(c, items.p, m);
         for (u64 i = 0; i < m; ++i) {

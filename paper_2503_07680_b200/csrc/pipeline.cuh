@@ -27,6 +27,18 @@ struct DevicePlan {
     std::vector<int32_t> h_iter_group, h_dev_index, h_member_index;
     std::vector<int64_t> h_iter_dev_offsets, h_dev_pack_offsets, h_pack_capacity, h_pack_total, h_pack_attention,
         h_pack_member_offsets;
+    // frees the device arrays (the host mirror stays valid)
+    void release_device() {
+        iter_group.release();
+        iter_dev_offsets.release();
+        dev_index.release();
+        dev_pack_offsets.release();
+        pack_capacity.release();
+        pack_total.release();
+        pack_attention.release();
+        pack_member_offsets.release();
+        member_index.release();
+    }
 };
 
 // Samples resident on the device after ingest.

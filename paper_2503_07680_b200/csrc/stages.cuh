@@ -59,9 +59,27 @@ struct FitResult {
 enum class FitMode { Ffd, Fill };
 
 // `leaves` (capacity max_bins) holds (residual << 32 | count) per bin; the
-// first `bins0` are live. items: sorted entries.
+// first `bins0` are live. items: sorted entries. Writes item -> (bin, slot),
+// kNone for items left unassigned (fill mode).
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
-                         FitMode mode, FitRecords rec, i64 max_records);
+                         FitMode mode, u32* item_bin, u32* item_slot);
+
+// chain.cu: first fit as a pipeline of bins. Bin b sees the items no bin
+// before it took, in order, and takes each one that fits, so bins form a
+// systolic chain: warp j owns 32 * m consecutive bins and passes, per run,
+// the count its bins left to warp j + 1. Runs [run_begin, run_end).
+struct ChainRuns {
+    const u32* run_item;
+    const u32* run_len;
+    u32 n_items, n_runs, run_begin, run_end;
+};
+// Bins [0, live) hold `leaves`; FFD: bins [live, n_bins) start empty
+// (residual cap). Returns false when n_bins is too large for one resident
+// chain. `used` = 1 + the highest bin holding items. `take` (n_items,
+// zeroed; pre-placed items marked as heads with take 1 and their bin/slot)
+// is scratch for the head expansion.
+bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins, u32 cap, bool ffd, u32* item_bin,
+               u32* item_slot, u32* take, u32& used);
 
 // item -> (bin, slot) for every item covered by a record; others get kNone.
 void expand_fit_records(Ctx& c, FitRecords rec, i64 n_records, i64 n_items, u32* item_bin, u32* item_slot);

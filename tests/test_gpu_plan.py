@@ -75,6 +75,21 @@ def test_build_plan_c1(ctx, oracle):
         assert getattr(mg, k) == pytest.approx(getattr(mo, k), rel=1e-9, abs=0)
 
 
+@pytest.mark.parametrize("groups", [
+    [(512, 1, 0), (1024, 2, 0), (2048, 2, 0), (4096, 2, 0), (8192, 2, 0), (16384, 2, 0), (32768, 2, 0),
+     (65536, 2, 0), (131072, 2, 0)],
+    [(1024, 1, 0), (65536, 8, 0), (131072, 8, 0)],
+    [(16384, 1, 0), (32768, 4, 0), (131072, 4, 0)],
+])
+def test_build_plan_many_groups(ctx, oracle, groups):
+    # C3 sweep shapes: fill from several pools, runs no pack can take
+    L = c1_lengths(oracle, 100_000)
+    lb = groups[0][0]
+    want = oracle.build_plan(None, L, groups, l_best=lb, device_count=8, seed=7)
+    got = ctx.build_plan(None, L, groups, l_best=lb, device_count=8, seed=7).flat()
+    assert_same_plan(got, want)
+
+
 @pytest.mark.parametrize("n,seed", [(300_000, 20250515), (1_000_000, 1)])
 def test_build_plan_c2_shape(ctx, oracle, n, seed):
     L = hybrid(oracle, n, seed)
@@ -150,3 +165,16 @@ def test_errors_match_reference(ctx, oracle):
         ctx.pack(None, np.array([3, 9, 2]), 4, "ffd")
     with pytest.raises(abi.ValidationError, match="empty corpus: python"):
         ctx.build_plan(None, np.array([], dtype=np.int64), TWO_LEVEL, 16384)
+
+
+def test_plan_outlives_context(oracle):
+    # a plan freed after its context: device arrays went with the context,
+    # the host view taken before stays valid
+    L = hybrid(oracle, 2000, 3)
+    c = abi.Context(0)
+    plan = c.build_plan(None, L, TWO_LEVEL, l_best=16384, device_count=4, seed=5)
+    flat = plan.flat()
+    c.close()
+    del plan
+    want = oracle.build_plan(None, L, TWO_LEVEL, l_best=16384, device_count=4, seed=5)
+    assert_same_plan(flat, want)

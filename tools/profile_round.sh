@@ -1,0 +1,23 @@
+#!/usr/bin/env bash
+# Profiles one C2 step on the GPU box (run under gpurun, one GPU):
+#   1. launch list (per-launch device time, clocks not pinned)
+#   2. DRAM traffic of every launch of the scan family (roofline "traffic")
+#   3. one full-set capture of the first-fit engine and of the largest scan
+# Outputs go to gpurun_out/; summaries are copied into profiles/ by hand.
+set -u
+OUT=${OUT:-gpurun_out}
+TAG=${TAG:-r01}
+mkdir -p "$OUT"
+STEP="python tools/profile_step.py --steps 1"
+
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file "$OUT/${TAG}_launches_c2.csv" $STEP > /dev/null 2>&1
+echo "launch list: $(grep -c '"gpu__time_duration.sum"' "$OUT/${TAG}_launches_c2.csv") launches"
+
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:k_scan_lookback --csv --log-file "$OUT/${TAG}_scan_traffic.csv" $STEP > /dev/null 2>&1
+echo "scan traffic rows: $(grep -c dram__bytes_read "$OUT/${TAG}_scan_traffic.csv")"
+
+ncu --set full --clock-control none --import-source on -k regex:k_fit_engine_v4 -c 2 \
+    -o "$OUT/${TAG}_engine" -f $STEP > /dev/null 2>&1
+echo "engine capture: $?"

@@ -32,9 +32,11 @@ namespace hbp_b200 {
 
 namespace {
 
-constexpr int kQ = 8;          // global ring depth per link, in blocks of 32 runs
-constexpr int kQs = 4;         // shared-memory ring depth
-constexpr int kWarps = 32;     // warps per CTA (one CTA per SM)
+constexpr int kQ = 32;         // global ring depth per link, in blocks of 32 runs
+constexpr int kQs = 16;        // shared-memory ring depth (dynamic shared memory)
+// warps per CTA (one CTA per SM): fewer for wide lanes so registers stay <= 128
+template <int M>
+__host__ __device__ constexpr int warps_for() { return M <= 4 ? 32 : 16; }
 constexpr u32 kStride = 32;    // u32 between global consumer counters (one 128 B line each)
 
 struct ChainArgs {
@@ -51,6 +53,8 @@ struct ChainArgs {
     u32* item_slot;
     u32* take;       // items in the take starting here (0: not a head)
     u32* out;                  // [0] 1 + highest bin with items, [1] FFD overflow
+    unsigned long long* prof;  // HBP_TRACE: per warp [wait in, serve, wait out, served runs]
+    u32 sleep;                 // ns of back-off per failed poll (idle warps yield issue slots)
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -71,8 +75,10 @@ __device__ __forceinline__ void st_relaxed_u32(u32* p, u32 v) {
 }
 
 template <int M>
-__global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
-    __shared__ unsigned long long s_ring[kWarps][kQs][32];  // warp w-1 -> w
+__global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a) {
+    constexpr int kWarps = warps_for<M>();
+    extern __shared__ unsigned long long s_ring_raw[];  // [kWarps][kQs][32]: warp w-1 -> w
+    auto s_ring = reinterpret_cast<unsigned long long (*)[kQs][32]>(s_ring_raw);
     __shared__ u32 s_cons[kWarps];                         // blocks warp w has read from s_ring[w]
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const u32 g = blockIdx.x;
@@ -82,20 +88,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
     __syncthreads();
     if (j >= a.J) return;  // no CTA-wide barriers below
 
-    const u64 first_bin = (static_cast<u64>(j) * 32 + lane) * M;
-    u32 R[M], N[M];
-    u32 lmax = 0;
+    // row-major: row i of the warp holds bins base + 32 i + lane, so a run
+    // walks the rows in bin order and stops at the row that uses it up
+    const u64 base = static_cast<u64>(j) * 32 * M;
+    u32 R[M], N[M], rowmax[M];
+    u32 wmax = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-        const u64 bin = first_bin + i;
+        const u64 bin = base + 32 * i + lane;
         u64 leaf = 0;
         if (bin < a.live) leaf = a.leaves[bin];
-        else if (a.ffd && bin < a.n_bins) leaf = static_cast<u64>(a.cap) << 32;
+        else if (a.ffd && bin < a.n_bins) leaf = static_cast<u64>(a.cap) << 32;  // empty bin
         R[i] = static_cast<u32>(leaf >> 32);
         N[i] = static_cast<u32>(leaf);
-        lmax = max(lmax, R[i]);
+        rowmax[i] = __reduce_max_sync(0xffffffffu, R[i]);
+        wmax = max(wmax, rowmax[i]);
     }
-    u32 wmax = __reduce_max_sync(0xffffffffu, lmax);
     const bool head = j == 0, tail = j + 1 == a.J;
     const bool in_global = w == 0, out_global = w + 1 == kWarps;
     volatile unsigned long long* sin = s_ring[w][0];
@@ -115,7 +123,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
     u32 s_n, e_n, st_n;
     load_runs(0, s_n, e_n, st_n);
 
+    unsigned long long pf[4] = {0, 0, 0, 0};
+    long long t0 = 0, t1 = 0;
     for (u32 b = 0; b < a.nblocks; ++b) {
+        if (a.prof) t0 = clock64();
         const u32 s = s_n, end_item = e_n, start_item = st_n;
         load_runs(b + 1, s_n, e_n, st_n);
         const unsigned long long tag = static_cast<unsigned long long>(b + 1) << 32;
@@ -124,18 +135,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
             c = end_item - start_item;
         } else if (in_global) {
             unsigned long long v;
-            do {
-                v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane);
-            } while ((v >> 32) != (b + 1));
+            while (((v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane)) >> 32) != (b + 1))
+                if (a.sleep) __nanosleep(a.sleep);
             c = static_cast<u32>(v);
         } else {
             unsigned long long v;
-            do {
-                v = sin[(b % kQs) * 32 + lane];
-            } while ((v >> 32) != (b + 1));
+            while (((v = sin[(b % kQs) * 32 + lane]) >> 32) != (b + 1))
+                if (a.sleep) __nanosleep(a.sleep);
             c = static_cast<u32>(v);
         }
         unsigned act = __ballot_sync(0xffffffffu, c > 0 && s <= wmax);  // every lane has its c
+        if (a.prof) {
+            t1 = clock64();
+            pf[0] += t1 - t0;
+            pf[3] += __popc(act);
+            t0 = t1;
+        }
         if (!head && lane == 0) {
             if (in_global) st_relaxed_u32(a.gcons + g * kStride, b + 1);
             else reinterpret_cast<volatile u32*>(s_cons)[w] = b + 1;
@@ -146,58 +161,58 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
             act &= act - 1;
             const u32 S = __shfl_sync(0xffffffffu, s, r);
             if (S > wmax) continue;
-            const u32 Cc = __shfl_sync(0xffffffffu, c, r);
-            const u32 I0 = __shfl_sync(0xffffffffu, end_item - c, r);
-            u32 capl[M];
-            u32 lsum = 0;
+            const u32 C0 = __shfl_sync(0xffffffffu, c, r);
+            u32 left = C0;
+            u32 off = __shfl_sync(0xffffffffu, end_item - c, r);
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                capl[i] = (lmax >= S && R[i] >= S) ? R[i] / S : 0u;
-                lsum += capl[i];
-            }
-            const u32 incl = warp_inclusive_scan(lsum);
-            const u32 excl = incl - lsum;
-            const u32 tot = __shfl_sync(0xffffffffu, incl, 31);
-            const u32 used = tot < Cc ? tot : Cc;
-            if (lsum > 0 && excl < Cc) {
-                u32 avail = min(lsum, Cc - excl);
-                u32 off = I0 + excl;
-                u32 nm = 0;
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    const u32 t = min(capl[i], avail);
-                    if (t > 0) {  // one head per take; expand_heads fills the rest
-                        a.item_bin[off] = static_cast<u32>(first_bin + i);
-                        a.item_slot[off] = N[i];
-                        a.take[off] = t;
-                        R[i] -= t * S;
-                        N[i] += t;
-                        avail -= t;
-                        off += t;
-                    }
-                    nm = max(nm, R[i]);
+                if (left == 0 || rowmax[i] < S) continue;  // warp-uniform
+                const u32 q = 32 * i + lane;
+                const u32 capl = R[i] >= S ? R[i] / S : 0u;
+                const u32 incl = warp_inclusive_scan(capl);
+                const u32 excl = incl - capl;
+                const u32 tot = __shfl_sync(0xffffffffu, incl, 31);
+                const u32 t = excl < left ? min(capl, left - excl) : 0u;
+                if (t > 0) {  // one head per take; expand_heads fills the rest
+                    a.item_bin[off + excl] = static_cast<u32>(base + q);
+                    a.item_slot[off + excl] = N[i];
+                    a.take[off + excl] = t;
+                    R[i] -= t * S;
+                    N[i] += t;
                 }
-                lmax = nm;
+                const u32 used = tot < left ? tot : left;
+                left -= used;
+                off += used;
+                rowmax[i] = __reduce_max_sync(0xffffffffu, R[i]);
             }
-            if (static_cast<int>(lane) == r) c = Cc - used;
-            if (used) wmax = __reduce_max_sync(0xffffffffu, lmax);
+            if (static_cast<int>(lane) == r) c = left;
+            if (left != C0) {
+                wmax = 0;
+#pragma unroll
+                for (int i = 0; i < M; ++i) wmax = max(wmax, rowmax[i]);
+            }
         }
 
+        if (a.prof) {
+            t1 = clock64();
+            pf[1] += t1 - t0;
+            t0 = t1;
+        }
         if (!tail) {
             const unsigned long long v = tag | c;
             if (out_global) {
                 if (b >= static_cast<u32>(kQ) && seen_cons + kQ <= b) {
                     if (lane == 0)
-                        while ((seen_cons = ld_relaxed_u32(a.gcons + (g + 1) * kStride)) + kQ <= b) {
-                        }
+                        while ((seen_cons = ld_relaxed_u32(a.gcons + (g + 1) * kStride)) + kQ <= b)
+                            if (a.sleep) __nanosleep(a.sleep);
                     seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
                 }
                 st_relaxed_u64(gout + (b % kQ) * 32 + lane, v);
             } else {
                 if (b >= static_cast<u32>(kQs) && seen_cons + kQs <= b) {
                     if (lane == 0)
-                        while ((seen_cons = reinterpret_cast<volatile u32*>(s_cons)[w + 1]) + kQs <= b) {
-                        }
+                        while ((seen_cons = reinterpret_cast<volatile u32*>(s_cons)[w + 1]) + kQs <= b)
+                            if (a.sleep) __nanosleep(a.sleep);
                     seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
                 }
                 sout[(b % kQs) * 32 + lane] = v;
@@ -205,12 +220,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
         } else if (a.ffd && c > 0) {
             atomicOr(a.out + 1, 1u);
         }
+        if (a.prof) pf[2] += clock64() - t0;
     }
+    if (a.prof && lane == 0)
+        for (int i = 0; i < 4; ++i) a.prof[4ull * j + i] = pf[i];
 
     u32 top = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-        const u64 bin = first_bin + i;
+        const u64 bin = base + 32 * i + lane;
         if (bin < a.n_bins) {
             if (bin < a.live || N[i] > 0) a.leaves[bin] = (static_cast<u64>(R[i]) << 32) | N[i];
             if (N[i] > 0) top = static_cast<u32>(bin + 1);
@@ -223,9 +241,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
 template <int M>
 bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
     const u32 J = static_cast<u32>((static_cast<u64>(a.n_bins) + 32ull * M - 1) / (32ull * M));
+    constexpr int kWarps = warps_for<M>();
     const u32 G = (J + kWarps - 1) / kWarps;
+    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32;
+    CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, 0));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, smem));
     if (per_sm <= 0 || G > static_cast<u32>(per_sm * sms)) return false;
     cudaStream_t s = c.stream;
     a.J = J;
@@ -237,6 +258,13 @@ bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
     a.gring = gring.p;
     a.gcons = gcons.p;
     a.out = out.p;
+    DevBuf<unsigned long long> prof;
+    a.prof = nullptr;
+    if (c.trace) {
+        prof.alloc(4ull * J, s);
+        prof.zero();
+        a.prof = prof.p;
+    }
     void* args[] = {&a};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c.trace) {
@@ -244,7 +272,7 @@ bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
         CUDA_CHECK(cudaEventCreate(&e1));
         CUDA_CHECK(cudaEventRecord(e0, s));
     }
-    LAUNCH_COOP(name, 0.0, k_ff_chain<M>, dim3(G), dim3(kWarps * 32), 0, s, args);
+    LAUNCH_COOP(name, 0.0, k_ff_chain<M>, dim3(G), dim3(kWarps * 32), smem, s, args);
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
     const auto o = read_vector(c, out.p, 2);
     if (o[1]) throw EngineError(HBP_ERR_CUDA, "first-fit chain: bin capacity exceeded");
@@ -257,6 +285,31 @@ bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
                      "[hbp trace] fit chain %s: runs %u..%u (%u blocks) bins %u (live %u) M %d warps %u ctas %u used %u: "
                      "%.3f ms\n",
                      a.ffd ? "ffd" : "fill", a.run_begin, a.run_end, a.nblocks, a.n_bins, a.live, M, J, G, o[0], ms);
+        const auto pf = read_vector(c, prof.p, 4ull * J);
+        if (const char* dump = std::getenv("HBP_CHAIN_DUMP")) {  // per-warp counters, appended
+            if (FILE* f = std::fopen(dump, "ab")) {
+                const u32 hdr[4] = {J, a.nblocks, static_cast<u32>(M), static_cast<u32>(a.ffd)};
+                std::fwrite(hdr, 4, 4, f);
+                std::fwrite(pf.data(), 8, pf.size(), f);
+                std::fclose(f);
+            }
+        }
+        double sum[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+        u32 arg[4] = {0, 0, 0, 0};
+        for (u32 jj = 0; jj < J; ++jj)
+            for (int i = 0; i < 4; ++i) {
+                const double v = static_cast<double>(pf[4ull * jj + i]);
+                sum[i] += v;
+                if (v > mx[i]) {
+                    mx[i] = v;
+                    arg[i] = jj;
+                }
+            }
+        std::fprintf(stderr,
+                     "[hbp trace]   per warp: wait-in avg %.2fM max %.2fM | serve avg %.3fM max %.2fM (warp %u) | "
+                     "wait-out avg %.3fM max %.2fM | served runs %.0f, max %.0f (warp %u)\n",
+                     sum[0] / J / 1e6, mx[0] / 1e6, sum[1] / J / 1e6, mx[1] / 1e6, arg[1], sum[2] / J / 1e6,
+                     mx[2] / 1e6, sum[3], mx[3], arg[3]);
     }
     a.out = nullptr;
     a.J = std::max(a.live, o[0]);  // reuse as the result
@@ -332,9 +385,11 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     a.item_bin = item_bin;
     a.item_slot = item_slot;
     a.take = take;
+    const char* es = std::getenv("HBP_CHAIN_SLEEP");
+    a.sleep = es ? static_cast<u32>(std::atoi(es)) : 0u;
     // fewest bins per lane whose chain is resident (HBP_CHAIN_M: lower bound)
     const char* em = std::getenv("HBP_CHAIN_M");
-    const int m0 = em ? std::atoi(em) : 1;
+    const int m0 = em ? std::atoi(em) : 8;  // 8 rows per warp measured best on C2 (tools/chain_sweep.py)
     bool ok = (m0 <= 1 && try_chain<1>(c, a, sms, "fit.chain")) || (m0 <= 2 && try_chain<2>(c, a, sms, "fit.chain")) ||
               (m0 <= 4 && try_chain<4>(c, a, sms, "fit.chain")) || (m0 <= 8 && try_chain<8>(c, a, sms, "fit.chain")) ||
               try_chain<16>(c, a, sms, "fit.chain");

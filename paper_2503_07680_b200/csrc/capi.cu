@@ -65,7 +65,11 @@ static hbp_plan* new_plan(hbp_ctx* ctx) {
 }
 
 static void delete_plan(hbp_plan* p) {
-    if (p->owner) p->owner->plans.erase(p);
+    if (p->owner) {
+        p->owner->plans.erase(p);
+        p->owner->host_pool.release(p->dp.host);  // keep the pinned block for the next plan
+        p->dp.host = HostBlock{};
+    }
     delete p;
 }
 
@@ -318,15 +322,15 @@ int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out) {
         v.n_devices = d.n_devices;
         v.n_packs = d.n_packs;
         v.n_members = d.n_members;
-        v.iter_group = d.h_iter_group.data();
-        v.iter_dev_offsets = d.h_iter_dev_offsets.data();
-        v.dev_index = d.h_dev_index.data();
-        v.dev_pack_offsets = d.h_dev_pack_offsets.data();
-        v.pack_capacity = d.h_pack_capacity.data();
-        v.pack_total = d.h_pack_total.data();
-        v.pack_attention = d.h_pack_attention.data();
-        v.pack_member_offsets = d.h_pack_member_offsets.data();
-        v.member_index = d.h_member_index.data();
+        v.iter_group = d.h_iter_group;
+        v.iter_dev_offsets = d.h_iter_dev_offsets;
+        v.dev_index = d.h_dev_index;
+        v.dev_pack_offsets = d.h_dev_pack_offsets;
+        v.pack_capacity = d.h_pack_capacity;
+        v.pack_total = d.h_pack_total;
+        v.pack_attention = d.h_pack_attention;
+        v.pack_member_offsets = d.h_pack_member_offsets;
+        v.member_index = d.h_member_index;
         *out = v;
     });
 }

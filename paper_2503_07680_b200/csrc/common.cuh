@@ -94,6 +94,47 @@ struct Pinned {
     }
 };
 
+// Pinned host blocks recycled across calls (plan host views): pinning
+// memory costs far more than copying into it.
+struct HostBlock {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct PinnedPool {
+    std::vector<HostBlock> free_blocks;
+    static constexpr size_t kKeep = 4;
+    HostBlock acquire(size_t bytes) {
+        size_t best = free_blocks.size();
+        for (size_t i = 0; i < free_blocks.size(); ++i)
+            if (free_blocks[i].bytes >= bytes && (best == free_blocks.size() || free_blocks[i].bytes < free_blocks[best].bytes))
+                best = i;
+        if (best < free_blocks.size()) {
+            HostBlock b = free_blocks[best];
+            free_blocks.erase(free_blocks.begin() + static_cast<std::ptrdiff_t>(best));
+            return b;
+        }
+        HostBlock b;
+        b.bytes = bytes + bytes / 4 + 4096;
+        CUDA_CHECK(cudaMallocHost(&b.p, b.bytes));
+        return b;
+    }
+    void release(HostBlock b) {
+        if (!b.p) return;
+        free_blocks.push_back(b);
+        if (free_blocks.size() > kKeep) {  // drop the smallest
+            size_t s = 0;
+            for (size_t i = 1; i < free_blocks.size(); ++i)
+                if (free_blocks[i].bytes < free_blocks[s].bytes) s = i;
+            cudaFreeHost(free_blocks[s].p);
+            free_blocks.erase(free_blocks.begin() + static_cast<std::ptrdiff_t>(s));
+        }
+    }
+    ~PinnedPool() {
+        for (auto& b : free_blocks) cudaFreeHost(b.p);
+    }
+};
+
 // ---------------------------------------------------------------------------
 // kernel launch accounting (bench.py reports gpu_launches)
 // ---------------------------------------------------------------------------

@@ -27,6 +27,7 @@ struct hbp_ctx {
     int64_t launches = 0;
     hbp_b200::ScanScratch scan;
     hbp_b200::Pinned pinned;
+    hbp_b200::PinnedPool host_pool;  // plan host views
     // stage trace (HBP_TRACE=1): wall time between marks, stream synchronised
     bool trace = std::getenv("HBP_TRACE") != nullptr;
     std::map<std::string, double> trace_ms;

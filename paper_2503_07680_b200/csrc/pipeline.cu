@@ -1021,12 +1021,17 @@ void pack_device(Ctx& c, DeviceCorpus& corpus, int64_t capacity, const hbp_strat
 
 void plan_to_host(Ctx& c, DevicePlan& p) {
     if (p.on_host) return;
-    auto cp = [&](auto& h, auto& d, size_t n) {
-        h.resize(n);
-        if (n) CUDA_CHECK(cudaMemcpyAsync(h.data(), d.p, sizeof(h[0]) * n, cudaMemcpyDeviceToHost, c.stream));
-    };
     const size_t I = static_cast<size_t>(p.n_iterations), D = static_cast<size_t>(p.n_devices),
                  P = static_cast<size_t>(p.n_packs), M = static_cast<size_t>(p.n_members);
+    const size_t bytes = 8 * ((I + 1) + (I + 1) + (D + 1) + (D + 1) + 4 * (P + 1) + (P + 1) + (M + 1) / 2 + 8);
+    if (!p.host.p) p.host = c.host_pool.acquire(bytes);
+    char* cur = static_cast<char*>(p.host.p);
+    auto cp = [&](auto*& h, auto& d, size_t n) {
+        using T = std::remove_pointer_t<std::remove_reference_t<decltype(h)>>;
+        h = reinterpret_cast<T*>(cur);
+        cur += (sizeof(T) * n + 7) / 8 * 8;
+        if (n) CUDA_CHECK(cudaMemcpyAsync(h, d.p, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
+    };
     cp(p.h_iter_group, p.iter_group, I);
     cp(p.h_iter_dev_offsets, p.iter_dev_offsets, I + 1);
     cp(p.h_dev_index, p.dev_index, D);

@@ -22,11 +22,19 @@ struct DevicePlan {
     DevBuf<int64_t> dev_pack_offsets;
     DevBuf<int64_t> pack_capacity, pack_total, pack_attention, pack_member_offsets;
     DevBuf<int32_t> member_index;
-    // host mirror
+    // host mirror, in one pinned block (returned to the context's pool when
+    // the plan is freed; freed here if the plan outlives its context)
     bool on_host = false;
-    std::vector<int32_t> h_iter_group, h_dev_index, h_member_index;
-    std::vector<int64_t> h_iter_dev_offsets, h_dev_pack_offsets, h_pack_capacity, h_pack_total, h_pack_attention,
-        h_pack_member_offsets;
+    HostBlock host{};
+    int32_t *h_iter_group = nullptr, *h_dev_index = nullptr, *h_member_index = nullptr;
+    int64_t *h_iter_dev_offsets = nullptr, *h_dev_pack_offsets = nullptr, *h_pack_capacity = nullptr,
+            *h_pack_total = nullptr, *h_pack_attention = nullptr, *h_pack_member_offsets = nullptr;
+    DevicePlan() = default;
+    DevicePlan(const DevicePlan&) = delete;
+    DevicePlan& operator=(const DevicePlan&) = delete;
+    ~DevicePlan() {
+        if (host.p) cudaFreeHost(host.p);
+    }
     // frees the device arrays (the host mirror stays valid)
     void release_device() {
         iter_group.release();

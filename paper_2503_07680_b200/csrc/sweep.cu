@@ -11,6 +11,7 @@
 #include <cmath>
 #include <limits>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -56,7 +57,7 @@ extern "C" int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples, const hbp_gro
         // one the reference would raise; the plan of the current length set
         // is kept in HBM and reused by every candidate that shares it.
         std::vector<int64_t> cur_set;
-        DevicePlan plan;
+        std::unique_ptr<DevicePlan> plan_p(new DevicePlan());
         bool have_plan = false;
         for (int64_t c = 0; c < n_candidates; ++c) {
             std::vector<hbp_group_config> g(cand_groups + cand_offsets[c], cand_groups + cand_offsets[c + 1]);
@@ -72,15 +73,16 @@ extern "C" int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples, const hbp_gro
                 a.balance_batching = options->balance_batching != 0;
                 a.greedy_fill = options->greedy_fill != 0;
                 a.seed = options->seed;
-                plan = DevicePlan();
+                plan_p.reset(new DevicePlan());
                 have_plan = false;
-                build_plan_device(*ctx, corpus, a, plan);  // validates groups, l_max, device count
+                build_plan_device(*ctx, corpus, a, *plan_p);  // validates groups, l_max, device count
                 have_plan = true;
                 cur_set = ls;
             } else {
                 validate_groups(g, g.back().length);
             }
             if (pc) fail_validation(cm_profile_message(pc));  // simulate -> profile.validate()
+            const DevicePlan& plan = *plan_p;
             const PlanArrays pa{plan.iter_group.p,    plan.iter_dev_offsets.p, plan.dev_pack_offsets.p,
                                 plan.pack_capacity.p, plan.pack_total.p,       plan.pack_attention.p,
                                 plan.n_iterations,    plan.n_devices};

@@ -2,8 +2,8 @@
 # Profiles one C2 step on the GPU box (run under gpurun, one GPU):
 #   1. launch list (per-launch device time, clocks not pinned)
 #   2. DRAM traffic of every launch of the scan family (roofline "traffic")
-#   3. one full-set capture of the first-fit engine and of the largest scan
-# Outputs go to gpurun_out/; summaries are copied into profiles/ by hand.
+#   3. one full-set capture of the first-fit chain and of the hottest scan
+# Outputs go to gpurun_out/; summaries are copied into profiles/.
 set -u
 OUT=${OUT:-gpurun_out}
 TAG=${TAG:-r01}
@@ -18,6 +18,9 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     -k regex:k_scan_lookback --csv --log-file "$OUT/${TAG}_scan_traffic.csv" $STEP > /dev/null 2>&1
 echo "scan traffic rows: $(grep -c dram__bytes_read "$OUT/${TAG}_scan_traffic.csv")"
 
-ncu --set full --clock-control none --import-source on -k regex:k_fit_engine_v4 -c 2 \
-    -o "$OUT/${TAG}_engine" -f $STEP > /dev/null 2>&1
-echo "engine capture: $?"
+ncu --set full --clock-control none --import-source on -k regex:k_ff_chain -c 3 \
+    -o "$OUT/${TAG}_chain" -f $STEP > /dev/null 2>&1
+echo "chain capture: $?"
+ncu --set full --clock-control none --import-source on -k regex:k_scan_lookback -s 20 -c 1 \
+    -o "$OUT/${TAG}_scan" -f $STEP > /dev/null 2>&1
+echo "scan capture: $?"

@@ -354,16 +354,33 @@ def profile_stages(ctx, lib, fn):
     return out
 
 
+TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_scan_traffic.json")
+
+
 def roofline(stages, peak, peak_kind):
-    """Dominant HBM-bound kernel family: algorithmic bytes / its device time."""
+    """Dominant HBM-bound kernel family: algorithmic bytes / its device time
+    (CUDA events around every launch of the family, summed). The step's
+    largest kernel overall, the first-fit chain, is latency-bound (a
+    dependency chain over bins) and is reported beside it with its
+    share of the step instead of a bandwidth fraction."""
     cands = {k: v for k, v in stages.items() if v["bytes"] > 0 and v["ms"] > 0}
     if not cands:
         return None
     k, v = max(cands.items(), key=lambda kv: kv[1]["ms"])
     achieved = v["bytes"] / (v["ms"] / 1000.0) / 1e9
+    traffic = None
+    if k == "scan" and os.path.exists(TRAFFIC_FILE):  # ncu --set full capture of the same step, per launch
+        with open(TRAFFIC_FILE) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    total_ms = sum(x["ms"] for x in stages.values())
+    top_k, top_v = max(stages.items(), key=lambda kv: kv[1]["ms"])
     return {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-            "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-            "launches": v["launches"], "algorithmic_bytes": v["bytes"], "ms": v["ms"]}
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "algorithmic_bytes_per_launch": v["bytes"] / max(v["launches"], 1),
+            "launches": v["launches"], "ms": v["ms"], "share_of_kernel_time": v["ms"] / total_ms,
+            "step_top_kernel": {"kernel": top_k, "ms": top_v["ms"], "share_of_kernel_time": top_v["ms"] / total_ms,
+                                "bound": "latency (first-fit dependency chain across resident warps)"
+                                if top_k.startswith("fit.chain") else "hbm"}}
 
 
 def cpu_baseline_leg(lib):

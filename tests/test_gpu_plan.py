@@ -103,6 +103,23 @@ def test_build_plan_c2_shape(ctx, oracle, n, seed):
     assert sg[0].switch_count == so[0].switch_count
 
 
+def test_build_plan_c2_full_size(ctx, oracle):
+    # BASELINE config C2 at its full 10M samples (the bench workload): the
+    # plan, report and simulate against the restatement (~15 s on one core)
+    L = hybrid(oracle, 10_000_000, 20250515)
+    want = oracle.build_plan(None, L, C2_GROUPS, l_best=16384, device_count=8, seed=1)
+    plan = ctx.build_plan(None, L, C2_GROUPS, l_best=16384, device_count=8, seed=1)
+    got = plan.flat()
+    assert_same_plan(got, want)
+    mg, _, _ = ctx.report(got)
+    mo, _, _ = oracle.report(want)
+    for k in ("dbr", "pr", "abr", "cr", "ave_t"):
+        assert getattr(mg, k) == pytest.approx(getattr(mo, k), rel=1e-9, abs=0)
+    sg, so = ctx.simulate(got), oracle.simulate(want)
+    assert np.array_equal(sg[1], so[1])
+    assert sg[0].total_seconds == pytest.approx(so[0].total_seconds, rel=1e-9)
+
+
 def test_general_ids(ctx, oracle):
     rng = np.random.default_rng(4)
     L = hybrid(oracle, 4000, 8, 0.04)

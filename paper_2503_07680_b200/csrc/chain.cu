@@ -45,6 +45,9 @@ struct ChainArgs {
     u32 n_items, n_runs, run_begin, run_end;
     u64* leaves;
     u32 live, n_bins, cap;
+    u32 bin0, bin_end;     // this pass covers bins [bin0, bin_end)
+    const u32* carry_in;   // per run: items the previous pass left (null: first pass)
+    u32* carry_out;        // per run: items this pass leaves
     int ffd;
     u32 J, nblocks;
     unsigned long long* gring;  // CTA g -> g+1: kQ * 32 tagged counts
@@ -90,15 +93,17 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
 
     // row-major: row i of the warp holds bins base + 32 i + lane, so a run
     // walks the rows in bin order and stops at the row that uses it up
-    const u64 base = static_cast<u64>(j) * 32 * M;
+    const u64 base = a.bin0 + static_cast<u64>(j) * 32 * M;
     u32 R[M], N[M], rowmax[M];
     u32 wmax = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         const u64 bin = base + 32 * i + lane;
         u64 leaf = 0;
-        if (bin < a.live) leaf = a.leaves[bin];
-        else if (a.ffd && bin < a.n_bins) leaf = static_cast<u64>(a.cap) << 32;  // empty bin
+        if (bin < a.bin_end) {
+            if (bin < a.live) leaf = a.leaves[bin];
+            else if (a.ffd) leaf = static_cast<u64>(a.cap) << 32;  // empty bin
+        }
         R[i] = static_cast<u32>(leaf >> 32);
         N[i] = static_cast<u32>(leaf);
         rowmax[i] = __reduce_max_sync(0xffffffffu, R[i]);
@@ -132,7 +137,8 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
         const unsigned long long tag = static_cast<unsigned long long>(b + 1) << 32;
         u32 c;
         if (head) {
-            c = end_item - start_item;
+            const u32 k = a.run_begin + b * 32 + lane;
+            c = a.carry_in ? (k < a.run_end ? a.carry_in[k] : 0u) : end_item - start_item;
         } else if (in_global) {
             unsigned long long v;
             while (((v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane)) >> 32) != (b + 1))
@@ -217,8 +223,10 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
                 }
                 sout[(b % kQs) * 32 + lane] = v;
             }
-        } else if (a.ffd && c > 0) {
-            atomicOr(a.out + 1, 1u);
+        } else {  // tail: hand the counts to the next pass
+            const u32 k = a.run_begin + b * 32 + lane;
+            if (k < a.run_end) a.carry_out[k] = c;
+            if (__any_sync(0xffffffffu, c > 0) && lane == 0) atomicOr(a.out + 1, 1u);
         }
         if (a.prof) pf[2] += clock64() - t0;
     }
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         const u64 bin = base + 32 * i + lane;
-        if (bin < a.n_bins) {
+        if (bin < a.bin_end) {
             if (bin < a.live || N[i] > 0) a.leaves[bin] = (static_cast<u64>(R[i]) << 32) | N[i];
             if (N[i] > 0) top = static_cast<u32>(bin + 1);
         }
@@ -238,16 +246,25 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
     if (lane == 0 && top) atomicMax(a.out, top);
 }
 
+// Bins one resident chain of width M can hold.
 template <int M>
-bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
-    const u32 J = static_cast<u32>((static_cast<u64>(a.n_bins) + 32ull * M - 1) / (32ull * M));
+u64 chain_capacity(int sms) {
     constexpr int kWarps = warps_for<M>();
-    const u32 G = (J + kWarps - 1) / kWarps;
     const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32;
     CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, smem));
-    if (per_sm <= 0 || G > static_cast<u32>(per_sm * sms)) return false;
+    return static_cast<u64>(per_sm > 0 ? per_sm : 0) * sms * kWarps * 32 * M;
+}
+
+// One pass over bins [a.bin0, a.bin_end); returns {1 + highest bin used, any carry}.
+template <int M>
+std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
+    const u64 pass_bins = a.bin_end - a.bin0;
+    const u32 J = static_cast<u32>((pass_bins + 32ull * M - 1) / (32ull * M));
+    constexpr int kWarps = warps_for<M>();
+    const u32 G = (J + kWarps - 1) / kWarps;
+    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32;
     cudaStream_t s = c.stream;
     a.J = J;
     DevBuf<unsigned long long> gring(static_cast<size_t>(G + 1) * kQ * 32, s);
@@ -275,16 +292,16 @@ bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
     LAUNCH_COOP(name, 0.0, k_ff_chain<M>, dim3(G), dim3(kWarps * 32), smem, s, args);
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
     const auto o = read_vector(c, out.p, 2);
-    if (o[1]) throw EngineError(HBP_ERR_CUDA, "first-fit chain: bin capacity exceeded");
     if (c.trace) {
         float ms = 0;
         CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         std::fprintf(stderr,
-                     "[hbp trace] fit chain %s: runs %u..%u (%u blocks) bins %u (live %u) M %d warps %u ctas %u used %u: "
-                     "%.3f ms\n",
-                     a.ffd ? "ffd" : "fill", a.run_begin, a.run_end, a.nblocks, a.n_bins, a.live, M, J, G, o[0], ms);
+                     "[hbp trace] fit chain %s: runs %u..%u (%u blocks) bins %u..%u (live %u) M %d warps %u ctas %u "
+                     "used %u carry %u: %.3f ms\n",
+                     a.ffd ? "ffd" : "fill", a.run_begin, a.run_end, a.nblocks, a.bin0, a.bin_end, a.live, M, J, G,
+                     o[0], o[1], ms);
         const auto pf = read_vector(c, prof.p, 4ull * J);
         if (const char* dump = std::getenv("HBP_CHAIN_DUMP")) {  // per-warp counters, appended
             if (FILE* f = std::fopen(dump, "ab")) {
@@ -312,8 +329,7 @@ bool try_chain(Ctx& c, ChainArgs& a, int sms, const char* name) {
                      mx[2] / 1e6, sum[3], mx[3], arg[3]);
     }
     a.out = nullptr;
-    a.J = std::max(a.live, o[0]);  // reuse as the result
-    return true;
+    return {o[0], o[1] != 0};
 }
 
 }  // namespace
@@ -360,12 +376,13 @@ void expand_heads(Ctx& c, u64 n, u32* item_bin, u32* item_slot, const u32* take)
 }
 
 bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins, u32 cap, bool ffd, u32* item_bin,
-               u32* item_slot, u32* take, u32& used) {
+               u32* item_slot, u32* take, u32 first_pass_bins, u32& used) {
     used = live;
     if (runs.run_begin >= runs.run_end || n_bins == 0) {
         expand_heads(c, runs.n_items, item_bin, item_slot, take);
         return true;
     }
+    cudaStream_t s = c.stream;
     int dev = 0, sms = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -387,14 +404,50 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     a.take = take;
     const char* es = std::getenv("HBP_CHAIN_SLEEP");
     a.sleep = es ? static_cast<u32>(std::atoi(es)) : 0u;
-    // fewest bins per lane whose chain is resident (HBP_CHAIN_M: lower bound)
+    // Bins are covered by consecutive passes: a pass's tail hands the counts
+    // its bins left (per run) to the next pass's head, exactly as one longer
+    // chain would. A pass uses the fewest rows per warp (>= HBP_CHAIN_M,
+    // default 8, measured best on C2) whose chain is resident; FFD's first
+    // pass is sized by the caller's estimate of the bins FFD opens, so the
+    // 2x bin bound costs a second pass only when the estimate is short.
     const char* em = std::getenv("HBP_CHAIN_M");
-    const int m0 = em ? std::atoi(em) : 8;  // 8 rows per warp measured best on C2 (tools/chain_sweep.py)
-    bool ok = (m0 <= 1 && try_chain<1>(c, a, sms, "fit.chain")) || (m0 <= 2 && try_chain<2>(c, a, sms, "fit.chain")) ||
-              (m0 <= 4 && try_chain<4>(c, a, sms, "fit.chain")) || (m0 <= 8 && try_chain<8>(c, a, sms, "fit.chain")) ||
-              try_chain<16>(c, a, sms, "fit.chain");
-    if (!ok) return false;
-    used = a.J;
+    const int m0 = em ? std::atoi(em) : 8;
+    const u64 cap_of[5] = {chain_capacity<1>(sms), chain_capacity<2>(sms), chain_capacity<4>(sms),
+                           chain_capacity<8>(sms), chain_capacity<16>(sms)};
+    const int widths[5] = {1, 2, 4, 8, 16};
+    DevBuf<u32> carry[2] = {DevBuf<u32>(runs.n_runs + 1, s), DevBuf<u32>(runs.n_runs + 1, s)};
+    u32 pos = 0, top = live;
+    bool left_over = false;
+    for (int pass = 0; pos < n_bins; ++pass) {
+        u64 want = n_bins - pos;
+        if (pass == 0 && first_pass_bins > 0 && first_pass_bins < want) want = first_pass_bins;
+        int wi = 0;
+        while (wi < 5 && (widths[wi] < m0 || cap_of[wi] < want)) ++wi;
+        if (wi == 5) {
+            wi = 4;
+            want = cap_of[4];
+        }
+        if (want == 0) return false;
+        a.bin0 = pos;
+        a.bin_end = static_cast<u32>(pos + want);
+        a.carry_in = pass == 0 ? nullptr : carry[(pass + 1) & 1].p;
+        a.carry_out = carry[pass & 1].p;
+        std::pair<u32, bool> r;
+        switch (widths[wi]) {
+            case 1: r = run_pass<1>(c, a, "fit.chain"); break;
+            case 2: r = run_pass<2>(c, a, "fit.chain"); break;
+            case 4: r = run_pass<4>(c, a, "fit.chain"); break;
+            case 8: r = run_pass<8>(c, a, "fit.chain"); break;
+            default: r = run_pass<16>(c, a, "fit.chain"); break;
+        }
+        top = std::max(top, r.first);
+        left_over = r.second;
+        pos = a.bin_end;
+        if (!left_over) break;
+    }
+    // FFD never runs past its bin bound; greedy fill leaves what no pack took
+    if (ffd && left_over) throw EngineError(HBP_ERR_CUDA, "first-fit chain: bin capacity exceeded");
+    used = top;
     expand_heads(c, runs.n_items, item_bin, item_slot, take);
     return true;
 }

@@ -1141,6 +1141,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     // first item would have fitted the earlier), so FFD opens at most
     // 2 * ceil(sum / cap) + 1 bins: size the tree by that, not by n.
     i64 tree_bins = max_bins;
+    i64 est_bins = 0;
     if (ffd) {
         if (h_runs.empty()) h_runs = read_vector(c, run_len.p, n_runs);
         const auto h_items = read_vector(c, run_item.p, n_runs);
@@ -1150,6 +1151,11 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
             sum += static_cast<long double>(h_runs[k]) * static_cast<long double>(e - h_items[k]);
         }
         const i64 bound = static_cast<i64>(2 * std::ceil(sum / cap)) + 2 + bins0;
+        // FFD of sorted items is near the volume bound for small items and
+        // one bin per item above cap / 2: first chain pass sized by both
+        const long double vol = std::ceil(sum / cap);
+        est_bins = static_cast<i64>(std::max<long double>(static_cast<long double>(bins0 + bulk) * 1.02L, vol * 1.02L)) +
+                   1024;
         if (bound < tree_bins) tree_bins = bound;
     }
     const u64 live = static_cast<u64>(bins0) + bulk;
@@ -1162,7 +1168,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         ChainRuns cr{run_item.p, run_len.p, static_cast<u32>(n), n_runs, run_begin, n_runs};
         u32 used = 0;
         if (chain_fit(c, cr, leaves, static_cast<u32>(live), static_cast<u32>(ffd ? tree_bins : live), cap, ffd,
-                      item_bin, item_slot, take.p, used)) {
+                      item_bin, item_slot, take.p, static_cast<u32>(std::min<i64>(est_bins, tree_bins)), used)) {
             out.bins = ffd ? std::max<i64>(static_cast<i64>(live), used) : bins0;
             return out;
         }

@@ -74,12 +74,12 @@ struct ChainRuns {
     u32 n_items, n_runs, run_begin, run_end;
 };
 // Bins [0, live) hold `leaves`; FFD: bins [live, n_bins) start empty
-// (residual cap). Returns false when n_bins is too large for one resident
-// chain. `used` = 1 + the highest bin holding items. `take` (n_items,
-// zeroed; pre-placed items marked as heads with take 1 and their bin/slot)
-// is scratch for the head expansion.
+// (residual cap). Bins are covered by as many resident-chain passes as
+// needed (the first sized by first_pass_bins when non-zero). `used` = 1 + the
+// highest bin holding items. `take` (n_items, zeroed; pre-placed items marked
+// as heads with take 1 and their bin/slot) is scratch for the head expansion.
 bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins, u32 cap, bool ffd, u32* item_bin,
-               u32* item_slot, u32* take, u32& used);
+               u32* item_slot, u32* take, u32 first_pass_bins, u32& used);
 
 // item -> (bin, slot) for every item covered by a record; others get kNone.
 void expand_fit_records(Ctx& c, FitRecords rec, i64 n_records, i64 n_items, u32* item_bin, u32* item_slot);

@@ -2,6 +2,8 @@
 against the oracle restatement (itself pinned to the compiled reference in
 tests/test_oracle.py). Bit-exact on plan contents; FP64 metrics per iteration
 bit-exact, run-level means within 1e-9 relative (north star: 1e-6)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -118,6 +120,16 @@ def test_build_plan_c2_full_size(ctx, oracle):
     sg, so = ctx.simulate(got), oracle.simulate(want)
     assert np.array_equal(sg[1], so[1])
     assert sg[0].total_seconds == pytest.approx(so[0].total_seconds, rel=1e-9)
+
+
+@pytest.mark.skipif(os.environ.get("HBP_SKIP_C4") == "1", reason="HBP_SKIP_C4=1")
+def test_build_plan_c4_full_size(ctx, oracle):
+    # BASELINE config C4's corpus (C2 spec at 100M samples): bit-exact
+    # against the restatement (~80 s on one host core, ~5 GB of host memory)
+    L = hybrid(oracle, 100_000_000, 20250515)
+    want = oracle.build_plan(None, L, C2_GROUPS, l_best=16384, device_count=8, seed=1)
+    got = ctx.build_plan(None, L, C2_GROUPS, l_best=16384, device_count=8, seed=1).flat()
+    assert_same_plan(got, want)
 
 
 def test_general_ids(ctx, oracle):

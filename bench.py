@@ -229,6 +229,7 @@ def run_ours(args, rank, world, local):
         ms = []
         out = None
         for _ in range(k):
+            out = None  # the previous step's plan is freed before the next one (one plan alive, as in use)
             flush.zero_()
             torch.cuda.synchronize()
             if dist is not None:
@@ -241,12 +242,15 @@ def run_ours(args, rank, world, local):
             ms.append(a.elapsed_time(b))
         return ms, out
 
+    # the clock sampler starts before the warm-up: nvidia-smi's start-up takes
+    # the driver for ~100 ms and would land inside the first timed steps
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(1.0)
     for _ in range(args.warmup):
         step_device()
         step_e2e()
     launches0 = ctx.launches
-    clocks = Clocks(local)
-    clocks.start()
     dev_ms, plan = timed(step_device, args.steps)
     launches = (ctx.launches - launches0) // max(1, args.steps)
     e2e_ms, e2e_out = timed(step_e2e, args.steps)
@@ -278,7 +282,8 @@ def run_ours(args, rank, world, local):
                        "samples_per_rank": n, "groups": C2_GROUPS, "dp_devices": DEVICES, "seed": PLAN_SEED,
                        "parallelism": f"replicas x{world}", "l2": "flushed (256 MB write) before every step"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": tot_e2e / args.steps},
+                    "ms_per_step": tot_e2e / args.steps, "ms_steps": [round(x, 3) for x in e2e_ms]},
+            "ms_steps": [round(x, 3) for x in dev_ms],
             "gpu_launches": int(launches),
             "roofline": roof,
             "stages_ms": {k: round(v["ms"], 4) for k, v in sorted(stages.items(), key=lambda kv: -kv[1]["ms"])[:12]},

@@ -31,9 +31,15 @@ __global__ void k_nf_next(const u64* __restrict__ P, u64 m, u64 cap, u32* __rest
     for (u64 s = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; s < m;
          s += static_cast<u64>(gridDim.x) * blockDim.x) {
         const u64 limit = P[s] + cap;
-        u64 lo = s + 1;
-        u64 hi = s + cap < m ? s + cap : m;
-        // fast probe: most packs hold few items
+        const u64 top = s + cap < m ? s + cap : m;
+        // gallop from s + 1 (packs hold few items: the probes stay in the
+        // same cache lines), then bisect the last doubling
+        u64 lo = s + 1, step = 1;
+        while (lo + step <= top && P[lo + step] <= limit) {
+            lo += step;
+            step <<= 1;
+        }
+        u64 hi = lo + step - 1 < top ? lo + step - 1 : top;
         while (lo < hi) {
             const u64 mid = (lo + hi + 1) >> 1;
             if (P[mid] <= limit) lo = mid;
@@ -165,68 +171,14 @@ __global__ void __launch_bounds__(NF_B) k_nf_flags(const u32* __restrict__ nxt, 
     }
 }
 
-// Per pack: totals, freeze decision, and the packed scan input.
-__global__ void k_nf_packs(const u32* __restrict__ pstart, const u32* __restrict__ nxt, const u64* __restrict__ P,
-                           const u32* __restrict__ npacks_p, u64 tmin, u64* __restrict__ scanval) {
-    const u32 np = *npacks_p;
-    for (u32 p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
-        const u32 s = pstart[p];
-        const u32 e = nxt[s];
-        const u64 total = P[e] - P[s];
-        const bool frozen = total >= tmin;
-        scanval[p] = frozen ? ((1ull << 32) | (e - s)) : 0ull;
-    }
-}
-
-__global__ void k_nf_emit(const u64* __restrict__ F, const u32* __restrict__ pstart, const u32* __restrict__ nxt,
-                          const u64* __restrict__ P, const u32* __restrict__ npacks_p,
-                          const u64* __restrict__ scanned, const u64* __restrict__ scanval, PackSink sink,
-                          u64* __restrict__ newpool) {
-    const u32 np = *npacks_p;
-    const u64 mbase = *sink.n_members;
-    const u64 pbase = *sink.n_packs;
-    for (u32 p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
-        const u32 s = pstart[p];
-        const u32 e = nxt[s];
-        const u64 sc = scanned[p];
-        const u64 fz_elems = sc & 0xffffffffull;  // frozen elements before this pack
-        if (scanval[p] != 0) {
-            const u64 q = pbase + (sc >> 32);
-            const u64 dst = mbase + fz_elems;
-            u64 att = 0;
-            for (u32 i = s; i < e; ++i) {
-                const u64 v = F[i];
-                const u64 l = ent_len(v);
-                att += l * l;
-                sink.members[dst + (i - s)] = v;
-            }
-            sink.pack_off[q] = dst;
-            sink.pack_total[q] = static_cast<u32>(P[e] - P[s]);
-            sink.pack_att[q] = att;
-        } else {
-            const u64 dst = s - fz_elems;
-            for (u32 i = s; i < e; ++i) newpool[dst + (i - s)] = F[i];
-        }
-    }
-}
-
-__global__ void k_nf_commit(const u32* __restrict__ npacks_p, const u64* __restrict__ scanned,
-                            const u64* __restrict__ scanval, PackSink sink, u64 m, u64* __restrict__ newm) {
-    const u32 np = *npacks_p;
-    u64 tot = 0;
-    if (np > 0) tot = scanned[np - 1] + scanval[np - 1];
-    const u64 fz_elems = tot & 0xffffffffull, fz_packs = tot >> 32;
-    *sink.n_members += fz_elems;
-    *sink.n_packs += fz_packs;
-    *newm = m - fz_elems;
-}
-
 }  // namespace
 
 // Packs one pool by next-fit over `F` (already in visiting order); packs
-// with total >= tmin go to `sink`, the rest to `newpool`. Returns the new
-// pool size (one host sync).
-i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSink sink, u64* newpool) {
+// with total >= tmin go to `sink` after the n_members / n_packs already
+// there (updated), the rest to `newpool`. Returns the new pool size (one
+// host sync).
+i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSink sink, u64* newpool,
+                   u64& n_members, u64& n_packs) {
     if (m_signed <= 0) return 0;
     const u64 m = static_cast<u64>(m_signed);
     cudaStream_t s = c.stream;
@@ -236,8 +188,7 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     DevBuf<u32> spec(static_cast<size_t>(ntiles) * (NF_T / 32), s), flags(static_cast<size_t>(ntiles) * (NF_T / 32), s);
     DevBuf<u32> exitpos(ntiles, s), entry(ntiles, s);
     DevBuf<u8> allconv(ntiles, s);
-    DevBuf<u32> pstart(m, s), npacks(1, s);
-    DevBuf<u64> scanval(m, s), scanned(m, s), newm(1, s);
+    DevBuf<u64> newm(3, s);
 
     // prefix sums of lengths in visiting order (m + 1 entries)
     {
@@ -251,36 +202,63 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, 0, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
     LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
     LAUNCH(k_nf_flags, ntiles, NF_B, 0, s, nxt.p, spec.p, entry.p, m, flags.p);
-    // enumerate pack starts
+    // One scan over positions enumerates the frozen packs and emits every
+    // pack from its start position: value (frozen packs << 31 | frozen
+    // items) at each frozen pack start; a frozen pack goes to the sink at
+    // (packs before, items before), any other pack back to the pool at its
+    // position minus the frozen items before it (pack order kept).
     {
         const u32* fl = flags.p;
-        u32* ps = pstart.p;
-        u32* np = npacks.p;
+        const u32* nx = nxt.p;
+        const u64* Pp = P.p;
+        u64* nm = newm.p;
         const i64 mm = static_cast<i64>(m);
-        scan_exclusive<u32>(
-            mm, [=] __device__(i64 i) { return (fl[i >> 5] >> (i & 31)) & 1u; },
-            [=] __device__(i64 i, u32 v) {
-                const u32 f = (fl[i >> 5] >> (i & 31)) & 1u;
-                if (f) ps[v] = static_cast<u32>(i);
-                if (i == mm - 1) *np = v + f;
-            },
-            s, c.scan);
-    }
-    // freeze decision + offsets. Packs <= m; the scan runs over m slots and
-    // the kernels read the live pack count from device memory.
-    CUDA_CHECK(cudaMemsetAsync(scanval.p, 0, sizeof(u64) * m, s));
-    LAUNCH(k_nf_packs, grid_for(m, 256, 148u * 16u), 256, 0, s, pstart.p, nxt.p, P.p, npacks.p, tmin, scanval.p);
-    {
-        const u64* sv = scanval.p;
-        u64* so = scanned.p;
+        const u64 mbase = n_members, pbase = n_packs;
+        constexpr u64 kElems = (1ull << 31) - 1;
+        auto frozen_value = [=] __device__(i64 i) -> u64 {
+            if (!((fl[i >> 5] >> (i & 31)) & 1u)) return 0ull;
+            const u32 e = nx[i];
+            return Pp[e] - Pp[i] >= tmin ? ((1ull << 31) | (e - static_cast<u64>(i))) : 0ull;
+        };
         scan_exclusive<u64>(
-            static_cast<i64>(m), [=] __device__(i64 i) { return sv[i]; }, [=] __device__(i64 i, u64 v) { so[i] = v; },
-            s, c.scan);
+            mm, frozen_value,
+            [=] __device__(i64 i, u64 v) {
+                const u64 own = frozen_value(i);
+                if (i == mm - 1) {  // totals: pool size and sink counters for the next round
+                    const u64 t = v + own;
+                    nm[0] = static_cast<u64>(mm) - (t & kElems);
+                    nm[1] = mbase + (t & kElems);
+                    nm[2] = pbase + (t >> 31);
+                    *sink.n_members = nm[1];
+                    *sink.n_packs = nm[2];
+                }
+                if (!((fl[i >> 5] >> (i & 31)) & 1u)) return;
+                const u32 e = nx[i];
+                const u64 fz_elems = v & kElems;
+                if (own) {
+                    const u64 q = pbase + (v >> 31);
+                    const u64 dst = mbase + fz_elems;
+                    u64 att = 0;
+                    for (u64 k = static_cast<u64>(i); k < e; ++k) {
+                        const u64 x = F[k];
+                        const u64 l = ent_len(x);
+                        att += l * l;
+                        sink.members[dst + (k - i)] = x;
+                    }
+                    sink.pack_off[q] = dst;
+                    sink.pack_total[q] = static_cast<u32>(Pp[e] - Pp[i]);
+                    sink.pack_att[q] = att;
+                } else {
+                    const u64 dst = static_cast<u64>(i) - fz_elems;
+                    for (u64 k = static_cast<u64>(i); k < e; ++k) newpool[dst + (k - i)] = F[k];
+                }
+            },
+            s, c.scan, "nf.freeze_emit", 24.0);
     }
-    LAUNCH(k_nf_emit, grid_for(m, 256, 148u * 16u), 256, 0, s, F, pstart.p, nxt.p, P.p, npacks.p, scanned.p,
-           scanval.p, sink, newpool);
-    LAUNCH(k_nf_commit, 1, 1, 0, s, npacks.p, scanned.p, scanval.p, sink, m, newm.p);
-    return static_cast<i64>(read_scalar(c, newm.p));
+    const auto t = read_vector(c, newm.p, 3);
+    n_members = t[1];
+    n_packs = t[2];
+    return static_cast<i64>(t[0]);
 }
 
 }  // namespace hbp_b200

@@ -480,6 +480,7 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
     DevBuf<u64> counters(2, s);
     counters.zero();
     PackSink sink{out.isf_members.p, out.isf_off.p, out.isf_total.p, out.isf_att.p, counters.p, counters.p + 1};
+    u64 n_members = 0, n_packs = 0;  // host copies of the sink counters
     DevBuf<u64> A(m, s), Bf(m, s);
     CUDA_CHECK(cudaMemcpyAsync(A.p, pool_in, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
     u64 cur = m;
@@ -499,7 +500,7 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
             fy_source_positions(c, rs, static_cast<i64>(cur), src.p);
             gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(cur));
             trace_mark(c, "isf.shuffle");
-            cur = static_cast<u64>(nextfit_freeze(c, Bf.p, static_cast<i64>(cur), cap, tmin, sink, A.p));
+            cur = static_cast<u64>(nextfit_freeze(c, Bf.p, static_cast<i64>(cur), cap, tmin, sink, A.p, n_members, n_packs));
             trace_mark(c, "isf.nextfit+freeze");
         }
         residue_ffd = st.kind == HBP_STRATEGY_ISF;
@@ -516,9 +517,8 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         throw EngineError(HBP_ERR_VALIDATION, "packing strategy not available in the GPU engine: " +
                                                   std::string(st.kind == HBP_STRATEGY_BFS ? "bfs" : "spfhp"));
     }
-    const auto cnts = read_vector(c, counters.p, 2);
-    out.n_isf_members = cnts[0];
-    out.n_isf = cnts[1];
+    out.n_isf_members = n_members;
+    out.n_isf = n_packs;
     out.n_residue = cur;
     out.leaves.alloc(out.n_isf + cur + 1, s);
     if (out.n_isf > 0) {

@@ -27,9 +27,11 @@ struct PackSink {
     u64* n_packs;
 };
 
-// nextfit.cu: next-fit over F, freeze packs with total >= tmin into sink,
-// the rest (in pack order) into newpool. Returns the new pool size.
-i64 nextfit_freeze(Ctx& c, const u64* F, i64 m, u32 cap, u64 tmin, PackSink sink, u64* newpool);
+// nextfit.cu: next-fit over F, freeze packs with total >= tmin into sink
+// (after the n_members / n_packs it already holds; both updated), the rest
+// (in pack order) into newpool. Returns the new pool size.
+i64 nextfit_freeze(Ctx& c, const u64* F, i64 m, u32 cap, u64 tmin, PackSink sink, u64* newpool, u64& n_members,
+                   u64& n_packs);
 
 // ---- first-fit by runs (firstfit.cu) -------------------------------------
 //

@@ -65,9 +65,12 @@ def dist_env():
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # The per-reason fields (clocks_event_reasons.hw_slowdown, ...) stall the
+    # driver for 10-40 ms per sample (measured: they land inside timed steps);
+    # the `active` bitmask carries the same reasons and does not.
+    Q = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
@@ -87,18 +90,18 @@ class Clocks:
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 5:
                 continue
             try:
                 sm.append(float(f[1]))
                 smax = float(f[2])
+                mask = int(f[4], 16)
             except ValueError:
                 continue
-            for name, v in zip(names, f[5:9]):
-                if v.lower() == "active":
+            for bit, name in self.BITS.items():
+                if mask & bit:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
                 "reasons": sorted(reasons), "samples": len(sm)}
@@ -214,13 +217,22 @@ def run_ours(args, rank, world, local):
         plan.simulate(prof)
         return plan
 
+    phases = os.environ.get("HBP_BENCH_PHASES") == "1"
+
     def step_e2e():
+        t0 = time.perf_counter()
         s, keep = abi.make_samples(None, h_len.numpy(), "bench")
         plan = ctx.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
+        t1 = time.perf_counter()
         m = plan.report()
         st = plan.simulate(prof)
+        t2 = time.perf_counter()
         v = abi.PlanView()
         ctx.check(lib.hbp_plan_view_get(ctx.h, plan.h, C.byref(v)))
+        if phases:
+            t3 = time.perf_counter()
+            print(f"e2e phases ms: build {1e3 * (t1 - t0):.1f} report+sim {1e3 * (t2 - t1):.1f} "
+                  f"view {1e3 * (t3 - t2):.1f}", file=sys.stderr, flush=True)
         d2h = (v.n_iterations * 4 + (v.n_iterations + 1) * 8 + v.n_devices * 4 + (v.n_devices + 1) * 8
                + v.n_packs * 24 + (v.n_packs + 1) * 8 + v.n_members * 4 + 5 * 8 + 3 * 8)
         return plan, d2h, m.abr, st.total_seconds

@@ -376,10 +376,10 @@ void expand_heads(Ctx& c, u64 n, u32* item_bin, u32* item_slot, const u32* take)
 }
 
 bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins, u32 cap, bool ffd, u32* item_bin,
-               u32* item_slot, u32* take, u32 first_pass_bins, u32& used) {
+               u32* item_slot, u32* take, u32 first_pass_bins, u32& used, bool expand) {
     used = live;
     if (runs.run_begin >= runs.run_end || n_bins == 0) {
-        expand_heads(c, runs.n_items, item_bin, item_slot, take);
+        if (expand) expand_heads(c, runs.n_items, item_bin, item_slot, take);
         return true;
     }
     cudaStream_t s = c.stream;
@@ -448,7 +448,7 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     // FFD never runs past its bin bound; greedy fill leaves what no pack took
     if (ffd && left_over) throw EngineError(HBP_ERR_CUDA, "first-fit chain: bin capacity exceeded");
     used = top;
-    expand_heads(c, runs.n_items, item_bin, item_slot, take);
+    if (expand) expand_heads(c, runs.n_items, item_bin, item_slot, take);
     return true;
 }
 

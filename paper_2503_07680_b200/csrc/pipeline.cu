@@ -99,7 +99,11 @@ __global__ void k_group_keys(const u32* __restrict__ len32, u64 n, const int64_t
         while (g < ng - 1 && static_cast<int64_t>(L) > glen[g]) ++g;
         key[i] = static_cast<u32>(g);
         val[i] = static_cast<u32>(i);
-        atomicAdd(&s_cnt[g < 64 ? g : 63], 1ull);
+        // one shared atomic per group present in the warp (not per sample:
+        // with two groups every lane hits the same counter)
+        const unsigned peers = __match_any_sync(__activemask(), g);
+        if ((threadIdx.x & 31u) == static_cast<unsigned>(__ffs(peers) - 1))
+            atomicAdd(&s_cnt[g < 64 ? g : 63], static_cast<unsigned long long>(__popc(peers)));
     }
     __syncthreads();
     for (int g = threadIdx.x; g < ng && g < 64; g += blockDim.x)

@@ -81,7 +81,9 @@ struct ChainRuns {
 // highest bin holding items. `take` (n_items, zeroed; pre-placed items marked
 // as heads with take 1 and their bin/slot) is scratch for the head expansion.
 bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins, u32 cap, bool ffd, u32* item_bin,
-               u32* item_slot, u32* take, u32 first_pass_bins, u32& used);
+               u32* item_slot, u32* take, u32 first_pass_bins, u32& used, bool expand = true);
+// Heads (item_bin / item_slot / take at each take's first item) -> every item.
+void expand_heads(Ctx& c, u64 n, u32* item_bin, u32* item_slot, const u32* take);
 
 // item -> (bin, slot) for every item covered by a record; others get kNone.
 void expand_fit_records(Ctx& c, FitRecords rec, i64 n_records, i64 n_items, u32* item_bin, u32* item_slot);

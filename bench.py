@@ -264,6 +264,7 @@ def run_ours(args, rank, world, local):
         step_e2e()
     launches0 = ctx.launches
     dev_ms, plan = timed(step_device, args.steps)
+    plan = None  # one plan alive at a time (the e2e loop would otherwise grow the memory pool in its first step)
     launches = (ctx.launches - launches0) // max(1, args.steps)
     e2e_ms, e2e_out = timed(step_e2e, args.steps)
     ck = clocks.stop()
@@ -413,7 +414,7 @@ def cpu_baseline_leg(lib):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=0, help="override corpus size (default 10M)")

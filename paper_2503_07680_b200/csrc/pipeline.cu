@@ -587,10 +587,16 @@ u64 batch_group(Ctx& c, const DeviceCorpus& corpus, PackTable& T, u64 pbase, u64
         DevBuf<u32> w(P, s), tk(P, s), tv(P, s);
         LAUNCH(k_iota, G(P), kB, 0, s, order.p, P);
         const u64* att = T.att.p + pbase;
+        // attention <= cap^2: sort only the bits it can have (one 32-bit
+        // pass set when cap^2 < 2^32, else the low word then the few high bits)
+        const u64 amax = static_cast<u64>(cap) * cap;
+        const int hi_bits = bits_for(amax >> 32);
         LAUNCH(k_att_words, G(P), kB, 0, s, att, order.p, P, false, w.p);
-        radix_sort_pairs(c, w.p, order.p, static_cast<i64>(P), 32, true, tk.p, tv.p);
-        LAUNCH(k_att_words, G(P), kB, 0, s, att, order.p, P, true, w.p);
-        radix_sort_pairs(c, w.p, order.p, static_cast<i64>(P), 32, true, tk.p, tv.p);
+        radix_sort_pairs(c, w.p, order.p, static_cast<i64>(P), (amax >> 32) ? 32 : bits_for(amax), true, tk.p, tv.p);
+        if (amax >> 32) {
+            LAUNCH(k_att_words, G(P), kB, 0, s, att, order.p, P, true, w.p);
+            radix_sort_pairs(c, w.p, order.p, static_cast<i64>(P), hi_bits, true, tk.p, tv.p);
+        }
     } else {
         fy_source_positions(c, derive_seed(seed, "pack-batching", static_cast<uint64_t>(gi)), static_cast<i64>(P),
                             order.p);
@@ -602,19 +608,27 @@ u64 batch_group(Ctx& c, const DeviceCorpus& corpus, PackTable& T, u64 pbase, u64
                slots.p, igroup.p);
     if (rem == 0) return nfull;
     // spill tail: gather its samples, sort (length desc, id asc), redistribute
-    std::vector<u32> tail = read_vector(c, order.p + nfull * N, rem);
-    for (auto& t : tail) t += static_cast<u32>(pbase);
-    std::vector<u32> tcnt(rem);
+    // tail packs and their sizes in one read-back
+    DevBuf<u32> dtail(rem, s), dtcnt(rem, s);
+    {
+        const u32* op = order.p + nfull * N;
+        const u32* cp = T.cnt.p;
+        u32* tp = dtail.p;
+        u32* np = dtcnt.p;
+        const u32 pb = static_cast<u32>(pbase);
+        for_each_index(c, rem, [=] __device__(u64 t) {
+            tp[t] = op[t] + pb;
+            np[t] = cp[op[t] + pb];
+        });
+    }
+    std::vector<u32> tail = read_vector(c, dtail.p, rem), tcnt = read_vector(c, dtcnt.p, rem);
     std::vector<u64> toff(rem);
     u64 k = 0;
     for (u32 t = 0; t < rem; ++t) {
-        tcnt[t] = read_vector(c, T.cnt.p + tail[t], 1)[0];
         toff[t] = k;
         k += tcnt[t];
     }
-    DevBuf<u32> dtail(rem, s);
     DevBuf<u64> dtoff(rem, s);
-    CUDA_CHECK(cudaMemcpyAsync(dtail.p, tail.data(), sizeof(u32) * rem, cudaMemcpyHostToDevice, s));
     CUDA_CHECK(cudaMemcpyAsync(dtoff.p, toff.data(), sizeof(u64) * rem, cudaMemcpyHostToDevice, s));
     DevBuf<u64> spill(k + 1, s);
     DevBuf<u32> dev_of(k + 1, s);

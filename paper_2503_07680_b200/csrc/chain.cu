@@ -15,8 +15,11 @@
 // consecutive bins (lane l holds bins j*32M + l*M + i, i < M, in registers).
 // Per block of 32 runs it receives the 32 counts its predecessor left,
 // marks the runs its bins can take (c > 0 and s <= its max residual), serves
-// those in order with one warp scan each, and passes the 32 remaining counts
-// on. Every warp is resident (cooperative launch), so after the chain fills
+// those in order and passes the 32 remaining counts on. The serve of the
+// frontier warp is on the critical path of every block, so the chain keeps
+// it short (see serve) and writes nothing but the input counts of its
+// active cells; a replay kernel re-serves those cells in parallel and
+// writes the heads (item -> bin, slot). Every warp is resident (cooperative launch), so after the chain fills
 // all bins work on different run blocks at once.
 //
 // Hand-off: each count travels as one 64-bit word (block tag << 32 | count)
@@ -58,7 +61,16 @@ struct ChainArgs {
     u32* out;                  // [0] 1 + highest bin with items, [1] FFD overflow
     unsigned long long* prof;  // HBP_TRACE: per warp [wait in, serve, wait out, served runs]
     u32 sleep;                 // ns of back-off per failed poll (idle warps yield issue slots)
+    u32* hist;                 // [J][nblocks][32] input counts of active cells (chain -> replay)
+    u32* hact;                 // [J][nblocks] active-run mask of every cell (0: nothing to serve)
+    unsigned long long* tl;    // HBP_CHAIN_TL: globaltimer when block b reached warp j [J][nblocks]
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
@@ -77,6 +89,131 @@ __device__ __forceinline__ void st_relaxed_u32(u32* p, u32 v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Serves one block of 32 runs (counts c, lengths s, item ends end_item; `act`
+// marks the runs with c > 0 and s <= wmax) against the warp's 32*M bins, in
+// run order, and leaves in c what passes on. STORE writes one head (bin,
+// slot, take) at the first item of every take; the chain serves without
+// storing (scattered stores would sit on its critical path) and the replay
+// re-serves with them.
+//
+// Per run the critical path is short: the lanes with room are known from
+// each lane's max residual (one ballot); every lane computes what its M bins
+// can take (independent divisions by a shuffled reciprocal) and their
+// in-lane prefix; the run then walks the lanes with room in order -- one
+// shuffle per lane, usually one or two lanes -- or, when it spans more,
+// one saturating warp scan. The takes themselves (residuals, counts, heads)
+// are off the path: every lane applies its own once it knows how many
+// items it receives.
+template <int M, bool STORE>
+__device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 end_item, u32& c, u32 (&R)[M],
+                                      u32 (&N)[M], u32& wmax, u64 base, u32 lane) {
+    const u32 inv_own = s ? 0xffffffffu / s : 0u;
+    u32 lmax = 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) lmax = max(lmax, R[i]);
+    while (act) {
+        const int r = __ffs(act) - 1;
+        act &= act - 1;
+        const u32 S = __shfl_sync(0xffffffffu, s, r);
+        const u32 inv = __shfl_sync(0xffffffffu, inv_own, r);
+        const u32 C0 = __shfl_sync(0xffffffffu, c, r);
+        u32 off = 0;
+        if (STORE) off = __shfl_sync(0xffffffffu, end_item - c, r);
+        unsigned room = __ballot_sync(0xffffffffu, lmax >= S);
+        if (!room) continue;
+        u32 capl[M], pre[M + 1];
+        pre[0] = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            u32 q = __umulhi(R[i], inv);  // floor(R / S): exact after two corrections
+            u32 rem = R[i] - q * S;
+            if (rem >= S) { ++q; rem -= S; }
+            if (rem >= S) ++q;
+            capl[i] = min(q, C0);  // no bin takes more than the run has
+            pre[i + 1] = min(pre[i] + capl[i], C0);
+        }
+        const u32 lsum = pre[M];
+        // walk the lanes with room in bin order
+        u32 left = C0, mine = 0;
+        for (int k = 0; k < 3 && left > 0 && room; ++k) {
+            const int f = __ffs(room) - 1;
+            room &= room - 1;
+            const u32 lf = __shfl_sync(0xffffffffu, lsum, f);
+            if (static_cast<int>(lane) == f) mine = left;
+            left -= min(lf, left);
+        }
+        if (left > 0 && room) {  // spans many lanes: one scan over the rest
+            const u32 v = (room >> lane) & 1u ? lsum : 0u;
+            u32 incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= static_cast<u32>(o)) incl = min(incl + t, left);
+            }
+            u32 excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 0;
+            if (v > 0 && excl < left) mine = left - excl;
+            left -= __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (static_cast<int>(lane) == r) c = left;
+        if (mine > 0) {  // this lane receives `mine` items of the run
+            u32 nl = 0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const u32 t = pre[i] < mine ? min(capl[i], mine - pre[i]) : 0u;
+                if (STORE && t > 0) {
+                    const u32 o = off + (C0 - mine) + pre[i];
+                    a.item_bin[o] = static_cast<u32>(base + lane * M + i);
+                    a.item_slot[o] = N[i];
+                    a.take[o] = t;
+                }
+                R[i] -= t * S;
+                N[i] += t;
+                nl = max(nl, R[i]);
+            }
+            lmax = nl;
+        }
+    }
+    wmax = __reduce_max_sync(0xffffffffu, lmax);
+}
+
+// Loads the warp's 32*M bins (lane-major) from the leaves; empty bins past
+// `live` open at capacity under FFD.
+template <int M>
+__device__ __forceinline__ u32 load_bins(const ChainArgs& a, u64 base, u32 lane, u32 (&R)[M], u32 (&N)[M]) {
+    u32 lmax = 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const u64 bin = base + lane * M + i;
+        u64 leaf = 0;
+        if (bin < a.bin_end) {
+            if (bin < a.live) leaf = a.leaves[bin];
+            else if (a.ffd) leaf = static_cast<u64>(a.cap) << 32;  // empty bin
+        }
+        R[i] = static_cast<u32>(leaf >> 32);
+        N[i] = static_cast<u32>(leaf);
+        lmax = max(lmax, R[i]);
+    }
+    return __reduce_max_sync(0xffffffffu, lmax);
+}
+
+// 1 + the highest bin of the warp holding items (0: none); with `write`,
+// stores the bins back to the leaves.
+template <int M>
+__device__ __forceinline__ u32 store_bins(const ChainArgs& a, u64 base, u32 lane, const u32 (&R)[M],
+                                          const u32 (&N)[M], bool write) {
+    u32 top = 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const u64 bin = base + lane * M + i;
+        if (bin < a.bin_end) {
+            if (write && (bin < a.live || N[i] > 0)) a.leaves[bin] = (static_cast<u64>(R[i]) << 32) | N[i];
+            if (N[i] > 0) top = static_cast<u32>(bin + 1);
+        }
+    }
+    return __reduce_max_sync(0xffffffffu, top);
+}
+
 template <int M>
 __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a) {
     constexpr int kWarps = warps_for<M>();
@@ -91,24 +228,10 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
     __syncthreads();
     if (j >= a.J) return;  // no CTA-wide barriers below
 
-    // row-major: row i of the warp holds bins base + 32 i + lane, so a run
-    // walks the rows in bin order and stops at the row that uses it up
+    // lane-major: lane l holds bins base + l*M + i (bin order = lane order)
     const u64 base = a.bin0 + static_cast<u64>(j) * 32 * M;
-    u32 R[M], N[M], rowmax[M];
-    u32 wmax = 0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        const u64 bin = base + 32 * i + lane;
-        u64 leaf = 0;
-        if (bin < a.bin_end) {
-            if (bin < a.live) leaf = a.leaves[bin];
-            else if (a.ffd) leaf = static_cast<u64>(a.cap) << 32;  // empty bin
-        }
-        R[i] = static_cast<u32>(leaf >> 32);
-        N[i] = static_cast<u32>(leaf);
-        rowmax[i] = __reduce_max_sync(0xffffffffu, R[i]);
-        wmax = max(wmax, rowmax[i]);
-    }
+    u32 R[M], N[M];
+    u32 wmax = load_bins<M>(a, base, lane, R, N);
     const bool head = j == 0, tail = j + 1 == a.J;
     const bool in_global = w == 0, out_global = w + 1 == kWarps;
     volatile unsigned long long* sin = s_ring[w][0];
@@ -150,55 +273,31 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
                 if (a.sleep) __nanosleep(a.sleep);
             c = static_cast<u32>(v);
         }
-        unsigned act = __ballot_sync(0xffffffffu, c > 0 && s <= wmax);  // every lane has its c
+        const unsigned act = __ballot_sync(0xffffffffu, c > 0 && s <= wmax);  // every lane has its c
+        const u32 n_act = __popc(act);
+        unsigned long long t_arr = 0;
+        if (a.tl) t_arr = globaltimer();
         if (a.prof) {
             t1 = clock64();
             pf[0] += t1 - t0;
-            pf[3] += __popc(act);
+            pf[3] += n_act;
             t0 = t1;
         }
         if (!head && lane == 0) {
             if (in_global) st_relaxed_u32(a.gcons + g * kStride, b + 1);
             else reinterpret_cast<volatile u32*>(s_cons)[w] = b + 1;
         }
-
-        while (act) {
-            const int r = __ffs(act) - 1;
-            act &= act - 1;
-            const u32 S = __shfl_sync(0xffffffffu, s, r);
-            if (S > wmax) continue;
-            const u32 C0 = __shfl_sync(0xffffffffu, c, r);
-            u32 left = C0;
-            u32 off = __shfl_sync(0xffffffffu, end_item - c, r);
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                if (left == 0 || rowmax[i] < S) continue;  // warp-uniform
-                const u32 q = 32 * i + lane;
-                const u32 capl = R[i] >= S ? R[i] / S : 0u;
-                const u32 incl = warp_inclusive_scan(capl);
-                const u32 excl = incl - capl;
-                const u32 tot = __shfl_sync(0xffffffffu, incl, 31);
-                const u32 t = excl < left ? min(capl, left - excl) : 0u;
-                if (t > 0) {  // one head per take; expand_heads fills the rest
-                    a.item_bin[off + excl] = static_cast<u32>(base + q);
-                    a.item_slot[off + excl] = N[i];
-                    a.take[off + excl] = t;
-                    R[i] -= t * S;
-                    N[i] += t;
-                }
-                const u32 used = tot < left ? tot : left;
-                left -= used;
-                off += used;
-                rowmax[i] = __reduce_max_sync(0xffffffffu, R[i]);
+        if (act) {
+            if (a.hist) {  // the replay re-serves this cell from its input counts
+                a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane] = c;
+                if (lane == 0) a.hact[static_cast<u64>(j) * a.nblocks + b] = act;
             }
-            if (static_cast<int>(lane) == r) c = left;
-            if (left != C0) {
-                wmax = 0;
-#pragma unroll
-                for (int i = 0; i < M; ++i) wmax = max(wmax, rowmax[i]);
-            }
+            serve<M, false>(a, act, s, end_item, c, R, N, wmax, base, lane);
+        } else if (a.hist && lane == 0) {
+            a.hact[static_cast<u64>(j) * a.nblocks + b] = 0;
         }
-
+        unsigned long long t_srv = 0;
+        if (a.tl) t_srv = globaltimer();
         if (a.prof) {
             t1 = clock64();
             pf[1] += t1 - t0;
@@ -229,21 +328,42 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
             if (__any_sync(0xffffffffu, c > 0) && lane == 0) atomicOr(a.out + 1, 1u);
         }
         if (a.prof) pf[2] += clock64() - t0;
+        if (a.tl && lane == 0) {  // arrival | serve ns << 40 | active runs << 56 (timeline)
+            const unsigned long long d = min(t_srv - t_arr, (1ull << 16) - 1);
+            a.tl[static_cast<u64>(j) * a.nblocks + b] =
+                (t_arr & ((1ull << 40) - 1)) | (d << 40) | (static_cast<unsigned long long>(n_act) << 56);
+        }
     }
     if (a.prof && lane == 0)
         for (int i = 0; i < 4; ++i) a.prof[4ull * j + i] = pf[i];
-
-    u32 top = 0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        const u64 bin = base + 32 * i + lane;
-        if (bin < a.bin_end) {
-            if (bin < a.live || N[i] > 0) a.leaves[bin] = (static_cast<u64>(R[i]) << 32) | N[i];
-            if (N[i] > 0) top = static_cast<u32>(bin + 1);
-        }
-    }
-    top = __reduce_max_sync(0xffffffffu, top);
+    // with a replay to follow, the bins stay as loaded for it
+    const u32 top = store_bins<M>(a, base, lane, R, N, a.hist == nullptr);
     if (lane == 0 && top) atomicMax(a.out, top);
+}
+
+// Replay of a chain pass: every warp re-serves, from the input counts the
+// chain recorded, the cells where runs were active, now writing the heads.
+// Warps are independent here, so the scattered head stores run in parallel
+// across the GPU instead of on the chain's critical path.
+template <int M>
+__global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
+    const u32 lane = threadIdx.x & 31u;
+    const u32 j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= a.J) return;
+    const u64 base = a.bin0 + static_cast<u64>(j) * 32 * M;
+    u32 R[M], N[M];
+    u32 wmax = load_bins<M>(a, base, lane, R, N);
+    for (u32 b = 0; b < a.nblocks; ++b) {
+        const u32 act = a.hact[static_cast<u64>(j) * a.nblocks + b];
+        if (!act) continue;
+        const u32 k = a.run_begin + b * 32 + lane;
+        const bool valid = k < a.run_end;
+        const u32 s = valid ? a.run_len[k] : 0u;
+        const u32 end_item = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
+        u32 c = a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane];
+        serve<M, true>(a, act, s, end_item, c, R, N, wmax, base, lane);
+    }
+    store_bins<M>(a, base, lane, R, N, true);
 }
 
 // Bins one resident chain of width M can hold.
@@ -275,12 +395,18 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     a.gring = gring.p;
     a.gcons = gcons.p;
     a.out = out.p;
-    DevBuf<unsigned long long> prof;
+    DevBuf<unsigned long long> prof, tl;
     a.prof = nullptr;
+    a.tl = nullptr;
     if (c.trace) {
         prof.alloc(4ull * J, s);
         prof.zero();
         a.prof = prof.p;
+        if (std::getenv("HBP_CHAIN_TL")) {
+            tl.alloc(static_cast<size_t>(J) * a.nblocks, s);
+            tl.zero();
+            a.tl = tl.p;
+        }
     }
     void* args[] = {&a};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -289,8 +415,20 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
         CUDA_CHECK(cudaEventCreate(&e1));
         CUDA_CHECK(cudaEventRecord(e0, s));
     }
+    // the chain serves without head stores and records the input counts of
+    // its active cells; the replay then writes the heads in parallel
+    const bool replay = std::getenv("HBP_CHAIN_NOREPLAY") == nullptr;
+    DevBuf<u32> hist, hact;
+    a.hist = a.hact = nullptr;
+    if (replay) {
+        hist.alloc(static_cast<size_t>(J) * a.nblocks * 32, s);
+        hact.alloc(static_cast<size_t>(J) * a.nblocks, s);
+        a.hist = hist.p;
+        a.hact = hact.p;
+    }
     LAUNCH_COOP(name, 0.0, k_ff_chain<M>, dim3(G), dim3(kWarps * 32), smem, s, args);
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
+    if (replay) LAUNCH_B("fit.replay", 0.0, k_ff_replay<M>, (J + 7) / 8, 256, 0, s, a);
     const auto o = read_vector(c, out.p, 2);
     if (c.trace) {
         float ms = 0;
@@ -303,6 +441,15 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
                      a.ffd ? "ffd" : "fill", a.run_begin, a.run_end, a.nblocks, a.bin0, a.bin_end, a.live, M, J, G,
                      o[0], o[1], ms);
         const auto pf = read_vector(c, prof.p, 4ull * J);
+        if (const char* tlf = std::getenv("HBP_CHAIN_TL")) {  // [J, nblocks, ffd, M] + timeline, appended
+            const auto tv = read_vector(c, tl.p, static_cast<size_t>(J) * a.nblocks);
+            if (FILE* f = std::fopen(tlf, "ab")) {
+                const u32 hdr[4] = {J, a.nblocks, static_cast<u32>(a.ffd), static_cast<u32>(M)};
+                std::fwrite(hdr, 4, 4, f);
+                std::fwrite(tv.data(), 8, tv.size(), f);
+                std::fclose(f);
+            }
+        }
         if (const char* dump = std::getenv("HBP_CHAIN_DUMP")) {  // per-warp counters, appended
             if (FILE* f = std::fopen(dump, "ab")) {
                 const u32 hdr[4] = {J, a.nblocks, static_cast<u32>(M), static_cast<u32>(a.ffd)};

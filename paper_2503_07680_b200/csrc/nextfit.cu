@@ -50,48 +50,73 @@ __global__ void k_nf_next(const u64* __restrict__ P, u64 m, u64 cap, u32* __rest
 }
 
 // Per tile: speculative chain from the tile start, its exit, and whether all
-// possible entries merge into it inside the tile.
+// possible entries merge into it inside the tile. By pointer doubling in
+// shared memory rather than a serial walk: with f(x) = next(x) while it
+// stays in the tile (else x), F_k = f^(2^k) for k <= 11 gives every
+// position's last node in the tile, last(x) = F_11(x); a chain from e
+// merges into the chain from the tile start iff last(e) == last(start); the
+// speculative chain's nodes f^t(start), t <= its length, are found by
+// binary lifting, 11 lookups each, all in parallel.
+constexpr int NF_LV = 12;  // F_0 .. F_11 (2^11 = NF_T)
+
 __global__ void __launch_bounds__(NF_B) k_nf_tiles(const u32* __restrict__ nxt, u64 m, u32* __restrict__ spec,
                                                    u32* __restrict__ exitpos, u8* __restrict__ allconv) {
-    __shared__ u32 s_next[NF_T];
+    extern __shared__ unsigned short s_F[];  // [NF_LV][NF_T]
     __shared__ u32 s_spec[NF_T / 32];
     __shared__ int s_ok;
+    __shared__ u32 s_h0;
     const u64 a = static_cast<u64>(blockIdx.x) * NF_T;
     const u64 end = a + NF_T < m ? a + NF_T : m;
     const u32 len = static_cast<u32>(end - a);
-    for (u32 i = threadIdx.x; i < NF_T; i += NF_B) s_next[i] = i < len ? nxt[a + i] : static_cast<u32>(end);
+    for (u32 i = threadIdx.x; i < NF_T; i += NF_B) {
+        u32 f = i;
+        if (i < len) {
+            const u64 nx = nxt[a + i];
+            if (nx < end) f = static_cast<u32>(nx - a);
+        }
+        s_F[i] = static_cast<unsigned short>(f);
+    }
     for (u32 i = threadIdx.x; i < NF_T / 32; i += NF_B) s_spec[i] = 0;
     if (threadIdx.x == 0) s_ok = 1;
     __syncthreads();
+    for (int k = 0; k + 1 < NF_LV; ++k) {
+        const unsigned short* Fk = s_F + k * NF_T;
+        unsigned short* Fn = s_F + (k + 1) * NF_T;
+        for (u32 i = threadIdx.x; i < NF_T; i += NF_B) Fn[i] = Fk[Fk[i]];
+        __syncthreads();
+    }
+    const unsigned short* last = s_F + (NF_LV - 1) * NF_T;
+    const u32 last0 = last[0];
     if (threadIdx.x == 0) {
-        u64 s = a;
-        while (s < end) {
-            const u32 r = static_cast<u32>(s - a);
-            s_spec[r >> 5] |= 1u << (r & 31);
-            s = s_next[r];
+        // h0 = steps from the start to last0: largest t with f^t(0) != last0, plus one
+        u32 x = 0, t = 0;
+        for (int k = NF_LV - 2; k >= 0; --k) {
+            const u32 y = s_F[k * NF_T + x];
+            if (y != last0) {
+                x = y;
+                t += 1u << k;
+            }
         }
-        exitpos[blockIdx.x] = static_cast<u32>(s);
+        s_h0 = x == last0 ? t : t + 1;
+        exitpos[blockIdx.x] = static_cast<u32>(nxt[a + last0]);
     }
     __syncthreads();
+    const u32 h0 = s_h0;
+    for (u32 t = threadIdx.x; t <= h0; t += NF_B) {
+        u32 x = 0;
+#pragma unroll
+        for (int k = 0; k + 1 < NF_LV; ++k)
+            if ((t >> k) & 1u) x = s_F[k * NF_T + x];
+        atomicOr(&s_spec[x >> 5], 1u << (x & 31));
+    }
     // entries into this tile lie in [a, next(a-1)]
     if (a > 0) {
         const u64 hi_entry = nxt[a - 1];
         if (hi_entry >= end) {
             if (threadIdx.x == 0) s_ok = 0;
         } else {
-            for (u64 e = a + threadIdx.x; e <= hi_entry; e += NF_B) {
-                u64 s = e;
-                bool conv = false;
-                while (s < end) {
-                    const u32 r = static_cast<u32>(s - a);
-                    if (s_spec[r >> 5] & (1u << (r & 31))) {
-                        conv = true;
-                        break;
-                    }
-                    s = s_next[r];
-                }
-                if (!conv) s_ok = 0;
-            }
+            for (u64 e = a + threadIdx.x; e <= hi_entry; e += NF_B)
+                if (last[e - a] != last0) s_ok = 0;
         }
     }
     __syncthreads();
@@ -137,11 +162,18 @@ __global__ void k_nf_entries(const u32* __restrict__ nxt, const u32* __restrict_
     }
 }
 
-// Final start flags: walk from the entry until the speculative chain, then copy it.
+// Final start flags: walk from the entry until the speculative chain, then
+// copy it. Also the tile's freeze totals: frozen packs and their items
+// among the packs starting here (fp << 31 | fe, both < 2^31), and 1 + the
+// last pack start in the tile (0: none) for the emit kernel's carry-in.
 __global__ void __launch_bounds__(NF_B) k_nf_flags(const u32* __restrict__ nxt, const u32* __restrict__ spec,
-                                                   const u32* __restrict__ entry, u64 m, u32* __restrict__ flags) {
+                                                   const u32* __restrict__ entry, const u64* __restrict__ P, u64 m,
+                                                   u64 tmin, u32* __restrict__ flags, u64* __restrict__ tval,
+                                                   u32* __restrict__ tlast) {
     __shared__ u32 s_flags[NF_T / 32];
     __shared__ u64 s_conv;
+    __shared__ u64 s_sum[2];
+    __shared__ u32 s_last[2];
     const u64 a = static_cast<u64>(blockIdx.x) * NF_T;
     const u64 end = a + NF_T < m ? a + NF_T : m;
     for (u32 i = threadIdx.x; i < NF_T / 32; i += NF_B) s_flags[i] = 0;
@@ -157,17 +189,169 @@ __global__ void __launch_bounds__(NF_B) k_nf_flags(const u32* __restrict__ nxt, 
     }
     __syncthreads();
     const u64 conv = s_conv;
-    for (u32 w = threadIdx.x; w < NF_T / 32; w += NF_B) {
+    if (threadIdx.x < NF_T / 32) {  // two warps, one flags word each
+        const u32 w = threadIdx.x;
         const u64 p0 = a + 32ull * w;
-        if (p0 >= end) {
-            flags[static_cast<u64>(blockIdx.x) * (NF_T / 32) + w] = 0;
-            continue;
+        u32 bits = 0;
+        if (p0 < end) {
+            bits = spec[static_cast<u64>(blockIdx.x) * (NF_T / 32) + w];
+            // keep speculative bits at positions >= conv only
+            if (conv >= p0 + 32) bits = 0;
+            else if (conv > p0) bits &= ~((1u << (conv - p0)) - 1u);
+            bits |= s_flags[w];
         }
-        u32 bits = spec[static_cast<u64>(blockIdx.x) * (NF_T / 32) + w];
-        // keep speculative bits at positions >= conv only
-        if (conv >= p0 + 32) bits = 0;
-        else if (conv > p0) bits &= ~((1u << (conv - p0)) - 1u);
-        flags[static_cast<u64>(blockIdx.x) * (NF_T / 32) + w] = bits | s_flags[w];
+        flags[static_cast<u64>(blockIdx.x) * (NF_T / 32) + w] = bits;
+        u64 fe = 0, fp = 0;
+        for (u32 b = bits; b; b &= b - 1) {
+            const u64 st = p0 + __ffs(b) - 1;
+            const u32 e = nxt[st];
+            if (P[e] - P[st] >= tmin) {
+                fe += e - st;
+                ++fp;
+            }
+        }
+        u64 v = warp_sum((fp << 31) | fe);
+        u32 last = bits ? static_cast<u32>(p0 - a) + 32u - __clz(bits) : 0u;  // 1 + last start, tile-relative
+        last = warp_max(last);
+        if ((threadIdx.x & 31u) == 0) {
+            s_sum[threadIdx.x >> 5] = v;
+            s_last[threadIdx.x >> 5] = last;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tval[blockIdx.x] = s_sum[0] + s_sum[1];
+        const u32 l = max(s_last[0], s_last[1]);
+        tlast[blockIdx.x] = l ? static_cast<u32>(a) + l : 0u;
+    }
+}
+
+// Block-wide exclusive max over threads (values >= 0; 0 before thread 0).
+__device__ __forceinline__ u32 block_exclusive_max(u32 v, u32* smem) {
+    const unsigned lane = lane_id(), wid = warp_id();
+    u32 inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= static_cast<unsigned>(o)) inc = max(inc, t);
+    }
+    if (lane == 31) smem[wid] = inc;
+    __syncthreads();
+    u32 before = 0;
+    for (unsigned q = 0; q < wid; ++q) before = max(before, smem[q]);
+    u32 ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = 0;
+    __syncthreads();
+    return max(before, ex);
+}
+
+// Freeze and emit, one tile per CTA. Every position knows its pack (the last
+// start at or before it: within the thread, the block, or carried in from an
+// earlier tile) and the inclusive count fz of frozen items up to it, so it
+// goes to the sink at mbase + fz - (end - i) when its pack froze, else back
+// to the pool at i - fz (pack order kept). Positions are read and written
+// striped through shared memory; the blocked per-thread walk only computes
+// destinations. Frozen pack starts also write (offset, total).
+constexpr int EM_ITEMS = NF_T / NF_B;  // 8 positions per thread
+constexpr u32 kToSink = 0x80000000u;
+
+__global__ void __launch_bounds__(NF_B) k_nf_emit(const u64* __restrict__ F, u64 m, const u32* __restrict__ flags,
+                                                  const u32* __restrict__ nxt, const u64* __restrict__ P, u64 tmin,
+                                                  const u64* __restrict__ tpre, const u32* __restrict__ tlast,
+                                                  PackSink sink, u64 mbase, u64 pbase, u64* __restrict__ newpool,
+                                                  u64* __restrict__ totals, u32 ntiles) {
+    constexpr u64 kElems = (1ull << 31) - 1;
+    __shared__ u64 s_F[NF_T + NF_T / 32];
+    __shared__ u32 s_dst[NF_T + NF_T / 32];
+    __shared__ u32 s_fl[NF_T / 32];
+    __shared__ u64 s_red[33];
+    __shared__ u32 s_mx[NF_B / 32];
+    __shared__ u32 s_carry;
+    auto pad = [](u32 i) { return i + (i >> 5); };
+    const u64 a = static_cast<u64>(blockIdx.x) * NF_T;
+    const u32 len = static_cast<u32>((a + NF_T < m ? a + NF_T : m) - a);
+    const u32 t = threadIdx.x;
+    if (t < NF_T / 32) s_fl[t] = flags[static_cast<u64>(blockIdx.x) * (NF_T / 32) + t];
+#pragma unroll
+    for (int k = 0; k < EM_ITEMS; ++k) {
+        const u32 li = k * NF_B + t;
+        if (li < len) s_F[pad(li)] = F[a + li];
+    }
+    if (t == 0) {  // last pack start before the tile (tile 0 starts with one)
+        u32 c = 0;
+        for (u32 k = blockIdx.x; k > 0 && c == 0; --k) c = tlast[k - 1];
+        s_carry = c;
+    }
+    __syncthreads();
+    const u32 p0 = t * EM_ITEMS;
+    const u32 bits = (s_fl[p0 >> 5] >> (p0 & 31)) & 0xffu;
+    // own starts: end and frozen status
+    u32 e_of[EM_ITEMS];
+    u32 tot_of[EM_ITEMS];
+    u64 v = 0;
+#pragma unroll
+    for (int j = 0; j < EM_ITEMS; ++j) {
+        e_of[j] = 0;
+        tot_of[j] = 0;
+        if ((bits >> j) & 1u) {
+            const u64 st = a + p0 + j;
+            const u32 e = nxt[st];
+            const u64 tot = P[e] - P[st];
+            e_of[j] = e;
+            tot_of[j] = static_cast<u32>(tot);
+            if (tot >= tmin) v += (1ull << 31) | (e - st);
+        }
+    }
+    u64 btot;
+    const u64 ex = block_exclusive_scan<u64>(v, s_red, btot);
+    const u32 my_last = bits ? static_cast<u32>(a) + p0 + 32u - __clz(bits) : 0u;  // 1 + last own start
+    u32 prev = block_exclusive_max(my_last, s_mx);
+    if (prev == 0) prev = s_carry;
+    u64 run = tpre[blockIdx.x] + ex;  // frozen (packs << 31 | items) before my first position
+    // the pack open at my first position, if it started earlier
+    u32 e_cur = 0;
+    bool frz = false;
+    if (!(bits & 1u) && p0 < len) {
+        const u64 st = prev - 1;
+        e_cur = nxt[st];
+        frz = P[e_cur] - P[st] >= tmin;
+    }
+#pragma unroll
+    for (int j = 0; j < EM_ITEMS; ++j) {
+        const u32 li = p0 + j;
+        if (li >= len) break;
+        const u64 i = a + li;
+        if ((bits >> j) & 1u) {
+            e_cur = e_of[j];
+            frz = tot_of[j] >= tmin;
+            if (frz) {
+                const u64 q = pbase + (run >> 31);
+                sink.pack_off[q] = mbase + (run & kElems);
+                sink.pack_total[q] = tot_of[j];
+                run += (1ull << 31) | (e_cur - i);
+            }
+        }
+        const u64 fz = run & kElems;
+        s_dst[pad(li)] = frz ? static_cast<u32>(mbase + fz - (e_cur - i)) | kToSink : static_cast<u32>(i - fz);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < EM_ITEMS; ++k) {
+        const u32 li = k * NF_B + t;
+        if (li < len) {
+            const u32 d = s_dst[pad(li)];
+            const u64 x = s_F[pad(li)];
+            if (d & kToSink) sink.members[d & ~kToSink] = x;
+            else newpool[d] = x;
+        }
+    }
+    if (blockIdx.x == ntiles - 1 && t == 0) {  // totals: pool size and sink counters for the next round
+        const u64 tt = tpre[blockIdx.x] + btot;
+        totals[0] = m - (tt & kElems);
+        totals[1] = mbase + (tt & kElems);
+        totals[2] = pbase + (tt >> 31);
+        *sink.n_members = totals[1];
+        *sink.n_packs = totals[2];
     }
 }
 
@@ -199,62 +383,26 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     }
     LAUNCH_B("nf.next", 12.0 * m, k_nf_next, grid_for(m, 256, 148u * 32u), 256, 0, s, P.p, m, static_cast<u64>(cap),
              nxt.p);
-    LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, 0, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
-    LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
-    LAUNCH(k_nf_flags, ntiles, NF_B, 0, s, nxt.p, spec.p, entry.p, m, flags.p);
-    // One scan over positions enumerates the frozen packs and emits every
-    // pack from its start position: value (frozen packs << 31 | frozen
-    // items) at each frozen pack start; a frozen pack goes to the sink at
-    // (packs before, items before), any other pack back to the pool at its
-    // position minus the frozen items before it (pack order kept).
     {
-        const u32* fl = flags.p;
-        const u32* nx = nxt.p;
-        const u64* Pp = P.p;
-        u64* nm = newm.p;
-        const i64 mm = static_cast<i64>(m);
-        const u64 mbase = n_members, pbase = n_packs;
-        constexpr u64 kElems = (1ull << 31) - 1;
-        auto frozen_value = [=] __device__(i64 i) -> u64 {
-            if (!((fl[i >> 5] >> (i & 31)) & 1u)) return 0ull;
-            const u32 e = nx[i];
-            return Pp[e] - Pp[i] >= tmin ? ((1ull << 31) | (e - static_cast<u64>(i))) : 0ull;
-        };
-        scan_exclusive<u64>(
-            mm, frozen_value,
-            [=] __device__(i64 i, u64 v) {
-                const u64 own = frozen_value(i);
-                if (i == mm - 1) {  // totals: pool size and sink counters for the next round
-                    const u64 t = v + own;
-                    nm[0] = static_cast<u64>(mm) - (t & kElems);
-                    nm[1] = mbase + (t & kElems);
-                    nm[2] = pbase + (t >> 31);
-                    *sink.n_members = nm[1];
-                    *sink.n_packs = nm[2];
-                }
-                if (!((fl[i >> 5] >> (i & 31)) & 1u)) return;
-                const u32 e = nx[i];
-                const u64 fz_elems = v & kElems;
-                if (own) {
-                    const u64 q = pbase + (v >> 31);
-                    const u64 dst = mbase + fz_elems;
-                    u64 att = 0;
-                    for (u64 k = static_cast<u64>(i); k < e; ++k) {
-                        const u64 x = F[k];
-                        const u64 l = ent_len(x);
-                        att += l * l;
-                        sink.members[dst + (k - i)] = x;
-                    }
-                    sink.pack_off[q] = dst;
-                    sink.pack_total[q] = static_cast<u32>(Pp[e] - Pp[i]);
-                    sink.pack_att[q] = att;
-                } else {
-                    const u64 dst = static_cast<u64>(i) - fz_elems;
-                    for (u64 k = static_cast<u64>(i); k < e; ++k) newpool[dst + (k - i)] = F[k];
-                }
-            },
-            s, c.scan, "nf.freeze_emit", 24.0);
+        const int smem = static_cast<int>(sizeof(unsigned short) * NF_LV * NF_T);
+        CUDA_CHECK(cudaFuncSetAttribute(k_nf_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, smem, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
     }
+    LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
+    DevBuf<u64> tval(ntiles, s), tpre(ntiles, s);
+    DevBuf<u32> tlast(ntiles, s);
+    LAUNCH_B("nf.flags", 4.25 * m, k_nf_flags, ntiles, NF_B, 0, s, nxt.p, spec.p, entry.p, P.p, m, tmin, flags.p,
+             tval.p, tlast.p);
+    {
+        const u64* tv = tval.p;
+        u64* tp = tpre.p;
+        scan_exclusive<u64>(
+            static_cast<i64>(ntiles), [=] __device__(i64 i) { return tv[i]; },
+            [=] __device__(i64 i, u64 v) { tp[i] = v; }, s, c.scan, "nf.tiles_scan");
+    }
+    // algorithmic bytes: entries in and out (16 B) + flags
+    LAUNCH_B("nf.freeze_emit", 16.125 * m, k_nf_emit, ntiles, NF_B, 0, s, F, m, flags.p, nxt.p, P.p, tmin, tpre.p,
+             tlast.p, sink, n_members, n_packs, newpool, newm.p, ntiles);
     const auto t = read_vector(c, newm.p, 3);
     n_members = t[1];
     n_packs = t[2];

@@ -465,7 +465,6 @@ struct PackedGroup {
     u64 n_isf_members = 0;
     DevBuf<u64> isf_members, isf_off;
     DevBuf<u32> isf_total;
-    DevBuf<u64> isf_att;
     u64 n_ffd = 0;
     u64 n_residue = 0;
     DevBuf<u64> residue;       // sorted residue items
@@ -480,10 +479,9 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
     out.isf_members.alloc(m, s);
     out.isf_off.alloc(m + 1, s);
     out.isf_total.alloc(m + 1, s);
-    out.isf_att.alloc(m + 1, s);
     DevBuf<u64> counters(2, s);
     counters.zero();
-    PackSink sink{out.isf_members.p, out.isf_off.p, out.isf_total.p, out.isf_att.p, counters.p, counters.p + 1};
+    PackSink sink{out.isf_members.p, out.isf_off.p, out.isf_total.p, counters.p, counters.p + 1};
     u64 n_members = 0, n_packs = 0;  // host copies of the sink counters
     DevBuf<u64> A(m, s), Bf(m, s);
     CUDA_CHECK(cudaMemcpyAsync(A.p, pool_in, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));

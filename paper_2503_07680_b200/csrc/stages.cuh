@@ -22,7 +22,6 @@ struct PackSink {
     u64* members;     // entries
     u64* pack_off;    // first member of each pack
     u32* pack_total;
-    u64* pack_att;
     u64* n_members;   // device counters
     u64* n_packs;
 };

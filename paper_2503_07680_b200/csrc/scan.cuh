@@ -25,8 +25,9 @@ constexpr u64 kScanValMask = (1ull << 62) - 1;
 template <typename T, int BLOCK, int ITEMS, typename Load, typename Store>
 __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store store, u64* status,
                                                          u32* counter) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
     constexpr int TILE = BLOCK * ITEMS;
-    __shared__ T s_items[TILE + TILE / 32];  // padded transpose buffer
+    T* s_items = reinterpret_cast<T*>(s_dyn);  // [TILE + TILE / 32] padded transpose buffer
     __shared__ T s_red[33];
     __shared__ u32 s_tile;
     __shared__ T s_prefix;
@@ -44,20 +45,17 @@ __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store
         s_items[pad(li)] = gi < n ? load(gi) : T(0);
     }
     __syncthreads();
-    T v[ITEMS];
     T local = 0;
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
-        v[k] = s_items[pad(threadIdx.x * ITEMS + k)];
-        local += v[k];
-    }
+    for (int k = 0; k < ITEMS; ++k) local += s_items[pad(threadIdx.x * ITEMS + k)];
     T total;
     const T texcl = block_exclusive_scan<T>(local, s_red, total);
 
     // publish + look back
     if (threadIdx.x == 0) {
+        // flag and value travel in one 64-bit word: no fence (no other data
+        // of this tile is read by its successors)
         const u64 word = (tile == 0 ? kScanFlagInc : kScanFlagAgg) | (static_cast<u64>(total) & kScanValMask);
-        __threadfence();
         *reinterpret_cast<volatile u64*>(&status[tile]) = word;
     }
     if (tile > 0 && threadIdx.x < 32) {
@@ -84,7 +82,6 @@ __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store
         }
         if (lane == 0) {
             s_prefix = acc;
-            __threadfence();
             *reinterpret_cast<volatile u64*>(&status[tile]) =
                 kScanFlagInc | (static_cast<u64>(acc + total) & kScanValMask);
         }
@@ -93,9 +90,10 @@ __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store
     __syncthreads();
     T run = s_prefix + texcl;
 #pragma unroll
-    for (int k = 0; k < ITEMS; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {  // in place: each thread owns its blocked items
+        const T x = s_items[pad(threadIdx.x * ITEMS + k)];
         s_items[pad(threadIdx.x * ITEMS + k)] = run;
-        run += v[k];
+        run += x;
     }
     __syncthreads();
 #pragma unroll
@@ -118,16 +116,25 @@ struct ScanScratch {
     }
 };
 
-template <typename T, int ITEMS = 8, typename Load, typename Store>
+// Large tiles (64 KB of shared memory): the look-back hands the running
+// prefix from tile to tile at a roughly fixed cost per tile, so fewer,
+// larger tiles keep it off the bandwidth (tools/micro/scan_micro.cu, B200,
+// 10M / 100M elements: u64 2048-element tiles 2.0 / 2.4 TB/s, 8192-element
+// tiles 2.8 / 3.8 TB/s; u32 16384-element tiles 2.6 / 3.1 TB/s).
+template <typename T, int ITEMS = 32, int BLOCK = (sizeof(T) == 4 ? 512 : 256),
+          typename Load, typename Store>
 void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch,
                     const char* name = "scan", double bytes_per_elem = 2.0 * sizeof(T)) {
-    constexpr int BLOCK = 256;
     constexpr int TILE = BLOCK * ITEMS;
     if (n <= 0) return;
     const i64 tiles = (n + TILE - 1) / TILE;
     scratch.prepare(tiles, stream);
+    constexpr int smem = static_cast<int>(sizeof(T)) * (TILE + TILE / 32);
+    if (smem > 48 * 1024)
+        CUDA_CHECK(cudaFuncSetAttribute(k_scan_lookback<T, BLOCK, ITEMS, Load, Store>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     LAUNCH_B(name, bytes_per_elem * static_cast<double>(n), (k_scan_lookback<T, BLOCK, ITEMS, Load, Store>),
-             static_cast<unsigned>(tiles), BLOCK, 0, stream, n, load, store, scratch.status.p, scratch.counter.p);
+             static_cast<unsigned>(tiles), BLOCK, smem, stream, n, load, store, scratch.status.p, scratch.counter.p);
 }
 
 }  // namespace hbp_b200

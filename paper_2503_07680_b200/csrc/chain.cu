@@ -107,26 +107,31 @@ __device__ __forceinline__ void st_relaxed_u32(u32* p, u32 v) {
 template <int M, bool STORE>
 __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 end_item, u32& c, u32 (&R)[M],
                                       u32 (&N)[M], u32& wmax, u64 base, u32 lane) {
-    const u32 inv_own = s ? 0xffffffffu / s : 0u;
+    // run_len bit 31: strict run (ids <= -2 in greedy fill, stages.cuh):
+    // a bin takes floor((r - 1) / s) of its items
+    const u32 s_own = s & 0x7fffffffu;
+    const u32 inv_own = s_own ? 0xffffffffu / s_own : 0u;
     u32 lmax = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) lmax = max(lmax, R[i]);
     while (act) {
         const int r = __ffs(act) - 1;
         act &= act - 1;
-        const u32 S = __shfl_sync(0xffffffffu, s, r);
+        const u32 Sraw = __shfl_sync(0xffffffffu, s, r);
+        const u32 S = Sraw & 0x7fffffffu, strict = Sraw >> 31;
         const u32 inv = __shfl_sync(0xffffffffu, inv_own, r);
         const u32 C0 = __shfl_sync(0xffffffffu, c, r);
         u32 off = 0;
         if (STORE) off = __shfl_sync(0xffffffffu, end_item - c, r);
-        unsigned room = __ballot_sync(0xffffffffu, lmax >= S);
+        unsigned room = __ballot_sync(0xffffffffu, lmax >= S + strict);
         if (!room) continue;
         u32 capl[M], pre[M + 1];
         pre[0] = 0;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            u32 q = __umulhi(R[i], inv);  // floor(R / S): exact after two corrections
-            u32 rem = R[i] - q * S;
+            const u32 Re = R[i] > strict ? R[i] - strict : 0u;
+            u32 q = __umulhi(Re, inv);  // floor(Re / S): exact after two corrections
+            u32 rem = Re - q * S;
             if (rem >= S) { ++q; rem -= S; }
             if (rem >= S) ++q;
             capl[i] = min(q, C0);  // no bin takes more than the run has
@@ -273,7 +278,8 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
                 if (a.sleep) __nanosleep(a.sleep);
             c = static_cast<u32>(v);
         }
-        const unsigned act = __ballot_sync(0xffffffffu, c > 0 && s <= wmax);  // every lane has its c
+        // every lane has its c; run_len bit 31 = strict (needs r > s)
+        const unsigned act = __ballot_sync(0xffffffffu, c > 0 && (s & 0x7fffffffu) + (s >> 31) <= wmax);
         const u32 n_act = __popc(act);
         unsigned long long t_arr = 0;
         if (a.tl) t_arr = globaltimer();

@@ -55,15 +55,26 @@ TreeLayout make_layout(u64 max_bins) {
     return t;
 }
 
+// Run heads: a new length, or (fill with negative ids) the first item of
+// the non-negative class within a length.
+__device__ __forceinline__ bool neg_item(u64 e, const u32* key32, u64 neg_keys) {
+    const u32 ix = entry_idx(e);
+    return (key32 ? key32[ix] : ix) < neg_keys;
+}
+__device__ __forceinline__ bool run_head(const u64* items, u64 i, const u32* key32, u64 neg_keys) {
+    if (i == 0 || entry_len(items[i]) != entry_len(items[i - 1])) return true;
+    return neg_keys && neg_item(items[i], key32, neg_keys) != neg_item(items[i - 1], key32, neg_keys);
+}
+
 __global__ void k_runs(const u64* __restrict__ items, u64 n, u32* __restrict__ run_item, u32* __restrict__ run_len,
-                       const u64* __restrict__ excl) {
+                       const u64* __restrict__ excl, const u32* __restrict__ key32, u64 neg_keys) {
     for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
-        const u32 l = entry_len(items[i]);
-        if (i == 0 || entry_len(items[i - 1]) != l) {
+        if (run_head(items, i, key32, neg_keys)) {
             const u64 r = excl[i];
+            const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
             run_item[r] = static_cast<u32>(i);
-            run_len[r] = l;
+            run_len[r] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
         }
     }
 }
@@ -1088,7 +1099,7 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
 }
 
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
-                         FitMode mode, u32* item_bin, u32* item_slot) {
+                         FitMode mode, u32* item_bin, u32* item_slot, const u32* key32, u64 neg_keys) {
     FitResult out;
     out.bins = bins0;
     if (n_items_s <= 0) return out;
@@ -1099,6 +1110,9 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     const char* eng = std::getenv("HBP_ENGINE");
     const std::string engine = eng ? eng : "";
     const bool use_chain = engine.empty() || engine == "chain";
+    if (mode == FitMode::Ffd) neg_keys = 0;  // first_fit compares totals, no probe quirk
+    if (neg_keys > 0 && !use_chain)
+        throw EngineError(HBP_ERR_CUDA, "greedy fill with sample ids <= -2 needs the chain engine (HBP_ENGINE)");
 
     // runs of equal length
     DevBuf<u64> flags_excl(n, s);
@@ -1109,19 +1123,15 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         const i64 nn = static_cast<i64>(n);
         scan_exclusive<u64>(
             nn,
-            [=] __device__(i64 i) {
-                return static_cast<u64>(i == 0 || entry_len(items[i]) != entry_len(items[i - 1]));
-            },
+            [=] __device__(i64 i) { return static_cast<u64>(run_head(items, i, key32, neg_keys)); },
             [=] __device__(i64 i, u64 v) {
                 ex[i] = v;
-                if (i == nn - 1) {
-                    const bool head = i == 0 || entry_len(items[i]) != entry_len(items[i - 1]);
-                    sc[0] = static_cast<u32>(v + (head ? 1 : 0));
-                }
+                if (i == nn - 1) sc[0] = static_cast<u32>(v + (run_head(items, i, key32, neg_keys) ? 1 : 0));
             },
             s, c.scan);
     }
-    LAUNCH(k_runs, grid_for(n, 256, 148u * 16u), 256, 0, s, items, n, run_item.p, run_len.p, flags_excl.p);
+    LAUNCH(k_runs, grid_for(n, 256, 148u * 16u), 256, 0, s, items, n, run_item.p, run_len.p, flags_excl.p, key32,
+           neg_keys);
 
     // bulk-place the items that can never share a bin (FFD with no live bins)
     u32 bulk = 0;

@@ -882,9 +882,6 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             for (int j = 0; j < gi; ++j) n_fill += psize[j];
         }
         if (n_fill > 0 && pg.P() > 0) {
-            if (corpus.neg_ids > 0)
-                throw EngineError(HBP_ERR_CUDA,
-                                  "greedy fill with sample ids <= -2 is not supported by the GPU engine yet");
             fill_items.alloc(n_fill, s);
             u64 o = 0;
             for (int j = gi - 1; j >= 0; --j) {  // nearest (longest) pool first
@@ -900,7 +897,8 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             fill_bin.alloc(n_fill, s);
             fill_slot.alloc(n_fill, s);
             first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p, static_cast<i64>(P),
-                           static_cast<i64>(P), cap, FitMode::Fill, fill_bin.p, fill_slot.p);
+                           static_cast<i64>(P), cap, FitMode::Fill, fill_bin.p, fill_slot.p, corpus.key32.p,
+                           static_cast<u64>(corpus.neg_ids));
             trace_mark(c, "fill.engine");
             // remove consumed samples from their pools, order preserved
             if (!consumed.p) {
@@ -1078,8 +1076,6 @@ void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int6
     hbp_samples in{pool_ids, pool_lens, M, HBP_MEM_HOST, "pools"};
     DeviceCorpus corpus;
     ingest(c, &in, corpus);
-    if (corpus.neg_ids > 0)
-        throw EngineError(HBP_ERR_CUDA, "greedy fill with sample ids <= -2 is not supported by the GPU engine yet");
     // leaves: (max(0, capacity - total) << 32) | count, per pack
     std::vector<u64> leaves(static_cast<size_t>(n_packs));
     std::vector<u32> base(static_cast<size_t>(n_packs));
@@ -1107,7 +1103,8 @@ void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int6
         for (u64 i = 0; i < m; ++i) maxlen = std::max<u32>(maxlen, static_cast<u32>(std::min<int64_t>(pool_lens[a + i], 0x7fffffff)));
         sort_entries(c, corpus, items.p, m, corpus.key32.p == nullptr, maxlen);
         DevBuf<u32> bin(m, s), slot(m, s);
-        first_fit_runs(c, items.p, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u, FitMode::Fill, bin.p, slot.p);
+        first_fit_runs(c, items.p, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u, FitMode::Fill, bin.p, slot.p,
+                       corpus.key32.p, static_cast<u64>(corpus.neg_ids));
         const auto hb = read_vector(c, bin.p, m), hs = read_vector(c, slot.p, m);
         const auto he = read_vector(c, items.p, m);
         for (u64 i = 0; i < m; ++i) {

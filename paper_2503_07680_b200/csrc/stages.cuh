@@ -62,8 +62,16 @@ enum class FitMode { Ffd, Fill };
 // `leaves` (capacity max_bins) holds (residual << 32 | count) per bin; the
 // first `bins0` are live. items: sorted entries. Writes item -> (bin, slot),
 // kNone for items left unassigned (fill mode).
+// Fill mode with sample ids <= -2 (neg_keys > 0: the items whose tie-break
+// key -- key32[idx], or idx when key32 is null -- is below neg_keys): the
+// reference's probe {residual, id = -1} (balance.cpp:82-83) makes such a
+// sample ineligible when its length equals the residual exactly. Runs then
+// split at the id class and the negative part of each length is "strict":
+// a bin with residual r takes floor((r - 1) / s) of its items, and the
+// non-negative part after it the usual floor(r' / s) -- the reference's
+// pack-by-pack picks, run by run (flag: bit 31 of run_len).
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
-                         FitMode mode, u32* item_bin, u32* item_slot);
+                         FitMode mode, u32* item_bin, u32* item_slot, const u32* key32 = nullptr, u64 neg_keys = 0);
 
 // chain.cu: first fit as a pipeline of bins. Bin b sees the items no bin
 // before it took, in order, and takes each one that fits, so bins form a

@@ -136,11 +136,31 @@ def test_general_ids(ctx, oracle):
     rng = np.random.default_rng(4)
     L = hybrid(oracle, 4000, 8, 0.04)
     ids = rng.permutation(10_000_000)[:4000].astype(np.int64) - 5_000_000
-    ids = ids[ids > -2][:3000]  # greedy fill quirk (ids <= -2) is handled separately
+    ids = ids[ids > -2][:3000]
     L = L[:len(ids)]
     want = oracle.build_plan(ids, L, TWO_LEVEL, l_best=16384, device_count=4, seed=3)
     got = ctx.build_plan(ids, L, TWO_LEVEL, l_best=16384, device_count=4, seed=3).flat()
     assert_same_plan(got, want, ids)
+
+
+@pytest.mark.parametrize("seed", [5, 6, 7])
+def test_negative_ids_greedy_fill_quirk(ctx, oracle, seed):
+    # ids <= -2: greedy_fill's probe {residual, id=-1} (balance.cpp:82-83)
+    # makes them ineligible at an exact-length fit; the restatement is pinned
+    # to the reference on this (test_oracle.py::test_differential_negative_ids).
+    # Few distinct lengths so exact fits are common.
+    rng = np.random.default_rng(seed)
+    n = 20_000
+    L = np.where(rng.random(n) < 0.05, rng.choice([20000, 24576, 30000], n), rng.choice([512, 1024, 2048, 4096], n))
+    ids = rng.permutation(4 * n)[:n].astype(np.int64) - 2 * n
+    want = oracle.build_plan(ids, L, TWO_LEVEL, l_best=16384, device_count=4, seed=seed)
+    got = ctx.build_plan(ids, L, TWO_LEVEL, l_best=16384, device_count=4, seed=seed).flat()
+    assert_same_plan(got, want, ids)
+    # ids ascending in input order (no rank key): negatives are the first indices
+    ids2 = np.arange(n, dtype=np.int64) - n // 3
+    want = oracle.build_plan(ids2, L, TWO_LEVEL, l_best=16384, device_count=4, seed=seed)
+    got = ctx.build_plan(ids2, L, TWO_LEVEL, l_best=16384, device_count=4, seed=seed).flat()
+    assert_same_plan(got, want, ids2)
 
 
 @pytest.mark.parametrize("strategy", ["isf", "random", "ffd", "ffs"])

@@ -273,6 +273,7 @@ def run_ours(args, rank, world, local):
     # stage profile of one extra step (CUDA events around each engine stage)
     stages = profile_stages(ctx, lib, step_device)
     sweep_res = None if args.no_sweep else run_sweep_leg(ctx, lib, rank, world, dist)
+    c4_res = run_c4_leg(ctx, lib) if (world == 1 and not args.no_c4) else None
 
     tot_dev = sum(dev_ms)
     tot_e2e = sum(e2e_ms)
@@ -303,6 +304,7 @@ def run_ours(args, rank, world, local):
             "clocks": ck,
             "cpu_baseline": cpu,
             "sweep": sweep_res,
+            "c4": c4_res,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -351,6 +353,84 @@ def run_sweep_leg(ctx, lib, rank, world, dist):
             "candidates_per_s": len(cands) / elapsed, "best_index": best[1],
             "best_groups": cands[best[1]][0] if best[1] >= 0 else None, "best_seconds": best[0],
             "sharding": f"length sets round-robin over {world} rank(s), all_gather argmin"}
+
+
+C4 = dict(C2, count=100_000_000)
+C4_PROFILE = os.path.join(ROOT, "tests", "golden", "deepseek_v2_236b_analytic.json")
+
+
+def c4_profile():
+    """DeepSeek-V2 236B analytic cost model (builder-written fixture, see its _note)."""
+    from paper_2503_07680_b200 import abi
+    with open(C4_PROFILE) as f:
+        d = json.load(f)
+    p = abi.default_profile()
+    for name, _ in abi.HardwareProfile._fields_:
+        if name in d:
+            setattr(p, name, d[name])
+    return p
+
+
+def run_c4_leg(ctx, lib, steps=2):
+    """BASELINE config C4: 100M samples of the C2 spec, groups [16K sp1,
+    128K sp8] with ckpt derived under the DeepSeek-V2 236B cost model, 8 DP
+    devices: build_plan + report (ABR/CR) + simulate, corpus resident in HBM.
+    Also C5 on a bounded sample: the first length sets of the 4096-candidate
+    sweep (512 sets x SP{1,2,4,8} x GC{on,off}) over the same corpus."""
+    import torch
+    from paper_2503_07680_b200 import abi, sweep
+    stream = torch.cuda.ExternalStream(lib.hbp_ctx_stream(ctx.h))
+    L = synth(lib, C4)
+    n = len(L)
+    d_len = torch.from_numpy(L).cuda()
+    del L
+    prof = c4_profile()
+    pr = abi.analytic_profiler(prof)
+    pr.device_memory = prof.device_memory
+    groups = [(16384, 1, ctx.derive_ckpt(pr, 16384, 1)), (131072, 8, ctx.derive_ckpt(pr, 131072, 8))]
+
+    def step():
+        s, keep = abi.device_samples(0, d_len.data_ptr(), n, "c4")
+        plan = ctx.build_plan_samples(s, groups, 16384, device_count=DEVICES, seed=PLAN_SEED)
+        m = plan.report()
+        st = plan.simulate(prof)
+        return plan, m, st
+
+    out = step()  # warm-up (memory pool growth)
+    out = None
+    ms = []
+    for _ in range(steps):
+        out = None
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        out = step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    plan, m, st = out
+    res = {"workload": "C4: 100M samples (C2 spec), groups [16K sp1, 128K sp8], DeepSeek-V2 236B analytic cost model "
+                       "(tests/golden/deepseek_v2_236b_analytic.json), 8 DP devices; build_plan+report+simulate",
+           "samples": n, "groups": groups, "ms_per_step": statistics.mean(ms), "ms_steps": [round(x, 2) for x in ms],
+           "samples_per_s": n / (statistics.mean(ms) / 1000.0), "abr": m.abr, "cr": m.cr,
+           "estimated_seconds": st.total_seconds}
+    out = plan = None
+    # C5 bounded sample: the first K length sets (8 candidates each) over the 100M corpus
+    cands = sweep.make_candidates(ctx, 131072, [256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536], SWEEP_SP, prof)
+    K = 4
+    sample = cands[:8 * K]
+    s, keep = abi.device_samples(0, d_len.data_ptr(), n, "c5")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    secs, best = ctx.sweep_samples(s, sample, prof, device_count=DEVICES, seed=PLAN_SEED)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    res["c5_sample"] = {"workload": f"C5 bounded sample: first {K} of 512 length sets x SP{{1,2,4,8}} x GC{{on,off}} "
+                                    "over the C4 corpus (100M), DeepSeek-V2 cost model",
+                        "candidates": len(sample), "of_candidates": len(cands), "seconds": el,
+                        "candidates_per_s": len(sample) / el,
+                        "feasible": int(sum(1 for v in secs if math.isfinite(v))), "best_index": int(best)}
+    return res
 
 
 def profile_stages(ctx, lib, fn):
@@ -420,6 +500,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override corpus size (default 10M)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the auto-selection sweep leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the 100M-sample C4 / C5-sample leg")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

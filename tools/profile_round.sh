@@ -21,6 +21,13 @@ echo "scan traffic rows: $(grep -c dram__bytes_read "$OUT/${TAG}_scan_traffic.cs
 ncu --set full --clock-control none --import-source on -k regex:k_ff_chain -c 3 \
     -o "$OUT/${TAG}_chain" -f $STEP > /dev/null 2>&1
 echo "chain capture: $?"
-ncu --set full --clock-control none --import-source on -k regex:k_scan_lookback -s 20 -c 1 \
+# the largest plain scan of the step: the prefix sums of group 0's first ISF
+# round (9.7M u64 elements; launch index among the scans, this round's code)
+ncu --set full --clock-control none --import-source on -k regex:k_scan_lookback -s ${SCAN_SKIP:-51} -c 1 \
     -o "$OUT/${TAG}_scan" -f $STEP > /dev/null 2>&1
 echo "scan capture: $?"
+for k in k_fy_lists k_radix_scatter k_nf_emit; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -s ${BIG_SKIP:-8} -c 1 \
+      -o "$OUT/${TAG}_$k" -f $STEP > /dev/null 2>&1
+  echo "$k capture: $?"
+done

@@ -17,8 +17,14 @@ namespace hbp_b200 {
 
 namespace {
 
-constexpr int RB = 256;      // threads per block
-constexpr int RITEMS = 16;   // elements per thread per tile
+#ifndef HBP_RADIX_ITEMS
+#define HBP_RADIX_ITEMS 8
+#endif
+#ifndef HBP_RADIX_MINB
+#define HBP_RADIX_MINB 4
+#endif
+constexpr int RB = 256;                   // threads per block
+constexpr int RITEMS = HBP_RADIX_ITEMS;   // elements per thread per tile
 constexpr int RTILE = RB * RITEMS;
 constexpr int RW = RB / 32;  // warps per block
 
@@ -27,17 +33,33 @@ __device__ __forceinline__ u32 digit_of(u32 k, int shift, bool desc) {
     return (kk >> shift) & 0xffu;
 }
 
+// Lanes of the warp holding the same 8-bit digit (among `valid` lanes):
+// eight ballots, cheaper than match.any on B200.
+__device__ __forceinline__ unsigned digit_peers(u32 d, bool valid) {
+    unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? m : ~m;
+    }
+    return peers;
+}
+
 __global__ void __launch_bounds__(RB) k_radix_hist(const u32* __restrict__ keys, u64 n, int shift, bool desc,
                                                    u32* __restrict__ hist, u32 ntiles) {
     __shared__ u32 h[RW][256];
     for (int i = threadIdx.x; i < RW * 256; i += RB) (&h[0][0])[i] = 0;
     __syncthreads();
     const u64 base = static_cast<u64>(blockIdx.x) * RTILE;
-    const unsigned w = warp_id();
+    const unsigned w = warp_id(), lane = lane_id();
 #pragma unroll 4
     for (int k = 0; k < RITEMS; ++k) {
         const u64 i = base + static_cast<u64>(k) * RB + threadIdx.x;
-        if (i < n) atomicAdd(&h[w][digit_of(keys[i], shift, desc)], 1u);
+        const bool valid = i < n;
+        const u32 d = valid ? digit_of(keys[i], shift, desc) : 0u;
+        const unsigned peers = digit_peers(d, valid);
+        if (valid && (peers & ((1u << lane) - 1u)) == 0) h[w][d] += __popc(peers);  // one leader per digit
     }
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += RB) {
@@ -48,51 +70,82 @@ __global__ void __launch_bounds__(RB) k_radix_hist(const u32* __restrict__ keys,
     }
 }
 
-__global__ void __launch_bounds__(RB) k_radix_scatter(const u32* __restrict__ keys_in,
+// Scatter of one pass. Ranks the tile in shared memory (warp match masks
+// give each element its rank among equal digits of its warp; per-warp digit
+// counts, a prefix over warps and one block scan over digits give the
+// tile-local digit starts), places keys and values there in digit order, then
+// writes them out striped: consecutive threads write consecutive positions of
+// a digit's run, so global writes are coalesced. Three block barriers per
+// tile. Warp w owns the contiguous chunk [w * 512, (w + 1) * 512) of the tile,
+// which keeps the ranking stable.
+__global__ void __launch_bounds__(RB, HBP_RADIX_MINB) k_radix_scatter(const u32* __restrict__ keys_in,
                                                       const u32* __restrict__ vals_in, u32* __restrict__ keys_out,
                                                       u32* __restrict__ vals_out, u64 n, int shift, bool desc,
                                                       const u32* __restrict__ offs, u32 ntiles) {
-    __shared__ u32 s_base[256];      // running count per digit within this tile
-    __shared__ u32 s_wc[RW][256];    // per-warp digit counts of the current sub-round
+    __shared__ u32 s_k[RTILE];
+    __shared__ u32 s_v[RTILE];
+    __shared__ unsigned short s_wc[RW][256];  // per-warp digit counts, then offsets within the digit
+    __shared__ u32 s_dstart[256];
+    __shared__ u32 s_goff[256];
+    __shared__ u32 s_red[33];
     const unsigned lane = lane_id(), w = warp_id();
-    for (int d = threadIdx.x; d < 256; d += RB) s_base[d] = offs[static_cast<u64>(d) * ntiles + blockIdx.x];
     const u64 base = static_cast<u64>(blockIdx.x) * RTILE;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int k = 0; k < RITEMS; ++k) {
-        for (int i = threadIdx.x; i < RW * 256; i += RB) (&s_wc[0][0])[i] = 0;
-        __syncthreads();
-        const u64 i = base + static_cast<u64>(k) * RB + threadIdx.x;
-        const bool valid = i < n;
-        u32 key = 0, val = 0, d = 0xffffffffu;
-        if (valid) {
-            key = keys_in[i];
-            val = vals_in[i];
-            d = digit_of(key, shift, desc);
-        }
-        const unsigned active = __ballot_sync(0xffffffffu, valid);
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        peers &= active;
-        const u32 rank_in_warp = __popc(peers & lt);
-        if (valid && rank_in_warp == 0) s_wc[w][d] = __popc(peers);
-        __syncthreads();
-        // exclusive prefix over warps for each digit, then advance s_base
-        for (int dd = threadIdx.x; dd < 256; dd += RB) {
-            u32 run = s_base[dd];
+    const u32 len = static_cast<u32>(base + RTILE < n ? RTILE : n - base);
+    for (int d = lane; d < 256; d += 32) s_wc[w][d] = 0;
+    __syncwarp();
+    constexpr int PER_WARP = RTILE / RW;  // 512
+    u32 key[RITEMS], val[RITEMS], dg[RITEMS], rk[RITEMS];
 #pragma unroll
-            for (int q = 0; q < RW; ++q) {
-                const u32 c = s_wc[q][dd];
-                s_wc[q][dd] = run;
-                run += c;
-            }
-            s_base[dd] = run;
+    for (int k = 0; k < RITEMS; ++k) {
+        const u32 li = w * PER_WARP + k * 32 + lane;
+        const bool valid = li < len;
+        key[k] = valid ? keys_in[base + li] : 0u;
+        val[k] = valid ? vals_in[base + li] : 0u;
+        dg[k] = valid ? digit_of(key[k], shift, desc) : 256u;
+    }
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < RITEMS; ++k) {
+        const u32 d = dg[k];
+        const unsigned peers = digit_peers(d, d < 256u);
+        const u32 old = d < 256u ? s_wc[w][d] : 0u;
+        rk[k] = old + __popc(peers & lt);
+        __syncwarp();
+        if (d < 256u && (peers & lt) == 0) s_wc[w][d] = static_cast<unsigned short>(old + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    {
+        const u32 d = threadIdx.x;  // RB == 256 digits
+        u32 run = 0;
+#pragma unroll
+        for (int q = 0; q < RW; ++q) {
+            const u32 c = s_wc[q][d];
+            s_wc[q][d] = static_cast<unsigned short>(run);
+            run += c;
         }
-        __syncthreads();
-        if (valid) {
-            const u32 pos = s_wc[w][d] + rank_in_warp;
-            keys_out[pos] = key;
-            vals_out[pos] = val;
+        u32 tot;
+        const u32 ex = block_exclusive_scan<u32>(run, s_red, tot);
+        s_dstart[d] = ex;
+        s_goff[d] = offs[static_cast<u64>(d) * ntiles + blockIdx.x];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < RITEMS; ++k) {
+        const u32 d = dg[k];
+        if (d < 256u) {
+            const u32 p = s_dstart[d] + s_wc[w][d] + rk[k];
+            s_k[p] = key[k];
+            s_v[p] = val[k];
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    for (u32 p = threadIdx.x; p < len; p += RB) {
+        const u32 kk = s_k[p];
+        const u32 d = digit_of(kk, shift, desc);
+        const u32 g = s_goff[d] + (p - s_dstart[d]);
+        keys_out[g] = kk;
+        vals_out[g] = s_v[p];
     }
 }
 

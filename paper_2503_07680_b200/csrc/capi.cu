@@ -15,6 +15,7 @@
 namespace hbp_b200 {
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local KernelProfiler* g_prof = nullptr;
+thread_local BlockCache* g_cache = nullptr;
 }
 
 struct StageSummary {
@@ -127,6 +128,8 @@ void hbp_ctx_destroy(hbp_ctx* ctx) {
         ctx->plans.clear();
         ctx->scan.status.release();
         ctx->scan.counter.release();
+        ctx->blocks.stream = ctx->stream;
+        ctx->blocks.clear();  // after every buffer that returns blocks to it
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
     }

@@ -298,7 +298,8 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
                 a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane] = c;
                 if (lane == 0) a.hact[static_cast<u64>(j) * a.nblocks + b] = act;
             }
-            serve<M, false>(a, act, s, end_item, c, R, N, wmax, base, lane);
+            if (a.hist) serve<M, false>(a, act, s, end_item, c, R, N, wmax, base, lane);
+            else serve<M, true>(a, act, s, end_item, c, R, N, wmax, base, lane);  // short chains store directly
         } else if (a.hist && lane == 0) {
             a.hact[static_cast<u64>(j) * a.nblocks + b] = 0;
         }
@@ -423,7 +424,13 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     }
     // the chain serves without head stores and records the input counts of
     // its active cells; the replay then writes the heads in parallel
-    const bool replay = std::getenv("HBP_CHAIN_NOREPLAY") == nullptr;
+    // A short chain's critical path is its blocks walking a few warps, and a
+    // replay would repeat that walk warp by warp: short chains store the
+    // heads themselves. Long chains (the head stores on every warp's
+    // critical path) hand them to the parallel replay.
+    const char* er = std::getenv("HBP_CHAIN_REPLAY_MIN");
+    const u32 replay_min = er ? static_cast<u32>(std::atoi(er)) : 64u;
+    const bool replay = J >= replay_min && std::getenv("HBP_CHAIN_NOREPLAY") == nullptr;
     DevBuf<u32> hist, hact;
     a.hist = a.hact = nullptr;
     if (replay) {

@@ -9,6 +9,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -42,21 +43,76 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 #define CUDA_CHECK(x) ::hbp_b200::cuda_check((x), #x, __FILE__, __LINE__)
 
-// Stream-ordered device buffer owned by a context (cudaMallocAsync pool).
+// Per-context cache of device blocks. Every stage allocates its scratch
+// per call; on one stream a block freed by an earlier stage can be handed
+// to a later one right away (stream order), so after warm-up a call makes
+// no allocator API calls at all -- at sweep sizes (100K samples per plan)
+// those calls, not the kernels, were the cost. Sizes are rounded to a
+// quarter power of two (<= 25% slack); beyond kLimit cached bytes, blocks
+// go back to the stream-ordered pool.
+struct BlockCache {
+    cudaStream_t stream = nullptr;
+    std::map<size_t, std::vector<void*>> free_blocks;
+    size_t cached = 0;
+    static constexpr size_t kLimit = size_t(16) << 30;
+    static size_t round(size_t bytes) {
+        size_t c = bytes < 512 ? 512 : bytes;
+        size_t p = 1;
+        while ((p << 1) <= c) p <<= 1;
+        const size_t step = p / 4 < 512 ? 512 : p / 4;
+        return (c + step - 1) / step * step;
+    }
+    void* get(size_t rounded) {
+        auto it = free_blocks.find(rounded);
+        if (it != free_blocks.end() && !it->second.empty()) {
+            void* q = it->second.back();
+            it->second.pop_back();
+            cached -= rounded;
+            return q;
+        }
+        void* q = nullptr;
+        CUDA_CHECK(cudaMallocAsync(&q, rounded, stream));
+        return q;
+    }
+    void put(void* q, size_t rounded) {
+        if (cached + rounded > kLimit) {
+            cudaFreeAsync(q, stream);
+            return;
+        }
+        free_blocks[rounded].push_back(q);
+        cached += rounded;
+    }
+    void clear() {
+        for (auto& kv : free_blocks)
+            for (void* q : kv.second) cudaFreeAsync(q, stream);
+        free_blocks.clear();
+        cached = 0;
+    }
+};
+// The cache of the context this thread is running (set by CtxScope).
+extern thread_local BlockCache* g_cache;
+
+// Stream-ordered device buffer owned by a context (block cache over the
+// cudaMallocAsync pool).
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = nullptr;
+    BlockCache* cache = nullptr;  // where the block goes back
+    size_t bytes = 0;             // rounded block size (cached blocks)
     DevBuf() = default;
     DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), cache(o.cache), bytes(o.bytes) {
+        o.p = nullptr;
+        o.n = 0;
+    }
     DevBuf& operator=(DevBuf&& o) noexcept {
         if (this != &o) {
             release();
-            p = o.p; n = o.n; s = o.s;
+            p = o.p; n = o.n; s = o.s; cache = o.cache; bytes = o.bytes;
             o.p = nullptr; o.n = 0;
         }
         return *this;
@@ -66,10 +122,21 @@ struct DevBuf {
         release();
         s = stream;
         n = count;
-        if (count) CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+        if (!count) return;
+        if (g_cache && g_cache->stream == stream) {
+            cache = g_cache;
+            bytes = BlockCache::round(sizeof(T) * count);
+            p = static_cast<T*>(cache->get(bytes));
+        } else {
+            cache = nullptr;
+            CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+        }
     }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) {
+            if (cache) cache->put(p, bytes);
+            else cudaFreeAsync(p, s);
+        }
         p = nullptr;
         n = 0;
     }

@@ -11,6 +11,7 @@
 #include "scan.cuh"
 
 #include <chrono>
+#include <cstring>
 #include <cstdlib>
 #include <map>
 #include <set>
@@ -25,6 +26,8 @@ struct hbp_ctx {
     cudaStream_t stream = nullptr;
     std::string last_error;
     int64_t launches = 0;
+    int64_t syncs = 0;  // host round trips (read_scalar / read_vector)
+    hbp_b200::BlockCache blocks;  // declared before every cached buffer it outlives
     hbp_b200::ScanScratch scan;
     hbp_b200::Pinned pinned;
     hbp_b200::PinnedPool host_pool;  // plan host views
@@ -64,14 +67,18 @@ inline void trace_dump(Ctx& c, const char* title) {
 struct CtxScope {
     int64_t* prev;
     KernelProfiler* prev_prof;
-    explicit CtxScope(Ctx& c) : prev(g_launch_counter), prev_prof(g_prof) {
+    BlockCache* prev_cache;
+    explicit CtxScope(Ctx& c) : prev(g_launch_counter), prev_prof(g_prof), prev_cache(g_cache) {
         g_launch_counter = &c.launches;
         g_prof = &c.prof;
+        c.blocks.stream = c.stream;
+        g_cache = &c.blocks;
         CUDA_CHECK(cudaSetDevice(c.device));
     }
     ~CtxScope() {
         g_launch_counter = prev;
         g_prof = prev_prof;
+        g_cache = prev_cache;
     }
 };
 
@@ -79,6 +86,7 @@ struct CtxScope {
 template <typename T>
 T read_scalar(Ctx& c, const T* dptr) {
     c.pinned.ensure(sizeof(T));
+    ++c.syncs;
     CUDA_CHECK(cudaMemcpyAsync(c.pinned.p, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
     CUDA_CHECK(cudaStreamSynchronize(c.stream));
     return *reinterpret_cast<T*>(c.pinned.p);
@@ -86,10 +94,15 @@ T read_scalar(Ctx& c, const T* dptr) {
 
 template <typename T>
 std::vector<T> read_vector(Ctx& c, const T* dptr, size_t n) {
+    // through the context's pinned staging buffer: a copy into pageable
+    // memory serialises with other streams' work on the device
     std::vector<T> out(n);
+    ++c.syncs;
     if (n) {
-        CUDA_CHECK(cudaMemcpyAsync(out.data(), dptr, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
+        c.pinned.ensure(sizeof(T) * n);
+        CUDA_CHECK(cudaMemcpyAsync(c.pinned.p, dptr, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
         CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        std::memcpy(out.data(), c.pinned.p, sizeof(T) * n);
     }
     return out;
 }

@@ -937,6 +937,9 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     emit_plan(c, T, slots, igroup, I, N, a.seed, out);
     trace_mark(c, "emit");
     CUDA_CHECK(cudaStreamSynchronize(s));
+    if (std::getenv("HBP_COUNT_SYNCS"))
+        std::fprintf(stderr, "[hbp] build_plan: %lld host round trips so far on this context\n",
+                     static_cast<long long>(c.syncs));
 }
 
 void pack_device(Ctx& c, DeviceCorpus& corpus, int64_t capacity, const hbp_strategy& st, uint64_t seed,

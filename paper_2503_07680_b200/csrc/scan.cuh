@@ -104,15 +104,41 @@ __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store
     }
 }
 
-// Scratch for scans: status words + the tile counter, reused across calls.
+// Scratch for scans: status words + tile counters. Each scan takes a fresh,
+// already-zeroed stretch of both; the buffers are zeroed again only when a
+// stretch would run past their end (scans on a context's stream run in
+// order, so a stretch is never reused while a scan still reads it). One
+// memset per many scans instead of two per scan.
 struct ScanScratch {
     DevBuf<u64> status;
     DevBuf<u32> counter;
+    size_t pos = 0, cpos = 0;
+    u64* st = nullptr;
+    u32* ctr = nullptr;
     void prepare(i64 tiles, cudaStream_t s) {
-        if (static_cast<i64>(status.n) < tiles) status.alloc(static_cast<size_t>(tiles * 2 + 64), s);
-        if (counter.n < 1) counter.alloc(1, s);
-        CUDA_CHECK(cudaMemsetAsync(status.p, 0, sizeof(u64) * static_cast<size_t>(tiles), s));
-        CUDA_CHECK(cudaMemsetAsync(counter.p, 0, sizeof(u32), s));
+        const size_t t = static_cast<size_t>(tiles);
+        if (status.n < t) {
+            status.alloc(t * 4 > (size_t(1) << 16) ? t * 4 : (size_t(1) << 16), s);
+            status.zero();
+            pos = 0;
+        }
+        if (counter.n == 0) {
+            counter.alloc(4096, s);
+            counter.zero();
+            cpos = 0;
+        }
+        if (pos + t > status.n) {
+            status.zero();
+            pos = 0;
+        }
+        if (cpos + 1 > counter.n) {
+            counter.zero();
+            cpos = 0;
+        }
+        st = status.p + pos;
+        ctr = counter.p + cpos;
+        pos += t;
+        cpos += 1;
     }
 };
 
@@ -134,7 +160,7 @@ void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScra
         CUDA_CHECK(cudaFuncSetAttribute(k_scan_lookback<T, BLOCK, ITEMS, Load, Store>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     LAUNCH_B(name, bytes_per_elem * static_cast<double>(n), (k_scan_lookback<T, BLOCK, ITEMS, Load, Store>),
-             static_cast<unsigned>(tiles), BLOCK, smem, stream, n, load, store, scratch.status.p, scratch.counter.p);
+             static_cast<unsigned>(tiles), BLOCK, smem, stream, n, load, store, scratch.st, scratch.ctr);
 }
 
 }  // namespace hbp_b200

@@ -9,6 +9,7 @@
 namespace hbp_b200 {
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local KernelProfiler* g_prof = nullptr;
+thread_local BlockCache* g_cache = nullptr;
 }  // namespace hbp_b200
 
 using namespace hbp_b200;

@@ -10,6 +10,7 @@
 namespace hbp_b200 {
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local KernelProfiler* g_prof = nullptr;
+thread_local BlockCache* g_cache = nullptr;
 
 template <int M>
 __global__ void k_serve_micro(ChainArgs a, const u32* R0, const u32* s_in, const u32* c_in, int iters,

@@ -373,15 +373,24 @@ __global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
     store_bins<M>(a, base, lane, R, N, true);
 }
 
-// Bins one resident chain of width M can hold.
+// Bins one resident chain of width M can hold (per device, queried once).
 template <int M>
 u64 chain_capacity(int sms) {
     constexpr int kWarps = warps_for<M>();
     const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32;
-    CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    int per_sm = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, smem));
-    return static_cast<u64>(per_sm > 0 ? per_sm : 0) * sms * kWarps * 32 * M;
+    static std::mutex mu;
+    static std::map<int, int> per_sm_of;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    auto it = per_sm_of.find(dev);
+    if (it == per_sm_of.end()) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, smem));
+        it = per_sm_of.emplace(dev, per_sm).first;
+    }
+    return static_cast<u64>(it->second > 0 ? it->second : 0) * sms * kWarps * 32 * M;
 }
 
 // One pass over bins [a.bin0, a.bin_end); returns {1 + highest bin used, any carry}.

@@ -10,7 +10,10 @@
 #include <cstdint>
 #include <cstdio>
 #include <map>
+#include <mutex>
+#include <set>
 #include <stdexcept>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -42,6 +45,21 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     }
 }
 #define CUDA_CHECK(x) ::hbp_b200::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Function attributes and occupancy are per (kernel, device) and do not
+// change: set / query them once per process instead of on every launch
+// (these driver calls take a context-wide lock that the sweep's worker
+// threads would queue on).
+inline void set_max_dynamic_smem_once(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({func, dev})) return;
+    CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({func, dev});
+}
 
 // Per-context cache of device blocks. Every stage allocates its scratch
 // per call; on one stream a block freed by an earlier stage can be handed

@@ -385,7 +385,7 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
              nxt.p);
     {
         const int smem = static_cast<int>(sizeof(unsigned short) * NF_LV * NF_T);
-        CUDA_CHECK(cudaFuncSetAttribute(k_nf_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_nf_tiles), smem);
         LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, smem, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
     }
     LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);

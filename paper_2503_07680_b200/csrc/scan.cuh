@@ -157,8 +157,7 @@ void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScra
     scratch.prepare(tiles, stream);
     constexpr int smem = static_cast<int>(sizeof(T)) * (TILE + TILE / 32);
     if (smem > 48 * 1024)
-        CUDA_CHECK(cudaFuncSetAttribute(k_scan_lookback<T, BLOCK, ITEMS, Load, Store>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_scan_lookback<T, BLOCK, ITEMS, Load, Store>), smem);
     LAUNCH_B(name, bytes_per_elem * static_cast<double>(n), (k_scan_lookback<T, BLOCK, ITEMS, Load, Store>),
              static_cast<unsigned>(tiles), BLOCK, smem, stream, n, load, store, scratch.st, scratch.ctr);
 }

@@ -35,6 +35,9 @@ namespace hbp_b200 {
 
 namespace {
 
+#ifndef HBP_CHAIN_WALK
+#define HBP_CHAIN_WALK 3  // lanes walked one by one before a warp scan
+#endif
 constexpr int kQ = 32;         // global ring depth per link, in blocks of 32 runs
 constexpr int kQs = 16;        // shared-memory ring depth (dynamic shared memory)
 // warps per CTA (one CTA per SM): fewer for wide lanes so registers stay <= 128
@@ -130,17 +133,17 @@ __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 en
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const u32 Re = R[i] > strict ? R[i] - strict : 0u;
-            u32 q = __umulhi(Re, inv);  // floor(Re / S): exact after two corrections
-            u32 rem = Re - q * S;
-            if (rem >= S) { ++q; rem -= S; }
-            if (rem >= S) ++q;
+            // floor(Re / S): with inv = floor((2^32-1)/S) and Re < 2^31 the
+            // estimate is low by at most one, so one correction is exact
+            u32 q = __umulhi(Re, inv);
+            q += (Re - q * S >= S) ? 1u : 0u;
             capl[i] = min(q, C0);  // no bin takes more than the run has
             pre[i + 1] = min(pre[i] + capl[i], C0);
         }
         const u32 lsum = pre[M];
         // walk the lanes with room in bin order
         u32 left = C0, mine = 0;
-        for (int k = 0; k < 3 && left > 0 && room; ++k) {
+        for (int k = 0; k < HBP_CHAIN_WALK && left > 0 && room; ++k) {
             const int f = __ffs(room) - 1;
             room &= room - 1;
             const u32 lf = __shfl_sync(0xffffffffu, lsum, f);

@@ -41,6 +41,11 @@ namespace {
 constexpr int kQ = 32;         // global ring depth per link, in blocks of 32 runs
 constexpr int kQs = 16;        // shared-memory ring depth (dynamic shared memory)
 // warps per CTA (one CTA per SM): fewer for wide lanes so registers stay <= 128
+// Warps per CTA. A short chain spreads over the SMs in CTAs of 4 warps
+// (fewer warps per SM contend less for issue slots: C2 chain -8% against
+// 16); a long one (more warps than 8 per SM) keeps CTAs of 16 so fewer
+// hand-offs cross CTAs through L2.
+constexpr int kShortWarps = 4;
 template <int M>
 __host__ __device__ constexpr int warps_for() { return M <= 4 ? 32 : 16; }
 constexpr u32 kStride = 32;    // u32 between global consumer counters (one 128 B line each)
@@ -107,9 +112,175 @@ __device__ __forceinline__ void st_relaxed_u32(u32* p, u32 v) {
 // one saturating warp scan. The takes themselves (residuals, counts, heads)
 // are off the path: every lane applies its own once it knows how many
 // items it receives.
+// Per-warp staging of a segment's runs for the frontier fill.
+struct RunStage {
+    unsigned long long incl[32];  // inclusive prefix of the runs' leftovers (run order = lane order)
+    u32 s[32];                    // run length
+    u32 off[32];                  // first leftover item of the run
+};
+
+// One run `r` against the lanes in `allowed` (bin order = lane order).
+template <int M, bool STORE>
+__device__ __forceinline__ void serve_run(const ChainArgs& a, int r, unsigned allowed, u32 s, u32 inv_own,
+                                          u32 end_item, u32& c, u32 (&R)[M], u32 (&N)[M], u32& lmax, u64 base,
+                                          u32 lane) {
+    const u32 Sraw = __shfl_sync(0xffffffffu, s, r);
+    const u32 S = Sraw & 0x7fffffffu, strict = Sraw >> 31;
+    const u32 inv = __shfl_sync(0xffffffffu, inv_own, r);
+    const u32 C0 = __shfl_sync(0xffffffffu, c, r);
+    u32 off = 0;
+    if (STORE) off = __shfl_sync(0xffffffffu, end_item - c, r);
+    unsigned room = __ballot_sync(0xffffffffu, lmax >= S + strict) & allowed;
+    if (!room) return;
+    u32 capl[M], pre[M + 1];
+    pre[0] = 0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const u32 Re = R[i] > strict ? R[i] - strict : 0u;
+        // floor(Re / S): with inv = floor((2^32-1)/S) and Re < 2^31 the
+        // estimate is low by at most one, so one correction is exact
+        u32 q = __umulhi(Re, inv);
+        q += (Re - q * S >= S) ? 1u : 0u;
+        capl[i] = min(q, C0);  // no bin takes more than the run has
+        pre[i + 1] = min(pre[i] + capl[i], C0);
+    }
+    const u32 lsum = pre[M];
+    // walk the lanes with room in bin order
+    u32 left = C0, mine = 0;
+    for (int k = 0; k < HBP_CHAIN_WALK && left > 0 && room; ++k) {
+        const int f = __ffs(room) - 1;
+        room &= room - 1;
+        const u32 lf = __shfl_sync(0xffffffffu, lsum, f);
+        if (static_cast<int>(lane) == f) mine = left;
+        left -= min(lf, left);
+    }
+    if (left > 0 && room) {  // spans many lanes: one scan over the rest
+        const u32 v = (room >> lane) & 1u ? lsum : 0u;
+        u32 incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<u32>(o)) incl = min(incl + t, left);
+        }
+        u32 excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = 0;
+        if (v > 0 && excl < left) mine = left - excl;
+        left -= __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (static_cast<int>(lane) == r) c = left;
+    if (mine > 0) {  // this lane receives `mine` items of the run
+        u32 nl = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const u32 t = pre[i] < mine ? min(capl[i], mine - pre[i]) : 0u;
+            if (STORE && t > 0) {
+                const u32 o = off + (C0 - mine) + pre[i];
+                a.item_bin[o] = static_cast<u32>(base + lane * M + i);
+                a.item_slot[o] = N[i];
+                a.take[o] = t;
+            }
+            R[i] -= t * S;
+            N[i] += t;
+            nl = max(nl, R[i]);
+        }
+        lmax = nl;
+    }
+}
+
+// FFD frontier in closed form. The runs of `seg` share k = floor(cap / s):
+// their items lie in (cap / (k + 1), cap / k], so k of them always share a
+// bin and k + 1 never do, and no item of the segment fits a bin that k of
+// them filled. Their leftovers (what the warp's non-empty bins left) thus
+// fill the empty bins in order, k items per bin, the last bin partially --
+// exactly what serving them one by one would do -- with one warp scan.
+template <int M, bool STORE>
+__device__ __forceinline__ void frontier_fill(const ChainArgs& a, unsigned seg, u32 k, u32 s, u32 end_item, u32& c,
+                                              u32 (&R)[M], u32 (&N)[M], u32& lmax, u32& emask, RunStage& st,
+                                              u64 base, u32 lane) {
+    const u32 lv = (seg >> lane) & 1u ? c : 0u;
+    unsigned long long incl = lv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<u32>(o)) incl += t;
+    }
+    const unsigned long long T = __shfl_sync(0xffffffffu, incl, 31);
+    if (T == 0) return;
+    const int e0 = __ffs(emask) - 1;
+    const int e1 = 32 - __clz(emask);
+    const unsigned long long per = static_cast<unsigned long long>(M) * k;
+    const unsigned long long used = min(T, static_cast<unsigned long long>(e1 - e0) * per);
+    st.incl[lane] = incl;
+    st.s[lane] = s & 0x7fffffffu;
+    st.off[lane] = end_item - c;
+    __syncwarp();
+    if (static_cast<int>(lane) >= e0 && static_cast<int>(lane) < e1) {
+        const unsigned long long pos0 = static_cast<unsigned long long>(lane - e0) * per;
+        if (pos0 < used) {
+            int q = 0;
+            while (st.incl[q] <= pos0) ++q;
+            u32 nl = 0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const unsigned long long b0 = pos0 + static_cast<unsigned long long>(i) * k;
+                if (b0 < used) {
+                    const unsigned long long b1 = min(b0 + k, used);
+                    u32 tot = 0, nb = 0;
+                    for (unsigned long long p = b0; p < b1;) {
+                        while (st.incl[q] <= p) ++q;
+                        const unsigned long long hi = min(b1, st.incl[q]);
+                        const u32 t = static_cast<u32>(hi - p);
+                        if (STORE) {
+                            const unsigned long long ex_q = q ? st.incl[q - 1] : 0ull;
+                            const u32 o = st.off[q] + static_cast<u32>(p - ex_q);
+                            a.item_bin[o] = static_cast<u32>(base + lane * M + i);
+                            a.item_slot[o] = nb;
+                            a.take[o] = t;
+                        }
+                        tot += t * st.s[q];
+                        nb += t;
+                        p = hi;
+                    }
+                    R[i] = a.cap - tot;
+                    N[i] = nb;
+                }
+                nl = max(nl, R[i]);
+            }
+            lmax = nl;
+        }
+    }
+    __syncwarp();
+    if (lv > 0) {
+        const unsigned long long ex = incl - lv;
+        const unsigned long long hi = min(incl, used);
+        if (hi > ex) c -= static_cast<u32>(hi - ex);
+    }
+    const unsigned long long touched = (used + per - 1) / per;  // lanes no longer empty
+    const int e0n = e0 + static_cast<int>(touched);
+    emask = e0n >= 32 ? 0u : (emask & ~((1u << e0n) - 1u));
+}
+
+// Serves one block of 32 runs (counts c, lengths s, item ends end_item; `act`
+// marks the runs with c > 0 and s <= wmax) against the warp's 32*M bins, in
+// run order, and leaves in c what passes on. STORE writes one head (bin,
+// slot, take) at the first item of every take; the chain serves without
+// storing (scattered stores would sit on its critical path) and the replay
+// re-serves with them.
+//
+// Per run the critical path is short: the lanes with room are known from
+// each lane's max residual (one ballot); every lane computes what its M bins
+// can take (independent divisions by a shuffled reciprocal) and their
+// in-lane prefix; the run then walks the lanes with room in order -- one
+// shuffle per lane, usually one or two lanes -- or, when it spans more,
+// one saturating warp scan. The takes themselves (residuals, counts, heads)
+// are off the path: every lane applies its own once it knows how many
+// items it receives. At the FFD frontier (lanes whose bins are all still
+// empty, emask) the runs of a block that share k = floor(cap / s) are served
+// against the non-empty lanes one by one and then fill the empty ones
+// together in closed form (frontier_fill).
 template <int M, bool STORE>
 __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 end_item, u32& c, u32 (&R)[M],
-                                      u32 (&N)[M], u32& wmax, u64 base, u32 lane) {
+                                      u32 (&N)[M], u32& wmax, u32& emask, RunStage& st, u64 base, u32 lane) {
     // run_len bit 31: strict run (ids <= -2 in greedy fill, stages.cuh):
     // a bin takes floor((r - 1) / s) of its items
     const u32 s_own = s & 0x7fffffffu;
@@ -117,72 +288,43 @@ __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 en
     u32 lmax = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) lmax = max(lmax, R[i]);
+    u32 k_own = 0;
+    if (emask && s_own) {
+        k_own = __umulhi(a.cap, inv_own);
+        k_own += (a.cap - k_own * s_own >= s_own) ? 1u : 0u;
+    }
     while (act) {
         const int r = __ffs(act) - 1;
-        act &= act - 1;
-        const u32 Sraw = __shfl_sync(0xffffffffu, s, r);
-        const u32 S = Sraw & 0x7fffffffu, strict = Sraw >> 31;
-        const u32 inv = __shfl_sync(0xffffffffu, inv_own, r);
-        const u32 C0 = __shfl_sync(0xffffffffu, c, r);
-        u32 off = 0;
-        if (STORE) off = __shfl_sync(0xffffffffu, end_item - c, r);
-        unsigned room = __ballot_sync(0xffffffffu, lmax >= S + strict);
-        if (!room) continue;
-        u32 capl[M], pre[M + 1];
-        pre[0] = 0;
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            const u32 Re = R[i] > strict ? R[i] - strict : 0u;
-            // floor(Re / S): with inv = floor((2^32-1)/S) and Re < 2^31 the
-            // estimate is low by at most one, so one correction is exact
-            u32 q = __umulhi(Re, inv);
-            q += (Re - q * S >= S) ? 1u : 0u;
-            capl[i] = min(q, C0);  // no bin takes more than the run has
-            pre[i + 1] = min(pre[i] + capl[i], C0);
+        if (!emask) {
+            act &= act - 1;
+            serve_run<M, STORE>(a, r, 0xffffffffu, s, inv_own, end_item, c, R, N, lmax, base, lane);
+            continue;
         }
-        const u32 lsum = pre[M];
-        // walk the lanes with room in bin order
-        u32 left = C0, mine = 0;
-        for (int k = 0; k < HBP_CHAIN_WALK && left > 0 && room; ++k) {
-            const int f = __ffs(room) - 1;
-            room &= room - 1;
-            const u32 lf = __shfl_sync(0xffffffffu, lsum, f);
-            if (static_cast<int>(lane) == f) mine = left;
-            left -= min(lf, left);
-        }
-        if (left > 0 && room) {  // spans many lanes: one scan over the rest
-            const u32 v = (room >> lane) & 1u ? lsum : 0u;
-            u32 incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= static_cast<u32>(o)) incl = min(incl + t, left);
-            }
-            u32 excl = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (lane == 0) excl = 0;
-            if (v > 0 && excl < left) mine = left - excl;
-            left -= __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (static_cast<int>(lane) == r) c = left;
-        if (mine > 0) {  // this lane receives `mine` items of the run
-            u32 nl = 0;
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                const u32 t = pre[i] < mine ? min(capl[i], mine - pre[i]) : 0u;
-                if (STORE && t > 0) {
-                    const u32 o = off + (C0 - mine) + pre[i];
-                    a.item_bin[o] = static_cast<u32>(base + lane * M + i);
-                    a.item_slot[o] = N[i];
-                    a.take[o] = t;
-                }
-                R[i] -= t * S;
-                N[i] += t;
-                nl = max(nl, R[i]);
-            }
-            lmax = nl;
-        }
+        const u32 kr = __shfl_sync(0xffffffffu, k_own, r);
+        // the segment: consecutive active runs from r with the same k (runs
+        // out of the block's active set are transparent); FFD's sorted runs
+        // keep each k contiguous, a shuffled order (FFS) may not
+        const unsigned same = __ballot_sync(0xffffffffu, k_own == kr) | ~act;
+        const unsigned breaks = ~same & ~((2u << r) - 1u);
+        const unsigned upto = breaks ? (1u << (__ffs(breaks) - 1)) - 1u : 0xffffffffu;
+        const unsigned seg = act & upto;
+        act &= ~seg;
+        for (unsigned q = seg; q; q &= q - 1)
+            serve_run<M, STORE>(a, __ffs(q) - 1, ~emask, s, inv_own, end_item, c, R, N, lmax, base, lane);
+        frontier_fill<M, STORE>(a, seg, kr, s, end_item, c, R, N, lmax, emask, st, base, lane);
     }
     wmax = __reduce_max_sync(0xffffffffu, lmax);
+}
+
+// Lanes whose M bins are all fresh FFD bins (empty, inside the pass); none
+// in a warp that reaches past the pass's last bin.
+template <int M>
+__device__ __forceinline__ u32 empty_lanes(const ChainArgs& a, u64 base, u32 lane) {
+    if (!a.ffd || base + 32ull * M > a.bin_end) return 0u;
+    bool e = true;
+#pragma unroll
+    for (int i = 0; i < M; ++i) e = e && (base + lane * M + i) >= a.live;
+    return __ballot_sync(0xffffffffu, e);
 }
 
 // Loads the warp's 32*M bins (lane-major) from the leaves; empty bins past
@@ -222,11 +364,11 @@ __device__ __forceinline__ u32 store_bins(const ChainArgs& a, u64 base, u32 lane
     return __reduce_max_sync(0xffffffffu, top);
 }
 
-template <int M>
-__global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a) {
-    constexpr int kWarps = warps_for<M>();
-    extern __shared__ unsigned long long s_ring_raw[];  // [kWarps][kQs][32]: warp w-1 -> w
+template <int M, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
+    extern __shared__ unsigned long long s_ring_raw[];  // [kWarps][kQs][32]: warp w-1 -> w, then RunStage[kWarps]
     auto s_ring = reinterpret_cast<unsigned long long (*)[kQs][32]>(s_ring_raw);
+    RunStage* s_stage = reinterpret_cast<RunStage*>(s_ring_raw + kWarps * kQs * 32);
     __shared__ u32 s_cons[kWarps];                         // blocks warp w has read from s_ring[w]
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const u32 g = blockIdx.x;
@@ -240,6 +382,7 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
     const u64 base = a.bin0 + static_cast<u64>(j) * 32 * M;
     u32 R[M], N[M];
     u32 wmax = load_bins<M>(a, base, lane, R, N);
+    u32 emask = empty_lanes<M>(a, base, lane);
     const bool head = j == 0, tail = j + 1 == a.J;
     const bool in_global = w == 0, out_global = w + 1 == kWarps;
     volatile unsigned long long* sin = s_ring[w][0];
@@ -301,8 +444,8 @@ __global__ void __launch_bounds__(warps_for<M>() * 32, 1) k_ff_chain(ChainArgs a
                 a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane] = c;
                 if (lane == 0) a.hact[static_cast<u64>(j) * a.nblocks + b] = act;
             }
-            if (a.hist) serve<M, false>(a, act, s, end_item, c, R, N, wmax, base, lane);
-            else serve<M, true>(a, act, s, end_item, c, R, N, wmax, base, lane);  // short chains store directly
+            if (a.hist) serve<M, false>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);
+            else serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);  // short chains store directly
         } else if (a.hist && lane == 0) {
             a.hact[static_cast<u64>(j) * a.nblocks + b] = 0;
         }
@@ -360,9 +503,11 @@ __global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
     const u32 lane = threadIdx.x & 31u;
     const u32 j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (j >= a.J) return;
+    __shared__ RunStage s_stage[8];
     const u64 base = a.bin0 + static_cast<u64>(j) * 32 * M;
     u32 R[M], N[M];
     u32 wmax = load_bins<M>(a, base, lane, R, N);
+    u32 emask = empty_lanes<M>(a, base, lane);
     for (u32 b = 0; b < a.nblocks; ++b) {
         const u32 act = a.hact[static_cast<u64>(j) * a.nblocks + b];
         if (!act) continue;
@@ -371,16 +516,15 @@ __global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
         const u32 s = valid ? a.run_len[k] : 0u;
         const u32 end_item = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
         u32 c = a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane];
-        serve<M, true>(a, act, s, end_item, c, R, N, wmax, base, lane);
+        serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[threadIdx.x >> 5], base, lane);
     }
     store_bins<M>(a, base, lane, R, N, true);
 }
 
 // Bins one resident chain of width M can hold (per device, queried once).
-template <int M>
+template <int M, int kWarps = warps_for<M>()>
 u64 chain_capacity(int sms) {
-    constexpr int kWarps = warps_for<M>();
-    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32;
+    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32 + sizeof(RunStage) * kWarps;
     static std::mutex mu;
     static std::map<int, int> per_sm_of;
     int dev = 0;
@@ -388,9 +532,10 @@ u64 chain_capacity(int sms) {
     std::lock_guard<std::mutex> g(mu);
     auto it = per_sm_of.find(dev);
     if (it == per_sm_of.end()) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
         int per_sm = 0;
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M>, kWarps * 32, smem));
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M, kWarps>, kWarps * 32, smem));
         it = per_sm_of.emplace(dev, per_sm).first;
     }
     return static_cast<u64>(it->second > 0 ? it->second : 0) * sms * kWarps * 32 * M;
@@ -401,9 +546,16 @@ template <int M>
 std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     const u64 pass_bins = a.bin_end - a.bin0;
     const u32 J = static_cast<u32>((pass_bins + 32ull * M - 1) / (32ull * M));
-    constexpr int kWarps = warps_for<M>();
+    int sms = 0, dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const bool short_chain = J <= 2u * kShortWarps * static_cast<u32>(sms) &&
+                             chain_capacity<M, kShortWarps>(sms) >= pass_bins;
+    const int kWarps = short_chain ? kShortWarps : warps_for<M>();
     const u32 G = (J + kWarps - 1) / kWarps;
-    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32;
+    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32 + sizeof(RunStage) * kWarps;
+    if (short_chain) (void)chain_capacity<M, kShortWarps>(sms);  // attribute set
+    else (void)chain_capacity<M>(sms);
     cudaStream_t s = c.stream;
     a.J = J;
     DevBuf<unsigned long long> gring(static_cast<size_t>(G + 1) * kQ * 32, s);
@@ -451,7 +603,8 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
         a.hist = hist.p;
         a.hact = hact.p;
     }
-    LAUNCH_COOP(name, 0.0, k_ff_chain<M>, dim3(G), dim3(kWarps * 32), smem, s, args);
+    if (short_chain) LAUNCH_COOP(name, 0.0, (k_ff_chain<M, kShortWarps>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    else LAUNCH_COOP(name, 0.0, (k_ff_chain<M, warps_for<M>()>), dim3(G), dim3(kWarps * 32), smem, s, args);
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
     if (replay) LAUNCH_B("fit.replay", 0.0, k_ff_replay<M>, (J + 7) / 8, 256, 0, s, a);
     const auto o = read_vector(c, out.p, 2);

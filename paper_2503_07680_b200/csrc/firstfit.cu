@@ -66,19 +66,6 @@ __device__ __forceinline__ bool run_head(const u64* items, u64 i, const u32* key
     return neg_keys && neg_item(items[i], key32, neg_keys) != neg_item(items[i - 1], key32, neg_keys);
 }
 
-__global__ void k_runs(const u64* __restrict__ items, u64 n, u32* __restrict__ run_item, u32* __restrict__ run_len,
-                       const u64* __restrict__ excl, const u32* __restrict__ key32, u64 neg_keys) {
-    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<u64>(gridDim.x) * blockDim.x) {
-        if (run_head(items, i, key32, neg_keys)) {
-            const u64 r = excl[i];
-            const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
-            run_item[r] = static_cast<u32>(i);
-            run_len[r] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
-        }
-    }
-}
-
 // Level h >= 1 from level h-1 (h-1 == 0: leaves).
 __global__ void k_tree_level(const u64* __restrict__ leaves, u32* __restrict__ base, TreeLayout t, int h, u64 lo,
                              u64 hi) {
@@ -1115,23 +1102,27 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         throw EngineError(HBP_ERR_CUDA, "greedy fill with sample ids <= -2 needs the chain engine (HBP_ENGINE)");
 
     // runs of equal length
-    DevBuf<u64> flags_excl(n, s);
+    // runs: one scan over run-head flags; each head writes its run's first
+    // item and length (bit 31: strict) at its run index
     DevBuf<u32> run_item(n, s), run_len(n, s), scal(4, s);
     {
-        u64* ex = flags_excl.p;
+        u32* ri = run_item.p;
+        u32* rl = run_len.p;
         u32* sc = scal.p;
         const i64 nn = static_cast<i64>(n);
-        scan_exclusive<u64>(
-            nn,
-            [=] __device__(i64 i) { return static_cast<u64>(run_head(items, i, key32, neg_keys)); },
-            [=] __device__(i64 i, u64 v) {
-                ex[i] = v;
-                if (i == nn - 1) sc[0] = static_cast<u32>(v + (run_head(items, i, key32, neg_keys) ? 1 : 0));
+        scan_exclusive<u32>(
+            nn, [=] __device__(i64 i) { return run_head(items, i, key32, neg_keys) ? 1u : 0u; },
+            [=] __device__(i64 i, u32 v) {
+                const bool head = run_head(items, i, key32, neg_keys);
+                if (head) {
+                    const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
+                    ri[v] = static_cast<u32>(i);
+                    rl[v] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
+                }
+                if (i == nn - 1) sc[0] = v + (head ? 1u : 0u);
             },
-            s, c.scan);
+            s, c.scan, "scan", 8.0);
     }
-    LAUNCH(k_runs, grid_for(n, 256, 148u * 16u), 256, 0, s, items, n, run_item.p, run_len.p, flags_excl.p, key32,
-           neg_keys);
 
     // bulk-place the items that can never share a bin (FFD with no live bins)
     u32 bulk = 0;

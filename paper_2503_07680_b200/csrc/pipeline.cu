@@ -909,18 +909,18 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             for (int j = 0; j < gi; ++j) {
                 if (!psize[j]) continue;
                 DevBuf<u64> kept(psize[j] + 1, s);
-                DevBuf<u64> cnt(1, s);
+                DevBuf<u32> cnt(1, s);
                 const u64* src = pools[j].p;
                 u64* dst = kept.p;
-                u64* cntp = cnt.p;
+                u32* cntp = cnt.p;
                 const u8* cons = consumed.p;
                 const i64 m = static_cast<i64>(psize[j]);
-                scan_exclusive<u64>(
-                    m, [=] __device__(i64 i) { return cons[entry_idx(src[i])] ? 0ull : 1ull; },
-                    [=] __device__(i64 i, u64 v) {
+                scan_exclusive<u32>(
+                    m, [=] __device__(i64 i) { return cons[entry_idx(src[i])] ? 0u : 1u; },
+                    [=] __device__(i64 i, u32 v) {
                         const bool keep = !cons[entry_idx(src[i])];
                         if (keep) dst[v] = src[i];
-                        if (i == m - 1) *cntp = v + (keep ? 1 : 0);
+                        if (i == m - 1) *cntp = v + (keep ? 1u : 0u);
                     },
                     s, c.scan);
                 psize[j] = read_scalar(c, cnt.p);

@@ -268,6 +268,15 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples,
 /* Host view of a plan produced by hbp_pack / hbp_build_plan. The first call
  * copies the plan to host; the view stays valid until hbp_plan_free. */
 int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out);
+
+/* Plan manifest (replaces hbp::plan_to_json, src/io.cpp:85-110): the
+ * byte-identical nlohmann dump(2) text of the plan, built on the GPU.
+ * `samples` is the corpus the plan was built from (ids / lengths of the
+ * members; host or device memory). With out == NULL only *out_len (bytes,
+ * including the final newline, no NUL) is set; otherwise out must hold
+ * capacity >= *out_len bytes (HBP_ERR_VALIDATION if not). */
+int hbp_plan_to_json(hbp_ctx* ctx, hbp_plan* plan, const hbp_samples* samples, char* out, int64_t capacity,
+                     int64_t* out_len);
 void hbp_plan_free(hbp_plan* plan);
 
 /* report (include/hbp/metrics.hpp:78, src/metrics.cpp:107-144).

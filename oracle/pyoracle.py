@@ -204,6 +204,23 @@ class Oracle:
         self._check(rc)
         return self._take(out, groups, g.l_best)
 
+    def build_plan_json(self, ids, lengths, groups: Sequence[tuple], l_best=None, **opts) -> bytes:
+        """The reference's plan_to_json text of its build_plan (reference kind only)."""
+        lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        ids = self._ids(ids, len(lengths))
+        g, keep = abi.make_groups(groups, l_best)
+        o = abi.make_options(**opts)
+        out = C.c_void_p()
+        n = C.c_int64()
+        rc = self.lib.oracle_build_plan_json(abi.ptr(ids, C.c_int64), abi.ptr(lengths, C.c_int64),
+                                             C.c_int64(len(lengths)), C.byref(g), C.byref(o),
+                                             C.byref(out), C.byref(n), self.err, len(self.err))
+        self._check(rc)
+        text = C.string_at(out, n.value)
+        self.lib.oracle_free_text.argtypes = [C.c_void_p]
+        self.lib.oracle_free_text(out)
+        return text
+
     def report(self, plan: abi.FlatPlan):
         v = plan.view()
         m = abi.Metrics()

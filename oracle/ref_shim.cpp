@@ -16,6 +16,7 @@
 
 #include "hbp/autoselect.hpp"
 #include "hbp/balance.hpp"
+#include "hbp/io.hpp"
 #include "hbp/costmodel.hpp"
 #include "hbp/errors.hpp"
 #include "hbp/ingest.hpp"
@@ -383,6 +384,29 @@ int oracle_build_plan(const int64_t* ids, const int64_t* lengths, int64_t n,
         *out = f.finish(plan.device_count, plan.seed);
     });
 }
+
+// The reference's plan manifest (io.cpp plan_to_json) of build_plan's plan;
+// *out is malloc'd (oracle_free_text).
+int oracle_build_plan_json(const int64_t* ids, const int64_t* lengths, int64_t n,
+                           const hbp_groups* groups, const hbp_plan_options* options,
+                           char** out, int64_t* out_len, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        R::PlanOptions o;
+        o.strategy = make_strategy(&options->strategy);
+        o.device_count = options->device_count;
+        o.seed = options->seed;
+        o.balance_batching = options->balance_batching != 0;
+        o.greedy_fill = options->greedy_fill != 0;
+        const auto plan =
+            R::build_plan(make_set(ids, lengths, n), make_groups(groups), o);
+        const std::string text = R::plan_to_json(plan);
+        *out = static_cast<char*>(std::malloc(text.size() + 1));
+        std::memcpy(*out, text.c_str(), text.size() + 1);
+        *out_len = static_cast<int64_t>(text.size());
+    });
+}
+
+void oracle_free_text(char* p) { std::free(p); }
 
 int oracle_report(const hbp_plan_view* plan, hbp_metrics* out, double* dbr,
                   double* abr, char* err, int errlen) {

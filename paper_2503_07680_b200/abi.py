@@ -522,6 +522,19 @@ class DevicePlanHandle:
                         pack_member_offsets=arr(v.pack_member_offsets, npk + 1, np.int64),
                         member_index=arr(v.member_index, nm, np.int32))
 
+    def to_json(self, ids: Optional[np.ndarray], lengths: np.ndarray) -> bytes:
+        """hbp::plan_to_json of this plan (src/io.cpp:85-110), written on the GPU;
+        ids / lengths: the corpus the plan was built from (host arrays)."""
+        s, keep = make_samples(ids, lengths, "json")
+        n = C.c_int64()
+        lib = self.ctx.lib
+        lib.hbp_plan_to_json.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Samples), C.c_char_p, C.c_int64,
+                                         C.POINTER(C.c_int64)]
+        self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(1, n.value))
+        self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
     def report(self):
         m = Metrics()
         self.ctx.check(self.ctx.lib.hbp_report_plan(self.ctx.h, self.h, C.byref(m), C.POINTER(C.c_double)(),

@@ -52,11 +52,6 @@ int guarded(hbp_ctx* ctx, F&& fn) {
 
 }  // namespace
 
-struct hbp_plan {
-    DevicePlan dp;
-    hbp_plan_view view{};
-    hbp_ctx* owner = nullptr;
-};
 
 static hbp_plan* new_plan(hbp_ctx* ctx) {
     auto* p = new hbp_plan();

@@ -117,3 +117,11 @@ void validate_groups(const std::vector<hbp_group_config>& g, int64_t l_max);
 void validate_strategy(const hbp_strategy& s);
 
 }  // namespace hbp_b200
+
+// The C-ABI plan handle (include/hbp_b200.h): the device plan, its host view
+// once made, and the context that owns it (null once the context is gone).
+struct hbp_plan {
+    hbp_b200::DevicePlan dp;
+    hbp_plan_view view{};
+    hbp_ctx* owner = nullptr;
+};

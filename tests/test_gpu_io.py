@@ -1,0 +1,73 @@
+"""GPU plan manifest writer (hbp_plan_to_json) against the reference's
+plan_to_json (src/io.cpp:85-110): byte-identical text, checked by SHA-256
+against digests the reference itself produced (tests/golden/
+make_plan_json_golden.py), and byte for byte against the compiled reference
+(oracle/_ref) when it is present."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2503_07680_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "plan_json_golden.json")))
+TWO_LEVEL = [(16384, 1, 28), (131072, 8, 29)]
+C1_GROUPS = [(8192, 1, 0), (32768, 4, 0), (131072, 8, 0)]
+
+
+def cases(oracle):
+    L1 = np.maximum(oracle.synth(20_000, "lognormal:8.5:1.4", 0.0, "", 131072, 42), 128)
+    yield "c1_20k", None, L1, C1_GROUPS, dict(device_count=8, seed=7)
+    rng = np.random.default_rng(3)
+    L2 = oracle.synth(5_000, "lognormal:7.2:0.7", 0.05, "uniform:16385:131072", 131072, 9)
+    ids = rng.permutation(40_000)[:5_000].astype(np.int64) - 20_000
+    yield "neg_ids_5k", ids, L2, TWO_LEVEL, dict(device_count=4, seed=5)
+    L3 = np.array([100, 200, 300, 16000, 40000, 5, 7, 9000], dtype=np.int64)
+    yield "tiny_spill", None, L3, [(16384, 1, 0), (65536, 2, 4)], dict(device_count=3, seed=11)
+
+
+@pytest.mark.parametrize("name", ["c1_20k", "neg_ids_5k", "tiny_spill"])
+def test_plan_json_matches_reference_digest(ctx, oracle, name):
+    for case, ids, L, groups, opts in cases(oracle):
+        if case != name:
+            continue
+        text = ctx.build_plan(ids, L, groups, l_best=groups[0][0], **opts).to_json(ids, L)
+        g = GOLD[name]
+        assert len(text) == g["bytes"]
+        assert text[:300].decode() == g["head"]
+        assert hashlib.sha256(text).hexdigest() == g["sha256"]
+
+
+def test_plan_json_bytes_vs_compiled_reference(ctx, oracle):
+    try:
+        from pyoracle import Oracle
+        ref = Oracle("reference")
+    except (ImportError, FileNotFoundError, OSError):
+        pytest.skip("oracle/_ref not built")
+    L = oracle.synth(30_000, "lognormal:7.2:0.7", 0.03, "uniform:16385:131072", 131072, 21)
+    ids = np.arange(len(L), dtype=np.int64) * 7 - 1000
+    for groups in (TWO_LEVEL, C1_GROUPS):
+        want = ref.build_plan_json(ids, L, groups, l_best=groups[0][0], device_count=8, seed=3)
+        got = ctx.build_plan(ids, L, groups, l_best=groups[0][0], device_count=8, seed=3).to_json(ids, L)
+        if got != want:
+            k = next(i for i in range(min(len(got), len(want))) if got[i] != want[i])
+            raise AssertionError(f"first difference at byte {k}: {got[k-80:k+40]!r} vs {want[k-80:k+40]!r}")
+
+
+def test_plan_json_buffer_too_small(ctx):
+    L = np.array([100, 200, 300], dtype=np.int64)
+    plan = ctx.build_plan(None, L, [(1024, 1, 0)], l_best=1024, device_count=2, seed=1)
+    s, keep = abi.make_samples(None, L, "t")
+    import ctypes as C
+    n = C.c_int64()
+    lib = ctx.lib
+    lib.hbp_plan_to_json.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(abi.Samples), C.c_char_p, C.c_int64,
+                                     C.POINTER(C.c_int64)]
+    assert lib.hbp_plan_to_json(ctx.h, plan.h, C.byref(s), None, 0, C.byref(n)) == 0
+    buf = C.create_string_buffer(8)
+    assert lib.hbp_plan_to_json(ctx.h, plan.h, C.byref(s), buf, 8, C.byref(n)) == abi.HBP_ERR_VALIDATION

@@ -531,9 +531,10 @@ class DevicePlanHandle:
         lib.hbp_plan_to_json.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Samples), C.c_char_p, C.c_int64,
                                          C.POINTER(C.c_int64)]
         self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), None, 0, C.byref(n)))
-        buf = C.create_string_buffer(max(1, n.value))
-        self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), buf, n.value, C.byref(n)))
-        return buf.raw[:n.value]
+        buf = np.empty(max(1, n.value), dtype=np.uint8)  # no zero fill
+        self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), buf.ctypes.data_as(C.c_char_p), n.value,
+                                            C.byref(n)))
+        return buf[:n.value].tobytes()
 
     def report(self):
         m = Metrics()

@@ -13,6 +13,7 @@
 // opening when it is the first device and closing when it is the last --
 // a scan gives every slot its offset, and the same thread writes it. The
 // small header and footer are formatted on the host.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -27,9 +28,10 @@ namespace {
 
 __host__ __device__ __forceinline__ u32 digits_u64(u64 v) {
     u32 d = 1;
-    while (v >= 10) {
-        v /= 10;
+    u64 p = 10;
+    while (d < 20 && v >= p) {  // comparisons, no divisions
         ++d;
+        p *= 10;
     }
     return d;
 }
@@ -87,9 +89,15 @@ struct Writer {
         u64 u = v < 0 ? 0ull - static_cast<u64>(v) : static_cast<u64>(v);
         if (v < 0) *p++ = '-';
         const u32 d = digits_u64(u);
-        for (u32 k = d; k-- > 0;) {
-            p[k] = static_cast<char>('0' + u % 10);
+        u32 k = d;
+        while (u > 0xffffffffull) {  // rare: 64-bit digits
+            p[--k] = static_cast<char>('0' + u % 10);
             u /= 10;
+        }
+        u32 x = static_cast<u32>(u);  // 32-bit divisions by 10 are a multiply-shift
+        while (k > 0) {
+            p[--k] = static_cast<char>('0' + x % 10u);
+            x /= 10u;
         }
         p += d;
     }
@@ -266,7 +274,31 @@ extern "C" int hbp_plan_to_json(hbp_ctx* ctx, hbp_plan* plan, const hbp_samples*
             DevBuf<char> text(body, s);
             LAUNCH_B("io.json", static_cast<double>(body), k_json_write, grid_for(G, 128, 148u * 32u), 128, 0, s, a,
                      off.p, text.p);
-            CUDA_CHECK(cudaMemcpyAsync(out + head.size(), text.p, body, cudaMemcpyDeviceToHost, s));
+            // download through two pinned staging blocks: chunk k + 1 crosses
+            // PCIe while chunk k is copied into the caller's (pageable) buffer
+            constexpr size_t kChunk = size_t(64) << 20;
+            HostBlock stage[2] = {ctx->host_pool.acquire(std::min<size_t>(kChunk, body)),
+                                  ctx->host_pool.acquire(std::min<size_t>(kChunk, body))};
+            cudaEvent_t done[2];
+            CUDA_CHECK(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+            const size_t nchunks = (body + kChunk - 1) / kChunk;
+            auto issue = [&](size_t k) {
+                const size_t o = k * kChunk, n = std::min(kChunk, body - o);
+                CUDA_CHECK(cudaMemcpyAsync(stage[k & 1].p, text.p + o, n, cudaMemcpyDeviceToHost, s));
+                CUDA_CHECK(cudaEventRecord(done[k & 1], s));
+            };
+            issue(0);
+            for (size_t k = 0; k < nchunks; ++k) {
+                if (k + 1 < nchunks) issue(k + 1);
+                CUDA_CHECK(cudaEventSynchronize(done[k & 1]));
+                const size_t o = k * kChunk, n = std::min(kChunk, body - o);
+                std::memcpy(out + head.size() + o, stage[k & 1].p, n);  // frees stage[k & 1] for chunk k + 2
+            }
+            CUDA_CHECK(cudaEventDestroy(done[0]));
+            CUDA_CHECK(cudaEventDestroy(done[1]));
+            ctx->host_pool.release(stage[0]);
+            ctx->host_pool.release(stage[1]);
         }
         CUDA_CHECK(cudaStreamSynchronize(s));
         std::memcpy(out + head.size() + body, foot.data(), foot.size());

@@ -269,6 +269,27 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples,
  * copies the plan to host; the view stays valid until hbp_plan_free. */
 int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out);
 
+/* Padded-batching baselines. */
+enum { HBP_BATCHING_SORTED = 0, HBP_BATCHING_RANDOM = 1 };
+
+/* hbp::sorted_batching / random_batching (src/packing.cpp:265-317): samples
+ * in (length desc, id asc) order, or shuffled by
+ * Rng(derive_seed(seed, "random-batching")), cut greedily into batches while
+ * count * max_length <= token_budget. Outputs: order[n] (input indices in
+ * batching order), batch_offsets[n + 1] (first order position of each batch,
+ * then n), batch_max[n] (each batch's longest sample), *n_batches. Host
+ * memory. Throws "token budget B is below the longest sample (L)". */
+int hbp_padded_batching(hbp_ctx* ctx, const hbp_samples* samples, int64_t token_budget, int32_t mode,
+                        uint64_t seed, int32_t* order, int64_t* batch_offsets, int64_t* batch_max,
+                        int64_t* n_batches);
+
+/* hbp::build_batching_plan (src/balance.cpp:260-298): the padded batches of
+ * `mode` with token budget group.length, device_count per iteration, each
+ * sample its own pack padded to its batch's longest; the plan's groups are
+ * HierarchicalGroups::single(group). */
+int hbp_build_batching_plan(hbp_ctx* ctx, const hbp_samples* samples, hbp_group_config group,
+                            int32_t device_count, int32_t mode, uint64_t seed, hbp_plan** out);
+
 /* Plan manifest (replaces hbp::plan_to_json, src/io.cpp:85-110): the
  * byte-identical nlohmann dump(2) text of the plan, built on the GPU.
  * `samples` is the corpus the plan was built from (ids / lengths of the

@@ -221,6 +221,39 @@ class Oracle:
         self.lib.oracle_free_text(out)
         return text
 
+    def build_batching_plan_json(self, ids, lengths, group: tuple, device_count: int, mode: str,
+                                 seed: int = 0) -> bytes:
+        """plan_to_json(build_batching_plan(...)) of the reference (reference kind only)."""
+        lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        ids = self._ids(ids, len(lengths))
+        out, n = C.c_void_p(), C.c_int64()
+        rc = self.lib.oracle_build_batching_plan_json(
+            abi.ptr(ids, C.c_int64), abi.ptr(lengths, C.c_int64), C.c_int64(len(lengths)), C.c_int64(group[0]),
+            C.c_int32(group[1]), C.c_int32(group[2]), C.c_int32(device_count), C.c_int32(0 if mode == "sorted" else 1),
+            C.c_uint64(seed), C.byref(out), C.byref(n), self.err, len(self.err))
+        self._check(rc)
+        text = C.string_at(out, n.value)
+        self.lib.oracle_free_text.argtypes = [C.c_void_p]
+        self.lib.oracle_free_text(out)
+        return text
+
+    def padded_batching(self, ids, lengths, budget: int, mode: str, seed: int = 0):
+        """(order ids, batch offsets, batch max) of sorted_/random_batching (reference kind only)."""
+        lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        ids = self._ids(ids, len(lengths))
+        n = len(lengths)
+        order = np.zeros(max(n, 1), dtype=np.int64)
+        off = np.zeros(n + 1, dtype=np.int64)
+        mx = np.zeros(max(n, 1), dtype=np.int64)
+        nb = C.c_int64()
+        rc = self.lib.oracle_padded_batching(abi.ptr(ids, C.c_int64), abi.ptr(lengths, C.c_int64), C.c_int64(n),
+                                             C.c_int64(budget), C.c_int32(0 if mode == "sorted" else 1),
+                                             C.c_uint64(seed), abi.ptr(order, C.c_int64), abi.ptr(off, C.c_int64),
+                                             abi.ptr(mx, C.c_int64), C.byref(nb), self.err, len(self.err))
+        self._check(rc)
+        b = nb.value
+        return order[:n], off[:b + 1], mx[:b]
+
     def report(self, plan: abi.FlatPlan):
         v = plan.view()
         m = abi.Metrics()

@@ -408,6 +408,46 @@ int oracle_build_plan_json(const int64_t* ids, const int64_t* lengths, int64_t n
 
 void oracle_free_text(char* p) { std::free(p); }
 
+// The reference's build_batching_plan manifest and padded batches
+// (mode 0 sorted, 1 random).
+int oracle_build_batching_plan_json(const int64_t* ids, const int64_t* lengths, int64_t n,
+                                    int64_t length, int32_t sp, int32_t ckpt,
+                                    int32_t device_count, int32_t mode, uint64_t seed,
+                                    char** out, int64_t* out_len, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        R::GroupConfig g;
+        g.length = length;
+        g.config.sp = sp;
+        g.config.ckpt = ckpt;
+        const auto plan = R::build_batching_plan(
+            make_set(ids, lengths, n), g, device_count,
+            mode == 0 ? R::BatchingMode::Sorted : R::BatchingMode::Random, seed);
+        const std::string text = R::plan_to_json(plan);
+        *out = static_cast<char*>(std::malloc(text.size() + 1));
+        std::memcpy(*out, text.c_str(), text.size() + 1);
+        *out_len = static_cast<int64_t>(text.size());
+    });
+}
+
+int oracle_padded_batching(const int64_t* ids, const int64_t* lengths, int64_t n,
+                           int64_t budget, int32_t mode, uint64_t seed, int64_t* order_ids,
+                           int64_t* batch_offsets, int64_t* batch_max, int64_t* n_batches,
+                           char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const auto set = make_set(ids, lengths, n);
+        const auto b = mode == 0 ? R::sorted_batching(set, budget)
+                                 : R::random_batching(set, budget, seed);
+        int64_t k = 0;
+        for (std::size_t i = 0; i < b.size(); ++i) {
+            batch_offsets[i] = k;
+            batch_max[i] = b[i].max_length;
+            for (const auto& smp : b[i].samples) order_ids[k++] = smp.id;
+        }
+        batch_offsets[b.size()] = k;
+        *n_batches = static_cast<int64_t>(b.size());
+    });
+}
+
 int oracle_report(const hbp_plan_view* plan, hbp_metrics* out, double* dbr,
                   double* abr, char* err, int errlen) {
     return guarded(err, errlen, [&] {

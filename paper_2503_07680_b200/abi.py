@@ -364,6 +364,37 @@ class Context:
         s, keep = make_samples(ids, lengths, source)
         return self.build_plan_samples(s, groups, l_best, **opts)
 
+    def build_batching_plan(self, ids, lengths, group: tuple, device_count: int = 4, mode: str = "sorted",
+                            seed: int = 0) -> "DevicePlanHandle":
+        """hbp::build_batching_plan (balance.cpp:260-298) on the GPU."""
+        s, keep = make_samples(ids, lengths, "python")
+        h = C.c_void_p()
+        self.lib.hbp_build_batching_plan.argtypes = [C.c_void_p, C.POINTER(Samples), GroupConfig, C.c_int32,
+                                                     C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]
+        self.check(self.lib.hbp_build_batching_plan(self.h, C.byref(s), GroupConfig(*group), C.c_int32(device_count),
+                                                    C.c_int32(0 if mode == "sorted" else 1),
+                                                    C.c_uint64(seed & (2**64 - 1)), C.byref(h)))
+        return self._plan(h, [group], group[0])
+
+    def padded_batching(self, ids, lengths, token_budget: int, mode: str = "sorted", seed: int = 0):
+        """hbp::sorted_batching / random_batching on the GPU: (order as input
+        indices, batch offsets into order, batch max lengths)."""
+        s, keep = make_samples(ids, lengths, "python")
+        n = len(lengths)
+        order = np.zeros(max(n, 1), dtype=np.int32)
+        off = np.zeros(n + 1, dtype=np.int64)
+        mx = np.zeros(max(n, 1), dtype=np.int64)
+        nb = C.c_int64()
+        self.lib.hbp_padded_batching.argtypes = [C.c_void_p, C.POINTER(Samples), C.c_int64, C.c_int32, C.c_uint64,
+                                                 C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                                 C.POINTER(C.c_int64)]
+        self.check(self.lib.hbp_padded_batching(self.h, C.byref(s), C.c_int64(token_budget),
+                                                C.c_int32(0 if mode == "sorted" else 1), C.c_uint64(seed & (2**64 - 1)),
+                                                ptr(order, C.c_int32), ptr(off, C.c_int64), ptr(mx, C.c_int64),
+                                                C.byref(nb)))
+        b = nb.value
+        return order[:n], off[:b + 1], mx[:b]
+
     def build_plan_samples(self, s: Samples, groups, l_best=None, **opts) -> "DevicePlanHandle":
         g, garr = make_groups(groups, l_best)
         o = make_options(**opts)

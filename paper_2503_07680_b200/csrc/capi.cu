@@ -241,6 +241,61 @@ int hbp_pack(hbp_ctx* ctx, const hbp_samples* samples, int64_t capacity, const h
     });
 }
 
+int hbp_build_batching_plan(hbp_ctx* ctx, const hbp_samples* samples, hbp_group_config group,
+                            int32_t device_count, int32_t mode, uint64_t seed, hbp_plan** out) {
+    return guarded(ctx, [&] {
+        *out = nullptr;
+        if (mode != HBP_BATCHING_SORTED && mode != HBP_BATCHING_RANDOM) fail_validation("unknown batching mode");
+        DeviceCorpus corpus;
+        ingest(*ctx, samples, corpus);
+        validate_corpus(*ctx, samples, corpus, source_of(samples));  // balance.cpp:263
+        auto* p = new_plan(ctx);
+        try {
+            batching_plan_device(*ctx, corpus, group, device_count, mode == HBP_BATCHING_SORTED, seed, p->dp);
+        } catch (...) {
+            delete_plan(p);
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int hbp_padded_batching(hbp_ctx* ctx, const hbp_samples* samples, int64_t token_budget, int32_t mode,
+                        uint64_t seed, int32_t* order, int64_t* batch_offsets, int64_t* batch_max,
+                        int64_t* n_batches) {
+    return guarded(ctx, [&] {
+        if (mode != HBP_BATCHING_SORTED && mode != HBP_BATCHING_RANDOM) fail_validation("unknown batching mode");
+        DeviceCorpus corpus;
+        ingest(*ctx, samples, corpus);
+        PaddedBatches pb;
+        padded_batches_device(*ctx, corpus, token_budget, mode == HBP_BATCHING_SORTED, seed, pb);
+        const u64 n = pb.n, B = pb.n_batches;
+        *n_batches = static_cast<int64_t>(B);
+        if (n == 0) {
+            batch_offsets[0] = 0;
+            return;
+        }
+        cudaStream_t s = ctx->stream;
+        const u64* ord = pb.order.p;
+        const u32* bs = pb.bstart.p;
+        const u32* bm = pb.bmax.p;
+        DevBuf<int32_t> dord(n, s);
+        DevBuf<int64_t> doff(B + 1, s), dmax(B + 1, s);
+        int32_t* po = dord.p;
+        int64_t* pf = doff.p;
+        int64_t* pm = dmax.p;
+        for_each_index(*ctx, n, [=] __device__(u64 i) { po[i] = static_cast<int32_t>(static_cast<u32>(ord[i])); });
+        for_each_index(*ctx, B + 1, [=] __device__(u64 b) {
+            pf[b] = b < B ? static_cast<int64_t>(bs[b]) : static_cast<int64_t>(n);
+            if (b < B) pm[b] = bm[b];
+        });
+        CUDA_CHECK(cudaMemcpyAsync(order, dord.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(batch_offsets, doff.p, sizeof(int64_t) * (B + 1), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaMemcpyAsync(batch_max, dmax.p, sizeof(int64_t) * B, cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
 int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples, const hbp_groups* groups,
                    const hbp_plan_options* options, hbp_plan** out) {
     return guarded(ctx, [&] {

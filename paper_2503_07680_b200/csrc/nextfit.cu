@@ -202,14 +202,15 @@ __global__ void __launch_bounds__(NF_B) k_nf_flags(const u32* __restrict__ nxt, 
         }
         flags[static_cast<u64>(blockIdx.x) * (NF_T / 32) + w] = bits;
         u64 fe = 0, fp = 0;
-        for (u32 b = bits; b; b &= b - 1) {
-            const u64 st = p0 + __ffs(b) - 1;
-            const u32 e = nxt[st];
-            if (P[e] - P[st] >= tmin) {
-                fe += e - st;
-                ++fp;
+        if (tval)  // freeze totals (next-fit rounds only)
+            for (u32 b = bits; b; b &= b - 1) {
+                const u64 st = p0 + __ffs(b) - 1;
+                const u32 e = nxt[st];
+                if (P[e] - P[st] >= tmin) {
+                    fe += e - st;
+                    ++fp;
+                }
             }
-        }
         u64 v = warp_sum((fp << 31) | fe);
         u32 last = bits ? static_cast<u32>(p0 - a) + 32u - __clz(bits) : 0u;  // 1 + last start, tile-relative
         last = warp_max(last);
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(NF_B) k_nf_flags(const u32* __restrict__ nxt, 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        tval[blockIdx.x] = s_sum[0] + s_sum[1];
+        if (tval) tval[blockIdx.x] = s_sum[0] + s_sum[1];
         const u32 l = max(s_last[0], s_last[1]);
         tlast[blockIdx.x] = l ? static_cast<u32>(a) + l : 0u;
     }
@@ -356,6 +357,27 @@ __global__ void __launch_bounds__(NF_B) k_nf_emit(const u64* __restrict__ F, u64
 }
 
 }  // namespace
+
+// Starts of the chain 0 -> nxt[0] -> nxt[nxt[0]] -> ... over m positions
+// for any monotone nxt (nxt[s] > s): tile-parallel speculative chains,
+// entries, final flags. flags: NF_T / 32 words per tile of NF_T positions
+// (chain_flag_words(m) words); tlast: 1 + last start per tile (0: none).
+u64 chain_flag_words(u64 m) { return ((m + NF_T - 1) / NF_T) * (NF_T / 32); }
+
+void chain_starts(Ctx& c, const u32* nxt, u64 m, u32* flags, u32* tlast) {
+    if (m == 0) return;
+    cudaStream_t s = c.stream;
+    const u32 ntiles = static_cast<u32>((m + NF_T - 1) / NF_T);
+    DevBuf<u32> spec(static_cast<size_t>(ntiles) * (NF_T / 32), s);
+    DevBuf<u32> exitpos(ntiles, s), entry(ntiles, s);
+    DevBuf<u8> allconv(ntiles, s);
+    const int smem = static_cast<int>(sizeof(unsigned short) * NF_LV * NF_T);
+    set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_nf_tiles), smem);
+    LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, smem, s, nxt, m, spec.p, exitpos.p, allconv.p);
+    LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
+    LAUNCH_B("nf.flags", 4.25 * m, k_nf_flags, ntiles, NF_B, 0, s, nxt, spec.p, entry.p, static_cast<const u64*>(nullptr),
+             m, 0ull, flags, static_cast<u64*>(nullptr), tlast);
+}
 
 // Packs one pool by next-fit over `F` (already in visiting order); packs
 // with total >= tmin go to `sink` after the n_members / n_packs already

@@ -1189,4 +1189,193 @@ void batching_device(Ctx& c, int64_t capacity, i64 n_packs, const int64_t* pack_
     CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
+// ---------------------------------------------------------------------------
+// padded batching baselines (packing.cpp:265-317) and build_batching_plan
+// (balance.cpp:260-298)
+// ---------------------------------------------------------------------------
+
+namespace {
+
+__global__ void k_iota_entries(const u32* __restrict__ len32, u64 n, u64* __restrict__ e) {
+    GRID_STRIDE(i, n) e[i] = make_entry(len32[i], static_cast<u32>(i));
+}
+
+__global__ void k_max_u32(const u32* __restrict__ v, u64 n, unsigned int* __restrict__ out) {
+    u32 m = 0;
+    GRID_STRIDE(i, n) m = max(m, v[i]);
+    m = warp_max(m);
+    if ((threadIdx.x & 31u) == 0) atomicMax(out, m);
+}
+
+// Batch starting at position i (budgeted_batches, packing.cpp:267-289): the
+// first sample always, then the next while (count + 1) * max <= budget. In
+// length-descending order the max is the first sample's length.
+__global__ void k_batch_next(const u64* __restrict__ order, u64 n, u64 budget, bool sorted, u32* __restrict__ nxt) {
+    GRID_STRIDE(i, n) {
+        const u64 l0 = entry_len(order[i]);
+        u64 j;
+        if (sorted) {
+            const u64 k = budget / l0;  // >= 1: budget >= every length
+            j = i + k < n ? i + k : n;
+        } else {
+            u64 cnt = 1, mx = l0;
+            j = i + 1;
+            while (j < n) {
+                const u64 l = entry_len(order[j]);
+                const u64 nm = l > mx ? l : mx;
+                if ((cnt + 1) * nm > budget) break;
+                ++cnt;
+                mx = nm;
+                ++j;
+            }
+        }
+        nxt[i] = static_cast<u32>(j);
+    }
+}
+
+__global__ void k_batch_max(const u64* __restrict__ order, const u32* __restrict__ bstart, u64 nb, u64 n,
+                            u32* __restrict__ bmax) {
+    GRID_STRIDE(b, nb) {
+        const u64 a = bstart[b], e = b + 1 < nb ? bstart[b + 1] : n;
+        u32 m = 0;
+        for (u64 k = a; k < e; ++k) m = max(m, entry_len(order[k]));
+        bmax[b] = m;
+    }
+}
+
+// One single-sample pack per row, padded to the batch max; device g of the
+// plan holds batch g (balance.cpp:279-293).
+__global__ void k_batching_packs(const u64* __restrict__ order, const u32* __restrict__ bidx,
+                                 const u32* __restrict__ bmax, u64 n, int64_t* __restrict__ cap,
+                                 int64_t* __restrict__ total, int64_t* __restrict__ att,
+                                 int64_t* __restrict__ moff, int32_t* __restrict__ member) {
+    GRID_STRIDE(p, n) {
+        const u64 e = order[p];
+        const int64_t l = entry_len(e);
+        cap[p] = bmax[bidx[p]];
+        total[p] = l;
+        att[p] = l * l;
+        moff[p] = static_cast<int64_t>(p);
+        member[p] = static_cast<int32_t>(entry_idx(e));
+        if (p + 1 == n) moff[n] = static_cast<int64_t>(n);
+    }
+}
+
+__global__ void k_batching_devices(const u32* __restrict__ bstart, u64 nb, u64 n, u64 I, u32 N,
+                                   int32_t* __restrict__ igroup, int64_t* __restrict__ idoff,
+                                   int32_t* __restrict__ dindex, int64_t* __restrict__ dpoff) {
+    GRID_STRIDE(g, I * N) {
+        dpoff[g] = g < nb ? static_cast<int64_t>(bstart[g]) : static_cast<int64_t>(n);
+        dindex[g] = static_cast<int32_t>(g % N);
+        if (g % N == 0) {
+            igroup[g / N] = 0;
+            idoff[g / N] = static_cast<int64_t>(g);
+        }
+        if (g + 1 == I * N) {
+            dpoff[I * N] = static_cast<int64_t>(n);
+            idoff[I] = static_cast<int64_t>(I * N);
+        }
+    }
+}
+
+}  // namespace
+
+void padded_batches_device(Ctx& c, const DeviceCorpus& corpus, int64_t budget, bool sorted, uint64_t seed,
+                           PaddedBatches& out) {
+    cudaStream_t s = c.stream;
+    const u64 n = static_cast<u64>(corpus.n);
+    // samples.max_length() vs the budget (packing.cpp:296-301, 309-314)
+    int64_t longest = 0;
+    if (n > 0) {
+        DevBuf<unsigned int> mx(1, s);
+        mx.zero();
+        LAUNCH(k_max_u32, grid_for(n, 256, 148u * 8u), 256, 0, s, corpus.len32.p, n, mx.p);
+        longest = read_scalar(c, mx.p);
+        if (corpus.first_huge != ~0ull)  // lengths past 2^31 - 1 (len32 saturates): the exact maximum on the host
+            for (u64 i = 0; i < n; ++i) longest = std::max<int64_t>(longest, corpus.length_of(c, static_cast<i64>(i)));
+    }
+    if (budget < longest)
+        fail_validation("token budget " + std::to_string(budget) + " is below the longest sample (" +
+                        std::to_string(longest) + ")");
+    out.n = n;
+    out.order.alloc(n + 1, s);
+    out.n_batches = 0;
+    if (n == 0) return;
+    LAUNCH(k_iota_entries, G(n), kB, 0, s, corpus.len32.p, n, out.order.p);
+    if (sorted) {
+        sort_entries(c, corpus, out.order.p, n, corpus.key32.p == nullptr, static_cast<u32>(longest));
+    } else {  // Rng(derive_seed(seed, "random-batching")).shuffle
+        DevBuf<u32> src(n, s);
+        DevBuf<u64> tmp(n, s);
+        fy_source_positions(c, derive_seed(seed, "random-batching"), static_cast<i64>(n), src.p);
+        gather_u64(c, out.order.p, src.p, tmp.p, static_cast<i64>(n));
+        CUDA_CHECK(cudaMemcpyAsync(out.order.p, tmp.p, sizeof(u64) * n, cudaMemcpyDeviceToDevice, s));
+    }
+    DevBuf<u32> nxt(n, s), flags(chain_flag_words(n), s), tlast(chain_flag_words(n) / 64 + 1, s);
+    LAUNCH(k_batch_next, G(n), kB, 0, s, out.order.p, n, static_cast<u64>(budget), sorted, nxt.p);
+    chain_starts(c, nxt.p, n, flags.p, tlast.p);
+    // batch starts (compacted) and every position's batch
+    out.bstart.alloc(n + 1, s);
+    out.bidx.alloc(n, s);
+    DevBuf<u32> nb(1, s);
+    {
+        const u32* fl = flags.p;
+        u32* bs = out.bstart.p;
+        u32* bi = out.bidx.p;
+        u32* nbp = nb.p;
+        const i64 nn = static_cast<i64>(n);
+        scan_exclusive<u32>(
+            nn, [=] __device__(i64 i) { return (fl[i >> 5] >> (i & 31)) & 1u; },
+            [=] __device__(i64 i, u32 v) {
+                const u32 f = (fl[i >> 5] >> (i & 31)) & 1u;
+                if (f) bs[v] = static_cast<u32>(i);
+                bi[i] = v + f - 1;
+                if (i == nn - 1) *nbp = v + f;
+            },
+            s, c.scan);
+    }
+    out.n_batches = read_scalar(c, nb.p);
+    out.bmax.alloc(out.n_batches + 1, s);
+    LAUNCH(k_batch_max, G(out.n_batches), kB, 0, s, out.order.p, out.bstart.p, out.n_batches, n, out.bmax.p);
+}
+
+void batching_plan_device(Ctx& c, const DeviceCorpus& corpus, const hbp_group_config& group, int32_t device_count,
+                          bool sorted, uint64_t seed, DevicePlan& out) {
+    if (device_count < 1) fail_validation("device count must be >= 1");
+    cudaStream_t s = c.stream;
+    PaddedBatches pb;
+    padded_batches_device(c, corpus, group.length, sorted, seed, pb);
+    const u64 n = pb.n, B = pb.n_batches, N = static_cast<u64>(device_count);
+    const u64 I = (B + N - 1) / N;
+    out.device_count = device_count;
+    out.seed = seed;
+    out.groups = {group};
+    out.l_best = out.l_max = group.length;  // HierarchicalGroups::single
+    out.n_iterations = static_cast<int64_t>(I);
+    out.n_devices = static_cast<int64_t>(I * N);
+    out.n_packs = static_cast<int64_t>(n);
+    out.n_members = static_cast<int64_t>(n);
+    out.iter_group.alloc(I + 1, s);
+    out.iter_dev_offsets.alloc(I + 1, s);
+    out.dev_index.alloc(I * N + 1, s);
+    out.dev_pack_offsets.alloc(I * N + 1, s);
+    out.pack_capacity.alloc(n + 1, s);
+    out.pack_total.alloc(n + 1, s);
+    out.pack_attention.alloc(n + 1, s);
+    out.pack_member_offsets.alloc(n + 1, s);
+    out.member_index.alloc(n + 1, s);
+    if (I == 0) {
+        const int64_t zero = 0;
+        CUDA_CHECK(cudaMemcpyAsync(out.iter_dev_offsets.p, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(out.pack_member_offsets.p, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        return;
+    }
+    LAUNCH(k_batching_devices, G(I * N), kB, 0, s, pb.bstart.p, B, n, I, static_cast<u32>(N), out.iter_group.p,
+           out.iter_dev_offsets.p, out.dev_index.p, out.dev_pack_offsets.p);
+    LAUNCH(k_batching_packs, G(n), kB, 0, s, pb.order.p, pb.bidx.p, pb.bmax.p, n, out.pack_capacity.p,
+           out.pack_total.p, out.pack_attention.p, out.pack_member_offsets.p, out.member_index.p);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
 }  // namespace hbp_b200

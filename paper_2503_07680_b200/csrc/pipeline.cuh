@@ -116,6 +116,24 @@ void batching_device(Ctx& c, int64_t capacity, i64 n_packs, const int64_t* pack_
 void validate_groups(const std::vector<hbp_group_config>& g, int64_t l_max);
 void validate_strategy(const hbp_strategy& s);
 
+// sorted_batching / random_batching (packing.cpp:265-317): samples in
+// (length desc, id asc) order or Rng(derive_seed(seed, "random-batching"))
+// order, cut greedily into batches while count * max <= budget -- the cut
+// positions are the chain of a monotone next(), found like next-fit's.
+struct PaddedBatches {
+    u64 n = 0, n_batches = 0;
+    DevBuf<u64> order;   // entries (len << 32 | corpus index) in batching order
+    DevBuf<u32> bstart;  // first position of each batch
+    DevBuf<u32> bidx;    // batch of each position
+    DevBuf<u32> bmax;    // longest sample of each batch
+};
+void padded_batches_device(Ctx& c, const DeviceCorpus& corpus, int64_t budget, bool sorted, uint64_t seed,
+                           PaddedBatches& out);
+// build_batching_plan (balance.cpp:260-298): device g of iteration i holds
+// batch i * N + g as single-sample packs padded to the batch's longest.
+void batching_plan_device(Ctx& c, const DeviceCorpus& corpus, const hbp_group_config& group, int32_t device_count,
+                          bool sorted, uint64_t seed, DevicePlan& out);
+
 }  // namespace hbp_b200
 
 // The C-ABI plan handle (include/hbp_b200.h): the device plan, its host view

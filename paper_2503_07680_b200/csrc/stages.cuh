@@ -29,6 +29,12 @@ struct PackSink {
 // nextfit.cu: next-fit over F, freeze packs with total >= tmin into sink
 // (after the n_members / n_packs it already holds; both updated), the rest
 // (in pack order) into newpool. Returns the new pool size.
+// Starts of the chain 0 -> nxt[0] -> ... (nxt monotone, nxt[s] > s) as bits:
+// chain_flag_words(m) u32 words (tiles of 2048 positions); tlast[tile] =
+// 1 + the tile's last start (0: none), chain_flag_words(m) / 64 entries.
+u64 chain_flag_words(u64 m);
+void chain_starts(Ctx& c, const u32* nxt, u64 m, u32* flags, u32* tlast);
+
 i64 nextfit_freeze(Ctx& c, const u64* F, i64 m, u32 cap, u64 tmin, PackSink sink, u64* newpool, u64& n_members,
                    u64& n_packs);
 

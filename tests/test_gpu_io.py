@@ -71,3 +71,47 @@ def test_plan_json_buffer_too_small(ctx):
     assert lib.hbp_plan_to_json(ctx.h, plan.h, C.byref(s), None, 0, C.byref(n)) == 0
     buf = C.create_string_buffer(8)
     assert lib.hbp_plan_to_json(ctx.h, plan.h, C.byref(s), buf, 8, C.byref(n)) == abi.HBP_ERR_VALIDATION
+
+
+def batching_cases(oracle):
+    L = np.maximum(oracle.synth(8_000, "lognormal:7.2:0.9", 0.0, "", 16384, 5), 1)
+    yield "batching_sorted_8k", None, L, (16384, 1, 0), 8, "sorted", 0
+    rng = np.random.default_rng(8)
+    ids = rng.permutation(30_000)[:8_000].astype(np.int64) - 10_000
+    yield "batching_random_8k", ids, L, (32768, 2, 4), 3, "random", 99
+
+
+@pytest.mark.parametrize("name", ["batching_sorted_8k", "batching_random_8k"])
+def test_batching_plan_matches_reference_digest(ctx, oracle, name):
+    # build_batching_plan (balance.cpp:260-298) -> plan_to_json, byte-identical
+    for case, ids, L, group, dc, mode, seed in batching_cases(oracle):
+        if case != name:
+            continue
+        plan = ctx.build_batching_plan(ids, L, group, device_count=dc, mode=mode, seed=seed)
+        text = plan.to_json(ids, L)
+        assert len(text) == GOLD[name]["bytes"]
+        assert hashlib.sha256(text).hexdigest() == GOLD[name]["sha256"]
+        # the plan feeds report / simulate like any other
+        assert plan.report().ave_t > 0
+
+
+@pytest.mark.parametrize("mode,budget", [("sorted", 16384), ("random", 16384), ("random", 131072)])
+def test_padded_batching_vs_compiled_reference(ctx, oracle, mode, budget):
+    try:
+        from pyoracle import Oracle
+        ref = Oracle("reference")
+    except (ImportError, FileNotFoundError, OSError):
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(budget)
+    L = np.maximum(oracle.synth(50_000, "lognormal:7.0:1.0", 0.0, "", 16384, 13), 1)
+    ids = rng.permutation(100_000)[:50_000].astype(np.int64) - 30_000
+    order, off, mx = ctx.padded_batching(ids, L, budget, mode, seed=4)
+    r_order, r_off, r_mx = ref.padded_batching(ids, L, budget, mode, seed=4)
+    assert np.array_equal(ids[order], r_order)
+    assert np.array_equal(off, r_off)
+    assert np.array_equal(mx, r_mx)
+
+
+def test_padded_batching_budget_error(ctx):
+    with pytest.raises(abi.ValidationError, match=r"token budget 100 is below the longest sample \(300\)"):
+        ctx.padded_batching(None, np.array([100, 300, 5], dtype=np.int64), 100, "sorted")

@@ -347,48 +347,32 @@ PackList pack(const SampleSet& samples, Tokens capacity, const PackingStrategy& 
 }
 
 namespace {
-std::vector<PaddedBatch> budgeted(const std::vector<Sample>& order, Tokens budget) {
-    std::vector<PaddedBatch> out;
-    PaddedBatch cur;
-    for (const auto& s : order) {
-        const Tokens next_max = std::max(cur.max_length, s.length);
-        if (!cur.samples.empty() && static_cast<Tokens>(cur.samples.size() + 1) * next_max > budget) {
-            cur.padded_tokens = static_cast<Tokens>(cur.samples.size()) * cur.max_length;
-            out.push_back(std::move(cur));
-            cur = PaddedBatch{};
-        }
-        cur.samples.push_back(s);
-        cur.max_length = std::max(cur.max_length, s.length);
-    }
-    if (!cur.samples.empty()) {
-        cur.padded_tokens = static_cast<Tokens>(cur.samples.size()) * cur.max_length;
-        out.push_back(std::move(cur));
+// hbp_padded_batching (GPU) -> PaddedBatch lists
+std::vector<PaddedBatch> padded(const SampleSet& samples, Tokens token_budget, int32_t mode, std::uint64_t seed) {
+    const SoA s = soa(samples.samples);
+    const hbp_samples v = s.view(samples.source);
+    const size_t n = samples.samples.size();
+    std::vector<int32_t> order(n ? n : 1);
+    std::vector<int64_t> off(n + 1), mx(n ? n : 1);
+    int64_t nb = 0;
+    check(hbp_padded_batching(ctx(), &v, token_budget, mode, seed, order.data(), off.data(), mx.data(), &nb));
+    std::vector<PaddedBatch> out(static_cast<size_t>(nb));
+    for (int64_t b = 0; b < nb; ++b) {
+        auto& pb = out[static_cast<size_t>(b)];
+        for (int64_t k = off[b]; k < off[b + 1]; ++k) pb.samples.push_back(samples.samples[order[k]]);
+        pb.max_length = mx[b];
+        pb.padded_tokens = static_cast<Tokens>(pb.samples.size()) * pb.max_length;
     }
     return out;
-}
-
-void check_budget(const SampleSet& samples, Tokens budget) {
-    if (budget < samples.max_length())
-        throw ValidationError("token budget " + std::to_string(budget) + " is below the longest sample (" +
-                              std::to_string(samples.max_length()) + ")");
 }
 }  // namespace
 
 std::vector<PaddedBatch> sorted_batching(const SampleSet& samples, Tokens token_budget) {
-    check_budget(samples, token_budget);
-    std::vector<Sample> order = samples.samples;
-    std::sort(order.begin(), order.end(), [](const Sample& a, const Sample& b) {
-        return a.length != b.length ? a.length > b.length : a.id < b.id;
-    });
-    return budgeted(order, token_budget);
+    return padded(samples, token_budget, HBP_BATCHING_SORTED, 0);
 }
 
 std::vector<PaddedBatch> random_batching(const SampleSet& samples, Tokens token_budget, std::uint64_t seed) {
-    check_budget(samples, token_budget);
-    std::vector<Sample> order = samples.samples;
-    Rng rng(derive_seed(seed, "random-batching"));
-    rng.shuffle(order);
-    return budgeted(order, token_budget);
+    return padded(samples, token_budget, HBP_BATCHING_RANDOM, seed);
 }
 
 // ---------------------------------------------------------------------------
@@ -488,30 +472,17 @@ Plan build_plan(const SampleSet& samples, const HierarchicalGroups& groups, cons
 
 Plan build_batching_plan(const SampleSet& samples, GroupConfig group, int device_count, BatchingMode mode,
                          std::uint64_t seed) {
-    samples.validate();
-    if (device_count < 1) throw ValidationError("device count must be >= 1");
-    const auto batches = mode == BatchingMode::Sorted ? sorted_batching(samples, group.length)
-                                                      : random_batching(samples, group.length, seed);
+    const SoA s = soa(samples.samples);
+    const hbp_samples v = s.view(samples.source);
+    const hbp_group_config g{group.length, group.config.sp, group.config.ckpt};
+    PlanHandle h;
+    check(hbp_build_batching_plan(ctx(), &v, g, device_count,
+                                  mode == BatchingMode::Sorted ? HBP_BATCHING_SORTED : HBP_BATCHING_RANDOM, seed, &h.p));
     Plan plan;
     plan.groups = HierarchicalGroups::single(group);
     plan.device_count = device_count;
     plan.seed = seed;
-    const bool sp = group.config.sp > 1;
-    const auto n = static_cast<std::size_t>(device_count);
-    for (std::size_t i = 0; i < batches.size(); i += n) {
-        Iteration it;
-        for (std::size_t d = 0; d < n; ++d) {
-            std::vector<Pack> packs;
-            if (i + d < batches.size())
-                for (const auto& s : batches[i + d].samples) {
-                    Pack p = Pack::make(batches[i + d].max_length);
-                    p.add(s);
-                    packs.push_back(std::move(p));
-                }
-            it.devices.push_back(DeviceBatch::build(static_cast<int>(d), std::move(packs), sp));
-        }
-        plan.iterations.push_back(std::move(it));
-    }
+    plan.iterations = iterations_from_view(h.view(), samples.samples, &plan.groups, false);
     return plan;
 }
 

@@ -137,6 +137,7 @@ typedef struct hbp_plan_view {
     const int64_t* pack_attention;      /* [n_packs] */
     const int64_t* pack_member_offsets; /* [n_packs + 1] */
     const int32_t* member_index;        /* [n_members] */
+    const int8_t* iter_phase;           /* [n_iterations]: 1 = warmup (curriculum_order); NULL: all hybrid */
 } hbp_plan_view;
 
 /* hbp::MetricsReport headline numbers (metrics.hpp:67-74). */
@@ -289,6 +290,24 @@ int hbp_padded_batching(hbp_ctx* ctx, const hbp_samples* samples, int64_t token_
  * HierarchicalGroups::single(group). */
 int hbp_build_batching_plan(hbp_ctx* ctx, const hbp_samples* samples, hbp_group_config group,
                             int32_t device_count, int32_t mode, uint64_t seed, hbp_plan** out);
+
+/* hbp::curriculum_order (src/schedule.cpp:10-63) of a device plan: a new
+ * plan whose first warmup_iterations iterations (phase warmup) are drawn,
+ * seeded by derive_seed(seed, "curriculum"), from groups below
+ * short_group_cutoff, the rest a seeded shuffle of what is left. Errors:
+ * "warmup_iterations must be >= 0", "short_group_cutoff must select ...",
+ * "curriculum needs W short-group iterations but the plan has only S". */
+int hbp_curriculum_order(hbp_ctx* ctx, hbp_plan* plan, int32_t warmup_iterations, int32_t short_group_cutoff,
+                         hbp_plan** out);
+
+/* hbp::assign_runtime (src/schedule.cpp:65-77): per-iteration sp / ckpt of
+ * its group (host arrays [n_iterations]) and the number of changes between
+ * consecutive iterations. */
+int hbp_assign_runtime(hbp_ctx* ctx, hbp_plan* plan, int32_t* sp, int32_t* ckpt, int64_t* switch_count);
+
+/* hbp::write_schedule_csv (src/schedule.cpp:79-89): "iteration,group,sp,
+ * ckpt,phase" rows; same buffer convention as hbp_plan_to_json. */
+int hbp_schedule_csv(hbp_ctx* ctx, hbp_plan* plan, char* out, int64_t capacity, int64_t* out_len);
 
 /* Plan manifest (replaces hbp::plan_to_json, src/io.cpp:85-110): the
  * byte-identical nlohmann dump(2) text of the plan, built on the GPU.

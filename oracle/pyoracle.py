@@ -254,6 +254,30 @@ class Oracle:
         b = nb.value
         return order[:n], off[:b + 1], mx[:b]
 
+    def curriculum(self, ids, lengths, groups, l_best, warmup: int, cutoff: int, **opts):
+        """(manifest, schedule csv, sp[], ckpt[], switch_count) of curriculum_order(build_plan(...))
+        in the reference (reference kind only)."""
+        lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+        ids = self._ids(ids, len(lengths))
+        g, keep = abi.make_groups(groups, l_best)
+        o = abi.make_options(**opts)
+        j, jn, c, cn = C.c_void_p(), C.c_int64(), C.c_void_p(), C.c_int64()
+        cap = len(lengths) + 1
+        sp = np.zeros(cap, dtype=np.int32)
+        ck = np.zeros(cap, dtype=np.int32)
+        sw = C.c_int64()
+        rc = self.lib.oracle_curriculum(abi.ptr(ids, C.c_int64), abi.ptr(lengths, C.c_int64), C.c_int64(len(lengths)),
+                                        C.byref(g), C.byref(o), C.c_int32(warmup), C.c_int32(cutoff), C.byref(j),
+                                        C.byref(jn), C.byref(c), C.byref(cn), abi.ptr(sp, C.c_int32),
+                                        abi.ptr(ck, C.c_int32), C.byref(sw), self.err, len(self.err))
+        self._check(rc)
+        jt, ct = C.string_at(j, jn.value), C.string_at(c, cn.value)
+        self.lib.oracle_free_text.argtypes = [C.c_void_p]
+        self.lib.oracle_free_text(j)
+        self.lib.oracle_free_text(c)
+        ni = ct.count(b"\n") - 1
+        return jt, ct, sp[:ni], ck[:ni], sw.value
+
     def report(self, plan: abi.FlatPlan):
         v = plan.view()
         m = abi.Metrics()

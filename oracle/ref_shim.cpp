@@ -17,6 +17,7 @@
 #include "hbp/autoselect.hpp"
 #include "hbp/balance.hpp"
 #include "hbp/io.hpp"
+#include "hbp/schedule.hpp"
 #include "hbp/costmodel.hpp"
 #include "hbp/errors.hpp"
 #include "hbp/ingest.hpp"
@@ -407,6 +408,44 @@ int oracle_build_plan_json(const int64_t* ids, const int64_t* lengths, int64_t n
 }
 
 void oracle_free_text(char* p) { std::free(p); }
+
+// curriculum_order(build_plan(...)): its manifest, schedule CSV and
+// runtime assignment (sp / ckpt per iteration, switch count).
+int oracle_curriculum(const int64_t* ids, const int64_t* lengths, int64_t n,
+                      const hbp_groups* groups, const hbp_plan_options* options,
+                      int32_t warmup, int32_t cutoff, char** json, int64_t* json_len,
+                      char** csv, int64_t* csv_len, int32_t* sp, int32_t* ckpt,
+                      int64_t* switch_count, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        R::PlanOptions o;
+        o.strategy = make_strategy(&options->strategy);
+        o.device_count = options->device_count;
+        o.seed = options->seed;
+        o.balance_batching = options->balance_batching != 0;
+        o.greedy_fill = options->greedy_fill != 0;
+        const auto plan =
+            R::build_plan(make_set(ids, lengths, n), make_groups(groups), o);
+        R::CurriculumSpec spec;
+        spec.warmup_iterations = warmup;
+        spec.short_group_cutoff = cutoff;
+        const auto cur = R::curriculum_order(plan, spec);
+        auto dup = [](const std::string& t, char** out, int64_t* len) {
+            *out = static_cast<char*>(std::malloc(t.size() + 1));
+            std::memcpy(*out, t.c_str(), t.size() + 1);
+            *len = static_cast<int64_t>(t.size());
+        };
+        dup(R::plan_to_json(cur), json, json_len);
+        std::ostringstream os;
+        R::write_schedule_csv(cur, os);
+        dup(os.str(), csv, csv_len);
+        const auto ra = R::assign_runtime(cur);
+        for (std::size_t i = 0; i < ra.per_iteration.size(); ++i) {
+            sp[i] = ra.per_iteration[i].sp;
+            ckpt[i] = ra.per_iteration[i].ckpt;
+        }
+        *switch_count = ra.switch_count;
+    });
+}
 
 // The reference's build_batching_plan manifest and padded batches
 // (mode 0 sorted, 1 random).

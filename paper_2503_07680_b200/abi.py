@@ -124,7 +124,8 @@ class PlanView(C.Structure):
                 ("pack_total", C.POINTER(C.c_int64)),
                 ("pack_attention", C.POINTER(C.c_int64)),
                 ("pack_member_offsets", C.POINTER(C.c_int64)),
-                ("member_index", C.POINTER(C.c_int32))]
+                ("member_index", C.POINTER(C.c_int32)),
+                ("iter_phase", C.POINTER(C.c_int8))]
 
 
 class Metrics(C.Structure):
@@ -564,6 +565,39 @@ class DevicePlanHandle:
         self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), None, 0, C.byref(n)))
         buf = np.empty(max(1, n.value), dtype=np.uint8)  # no zero fill
         self.ctx.check(lib.hbp_plan_to_json(self.ctx.h, self.h, C.byref(s), buf.ctypes.data_as(C.c_char_p), n.value,
+                                            C.byref(n)))
+        return buf[:n.value].tobytes()
+
+    def curriculum_order(self, warmup_iterations: int = 500, short_group_cutoff: int = 1) -> "DevicePlanHandle":
+        """hbp::curriculum_order (schedule.cpp:10-63) on the GPU: a new device plan."""
+        lib = self.ctx.lib
+        h = C.c_void_p()
+        lib.hbp_curriculum_order.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+        self.ctx.check(lib.hbp_curriculum_order(self.ctx.h, self.h, warmup_iterations, short_group_cutoff,
+                                                C.byref(h)))
+        return DevicePlanHandle(self.ctx, h, self.groups, self.l_best)
+
+    def assign_runtime(self):
+        """hbp::assign_runtime: (sp[], ckpt[], switch_count)."""
+        lib = self.ctx.lib
+        n = self.flat().iter_group.shape[0]
+        sp = np.zeros(max(n, 1), dtype=np.int32)
+        ck = np.zeros(max(n, 1), dtype=np.int32)
+        sw = C.c_int64()
+        lib.hbp_assign_runtime.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int64)]
+        self.ctx.check(lib.hbp_assign_runtime(self.ctx.h, self.h, ptr(sp, C.c_int32), ptr(ck, C.c_int32),
+                                              C.byref(sw)))
+        return sp[:n], ck[:n], sw.value
+
+    def schedule_csv(self) -> bytes:
+        """hbp::write_schedule_csv text, written on the GPU."""
+        lib = self.ctx.lib
+        n = C.c_int64()
+        lib.hbp_schedule_csv.argtypes = [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+        self.ctx.check(lib.hbp_schedule_csv(self.ctx.h, self.h, None, 0, C.byref(n)))
+        buf = np.empty(max(1, n.value), dtype=np.uint8)
+        self.ctx.check(lib.hbp_schedule_csv(self.ctx.h, self.h, buf.ctypes.data_as(C.c_char_p), n.value,
                                             C.byref(n)))
         return buf[:n.value].tobytes()
 

@@ -60,6 +60,10 @@ static hbp_plan* new_plan(hbp_ctx* ctx) {
     return p;
 }
 
+static void delete_plan(hbp_plan* p);
+hbp_plan* hbp_b200_new_plan(hbp_ctx* ctx) { return new_plan(ctx); }
+void hbp_b200_delete_plan(hbp_plan* p) { delete_plan(p); }
+
 static void delete_plan(hbp_plan* p) {
     if (p->owner) {
         p->owner->plans.erase(p);
@@ -384,6 +388,7 @@ int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out) {
         v.pack_attention = d.h_pack_attention;
         v.pack_member_offsets = d.h_pack_member_offsets;
         v.member_index = d.h_member_index;
+        v.iter_phase = d.h_iter_phase;
         *out = v;
     });
 }

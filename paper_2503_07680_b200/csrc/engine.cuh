@@ -123,7 +123,10 @@ void for_each_index(Ctx& c, u64 n, F f) {
 // ---- stage: exact Fisher-Yates (shuffle.cu) --------------------------------
 // src[p] = the input position whose element Rng(seed).shuffle() leaves at
 // output position p, for a vector of m elements (reference rng.hpp:61-68).
-void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src);
+// draw_base: draws of the same Rng already consumed (a second shuffle with
+// one generator, schedule.cpp:39-48); draws_used: draws this one consumed.
+void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src, uint64_t draw_base = 0,
+                         uint64_t* draws_used = nullptr);
 // out[p] = in[src[p]] for 8-byte elements.
 void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m);
 void gather_u32(Ctx& c, const u32* in, const u32* src, u32* out, i64 m);

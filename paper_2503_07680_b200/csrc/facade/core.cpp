@@ -78,6 +78,7 @@ std::vector<Iteration> iterations_from_view(const hbp_plan_view& v, const std::v
     for (int64_t i = 0; i < v.n_iterations; ++i) {
         Iteration& it = out[static_cast<size_t>(i)];
         it.group_index = v.iter_group[i];
+        it.phase = (v.iter_phase && v.iter_phase[i]) ? Phase::Warmup : Phase::Hybrid;
         const bool sp = groups ? groups->groups.at(static_cast<size_t>(it.group_index)).config.sp > 1 : sp_comm_fixed;
         for (int64_t d = v.iter_dev_offsets[i]; d < v.iter_dev_offsets[i + 1]; ++d) {
             std::vector<Pack> packs;

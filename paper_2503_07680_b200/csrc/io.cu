@@ -53,6 +53,7 @@ __host__ __device__ __forceinline__ u32 digits_i64(int64_t v) {
 #define J_SAMPLE_CLOSE "\n              ]"
 #define J_ITER_CLOSE "\n      ],\n      \"group\": "
 #define J_ITER_PHASE ",\n      \"phase\": \"hybrid\"\n    }"
+#define J_ITER_PHASE_W ",\n      \"phase\": \"warmup\"\n    }"
 #define JLEN(s) (sizeof(s) - 1)
 
 struct JsonArgs {
@@ -64,6 +65,7 @@ struct JsonArgs {
     const int32_t* member_index;
     const int64_t* ids;  // null: ids are the corpus indices
     const int64_t* lengths;
+    const int8_t* phase;  // null: all hybrid
     int64_t n_iterations, n_devices;
 };
 
@@ -172,11 +174,13 @@ __device__ u64 slot_text(const JsonArgs& a, int64_t g, char* out) {
     }
     if (last) {
         const int64_t grp = a.iter_group[i];
-        n += JLEN(J_ITER_CLOSE) + digits_i64(grp) + JLEN(J_ITER_PHASE);
+        const bool warm = a.phase && a.phase[i];
+        n += JLEN(J_ITER_CLOSE) + digits_i64(grp) + (warm ? JLEN(J_ITER_PHASE_W) : JLEN(J_ITER_PHASE));
         if (WRITE) {
             w.lit(J_ITER_CLOSE, JLEN(J_ITER_CLOSE));
             w.num(grp);
-            w.lit(J_ITER_PHASE, JLEN(J_ITER_PHASE));
+            if (warm) w.lit(J_ITER_PHASE_W, JLEN(J_ITER_PHASE_W));
+            else w.lit(J_ITER_PHASE, JLEN(J_ITER_PHASE));
         }
     }
     return n;
@@ -246,7 +250,8 @@ extern "C" int hbp_plan_to_json(hbp_ctx* ctx, hbp_plan* plan, const hbp_samples*
             }
         }
         JsonArgs a{dp.iter_group.p, dp.iter_dev_offsets.p, dp.dev_pack_offsets.p, dp.pack_capacity.p,
-                   dp.pack_member_offsets.p, dp.member_index.p, ids, lens, dp.n_iterations, dp.n_devices};
+                   dp.pack_member_offsets.p, dp.member_index.p, ids, lens, dp.iter_phase.p, dp.n_iterations,
+                   dp.n_devices};
         const u64 G = static_cast<u64>(dp.n_devices);
         DevBuf<u64> len(G + 1, s), off(G + 1, s);
         u64 body = 0;

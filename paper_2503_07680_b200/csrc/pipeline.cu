@@ -1040,7 +1040,7 @@ void plan_to_host(Ctx& c, DevicePlan& p) {
     if (p.on_host) return;
     const size_t I = static_cast<size_t>(p.n_iterations), D = static_cast<size_t>(p.n_devices),
                  P = static_cast<size_t>(p.n_packs), M = static_cast<size_t>(p.n_members);
-    const size_t bytes = 8 * ((I + 1) + (I + 1) + (D + 1) + (D + 1) + 4 * (P + 1) + (P + 1) + (M + 1) / 2 + 8);
+    const size_t bytes = 8 * ((I + 1) + (I + 1) + (D + 1) + (D + 1) + 4 * (P + 1) + (P + 1) + (M + 1) / 2 + I / 8 + 10);
     if (!p.host.p) p.host = c.host_pool.acquire(bytes);
     char* cur = static_cast<char*>(p.host.p);
     auto cp = [&](auto*& h, auto& d, size_t n) {
@@ -1058,6 +1058,8 @@ void plan_to_host(Ctx& c, DevicePlan& p) {
     cp(p.h_pack_attention, p.pack_attention, P);
     cp(p.h_pack_member_offsets, p.pack_member_offsets, P + 1);
     cp(p.h_member_index, p.member_index, M);
+    if (p.iter_phase.p) cp(p.h_iter_phase, p.iter_phase, I);
+    else p.h_iter_phase = nullptr;
     CUDA_CHECK(cudaStreamSynchronize(c.stream));
     p.on_host = true;
 }

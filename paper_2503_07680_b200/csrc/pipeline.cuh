@@ -22,11 +22,13 @@ struct DevicePlan {
     DevBuf<int64_t> dev_pack_offsets;
     DevBuf<int64_t> pack_capacity, pack_total, pack_attention, pack_member_offsets;
     DevBuf<int32_t> member_index;
+    DevBuf<int8_t> iter_phase;  // 1 = warmup (curriculum_order); empty: every iteration hybrid
     // host mirror, in one pinned block (returned to the context's pool when
     // the plan is freed; freed here if the plan outlives its context)
     bool on_host = false;
     HostBlock host{};
     int32_t *h_iter_group = nullptr, *h_dev_index = nullptr, *h_member_index = nullptr;
+    int8_t* h_iter_phase = nullptr;
     int64_t *h_iter_dev_offsets = nullptr, *h_dev_pack_offsets = nullptr, *h_pack_capacity = nullptr,
             *h_pack_total = nullptr, *h_pack_attention = nullptr, *h_pack_member_offsets = nullptr;
     DevicePlan() = default;
@@ -46,6 +48,7 @@ struct DevicePlan {
         pack_attention.release();
         pack_member_offsets.release();
         member_index.release();
+        iter_phase.release();
     }
 };
 

@@ -25,20 +25,20 @@ namespace hbp_b200 {
 namespace {
 
 // Draw for step i (m >= i >= 2) with `shift` rejected draws before it.
-__device__ __forceinline__ u32 fy_target(u64 seed, u64 m, u64 i, u64 shift, bool& rejected) {
-    const u64 v = splitmix_draw(seed, m - i + 1 + shift);
+__device__ __forceinline__ u32 fy_target(u64 seed, u64 base, u64 m, u64 i, u64 shift, bool& rejected) {
+    const u64 v = splitmix_draw(seed, base + m - i + 1 + shift);
     const u64 r = v % i;
     // v >= UINT64_MAX - UINT64_MAX % i  <=>  (v - r) + i overflows
     rejected = (v - r) > (~0ull - i);
     return static_cast<u32>(r);
 }
 
-__global__ void k_fy_targets(u64 seed, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
+__global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
                              unsigned long long* __restrict__ rej) {
     for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
         bool bad;
-        const u32 j = fy_target(seed, m, i, 0, bad);
+        const u32 j = fy_target(seed, base, m, i, 0, bad);
         if (bad) atomicMax(rej, static_cast<unsigned long long>(i));
         tgt[i] = j;
         atomicAdd(&cnt[j], 1u);
@@ -47,8 +47,8 @@ __global__ void k_fy_targets(u64 seed, u64 m, u32* __restrict__ tgt, u32* __rest
 
 // Rare path: a draw at step `rej` was rejected. Every step i <= rej then
 // uses one more draw; repeat until no rejection remains.
-__global__ void k_fy_fix(u64 seed, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
-                         unsigned long long* __restrict__ rej) {
+__global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
+                         unsigned long long* __restrict__ rej, unsigned long long* __restrict__ used) {
     __shared__ unsigned long long s_rej;
     __shared__ unsigned long long s_next;
     u64 shift = 0;
@@ -61,7 +61,7 @@ __global__ void k_fy_fix(u64 seed, u64 m, u32* __restrict__ tgt, u32* __restrict
         __syncthreads();
         for (u64 i = 2 + threadIdx.x; i <= upto; i += blockDim.x) {
             bool bad;
-            const u32 j = fy_target(seed, m, i, shift, bad);
+            const u32 j = fy_target(seed, base, m, i, shift, bad);
             // a rejection strictly inside the shifted suffix needs another pass
             if (bad) atomicMax(&s_next, static_cast<unsigned long long>(i));
             const u32 old = tgt[i];
@@ -77,6 +77,8 @@ __global__ void k_fy_fix(u64 seed, u64 m, u32* __restrict__ tgt, u32* __restrict
         if (threadIdx.x == 0) s_rej = s_next;
         __syncthreads();
     }
+    // draws the shuffle consumed: one per step plus one per rejection
+    if (used && threadIdx.x == 0) *used = (m - 1) + shift;
 }
 
 __global__ void k_fy_scatter(u64 m, const u32* __restrict__ tgt, const u32* __restrict__ off,
@@ -161,7 +163,8 @@ __global__ void k_gather(const T* __restrict__ in, const u32* __restrict__ src, 
 
 }  // namespace
 
-void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src) {
+void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src, uint64_t draw_base, uint64_t* draws_used) {
+    if (draws_used) *draws_used = 0;
     if (m_signed <= 0) return;
     const u64 m = static_cast<u64>(m_signed);
     cudaStream_t s = c.stream;
@@ -169,6 +172,7 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src) {
         CUDA_CHECK(cudaMemsetAsync(src, 0, sizeof(u32), s));
         return;
     }
+    DevBuf<unsigned long long> used(draws_used ? 1 : 0, s);
     DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), off(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s),
         root(m + 1, s);
     DevBuf<unsigned long long> rej(1, s);
@@ -177,8 +181,8 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src) {
     rej.zero();
     const unsigned B = 256;
     const unsigned G = grid_for(m, B, 148u * 32u);
-    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, m, tgt.p, cnt.p, rej.p);
-    LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, m, tgt.p, cnt.p, rej.p);
+    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p);
+    LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
     // exclusive scan of per-target counts -> list offsets (m + 1 entries)
     const u32* cntp = cnt.p;
     u32* offp = off.p;
@@ -190,6 +194,7 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src) {
     LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);
     LAUNCH_B("fy.roots", 8.0 * m, k_fy_roots, G, B, 0, s, m, link.p, root.p);
     LAUNCH_B("fy.sources", 16.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, src);
+    if (draws_used) *draws_used = read_scalar(c, used.p);
 }
 
 void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m) {

@@ -371,7 +371,7 @@ def c4_profile():
     return p
 
 
-def run_c4_leg(ctx, lib, steps=2):
+def run_c4_leg(ctx, lib, steps=3, warmup=3):
     """BASELINE config C4: 100M samples of the C2 spec, groups [16K sp1,
     128K sp8] with ckpt derived under the DeepSeek-V2 236B cost model, 8 DP
     devices: build_plan + report (ABR/CR) + simulate, corpus resident in HBM.
@@ -396,8 +396,9 @@ def run_c4_leg(ctx, lib, steps=2):
         st = plan.simulate(prof)
         return plan, m, st
 
-    out = step()  # warm-up (memory pool growth)
-    out = None
+    for _ in range(warmup):  # memory pool / block cache growth at this size takes a few steps
+        out = step()
+        out = None
     ms = []
     for _ in range(steps):
         out = None

@@ -270,6 +270,32 @@ int hbp_build_plan(hbp_ctx* ctx, const hbp_samples* samples,
  * copies the plan to host; the view stays valid until hbp_plan_free. */
 int hbp_plan_view_get(hbp_ctx* ctx, hbp_plan* plan, hbp_plan_view* out);
 
+/* Report / simulate sharded by data-parallel column.
+ * Per-iteration DEVICE buffers (n_iterations entries each) the caller
+ * allocates and all-reduces between the calls:
+ *   phase 0 on columns [col0, col1): tmax, amax, busy (all-reduce MAX),
+ *           tokens, pad_gap, pad_cap (SUM), sim_err (one int64, MIN);
+ *   phase 1: tgap, agap (SUM);
+ *   finish:  metrics and simulate totals, bit-identical to hbp_report_plan /
+ *            hbp_simulate_plan on the whole plan (gaps are integers).
+ * profile NULL: report only (busy and sim_err may be NULL). */
+typedef struct hbp_eval_columns_bufs {
+    int64_t* tmax;
+    int64_t* amax;
+    int64_t* tokens;
+    int64_t* pad_gap;
+    int64_t* pad_cap;
+    double* busy;
+    int64_t* tgap;
+    int64_t* agap;
+    int64_t* sim_err;
+} hbp_eval_columns_bufs;
+
+int hbp_eval_columns(hbp_ctx* ctx, hbp_plan* plan, int32_t phase, int32_t col0, int32_t col1,
+                     const hbp_hardware_profile* profile, const hbp_eval_columns_bufs* bufs);
+int hbp_eval_columns_finish(hbp_ctx* ctx, hbp_plan* plan, const hbp_hardware_profile* profile,
+                            const hbp_eval_columns_bufs* bufs, hbp_metrics* out, hbp_sim_totals* sim);
+
 /* Padded-batching baselines. */
 enum { HBP_BATCHING_SORTED = 0, HBP_BATCHING_RANDOM = 1 };
 

@@ -520,6 +520,33 @@ int hbp_simulate_plan(hbp_ctx* ctx, hbp_plan* plan, const hbp_hardware_profile* 
     });
 }
 
+int hbp_eval_columns(hbp_ctx* ctx, hbp_plan* plan, int32_t phase, int32_t col0, int32_t col1,
+                     const hbp_hardware_profile* profile, const hbp_eval_columns_bufs* bufs) {
+    return guarded(ctx, [&] {
+        if (plan == nullptr || bufs == nullptr) fail_validation("null plan or buffers");
+        if (phase != 0 && phase != 1) fail_validation("eval_columns: phase must be 0 or 1");
+        if (col0 < 0 || col1 < col0) fail_validation("eval_columns: bad column range");
+        eval_columns(*ctx, arrays_of(plan->dp), plan->dp.groups, profile, phase, col0, col1, *bufs);
+    });
+}
+
+int hbp_eval_columns_finish(hbp_ctx* ctx, hbp_plan* plan, const hbp_hardware_profile* profile,
+                            const hbp_eval_columns_bufs* bufs, hbp_metrics* out, hbp_sim_totals* sim) {
+    return guarded(ctx, [&] {
+        if (plan == nullptr || bufs == nullptr) fail_validation("null plan or buffers");
+        EvalOut eo;
+        eval_columns_finish(*ctx, arrays_of(plan->dp), plan->dp.device_count, plan->dp.groups, profile, *bufs, eo);
+        if (out) *out = eo.m;
+        if (sim) {
+            sim->metrics = eo.m;
+            sim->total_seconds = eo.total_seconds;
+            sim->gpu_days = eo.total_seconds * static_cast<double>(plan->dp.device_count) / 86400.0;
+            sim->switch_count = eo.switch_count;
+            sim->device_count = plan->dp.device_count;
+        }
+    });
+}
+
 int hbp_memory_used(hbp_ctx* ctx, int64_t length, int32_t sp, int32_t ckpt, const hbp_hardware_profile* profile,
                     int64_t* out) {
     return guarded(ctx, [&] {

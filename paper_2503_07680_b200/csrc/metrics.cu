@@ -235,4 +235,218 @@ void eval_plan(Ctx& c, const PlanArrays& p, int32_t device_count, const std::vec
     out.switch_count = static_cast<int32_t>(tot.switches);
 }
 
+// ---------------------------------------------------------------------------
+// Evaluation sharded by data-parallel column: the rank
+// owning device columns [c0, c1) of every iteration computes their maxima,
+// sums and simulated busy times (phase 0), then -- after an all-reduce MAX
+// of the maxima -- their gaps to the maxima (phase 1); after an all-reduce
+// SUM of the gaps every rank finishes identically. Gaps are integers, so
+// their sum is exact in any order and DBR / ABR per iteration, and the
+// run-level reduction (same grid, same order as k_eval), are bit-identical
+// to the single-GPU report / simulate.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct ColArgs {
+    PlanArrays p;
+    const hbp_group_config* groups;
+    bool simulate;
+    hbp_hardware_profile prof;
+    int32_t c0, c1;
+    hbp_eval_columns_bufs b;
+};
+
+__global__ void __launch_bounds__(EB) k_cols_phase0(ColArgs a) {
+    const PlanArrays& P = a.p;
+    for (i64 i = blockIdx.x * static_cast<i64>(EB) + threadIdx.x; i < P.I; i += static_cast<i64>(gridDim.x) * EB) {
+        const i64 d0 = P.iter_dev_offsets[i], d1 = P.iter_dev_offsets[i + 1];
+        const hbp_group_config cfg = a.groups[P.iter_group[i]];
+        const i64 lo = d0 + a.c0 < d1 ? d0 + a.c0 : d1, hi = d0 + a.c1 < d1 ? d0 + a.c1 : d1;
+        int64_t tmax = 0, amax = 0, tokens = 0, pg = 0, pc = 0;
+        double imax = 0.0;
+        for (i64 d = lo; d < hi; ++d) {
+            int64_t t = 0, at = 0, padded = 0, attn = 0, maxcap = 0;
+            for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
+                const int64_t cap = P.pack_capacity[k], tot = P.pack_total[k];
+                t += tot;
+                at += P.pack_attention[k];
+                pg += cap - tot;
+                pc += cap;
+                padded += cap;
+                attn += P.pack_attention[k] + (cap - tot) * (cap - tot);
+                maxcap = cap > maxcap ? cap : maxcap;
+            }
+            tmax = t > tmax ? t : tmax;
+            amax = at > amax ? at : amax;
+            tokens += t;
+            if (a.simulate && padded != 0) {
+                bool bad = cfg.sp < 1 || cfg.ckpt < 0 || cfg.ckpt > a.prof.layer_count;
+                if (!bad) bad = cm_memory_used(maxcap, cfg.sp, cfg.ckpt, a.prof) > a.prof.device_memory;
+                if (bad) {
+                    atomicMin(reinterpret_cast<unsigned long long*>(a.b.sim_err),
+                              (static_cast<unsigned long long>(i) << 20) | static_cast<unsigned long long>(d - d0));
+                } else {
+                    const double busy = cm_iter_time(padded, attn, cfg.sp, cfg.ckpt, a.prof);
+                    imax = busy > imax ? busy : imax;
+                }
+            }
+        }
+        a.b.tmax[i] = tmax;
+        a.b.amax[i] = amax;
+        a.b.tokens[i] = tokens;
+        a.b.pad_gap[i] = pg;
+        a.b.pad_cap[i] = pc;
+        if (a.b.busy) a.b.busy[i] = imax;
+    }
+}
+
+__global__ void __launch_bounds__(EB) k_cols_phase1(ColArgs a) {
+    const PlanArrays& P = a.p;
+    for (i64 i = blockIdx.x * static_cast<i64>(EB) + threadIdx.x; i < P.I; i += static_cast<i64>(gridDim.x) * EB) {
+        const i64 d0 = P.iter_dev_offsets[i], d1 = P.iter_dev_offsets[i + 1];
+        const i64 lo = d0 + a.c0 < d1 ? d0 + a.c0 : d1, hi = d0 + a.c1 < d1 ? d0 + a.c1 : d1;
+        const int64_t tmax = a.b.tmax[i], amax = a.b.amax[i];
+        int64_t tg = 0, ag = 0;
+        for (i64 d = lo; d < hi; ++d) {
+            int64_t t = 0, at = 0;
+            for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
+                t += P.pack_total[k];
+                at += P.pack_attention[k];
+            }
+            tg += tmax - t;
+            ag += amax - at;
+        }
+        a.b.tgap[i] = tg;
+        a.b.agap[i] = ag;
+    }
+}
+
+// the run-level accumulation of k_eval over the reduced per-iteration values
+__global__ void __launch_bounds__(EB) k_cols_finish(ColArgs a, Partial* partials, unsigned long long* report_err) {
+    Partial acc{0, 0, 0, 0, 0, 0, 0, 0};
+    const PlanArrays& P = a.p;
+    for (i64 i = blockIdx.x * static_cast<i64>(EB) + threadIdx.x; i < P.I; i += static_cast<i64>(gridDim.x) * EB) {
+        const i64 d0 = P.iter_dev_offsets[i], d1 = P.iter_dev_offsets[i + 1];
+        const hbp_group_config cfg = a.groups[P.iter_group[i]];
+        if (i > 0) {
+            const hbp_group_config prev = a.groups[P.iter_group[i - 1]];
+            if (prev.sp != cfg.sp || prev.ckpt != cfg.ckpt) acc.switches += 1;
+        }
+        const double nd = static_cast<double>(d1 - d0);
+        if (d1 == d0) {
+            atomicMin(report_err, static_cast<unsigned long long>(2 * i));
+            continue;
+        }
+        const int64_t tmax = a.b.tmax[i], amax = a.b.amax[i], tokens = a.b.tokens[i];
+        acc.pad_gap += static_cast<unsigned long long>(a.b.pad_gap[i]);
+        acc.pad_cap += static_cast<unsigned long long>(a.b.pad_cap[i]);
+        acc.tokens += static_cast<unsigned long long>(tokens);
+        if (cfg.sp > 1) acc.comm += static_cast<unsigned long long>(tokens);
+        double dbr = 0.0, abr = 0.0;
+        if (tmax == 0) {
+            atomicMin(report_err, static_cast<unsigned long long>(2 * i));
+        } else if (amax == 0) {
+            atomicMin(report_err, static_cast<unsigned long long>(2 * i + 1));
+        } else {
+            dbr = __ddiv_rn(static_cast<double>(a.b.tgap[i]), __dmul_rn(static_cast<double>(tmax), nd));
+            abr = __ddiv_rn(static_cast<double>(a.b.agap[i]), __dmul_rn(static_cast<double>(amax), nd));
+        }
+        acc.dbr += dbr;
+        acc.abr += abr;
+        if (a.simulate) acc.seconds += a.b.busy[i];
+    }
+    __shared__ Partial s[EB];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = EB / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < static_cast<unsigned>(w)) add_partial(s[threadIdx.x], s[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
+}  // namespace
+
+void eval_columns(Ctx& c, const PlanArrays& p, const std::vector<hbp_group_config>& groups,
+                  const hbp_hardware_profile* profile, int phase, int32_t c0, int32_t c1,
+                  const hbp_eval_columns_bufs& b) {
+    cudaStream_t s = c.stream;
+    if (profile) {
+        const int pc = cm_profile_check(*profile);
+        if (pc) fail_validation(cm_profile_message(pc));
+    }
+    if (p.I == 0) fail_validation("metrics report: empty plan");
+    DevBuf<hbp_group_config> dg(groups.size(), s);
+    CUDA_CHECK(cudaMemcpyAsync(dg.p, groups.data(), sizeof(hbp_group_config) * groups.size(), cudaMemcpyHostToDevice, s));
+    ColArgs a{p, dg.p, profile != nullptr, profile ? *profile : hbp_hardware_profile{}, c0, c1, b};
+    const int grid = static_cast<int>(std::min<i64>(EG, (p.I + EB - 1) / EB));
+    if (phase == 0) {
+        if (b.sim_err) CUDA_CHECK(cudaMemsetAsync(b.sim_err, 0x7f, sizeof(int64_t), s));  // "none" = large
+        LAUNCH(k_cols_phase0, grid, EB, 0, s, a);
+    } else {
+        LAUNCH(k_cols_phase1, grid, EB, 0, s, a);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void eval_columns_finish(Ctx& c, const PlanArrays& p, int32_t device_count,
+                         const std::vector<hbp_group_config>& groups, const hbp_hardware_profile* profile,
+                         const hbp_eval_columns_bufs& b, EvalOut& out) {
+    cudaStream_t s = c.stream;
+    if (p.I == 0) fail_validation("metrics report: empty plan");
+    DevBuf<hbp_group_config> dg(groups.size(), s);
+    CUDA_CHECK(cudaMemcpyAsync(dg.p, groups.data(), sizeof(hbp_group_config) * groups.size(), cudaMemcpyHostToDevice, s));
+    DevBuf<Partial> partials(EG + 1, s);
+    DevBuf<unsigned long long> errs(1, s);
+    CUDA_CHECK(cudaMemsetAsync(errs.p, 0xff, sizeof(unsigned long long), s));
+    ColArgs a{p, dg.p, profile != nullptr, profile ? *profile : hbp_hardware_profile{}, 0, 0, b};
+    const int grid = static_cast<int>(std::min<i64>(EG, (p.I + EB - 1) / EB));
+    LAUNCH(k_cols_finish, grid, EB, 0, s, a, partials.p, errs.p);
+    LAUNCH(k_eval_final, 1, 32, 0, s, partials.p, grid, partials.p + EG);
+    const auto e = read_vector(c, errs.p, 1);
+    if (e[0] != ~0ull) {
+        const i64 i = static_cast<i64>(e[0] >> 1);
+        const bool abr = e[0] & 1;
+        const auto offs = read_vector(c, p.iter_dev_offsets + i, 2);
+        if (!abr && offs[1] == offs[0]) fail_validation("dbr: no devices");
+        fail_validation(abr ? "abr undefined: all devices carry zero attention"
+                            : "dbr undefined: all devices carry zero tokens");
+    }
+    if (profile && b.sim_err) {
+        const int64_t key = read_vector(c, b.sim_err, 1)[0];
+        if (key != 0x7f7f7f7f7f7f7f7fll) {
+            const i64 i = static_cast<i64>(static_cast<u64>(key) >> 20);
+            const i64 dd = static_cast<i64>(static_cast<u64>(key) & 0xfffff);
+            const int g = read_vector(c, p.iter_group + i, 1)[0];
+            const hbp_group_config cfg = groups.at(static_cast<size_t>(g));
+            if (cfg.sp < 1) fail_validation("sp must be >= 1");
+            if (cfg.ckpt < 0 || cfg.ckpt > profile->layer_count) fail_validation("ckpt must lie in [0, layer_count]");
+            const i64 d = read_vector(c, p.iter_dev_offsets + i, 1)[0] + dd;
+            const auto po = read_vector(c, p.dev_pack_offsets + d, 2);
+            const auto caps = read_vector(c, p.pack_capacity + po[0], static_cast<size_t>(po[1] - po[0]));
+            int64_t maxcap = 0;
+            for (auto v : caps) maxcap = v > maxcap ? v : maxcap;
+            const int64_t used = cm_memory_used(maxcap, cfg.sp, cfg.ckpt, *profile);
+            fail_infeasible("iteration " + std::to_string(i) + ": configuration sp=" + std::to_string(cfg.sp) +
+                            " ckpt=" + std::to_string(cfg.ckpt) + " at length " + std::to_string(maxcap) +
+                            " requires " + std::to_string(used) + " bytes, " + std::to_string(profile->device_memory) +
+                            " available");
+        }
+    }
+    const Partial tot = read_scalar(c, partials.p + EG);
+    const double ni = static_cast<double>(p.I);
+    const double total = static_cast<double>(tot.tokens);
+    const double comm = static_cast<double>(tot.comm);
+    const double pad_gap = static_cast<double>(tot.pad_gap);
+    const double pad_cap = static_cast<double>(tot.pad_cap);
+    out.m.dbr = tot.dbr / ni;
+    out.m.abr = tot.abr / ni;
+    out.m.cr = total > 0.0 ? comm / total : 0.0;
+    out.m.pr = pad_cap > 0.0 ? pad_gap / pad_cap : 0.0;
+    out.m.ave_t = total / (ni * static_cast<double>(device_count));
+    out.total_seconds = tot.seconds;
+    out.switch_count = static_cast<int32_t>(tot.switches);
+}
+
 }  // namespace hbp_b200

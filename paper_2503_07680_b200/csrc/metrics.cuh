@@ -29,4 +29,13 @@ void eval_plan(Ctx& c, const PlanArrays& p, int32_t device_count, const std::vec
                const hbp_hardware_profile* profile, EvalOut& out, double* d_dbr, double* d_abr, double* d_secs,
                double* d_dcomp, double* d_dcomm, double* d_didle);
 
+// Sharded by DP column; phase 0 / 1 on device columns
+// [c0, c1) of every iteration, finish on the all-reduced buffers.
+void eval_columns(Ctx& c, const PlanArrays& p, const std::vector<hbp_group_config>& groups,
+                  const hbp_hardware_profile* profile, int phase, int32_t c0, int32_t c1,
+                  const hbp_eval_columns_bufs& b);
+void eval_columns_finish(Ctx& c, const PlanArrays& p, int32_t device_count,
+                         const std::vector<hbp_group_config>& groups, const hbp_hardware_profile* profile,
+                         const hbp_eval_columns_bufs& b, EvalOut& out);
+
 }  // namespace hbp_b200

@@ -273,7 +273,7 @@ def run_ours(args, rank, world, local):
     # stage profile of one extra step (CUDA events around each engine stage)
     stages = profile_stages(ctx, lib, step_device)
     sweep_res = None if args.no_sweep else run_sweep_leg(ctx, lib, rank, world, dist)
-    c4_res = run_c4_leg(ctx, lib) if (world == 1 and not args.no_c4) else None
+    c4_res = run_c4_leg(ctx, lib, rank, world, dist) if not args.no_c4 else None
 
     tot_dev = sum(dev_ms)
     tot_e2e = sum(e2e_ms)
@@ -371,7 +371,7 @@ def c4_profile():
     return p
 
 
-def run_c4_leg(ctx, lib, steps=3, warmup=3):
+def run_c4_leg(ctx, lib, rank=0, world=1, dist=None, steps=3, warmup=3):
     """BASELINE config C4: 100M samples of the C2 spec, groups [16K sp1,
     128K sp8] with ckpt derived under the DeepSeek-V2 236B cost model, 8 DP
     devices: build_plan + report (ABR/CR) + simulate, corpus resident in HBM.
@@ -415,7 +415,37 @@ def run_c4_leg(ctx, lib, steps=3, warmup=3):
            "samples": n, "groups": groups, "ms_per_step": statistics.mean(ms), "ms_steps": [round(x, 2) for x in ms],
            "samples_per_s": n / (statistics.mean(ms) / 1000.0), "abr": m.abr, "cr": m.cr,
            "estimated_seconds": st.total_seconds}
+    # report + simulate sharded by DP column across the ranks (NCCL all-reduce
+    # of per-iteration vectors), against the single-GPU evaluation
+    from paper_2503_07680_b200 import sharded_eval as se
+    ar = se.torch_all_reduce(dist) if dist is not None else None
+
+    def timed_eval(fn):
+        best = math.inf
+        for _ in range(3):
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            r = fn()
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            if dist is not None:
+                tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                el = float(tt.item())
+            best = min(best, el)
+        return r, best
+
+    (m1, st1), single_s = timed_eval(lambda: (plan.report(), plan.simulate(prof)))
+    (m2, st2), shard_s = timed_eval(lambda: se.sharded_evaluate(ctx, plan, rank, world, ar, prof))
+    res["sharded_eval"] = {"ranks": world, "dp_columns": DEVICES, "ms": 1e3 * shard_s, "single_gpu_ms": 1e3 * single_s,
+                           "identical": bool(m1.abr == m2.abr and m1.dbr == m2.dbr and m1.cr == m2.cr
+                                             and st1.total_seconds == st2.total_seconds),
+                           "exchange": "all_reduce MAX/SUM/MIN of 6 per-iteration vectors, then SUM of 2 (NCCL)"}
     out = plan = None
+    if world > 1:
+        return res
     # C5 bounded sample: the first K length sets (8 candidates each) over the 100M corpus
     cands = sweep.make_candidates(ctx, 131072, [256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536], SWEEP_SP, prof)
     K = 4

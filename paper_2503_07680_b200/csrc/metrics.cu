@@ -152,11 +152,36 @@ __global__ void __launch_bounds__(EB) k_eval(EvalArgs a) {
     if (threadIdx.x == 0) a.partials[blockIdx.x] = s[0];
 }
 
+// Fixed-order final reduction of the block partials by one warp: lane l
+// sums partials l, l + 32, ... in order, then a fixed butterfly.
+__device__ __forceinline__ Partial shfl_xor_partial(const Partial& p, int o) {
+    Partial q;
+    q.dbr = __shfl_xor_sync(0xffffffffu, p.dbr, o);
+    q.abr = __shfl_xor_sync(0xffffffffu, p.abr, o);
+    q.seconds = __shfl_xor_sync(0xffffffffu, p.seconds, o);
+    q.tokens = __shfl_xor_sync(0xffffffffu, p.tokens, o);
+    q.comm = __shfl_xor_sync(0xffffffffu, p.comm, o);
+    q.pad_gap = __shfl_xor_sync(0xffffffffu, p.pad_gap, o);
+    q.pad_cap = __shfl_xor_sync(0xffffffffu, p.pad_cap, o);
+    q.switches = __shfl_xor_sync(0xffffffffu, p.switches, o);
+    return q;
+}
+
 __global__ void k_eval_final(const Partial* __restrict__ partials, int n, Partial* __restrict__ out) {
-    if (threadIdx.x != 0) return;
+    const int lane = threadIdx.x & 31;
     Partial acc{0, 0, 0, 0, 0, 0, 0, 0};
-    for (int b = 0; b < n; ++b) add_partial(acc, partials[b]);
-    *out = acc;
+    for (int b = lane; b < n; b += 32) add_partial(acc, partials[b]);
+    for (int o = 1; o < 32; o <<= 1) {  // lanes l and l ^ o hold the same pair after each step: order fixed
+        const Partial q = shfl_xor_partial(acc, o);
+        if (lane & o) {
+            Partial t = q;
+            add_partial(t, acc);
+            acc = t;
+        } else {
+            add_partial(acc, q);
+        }
+    }
+    if (threadIdx.x == 0) *out = acc;
 }
 
 }  // namespace

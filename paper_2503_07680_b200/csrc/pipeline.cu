@@ -222,7 +222,8 @@ __global__ void k_full_iterations(const u32* __restrict__ order, u64 nfull, u32 
 // Spill tail (balance.cpp:121-151): samples sorted (length desc, id asc)
 // go one by one to the device with the least attention that still fits
 // (lowest device on ties); unpadded capacity; fallback keeps the packs.
-__global__ void k_spill(const u64* __restrict__ sorted, u64 k, u32 N, u32 cap, const u32* __restrict__ tail_packs,
+// device_count > 256: one thread (the warp version keeps 8 devices per lane)
+__global__ void k_spill_serial(const u64* __restrict__ sorted, u64 k, u32 N, u32 cap, const u32* __restrict__ tail_packs,
                         u32 rem, u32 spill_pbase, u64 spill_mbase, int gi, u64 iter, u64* __restrict__ g_members,
                         u64* __restrict__ g_moff, u32* __restrict__ g_cnt, u32* __restrict__ g_cap,
                         u32* __restrict__ g_total, u64* __restrict__ g_att, u32* __restrict__ dev_of,
@@ -273,6 +274,109 @@ __global__ void k_spill(const u64* __restrict__ sorted, u64 k, u32 N, u32 cap, c
         for (u32 d = 0; d < N; ++d) slots[iter * N + d] = g_cnt[spill_pbase + d] ? spill_pbase + d : kNone;
     } else {
         for (u32 d = 0; d < N; ++d) slots[iter * N + d] = d < rem ? tail_packs[d] : kNone;
+    }
+}
+
+// One warp: device d's running total / attention live in lane d % 32 (slot
+// d / 32), so each sample is one warp argmin over (attention, device) among
+// the devices it fits -- no dependent global memory on the sample loop.
+constexpr u32 kSpillSlots = 8;  // devices per lane: device_count <= 256 on this path
+template <u32 kSlots>
+__global__ void k_spill(const u64* __restrict__ sorted, u64 k, u32 N, u32 cap, const u32* __restrict__ tail_packs,
+                        u32 rem, u32 spill_pbase, u64 spill_mbase, int gi, u64 iter, u64* __restrict__ g_members,
+                        u64* __restrict__ g_moff, u32* __restrict__ g_cnt, u32* __restrict__ g_cap,
+                        u32* __restrict__ g_total, u64* __restrict__ g_att, u32* __restrict__ dev_of,
+                        u32* __restrict__ slots, int32_t* __restrict__ igroup) {
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    const u32 lane = threadIdx.x;
+    u32 tot[kSlots], cnt[kSlots];
+    u64 att[kSlots];
+#pragma unroll
+    for (u32 q = 0; q < kSlots; ++q) {
+        tot[q] = 0;
+        cnt[q] = 0;
+        att[q] = 0;
+    }
+    bool ok = true;
+    u32 chunk = 0;  // lengths of items [i & ~31, +32), one per lane, loaded together
+    for (u64 i = 0; i < k; ++i) {
+        if ((i & 31u) == 0) chunk = i + lane < k ? entry_len(sorted[i + lane]) : 0u;
+        const u32 L = __shfl_sync(0xffffffffu, chunk, static_cast<int>(i & 31u));
+        // this lane's best fitting device (least attention, lowest index)
+        u64 ba = ~0ull;
+        u32 bd = 0xffffffffu;
+#pragma unroll
+        for (u32 q = 0; q < kSlots; ++q) {
+            const u32 d = q * 32 + lane;
+            if (d < N && cap - tot[q] >= L && (att[q] < ba || (att[q] == ba && d < bd))) {
+                ba = att[q];
+                bd = d;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 oa = __shfl_xor_sync(0xffffffffu, ba, o);
+            const u32 od = __shfl_xor_sync(0xffffffffu, bd, o);
+            if (oa < ba || (oa == ba && od < bd)) {
+                ba = oa;
+                bd = od;
+            }
+        }
+        if (bd == 0xffffffffu) {
+            ok = false;
+            break;
+        }
+        if (lane == (bd & 31u)) {
+            const u32 q = bd >> 5;
+#pragma unroll
+            for (u32 qq = 0; qq < kSlots; ++qq)
+                if (qq == q) {
+                    tot[qq] += L;
+                    att[qq] += static_cast<u64>(L) * L;
+                    dev_of[i] = bd | (cnt[qq] << 16);  // device | slot within it (both < 2^16)
+                    cnt[qq] += 1;
+                }
+        }
+    }
+    if (lane == 0) igroup[iter] = gi;
+    if (ok) {
+        // members grouped by device, in assignment order
+        u64 base = spill_mbase;  // members of the devices before each slot row
+#pragma unroll
+        for (u32 q = 0; q < kSlots; ++q) {
+            const u32 d = q * 32 + lane;
+            const u32 c = d < N ? cnt[q] : 0u;
+            u32 incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= static_cast<u32>(o)) incl += t;
+            }
+            const u32 row_total = __shfl_sync(0xffffffffu, incl, 31);
+            if (d < N) {
+                g_moff[spill_pbase + d] = base + (incl - c);
+                g_cap[spill_pbase + d] = tot[q];
+                g_total[spill_pbase + d] = tot[q];
+                g_att[spill_pbase + d] = att[q];
+                g_cnt[spill_pbase + d] = c;
+                slots[iter * N + d] = c ? spill_pbase + d : kNone;
+            }
+            base += row_total;
+        }
+        __syncwarp();
+        // members in assignment order within each device: every item knows
+        // its slot, so the lanes place them independently
+        for (u64 i = lane; i < k; i += 32) {
+            const u32 w = dev_of[i];
+            g_members[g_moff[spill_pbase + (w & 0xffffu)] + (w >> 16)] = sorted[i];
+        }
+    } else {
+        for (u32 d = lane; d < N; d += 32) {
+            g_total[spill_pbase + d] = 0;
+            g_att[spill_pbase + d] = 0;
+            g_cnt[spill_pbase + d] = 0;
+            slots[iter * N + d] = d < rem ? tail_packs[d] : kNone;
+        }
     }
 }
 
@@ -630,10 +734,20 @@ u64 batch_group(Ctx& c, const DeviceCorpus& corpus, PackTable& T, u64 pbase, u64
     CUDA_CHECK(cudaMemcpyAsync(dtoff.p, toff.data(), sizeof(u64) * rem, cudaMemcpyHostToDevice, s));
     DevBuf<u64> spill(k + 1, s);
     DevBuf<u32> dev_of(k + 1, s);
+    if (c.trace) std::fprintf(stderr, "[hbp trace] spill group %d: %u tail packs, %llu samples\n", gi, rem,
+                              static_cast<unsigned long long>(k));
     LAUNCH(k_gather_spill, rem, 256, 0, s, T.members.p, T.moff.p, T.cnt.p, dtail.p, rem, dtoff.p, spill.p);
     sort_entries(c, corpus, spill.p, k, false, cap);
     const u32 spill_pbase = static_cast<u32>(T.n_packs);
-    LAUNCH(k_spill, 1, 32, 0, s, spill.p, k, N, cap, dtail.p, rem, spill_pbase, T.n_members, gi, ibase + nfull,
+    if (N > 32 * kSpillSlots || k >= 65536)
+        LAUNCH(k_spill_serial, 1, 32, 0, s, spill.p, k, N, cap, dtail.p, rem, spill_pbase, T.n_members, gi,
+               ibase + nfull, T.members.p, T.moff.p, T.cnt.p, T.cap.p, T.total.p, T.att.p, dev_of.p, slots.p,
+               igroup.p);
+    else if (N <= 32)
+        LAUNCH(k_spill<1>, 1, 32, 0, s, spill.p, k, N, cap, dtail.p, rem, spill_pbase, T.n_members, gi, ibase + nfull,
+               T.members.p, T.moff.p, T.cnt.p, T.cap.p, T.total.p, T.att.p, dev_of.p, slots.p, igroup.p);
+    else
+    LAUNCH(k_spill<kSpillSlots>, 1, 32, 0, s, spill.p, k, N, cap, dtail.p, rem, spill_pbase, T.n_members, gi, ibase + nfull,
            T.members.p, T.moff.p, T.cnt.p, T.cap.p, T.total.p, T.att.p, dev_of.p, slots.p, igroup.p);
     CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors above go out of scope
     T.n_packs += N;

@@ -428,14 +428,16 @@ __global__ void k_out_packs(const u32* __restrict__ src, u64 I, u32 N, const u32
 __global__ void k_out_members(const u32* __restrict__ pglobal, u64 P, const int64_t* __restrict__ moff,
                               const u64* __restrict__ g_moff, const u32* __restrict__ g_cnt,
                               const u64* __restrict__ g_members, int32_t* __restrict__ out) {
-    // one warp per output pack
-    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
-    for (u64 q = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; q < P; q += warps) {
+    // eight lanes per output pack (packs hold ~10 members): four packs in
+    // flight per warp
+    const u64 groups = (static_cast<u64>(gridDim.x) * blockDim.x) >> 3;
+    const u32 sub = threadIdx.x & 7u;
+    for (u64 q = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 3; q < P; q += groups) {
         const u32 g = pglobal[q];
         const u64 a = g_moff[g];
         const u32 c = g_cnt[g];
         const int64_t d = moff[q];
-        for (u32 k = lane_id(); k < c; k += 32) out[d + k] = static_cast<int32_t>(entry_idx(g_members[a + k]));
+        for (u32 k = sub; k < c; k += 8) out[d + k] = static_cast<int32_t>(entry_idx(g_members[a + k]));
     }
 }
 
@@ -816,7 +818,7 @@ void emit_plan(Ctx& c, PackTable& T, DevBuf<u32>& slots, DevBuf<int32_t>& igroup
     const u64 M = static_cast<u64>(read_vector(c, out.pack_member_offsets.p + P, 1)[0]);
     out.n_members = static_cast<int64_t>(M);
     out.member_index.alloc(M + 1, s);
-    LAUNCH(k_out_members, grid_for(P * 32, kB, 148u * 16u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
+    LAUNCH(k_out_members, grid_for(P * 8, kB, 148u * 64u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
            T.moff.p, T.cnt.p, T.members.p, out.member_index.p);
 }
 
@@ -1145,7 +1147,7 @@ void pack_device(Ctx& c, DeviceCorpus& corpus, int64_t capacity, const hbp_strat
         },
         s, c.scan);
     if (P > 0)
-        LAUNCH(k_out_members, grid_for(P * 32, kB, 148u * 16u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
+        LAUNCH(k_out_members, grid_for(P * 8, kB, 148u * 64u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
                T.moff.p, T.cnt.p, T.members.p, out.member_index.p);
     CUDA_CHECK(cudaStreamSynchronize(s));
 }

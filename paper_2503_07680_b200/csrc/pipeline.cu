@@ -621,9 +621,14 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         fy_source_positions(c, derive_seed(seed, "ffs"), static_cast<i64>(m), src.p);
         gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(m));
         CUDA_CHECK(cudaMemcpyAsync(A.p, Bf.p, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
+    } else if (st.kind == HBP_STRATEGY_BFS) {
+        // best fit over a seeded shuffle (packing.cpp:244-248)
+        DevBuf<u32> src(m, s);
+        fy_source_positions(c, derive_seed(seed, "bfs"), static_cast<i64>(m), src.p);
+        gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(m));
+        CUDA_CHECK(cudaMemcpyAsync(A.p, Bf.p, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
     } else {
-        throw EngineError(HBP_ERR_VALIDATION, "packing strategy not available in the GPU engine: " +
-                                                  std::string(st.kind == HBP_STRATEGY_BFS ? "bfs" : "spfhp"));
+        residue_ffd = true;  // SPFHP walks lengths longest first, ids ascending (packing.cpp:135-137)
     }
     out.n_isf_members = n_members;
     out.n_isf = n_packs;
@@ -640,8 +645,12 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         trace_mark(c, "ffd.sort");
         out.res_bin.alloc(cur, s);
         out.res_slot.alloc(cur, s);
-        const FitResult fr = first_fit_runs(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf, 0,
-                                            static_cast<i64>(cur), cap, FitMode::Ffd, out.res_bin.p, out.res_slot.p);
+        const bool scan_rule = st.kind == HBP_STRATEGY_BFS || st.kind == HBP_STRATEGY_SPFHP;
+        const FitResult fr =
+            scan_rule ? scan_fit(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf,
+                                 static_cast<i64>(cur), cap, st.kind == HBP_STRATEGY_SPFHP, out.res_bin.p, out.res_slot.p)
+                      : first_fit_runs(c, out.residue.p, static_cast<i64>(cur), out.leaves.p + out.n_isf, 0,
+                                       static_cast<i64>(cur), cap, FitMode::Ffd, out.res_bin.p, out.res_slot.p);
         out.n_ffd = static_cast<u64>(fr.bins);
         trace_mark(c, "ffd.engine");
     }

@@ -1,0 +1,188 @@
+// scanfit.cu — best fit (BFS) and shortest-pack-first (SPFHP) packing.
+//
+// Both place items one at a time in a given order into the open pack picked
+// by a rule over ALL open packs, else open a new one:
+//   best fit  (packing.cpp:105-127, order = seeded shuffle, :244-248)
+//             tightest pack with residual >= s, lowest index on ties;
+//   SPFHP     (packing.cpp:129-162, order = length desc / id asc, the
+//             histogram buckets walked longest first)
+//             emptiest pack (largest residual) with residual >= s, lowest
+//             index on ties -- the std::map<residual, set<index>> of the
+//             reference, whose last key is the largest residual.
+// Neither decomposes into runs the way first fit does (the pick depends on
+// every residual), so one 1024-thread CTA owns the residual array -- in
+// shared memory while it fits (57K packs), else in global memory (L2) -- and
+// thread t owns packs t, t + 1024, ...: per item every thread scans its
+// packs, two warp REDUX steps and one cross-warp step pick the pack, and the
+// owner updates its residual in place (no barrier needed: the owner is the
+// only reader). One __syncthreads per item.
+//
+// Output matches first_fit_runs: item -> (bin, slot) and leaves
+// (residual << 32 | count) per bin, bins in creation order. Slots (rank of
+// an item inside its bin) come from a stable radix sort of the bin column.
+#include <cstdlib>
+
+#include "radix.cuh"
+#include "scan.cuh"
+#include "stages.cuh"
+
+namespace hbp_b200 {
+namespace {
+
+constexpr int kFitThreads = 1024;
+constexpr int kFitWarps = kFitThreads / 32;
+constexpr int kFitChunk = 1024;  // items staged per round
+constexpr unsigned kFull = 0xffffffffu;
+
+// Fixed shared memory: lengths + bins of one chunk, two reduction buffers.
+constexpr size_t kFitFixedSmem = sizeof(u32) * 2 * kFitChunk + sizeof(u64) * 2 * kFitWarps;
+
+template <bool WORST>
+__device__ __forceinline__ u64 warp_pick(u32 hi, u32 lo) {
+    const u32 m = WORST ? __reduce_max_sync(kFull, hi) : __reduce_min_sync(kFull, hi);
+    const u32 l = WORST ? __reduce_max_sync(kFull, hi == m ? lo : 0u) : __reduce_min_sync(kFull, hi == m ? lo : ~0u);
+    return (static_cast<u64>(m) << 32) | l;
+}
+
+template <bool WORST, bool SMEM>
+__global__ void __launch_bounds__(kFitThreads, 1)
+    k_scan_fit(const u64* __restrict__ items, i64 n, u32 cap, u32* __restrict__ g_res, u32* __restrict__ bin_out,
+               u32* __restrict__ cnt, u32* __restrict__ n_bins) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    u64* s_red = reinterpret_cast<u64*>(smem);                 // [2][32]
+    u32* s_len = reinterpret_cast<u32*>(s_red + 2 * kFitWarps);
+    u32* s_bin = s_len + kFitChunk;
+    u32* R = SMEM ? (s_bin + kFitChunk) : g_res;
+    const u32 tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+
+    u32 P = 0;  // bins opened so far (identical in every thread)
+    for (i64 base = 0; base < n; base += kFitChunk) {
+        const int cnt_c = static_cast<int>(n - base < kFitChunk ? n - base : kFitChunk);
+        if (static_cast<int>(tid) < cnt_c) s_len[tid] = entry_len(items[base + tid]);
+        __syncthreads();
+        for (int j = 0; j < cnt_c; ++j) {
+            const u32 s = s_len[j];
+            u32 br = WORST ? 0u : ~0u, bi = ~0u;
+            for (u32 k = tid; k < P; k += kFitThreads) {
+                const u32 r = R[k];
+                if (r >= s && (WORST ? r > br : r < br)) {
+                    br = r;
+                    bi = k;
+                }
+            }
+            const u64 wk = warp_pick<WORST>(br, WORST ? static_cast<u32>(~bi) : bi);
+            u64* red = s_red + (j & 1) * kFitWarps;
+            if (lane == 0) red[warp] = wk;
+            __syncthreads();
+            const u64 v = red[lane];
+            const u64 bk = warp_pick<WORST>(static_cast<u32>(v >> 32), static_cast<u32>(v));
+            const u32 hi = static_cast<u32>(bk >> 32);
+            const bool found = WORST ? hi != 0u : hi != ~0u;
+            u32 b;
+            u32 nr;
+            if (found) {
+                b = WORST ? ~static_cast<u32>(bk) : static_cast<u32>(bk);
+                nr = hi - s;
+            } else {
+                b = P++;
+                nr = cap - s;
+            }
+            if ((b & (kFitThreads - 1)) == tid) {
+                R[b] = nr;
+                atomicAdd(cnt + b, 1u);
+                s_bin[j] = b;
+            }
+        }
+        __syncthreads();
+        if (static_cast<int>(tid) < cnt_c) bin_out[base + tid] = s_bin[tid];
+        // s_len / s_bin are rewritten next round only after this barrier
+        __syncthreads();
+    }
+    if (SMEM)
+        for (u32 k = tid; k < P; k += kFitThreads) g_res[k] = R[k];
+    if (tid == 0) *n_bins = P;
+}
+
+__global__ void k_fit_leaves(const u32* __restrict__ res, const u32* __restrict__ cnt, u64 P, u64* __restrict__ leaves) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < P;
+         i += static_cast<u64>(gridDim.x) * blockDim.x)
+        leaves[i] = (static_cast<u64>(res[i]) << 32) | cnt[i];
+}
+
+// sorted (bin, position) pairs -> slot of each position
+__global__ void k_fit_slots(const u32* __restrict__ sbin, const u32* __restrict__ spos, u64 n,
+                            const u64* __restrict__ start, u32* __restrict__ slot) {
+    for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < n;
+         j += static_cast<u64>(gridDim.x) * blockDim.x)
+        slot[spos[j]] = static_cast<u32>(j - start[sbin[j]]);
+}
+
+__global__ void k_iota_u32(u32* __restrict__ v, u64 n) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<u64>(gridDim.x) * blockDim.x)
+        v[i] = static_cast<u32>(i);
+}
+
+template <bool WORST, bool SMEM>
+void launch_fit(Ctx& c, const u64* items, i64 n, u32 cap, u32* res, u32* bins, u32* cnt, u32* nb, size_t smem,
+                int smem_optin) {
+    set_max_dynamic_smem_once(reinterpret_cast<const void*>(&k_scan_fit<WORST, SMEM>), smem_optin);
+    LAUNCH_B("fit.scan", 12.0 * static_cast<double>(n), (k_scan_fit<WORST, SMEM>), 1, kFitThreads, smem, c.stream,
+             items, n, cap, res, bins, cnt, nb);
+}
+
+int fit_bits(u64 maxval) {
+    int b = 0;
+    while (b < 32 && (maxval >> b) != 0) ++b;
+    return b;
+}
+
+}  // namespace
+
+FitResult scan_fit(Ctx& c, const u64* items, i64 n, u64* leaves, i64 max_bins, u32 cap, bool worst, u32* item_bin,
+                   u32* item_slot) {
+    FitResult fr;
+    if (n <= 0) return fr;
+    cudaStream_t s = c.stream;
+    const u64 N = static_cast<u64>(n);
+    const u64 pmax = std::min<u64>(N, static_cast<u64>(max_bins));
+    DevBuf<u32> res(pmax, s), cnt(pmax, s), nb(1, s);
+    cnt.zero();
+    int dev = 0, smem_optin = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t need = kFitFixedSmem + sizeof(u32) * pmax;
+    const char* fg = std::getenv("HBP_FIT_GLOBAL");  // tests: exercise the L2-resident residual array
+    const bool force_global = fg && *fg && *fg != '0';
+    const bool in_smem = !force_global && need <= static_cast<size_t>(smem_optin);
+    const size_t smem = in_smem ? need : kFitFixedSmem;
+    if (worst) {
+        if (in_smem) launch_fit<true, true>(c, items, n, cap, res.p, item_bin, cnt.p, nb.p, smem, smem_optin);
+        else launch_fit<true, false>(c, items, n, cap, res.p, item_bin, cnt.p, nb.p, smem, smem_optin);
+    } else {
+        if (in_smem) launch_fit<false, true>(c, items, n, cap, res.p, item_bin, cnt.p, nb.p, smem, smem_optin);
+        else launch_fit<false, false>(c, items, n, cap, res.p, item_bin, cnt.p, nb.p, smem, smem_optin);
+    }
+    const u64 P = read_vector(c, nb.p, 1)[0];
+    LAUNCH(k_fit_leaves, grid_for(P, 256), 256, 0, s, res.p, cnt.p, P, leaves);
+    // slots: stable sort of positions by bin, rank inside each bin
+    DevBuf<u32> kb(N, s), pos(N, s), tk(N, s), tv(N, s);
+    DevBuf<u64> start(P + 1, s);
+    CUDA_CHECK(cudaMemcpyAsync(kb.p, item_bin, sizeof(u32) * N, cudaMemcpyDeviceToDevice, s));
+    LAUNCH(k_iota_u32, grid_for(N, 256), 256, 0, s, pos.p, N);
+    radix_sort_pairs(c, kb.p, pos.p, n, fit_bits(P - 1), false, tk.p, tv.p);
+    {
+        const u32* cp = cnt.p;
+        u64* sp = start.p;
+        const i64 PP = static_cast<i64>(P);
+        scan_exclusive<u64>(
+            PP + 1, [=] __device__(i64 i) { return i < PP ? static_cast<u64>(cp[i]) : 0ull; },
+            [=] __device__(i64 i, u64 v) { sp[i] = v; }, s, c.scan);
+    }
+    LAUNCH(k_fit_slots, grid_for(N, 256), 256, 0, s, kb.p, pos.p, N, start.p, item_slot);
+    fr.bins = static_cast<i64>(P);
+    fr.records = n;
+    return fr;
+}
+
+}  // namespace hbp_b200

@@ -79,6 +79,12 @@ enum class FitMode { Ffd, Fill };
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
                          FitMode mode, u32* item_bin, u32* item_slot, const u32* key32 = nullptr, u64 neg_keys = 0);
 
+// scanfit.cu: best fit (worst = false, packing.cpp:105-127) or the
+// emptiest-pack rule of SPFHP (worst = true, packing.cpp:129-162) of the
+// items in the given order into fresh bins; same outputs as first_fit_runs.
+FitResult scan_fit(Ctx& c, const u64* items, i64 n, u64* leaves, i64 max_bins, u32 cap, bool worst, u32* item_bin,
+                   u32* item_slot);
+
 // chain.cu: first fit as a pipeline of bins. Bin b sees the items no bin
 // before it took, in order, and takes each one that fits, so bins form a
 // systolic chain: warp j owns 32 * m consecutive bins and passes, per run,

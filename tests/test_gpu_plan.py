@@ -56,7 +56,7 @@ def test_build_plan_options(ctx, oracle, balance, fill):
     assert_same_plan(got, want)
 
 
-@pytest.mark.parametrize("strategy", ["isf", "random", "ffd", "ffs"])
+@pytest.mark.parametrize("strategy", ["isf", "random", "ffd", "ffs", "bfs", "spfhp"])
 def test_build_plan_strategies(ctx, oracle, strategy):
     L = hybrid(oracle, 5000, 3, 0.03)
     kw = dict(device_count=4, seed=1, strategy=strategy)
@@ -163,7 +163,7 @@ def test_negative_ids_greedy_fill_quirk(ctx, oracle, seed):
     assert_same_plan(got, want, ids2)
 
 
-@pytest.mark.parametrize("strategy", ["isf", "random", "ffd", "ffs"])
+@pytest.mark.parametrize("strategy", ["isf", "random", "ffd", "ffs", "bfs", "spfhp"])
 @pytest.mark.parametrize("cap", [4, 1024, 131072])
 def test_pack(ctx, oracle, strategy, cap):
     rng = np.random.default_rng(cap)
@@ -173,6 +173,28 @@ def test_pack(ctx, oracle, strategy, cap):
     for k in ("pack_capacity", "pack_total", "pack_attention", "pack_member_offsets"):
         assert np.array_equal(getattr(got, k), getattr(want, k)), k
     assert np.array_equal(got.members_as_ids(None), want.member_id)
+
+
+@pytest.mark.parametrize("strategy", ["bfs", "spfhp"])
+@pytest.mark.parametrize("where", ["smem", "global"])
+def test_scan_fit_large(ctx, oracle, strategy, where, monkeypatch):
+    # 40K items over ~20K packs: the residual array in shared memory, and
+    # (HBP_FIT_GLOBAL) the same walk over the L2-resident array
+    if where == "global":
+        monkeypatch.setenv("HBP_FIT_GLOBAL", "1")
+    rng = np.random.default_rng(77)
+    L = rng.integers(1, 65, size=40_000)
+    want = oracle.pack(None, L, 64, strategy, seed=99)
+    got = ctx.pack(None, L, 64, strategy, seed=99).flat()
+    for k in ("pack_capacity", "pack_total", "pack_attention", "pack_member_offsets"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert np.array_equal(got.members_as_ids(None), want.member_id)
+
+
+def test_spfhp_hand_run(ctx):
+    # test_packing.cpp:183-193: 6x512 + 4x256 at 1024 -> 4 full packs
+    got = ctx.pack(None, np.array([512] * 6 + [256] * 4), 1024, "spfhp").flat()
+    assert len(got.pack_total) == 4 and list(got.pack_total) == [1024] * 4
 
 
 def test_ffd_hand_run(ctx):

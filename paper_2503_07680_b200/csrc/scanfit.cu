@@ -44,6 +44,55 @@ __device__ __forceinline__ u64 warp_pick(u32 hi, u32 lo) {
     return (static_cast<u64>(m) << 32) | l;
 }
 
+// Best fit: this thread's tightest pack with residual >= s (lowest index on
+// ties: k ascending, strict <). Eight loads in flight per step.
+__device__ __forceinline__ void best_of_mine(const u32* R, u32 tid, u32 P, u32 s, u32& br, u32& bi) {
+    u32 k = tid;
+    for (; k + 7u * kFitThreads < P; k += 8u * kFitThreads) {
+        u32 r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = R[k + q * kFitThreads];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (r[q] >= s && r[q] < br) {
+                br = r[q];
+                bi = k + q * kFitThreads;
+            }
+    }
+    for (; k < P; k += kFitThreads) {
+        const u32 r = R[k];
+        if (r >= s && r < br) {
+            br = r;
+            bi = k;
+        }
+    }
+}
+
+// SPFHP: this thread's emptiest pack (largest residual, lowest index).
+__device__ __forceinline__ void max_of_mine(const u32* R, u32 tid, u32 P, u32& lm, u32& li) {
+    lm = 0u;
+    li = ~0u;
+    u32 k = tid;
+    for (; k + 7u * kFitThreads < P; k += 8u * kFitThreads) {
+        u32 r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = R[k + q * kFitThreads];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (r[q] > lm) {
+                lm = r[q];
+                li = k + q * kFitThreads;
+            }
+    }
+    for (; k < P; k += kFitThreads) {
+        const u32 r = R[k];
+        if (r > lm) {
+            lm = r;
+            li = k;
+        }
+    }
+}
+
 template <bool WORST, bool SMEM>
 __global__ void __launch_bounds__(kFitThreads, 1)
     k_scan_fit(const u64* __restrict__ items, i64 n, u32 cap, u32* __restrict__ g_res, u32* __restrict__ bin_out,
@@ -55,20 +104,24 @@ __global__ void __launch_bounds__(kFitThreads, 1)
     u32* R = SMEM ? (s_bin + kFitChunk) : g_res;
     const u32 tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
 
-    u32 P = 0;  // bins opened so far (identical in every thread)
+    u32 P = 0;              // bins opened so far (identical in every thread)
+    u32 lm = 0u, li = ~0u;  // SPFHP: this thread's emptiest pack, kept current
     for (i64 base = 0; base < n; base += kFitChunk) {
         const int cnt_c = static_cast<int>(n - base < kFitChunk ? n - base : kFitChunk);
         if (static_cast<int>(tid) < cnt_c) s_len[tid] = entry_len(items[base + tid]);
         __syncthreads();
         for (int j = 0; j < cnt_c; ++j) {
             const u32 s = s_len[j];
-            u32 br = WORST ? 0u : ~0u, bi = ~0u;
-            for (u32 k = tid; k < P; k += kFitThreads) {
-                const u32 r = R[k];
-                if (r >= s && (WORST ? r > br : r < br)) {
-                    br = r;
-                    bi = k;
-                }
+            u32 br, bi;
+            if (WORST) {
+                // the emptiest pack only competes when it fits (packing.cpp:
+                // 147-150: lower_bound(len) == end -> new pack)
+                br = lm >= s ? lm : 0u;
+                bi = lm >= s ? li : ~0u;
+            } else {
+                br = ~0u;
+                bi = ~0u;
+                best_of_mine(R, tid, P, s, br, bi);
             }
             const u64 wk = warp_pick<WORST>(br, WORST ? static_cast<u32>(~bi) : bi);
             u64* red = s_red + (j & 1) * kFitWarps;
@@ -91,6 +144,14 @@ __global__ void __launch_bounds__(kFitThreads, 1)
                 R[b] = nr;
                 atomicAdd(cnt + b, 1u);
                 s_bin[j] = b;
+                if (WORST) {
+                    if (found) {
+                        max_of_mine(R, tid, P, lm, li);  // b was this thread's emptiest pack
+                    } else if (nr > lm) {
+                        lm = nr;  // a new pack has the highest index: it wins strictly larger only
+                        li = b;
+                    }
+                }
             }
         }
         __syncthreads();

@@ -213,6 +213,23 @@ int hbp_ctx_stage_stats(hbp_ctx* ctx, int32_t index, char* name, int32_t name_le
 int hbp_synth_lengths(int64_t count, const char* short_dist, double long_fraction, const char* long_dist,
                       int64_t max_length, uint64_t seed, int64_t* out_lengths, char* err, int errlen);
 
+/* ---- L1: corpus files ----------------------------------------------------- */
+
+enum hbp_corpus_format { HBP_CORPUS_JSONL = 0, HBP_CORPUS_CSV = 1, HBP_CORPUS_RAW = 2 };
+
+/* load_lengths(istream, format, source) (include/hbp/ingest.hpp:23-24,
+ * src/ingest.cpp:57-160) over the bytes of a corpus file already read into
+ * host memory (the reference reads an istream). Raw-lengths and CSV are
+ * parsed on the GPU; JSONL returns HBP_ERR_VALIDATION ("not available").
+ * Errors are the reference's: the first malformed line in file order
+ * ("line N: not an integer length: '...'", "... trailing garbage ...",
+ * "... length must be >= 1, got V", "... too few columns", the CSV header
+ * message, "empty corpus: <source>"). The samples' ids are 0..n-1; their
+ * lengths go to out_lengths (`out_memory`), which holds `capacity` entries:
+ * (bytes + 1) / 2 always suffices. *out_count = n. */
+int hbp_load_lengths(hbp_ctx* ctx, const char* text, int64_t bytes, int32_t format, const char* source,
+                     int64_t* out_lengths, int64_t capacity, int32_t out_memory, int64_t* out_count);
+
 /* ---- L0: validation ---------------------------------------------------- */
 
 /* SampleSet::validate (src/types.cpp:8-24): non-empty, length >= 1, unique

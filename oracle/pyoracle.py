@@ -278,6 +278,19 @@ class Oracle:
         ni = ct.count(b"\n") - 1
         return jt, ct, sp[:ni], ck[:ni], sw.value
 
+    def load_lengths(self, text: bytes, fmt: str, source: str = "corpus"):
+        """(ids, lengths) of load_lengths(istream, format, source) in the reference (reference kind only)."""
+        cap = len(text) // 2 + 2
+        lens = np.zeros(cap, dtype=np.int64)
+        ids = np.zeros(cap, dtype=np.int64)
+        n = C.c_int64()
+        code = {"jsonl": 0, "csv": 1, "raw-lengths": 2, "raw": 2}[fmt]
+        rc = self.lib.oracle_load_lengths(C.c_char_p(text), C.c_int64(len(text)), C.c_int32(code),
+                                          source.encode(), abi.ptr(lens, C.c_int64), abi.ptr(ids, C.c_int64),
+                                          C.c_int64(cap), C.byref(n), self.err, len(self.err))
+        self._check(rc)
+        return ids[:n.value], lens[:n.value]
+
     def report(self, plan: abi.FlatPlan):
         v = plan.view()
         m = abi.Metrics()

@@ -487,6 +487,24 @@ int oracle_padded_batching(const int64_t* ids, const int64_t* lengths, int64_t n
     });
 }
 
+// load_lengths(istream, format, source) (ingest.cpp:147-160) over a text
+// buffer: lengths[capacity] (ids are 0..n-1 for csv / raw).
+int oracle_load_lengths(const char* text, int64_t bytes, int32_t format, const char* source,
+                        int64_t* lengths, int64_t* ids, int64_t capacity, int64_t* n, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        std::istringstream in(std::string(text, static_cast<std::size_t>(bytes)));
+        const R::CorpusFormat f = format == 0 ? R::CorpusFormat::Jsonl
+                                 : format == 1 ? R::CorpusFormat::Csv : R::CorpusFormat::RawLengths;
+        const auto set = R::load_lengths(in, f, source);
+        if (static_cast<int64_t>(set.samples.size()) > capacity) throw R::ValidationError("oracle capacity");
+        for (std::size_t i = 0; i < set.samples.size(); ++i) {
+            lengths[i] = set.samples[i].length;
+            ids[i] = set.samples[i].id;
+        }
+        *n = static_cast<int64_t>(set.samples.size());
+    });
+}
+
 int oracle_report(const hbp_plan_view* plan, hbp_metrics* out, double* dbr,
                   double* abr, char* err, int errlen) {
     return guarded(err, errlen, [&] {

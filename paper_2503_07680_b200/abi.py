@@ -377,6 +377,28 @@ class Context:
                                                     C.c_uint64(seed & (2**64 - 1)), C.byref(h)))
         return self._plan(h, [group], group[0])
 
+    CORPUS_FORMATS = {"jsonl": 0, "csv": 1, "raw-lengths": 2, "raw": 2}
+
+    def load_lengths(self, text: bytes, fmt: str, source: str = "corpus", device_out=None):
+        """hbp::load_lengths(istream, format, source) on the GPU (raw-lengths,
+        csv): the lengths as int64 numpy (ids are 0..n-1), or written into the
+        torch int64 CUDA tensor `device_out` (returns the count)."""
+        if fmt not in self.CORPUS_FORMATS:
+            raise ValidationError("unknown corpus format: " + fmt)
+        cap = len(text) // 2 + 1 if device_out is None else device_out.numel()
+        n = C.c_int64()
+        self.lib.hbp_load_lengths.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int32, C.c_char_p, C.c_void_p,
+                                              C.c_int64, C.c_int32, C.POINTER(C.c_int64)]
+        if device_out is None:
+            out = np.zeros(max(cap, 1), dtype=np.int64)
+            dst, mem = out.ctypes.data, 0
+        else:
+            dst, mem = device_out.data_ptr(), 1
+        self.check(self.lib.hbp_load_lengths(self.h, text, C.c_int64(len(text)), C.c_int32(self.CORPUS_FORMATS[fmt]),
+                                             source.encode(), C.c_void_p(dst), C.c_int64(cap), C.c_int32(mem),
+                                             C.byref(n)))
+        return out[:n.value] if device_out is None else n.value
+
     def padded_batching(self, ids, lengths, token_budget: int, mode: str = "sorted", seed: int = 0):
         """hbp::sorted_batching / random_batching on the GPU: (order as input
         indices, batch offsets into order, batch max lengths)."""

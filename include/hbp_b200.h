@@ -219,16 +219,19 @@ enum hbp_corpus_format { HBP_CORPUS_JSONL = 0, HBP_CORPUS_CSV = 1, HBP_CORPUS_RA
 
 /* load_lengths(istream, format, source) (include/hbp/ingest.hpp:23-24,
  * src/ingest.cpp:57-160) over the bytes of a corpus file already read into
- * host memory (the reference reads an istream). Raw-lengths and CSV are
- * parsed on the GPU; JSONL returns HBP_ERR_VALIDATION ("not available").
+ * host memory (the reference reads an istream), parsed on the GPU.
  * Errors are the reference's: the first malformed line in file order
  * ("line N: not an integer length: '...'", "... trailing garbage ...",
- * "... length must be >= 1, got V", "... too few columns", the CSV header
- * message, "empty corpus: <source>"). The samples' ids are 0..n-1; their
- * lengths go to out_lengths (`out_memory`), which holds `capacity` entries:
- * (bytes + 1) / 2 always suffices. *out_count = n. */
+ * "... length must be >= 1, got V", "... too few columns",
+ * "... invalid JSON: <nlohmann parse_error text>", "... expected object
+ * with integer \"length\"", the CSV header message, "empty corpus:
+ * <source>"), then SampleSet::validate (duplicate explicit JSONL ids).
+ * Ids are the record index unless a JSONL record has an integer "id".
+ * out_ids (may be NULL) and out_lengths (`out_memory`) hold `capacity`
+ * entries: (bytes + 1) / 2 always suffices. *out_count = n. */
 int hbp_load_lengths(hbp_ctx* ctx, const char* text, int64_t bytes, int32_t format, const char* source,
-                     int64_t* out_lengths, int64_t capacity, int32_t out_memory, int64_t* out_count);
+                     int64_t* out_ids, int64_t* out_lengths, int64_t capacity, int32_t out_memory,
+                     int64_t* out_count);
 
 /* ---- L0: validation ---------------------------------------------------- */
 

@@ -64,7 +64,7 @@ class Oracle:
 
     # -- helpers -----------------------------------------------------------
     def _check(self, rc: int) -> None:
-        abi.raise_status(rc, self.err.value.decode())
+        abi.raise_status(rc, self.err.value.decode("utf-8", "backslashreplace"))
 
     def _take(self, p: C.POINTER(OraclePlan), groups=None, l_best=None) -> abi.FlatPlan:
         o = p.contents

@@ -326,7 +326,7 @@ class Context:
 
     def check(self, rc: int) -> None:
         if rc != HBP_OK:
-            raise_status(rc, self.lib.hbp_last_error(self.h).decode())
+            raise_status(rc, self.lib.hbp_last_error(self.h).decode("utf-8", "backslashreplace"))
 
     @property
     def launches(self) -> int:
@@ -379,25 +379,31 @@ class Context:
 
     CORPUS_FORMATS = {"jsonl": 0, "csv": 1, "raw-lengths": 2, "raw": 2}
 
-    def load_lengths(self, text: bytes, fmt: str, source: str = "corpus", device_out=None):
-        """hbp::load_lengths(istream, format, source) on the GPU (raw-lengths,
-        csv): the lengths as int64 numpy (ids are 0..n-1), or written into the
-        torch int64 CUDA tensor `device_out` (returns the count)."""
+    def load_lengths(self, text: bytes, fmt: str, source: str = "corpus", device_out=None, with_ids=False):
+        """hbp::load_lengths(istream, format, source) on the GPU (jsonl, csv,
+        raw-lengths): the lengths as int64 numpy ((ids, lengths) with
+        with_ids), or written into the torch int64 CUDA tensor `device_out`
+        (returns the count)."""
         if fmt not in self.CORPUS_FORMATS:
             raise ValidationError("unknown corpus format: " + fmt)
         cap = len(text) // 2 + 1 if device_out is None else device_out.numel()
         n = C.c_int64()
         self.lib.hbp_load_lengths.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.c_int32, C.c_char_p, C.c_void_p,
-                                              C.c_int64, C.c_int32, C.POINTER(C.c_int64)]
+                                              C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int64)]
+        ids = None
         if device_out is None:
             out = np.zeros(max(cap, 1), dtype=np.int64)
             dst, mem = out.ctypes.data, 0
+            if with_ids:
+                ids = np.zeros(max(cap, 1), dtype=np.int64)
         else:
             dst, mem = device_out.data_ptr(), 1
         self.check(self.lib.hbp_load_lengths(self.h, text, C.c_int64(len(text)), C.c_int32(self.CORPUS_FORMATS[fmt]),
-                                             source.encode(), C.c_void_p(dst), C.c_int64(cap), C.c_int32(mem),
-                                             C.byref(n)))
-        return out[:n.value] if device_out is None else n.value
+                                             source.encode(), C.c_void_p(ids.ctypes.data if ids is not None else None),
+                                             C.c_void_p(dst), C.c_int64(cap), C.c_int32(mem), C.byref(n)))
+        if device_out is not None:
+            return n.value
+        return (ids[:n.value], out[:n.value]) if with_ids else out[:n.value]
 
     def padded_batching(self, ids, lengths, token_budget: int, mode: str = "sorted", seed: int = 0):
         """hbp::sorted_batching / random_batching on the GPU: (order as input

@@ -203,16 +203,18 @@ static std::vector<hbp_group_config> groups_of(const hbp_groups* g) {
 static std::string source_of(const hbp_samples* s) { return (s && s->source) ? s->source : ""; }
 
 int hbp_load_lengths(hbp_ctx* ctx, const char* text, int64_t bytes, int32_t format, const char* source,
-                     int64_t* out_lengths, int64_t capacity, int32_t out_memory, int64_t* out_count) {
+                     int64_t* out_ids, int64_t* out_lengths, int64_t capacity, int32_t out_memory,
+                     int64_t* out_count) {
     return guarded(ctx, [&] {
         if (bytes < 0 || (bytes > 0 && text == nullptr)) fail_validation("corpus text is null");
-        DevBuf<int64_t> lens;
-        const i64 n = parse_corpus_text(*ctx, text, static_cast<u64>(bytes), format, source ? source : "", lens);
+        DevBuf<int64_t> lens, ids;
+        const i64 n =
+            parse_corpus_text(*ctx, text, static_cast<u64>(bytes), format, source ? source : "", lens, ids);
         if (n > capacity)
             fail_validation("output capacity " + std::to_string(capacity) + " < " + std::to_string(n) + " samples");
-        CUDA_CHECK(cudaMemcpyAsync(out_lengths, lens.p, sizeof(int64_t) * n,
-                                   out_memory == HBP_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                                   ctx->stream));
+        const cudaMemcpyKind kind = out_memory == HBP_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        CUDA_CHECK(cudaMemcpyAsync(out_lengths, lens.p, sizeof(int64_t) * n, kind, ctx->stream));
+        if (out_ids) CUDA_CHECK(cudaMemcpyAsync(out_ids, ids.p, sizeof(int64_t) * n, kind, ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         *out_count = n;
     });

@@ -137,10 +137,10 @@ void padded_batches_device(Ctx& c, const DeviceCorpus& corpus, int64_t budget, b
 void batching_plan_device(Ctx& c, const DeviceCorpus& corpus, const hbp_group_config& group, int32_t device_count,
                           bool sorted, uint64_t seed, DevicePlan& out);
 
-// corpus.cu: load_lengths of a raw-lengths / CSV text (ingest.cpp:57-160);
-// returns the sample count, lengths in `lengths` (device).
+// corpus.cu: load_lengths of a JSONL / CSV / raw-lengths text
+// (ingest.cpp:57-160); returns the sample count, ids and lengths (device).
 i64 parse_corpus_text(Ctx& c, const char* text, u64 bytes, int format, const std::string& source,
-                      DevBuf<int64_t>& lengths);
+                      DevBuf<int64_t>& lengths, DevBuf<int64_t>& ids);
 
 }  // namespace hbp_b200
 

@@ -25,16 +25,54 @@ CSV_CASES = [
 ]
 
 
+JSONL_CASES = [
+    b'{"length":4096}\n{"length":131072}\n', b'{"id":7,"length":10}\n\n{"length":20}\n',
+    b'  {"length" : 5 , "x": [1, {"a": [true, false, null]}, "s"]}  \r\n{"length":6}',
+    b'{"\\u006cength":9, "i\\u0064": -4}\n', b'{"length":1,"length":2}\n', b'{"id":"a","length":3}\n',
+    b'{"id":3,"id":1.5,"length":3}\n', b'\xef\xbb\xbf{"length":8}\n', b'{"length":8, "k": "\xc3\xa9\xe2\x82\xac\xf0\x9f\x98\x80"}\n',
+    b'{"s":"\\ud83d\\ude00 \\n\\t\\"\\\\\\/","length":11}\n', b'{"length":12,"n":-0.5e+3}\n',
+    b'{"length":1}\n' * 4000, b'{"length":5,"id":18446744073709551615}\n',
+    # errors
+    b'', b'\n \n', b'{"length":0}\n', b'{"length":-3}\n', b'{"length":1.0}\n', b'{"length":"5"}\n', b'[1,2]\n',
+    b'{"len":5}\n', b'{"length":5}x\n', b'{"length":5\n', b'{"length":05}\n', b'{"length":5,}\n',
+    b'{"length":tru}\n', b'{"a":"\x01","length":1}\n', b'{"a":"\\x","length":1}\n', b'{"a":"\xff","length":1}\n',
+    b'{"a":"\\ud800","length":1}\n', b'{"a":"\\udc00","length":1}\n', b'{"a":"\xed\xa0\x80","length":1}\n',
+    b'{"length":18446744073709551615}\n', b'{"length":18446744073709551616}\n', b'{"length":-9223372036854775809}\n',
+    b'{"id":1,"length":2}\n{"id":1,"length":3}\n', b'{"length":2}\n{"id":0,"length":3}\n',
+    b'\xef\xbb{"length":8}\n', b'{"length":1}\n' * 3000 + b'{"length": 2,}\n', b'"x"\n', b'{} {}\n',
+    b'{"length":2, "a":[' + b'[' * 50 + b']' * 50 + b']}\n', b'{"length":2, "a":[' + b'[' * 50 + b']' * 49 + b'}\n',
+    b'{"length":5}\x00\n', b'{"length":5}\x00garbage\n', b'\x00{"length":5}\n', b'{"length":5\x00}\n', b'{"length":5,"v":1e}\n', b'{"length":5,"v":-}\n', b'{"length":5,"v":1.}\n',
+]
+
+
 def _both(ctx, oracle, text, fmt):
     try:
-        want = ("ok", oracle.load_lengths(text, fmt, "corpus.txt")[1].tolist())
+        want = ("ok",) + tuple(a.tolist() for a in oracle.load_lengths(text, fmt, "corpus.txt"))
     except Exception as e:  # noqa: BLE001
         want = (type(e).__name__, str(e))
     try:
-        got = ("ok", ctx.load_lengths(text, fmt, "corpus.txt").tolist())
+        got = ("ok",) + tuple(a.tolist() for a in ctx.load_lengths(text, fmt, "corpus.txt", with_ids=True))
     except abi.ValidationError as e:
         got = ("ValidationError", str(e))
     return got, want
+
+
+@pytest.mark.parametrize("i", range(len(JSONL_CASES)))
+def test_jsonl(ctx, reference, i):
+    got, want = _both(ctx, reference, JSONL_CASES[i], "jsonl")
+    assert got == want
+
+
+def test_jsonl_large_random(ctx, reference):
+    rng = np.random.default_rng(8)
+    L = rng.integers(1, 131073, size=200_000)
+    ids = rng.permutation(10**6)[:len(L)] + 10**7  # explicit ids clear of the record indices
+    rows = [(b'{"id":%d,"length":%d}' % (i, v)) if k % 3 else (b'{"length": %d, "src": "web"}' % v)
+            for k, (i, v) in enumerate(zip(ids, L))]
+    text = b"\n".join(rows) + b"\n"
+    got_ids, got = ctx.load_lengths(text, "jsonl", with_ids=True)
+    want_ids, want = reference.load_lengths(text, "jsonl")
+    assert np.array_equal(got, L) and np.array_equal(got, want) and np.array_equal(got_ids, want_ids)
 
 
 @pytest.mark.parametrize("i", range(len(RAW_CASES)))
@@ -68,3 +106,27 @@ def test_csv_device_output(ctx, reference):
     n = ctx.load_lengths(text, "csv", device_out=out)
     assert n == len(L) and np.array_equal(out.cpu().numpy(), L)
     assert np.array_equal(reference.load_lengths(text, "csv")[1], L)
+
+
+def test_jsonl_fuzz(ctx, reference):
+    # single-line corpora from mutated records: the GPU's accept / reject
+    # and the message must be the reference's (nlohmann) on every one
+    rng = np.random.default_rng(11)
+    base = [b'{"id":12,"length":345}', b'{"length": 7, "tags": ["a", {"b": null}], "f": -1.5e3}',
+            b'{"\\u0069d": 3, "length": 9, "s": "x\\"y\\\\z\\u00e9"}', b'[{"length":1}]', b'{"length":true}']
+    alphabet = list(b'{}[]:,"\\ -+.eE0123456789tfnulrsaxyz\t\r') + [0x00, 0x01, 0x7f, 0xc3, 0xa9, 0xff, 0xed, 0xf0]
+    for k in range(1500):
+        line = bytearray(base[k % len(base)])
+        for _ in range(int(rng.integers(1, 4))):
+            op = int(rng.integers(0, 3))
+            pos = int(rng.integers(0, len(line) + 1))
+            ch = int(alphabet[int(rng.integers(0, len(alphabet)))])
+            if op == 0:
+                line.insert(pos, ch)
+            elif op == 1 and pos < len(line):
+                del line[pos]
+            elif pos < len(line):
+                line[pos] = ch
+        text = bytes(line).replace(b"\n", b" ") + b"\n"
+        got, want = _both(ctx, reference, text, "jsonl")
+        assert got == want, text

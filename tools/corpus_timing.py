@@ -16,7 +16,8 @@ L = bench.synth(lib, dict(bench.C2, count=n))
 raw = ("\n".join(map(str, L.tolist())) + "\n").encode()
 csv = ("id,length\n" + "".join(f"{i},{v}\n" for i, v in enumerate(L.tolist()))).encode()
 ref = pyoracle.Oracle("reference") if pyoracle.available("reference") else None
-for fmt, text in (("raw-lengths", raw), ("csv", csv)):
+jsonl = "".join(f'{{"id":{i},"length":{v}}}\n' for i, v in enumerate(L.tolist())).encode()
+for fmt, text in (("raw-lengths", raw), ("csv", csv), ("jsonl", jsonl)):
     for _ in range(2):
         got = ctx.load_lengths(text, fmt)
     t0 = time.perf_counter()
@@ -33,7 +34,7 @@ for fmt, text in (("raw-lengths", raw), ("csv", csv)):
     r = float("nan")
     if ref is not None:
         t0 = time.perf_counter()
-        _, want = ref.load_lengths(text, fmt)
+        _, want = ref.load_lengths(text, fmt, "corpus")
         r = time.perf_counter() - t0
         assert np.array_equal(want, L)
     dev = sum(v[0] for v in st.values())  # ms

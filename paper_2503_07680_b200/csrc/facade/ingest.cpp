@@ -1,13 +1,56 @@
-// ingest.cpp — façade for synthetic corpora; generation is hbp_synth_lengths.
+// ingest.cpp — façade for corpus files (parsed on the GPU by
+// hbp_load_lengths) and synthetic corpora (hbp_synth_lengths).
 #include <cstdio>
+#include <fstream>
+#include <iterator>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "engine_ctx.hpp"
 #include "hbp/ingest.hpp"
 #include "hbp_b200.h"
 
 namespace hbp {
+
+CorpusFormat parse_corpus_format(const std::string& name) {  // ingest.cpp:140-145
+    if (name == "jsonl") return CorpusFormat::Jsonl;
+    if (name == "csv") return CorpusFormat::Csv;
+    if (name == "raw-lengths" || name == "raw") return CorpusFormat::RawLengths;
+    throw ValidationError("unknown corpus format: " + name);
+}
+
+SampleSet load_lengths(std::istream& in, CorpusFormat format, const std::string& source_name) {
+    const std::string text{std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>()};
+    const int32_t f = format == CorpusFormat::Jsonl ? HBP_CORPUS_JSONL
+                      : format == CorpusFormat::Csv ? HBP_CORPUS_CSV : HBP_CORPUS_RAW;
+    const int64_t cap = static_cast<int64_t>(text.size() / 2 + 1);
+    std::vector<int64_t> ids(static_cast<size_t>(cap)), lengths(static_cast<size_t>(cap));
+    int64_t n = 0;
+    detail::check(hbp_load_lengths(detail::ctx(), text.data(), static_cast<int64_t>(text.size()), f,
+                                   source_name.c_str(), ids.data(), lengths.data(), cap, HBP_MEM_HOST, &n));
+    SampleSet set;
+    set.source = source_name;
+    set.samples.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) set.samples[static_cast<size_t>(i)] = Sample{ids[i], lengths[i]};
+    return set;
+}
+
+SampleSet load_lengths(const std::filesystem::path& path, CorpusFormat format) {  // ingest.cpp:162-168
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open corpus file: " + path.string());
+    return load_lengths(in, format, path.string());
+}
+
+void write_jsonl(const SampleSet& set, std::ostream& out) {  // ingest.cpp:170-174
+    for (const auto& s : set.samples) out << "{\"id\":" << s.id << ",\"length\":" << s.length << "}\n";
+}
+
+void write_jsonl(const SampleSet& set, const std::filesystem::path& path) {
+    std::ofstream out(path);
+    if (!out) throw IoError("cannot write corpus file: " + path.string());
+    write_jsonl(set, out);
+}
 
 void LengthDistribution::validate() const {
     switch (family) {

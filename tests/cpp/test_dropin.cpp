@@ -120,13 +120,53 @@ int main() {
         const std::multiset<std::vector<Tokens>> want = {{1, 3}, {1, 3}, {2, 2}};
         CHECK(compositions(l) == want);
         EXPECT_THROW(ValidationError, pack(make_set({3, 9, 2}), 4, ffd, 0), "sample 1");  // :106-110
-        for (auto kind : {StrategyKind::Random, StrategyKind::Isf, StrategyKind::Ffs, StrategyKind::Ffd}) {
+        {
+            PackingStrategy sp;
+            sp.kind = StrategyKind::Spfhp;  // :183-193
+            const auto l2 = pack(make_set({512, 512, 512, 512, 512, 512, 256, 256, 256, 256}), 1024, sp, 0);
+            CHECK(l2.packs.size() == 4);
+            for (const auto& p : l2.packs) CHECK(p.total == 1024);
+        }
+        for (auto kind : {StrategyKind::Random, StrategyKind::Isf, StrategyKind::Ffs, StrategyKind::Ffd,
+                          StrategyKind::Bfs, StrategyKind::Spfhp}) {
             PackingStrategy s;
             s.kind = kind;
             const auto r = pack(make_set({4, 4, 4, 4}), 4, s, 1);  // :71-82
             CHECK(r.packs.size() == 4);
             for (const auto& p : r.packs) CHECK(p.total == 4 && p.samples.size() == 1);
         }
+    }
+    // ---- ingest (test_ingest.cpp:12-86) ----
+    {
+        std::istringstream a("{\"length\":4096}\n{\"length\":131072}\n");
+        const auto s1 = load_lengths(a, CorpusFormat::Jsonl, "mem");
+        CHECK(s1.samples.size() == 2 && s1.samples[1].length == 131072 && s1.samples[1].id == 1);
+        std::istringstream b("{\"id\":7,\"length\":10}\n\n{\"length\":20}\n");
+        const auto s2 = load_lengths(b, CorpusFormat::Jsonl, "mem");
+        CHECK(s2.samples.size() == 2 && s2.samples[0].id == 7 && s2.samples[1].id == 1);
+        std::istringstream e("");
+        EXPECT_THROW(ValidationError, load_lengths(e, CorpusFormat::Jsonl, "mem"), "empty corpus");
+        std::istringstream c("name,length,extra\na,1,x\nb,2,y\nc,3,z\n");
+        const auto s3 = load_lengths(c, CorpusFormat::Csv, "mem");
+        CHECK(s3.samples.size() == 3 && s3.samples[2].length == 3 && s3.samples[2].id == 2);
+        std::istringstream nc("tokens\n5\n");
+        EXPECT_THROW(ValidationError, load_lengths(nc, CorpusFormat::Csv, "mem"), "no \"length\" column");
+        std::istringstream r("12\n34\n56\n");
+        CHECK(load_lengths(r, CorpusFormat::RawLengths, "mem").samples[2].length == 56);
+        std::istringstream bad("10\nnonsense\n30\n");
+        EXPECT_THROW(ValidationError, load_lengths(bad, CorpusFormat::RawLengths, "mem"), "line 2");
+        std::istringstream z("{\"length\":0}\n"), neg("{\"length\":-3}\n");
+        EXPECT_THROW(ValidationError, load_lengths(z, CorpusFormat::Jsonl, "mem"), "length must be >= 1");
+        EXPECT_THROW(ValidationError, load_lengths(neg, CorpusFormat::Jsonl, "mem"), "got -3");
+        SampleSet set;
+        set.source = "rt";
+        set.samples = {Sample{5, 100}, Sample{9, 7}};
+        std::ostringstream out;
+        write_jsonl(set, out);
+        std::istringstream back(out.str());
+        const auto s4 = load_lengths(back, CorpusFormat::Jsonl, "mem");
+        CHECK(s4.samples.size() == 2 && s4.samples[0].id == 5 && s4.samples[1].length == 7);
+        EXPECT_THROW(ValidationError, parse_corpus_format("xml"), "unknown corpus format: xml");
     }
     // ---- balance (test_balance.cpp) ----
     {

@@ -80,8 +80,27 @@ def test_python_exceptions(hbp):
 def test_python_pack_strategies(hbp, oracle):
     rng = np.random.default_rng(5)
     L = rng.integers(1, 978, size=500)
-    for kind in ["isf", "random", "ffd", "ffs"]:
+    for kind in ["isf", "random", "ffd", "ffs", "bfs", "spfhp"]:
         got = hbp.pack(hbp.SampleSet(L.tolist()), 1024, kind, 77)
         want = oracle.pack(None, L, 1024, kind, seed=77)
         ids = [s.id for p in got.packs for s in p.samples]
         assert ids == want.member_id.tolist(), kind
+
+
+def test_python_load_lengths(hbp, tmp_path):
+    # ingest.hpp:22 / py_hbp.cpp:74-78: load_lengths(path, format="jsonl")
+    p = tmp_path / "c.jsonl"
+    p.write_bytes(b'{"id":7,"length":10}\n\n{"length":20}\n')
+    s = hbp.load_lengths(str(p))
+    assert [(x.id, x.length) for x in s.samples] == [(7, 10), (1, 20)] and s.source == str(p)
+    q = tmp_path / "c.csv"
+    q.write_bytes(b"name,length\na,3\nb,4\n")
+    assert hbp.load_lengths(str(q), "csv").lengths == [3, 4]
+    r = tmp_path / "c.txt"
+    r.write_bytes(b"10\nnonsense\n30\n")
+    with pytest.raises(ValueError, match="line 2: not an integer length: 'nonsense'"):
+        hbp.load_lengths(str(r), "raw-lengths")
+    with pytest.raises(OSError, match="cannot open corpus file"):
+        hbp.load_lengths(str(tmp_path / "missing.txt"), "raw")
+    with pytest.raises(ValueError, match="unknown corpus format: xml"):
+        hbp.load_lengths(str(r), "xml")

@@ -1023,7 +1023,7 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
         const i64 PP = P;
         scan_exclusive<u64>(
             PP + 1, [=] __device__(i64 i) { return i < PP ? static_cast<u64>(np[i]) : 0ull; },
-            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan);
+            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan, "scan.ff1");
     }
     const u64 R = read_vector(c, off.p + P, 1)[0];
     DevBuf<unsigned long long> demand(n_runs + 1, s);
@@ -1070,7 +1070,7 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
                 sp[j] = v;
                 if (kp[j] < kk && (j == RR - 1 || kp[j + 1] >= kk)) *vc = static_cast<u64>(j + 1);
             },
-            s, c.scan);
+            s, c.scan, "scan.ff2");
     }
     const u64 V = read_scalar(c, vcount.p);
     if (V > 0) {
@@ -1121,7 +1121,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
                 }
                 if (i == nn - 1) sc[0] = v + (head ? 1u : 0u);
             },
-            s, c.scan, "scan", 8.0);
+            s, c.scan, "scan.ff3", 8.0);
     }
 
     // bulk-place the items that can never share a bin (FFD with no live bins)

@@ -401,7 +401,7 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
         u64* Pp = P.p;
         scan_exclusive<u64>(
             static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? (F[i] >> 32) : 0ull; },
-            [=] __device__(i64 i, u64 v) { Pp[i] = v; }, s, c.scan);
+            [=] __device__(i64 i, u64 v) { Pp[i] = v; }, s, c.scan, "scan.nf1");
     }
     LAUNCH_B("nf.next", 12.0 * m, k_nf_next, grid_for(m, 256, 148u * 32u), 256, 0, s, P.p, m, static_cast<u64>(cap),
              nxt.p);

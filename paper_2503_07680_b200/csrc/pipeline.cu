@@ -670,7 +670,7 @@ u64 layout_group(Ctx& c, PackedGroup& pg, const u64* fill_items, u64 n_fill, con
         const i64 PP = static_cast<i64>(P);
         scan_exclusive<u64>(
             PP + 1, [=] __device__(i64 i) { return i < PP ? static_cast<u64>(static_cast<u32>(lv[i])) : 0ull; },
-            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan);
+            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan, "scan.plan1");
     }
     const u64 M = read_vector(c, off.p + P, 1)[0];
     u64* dst = T.members.p + T.n_members;
@@ -804,7 +804,7 @@ void emit_plan(Ctx& c, PackTable& T, DevBuf<u32>& slots, DevBuf<int32_t>& igroup
                 if (x >= D) return 0;
                 return sl[static_cast<u64>(sp[x / NN]) * NN + (x % NN)] != kNone ? 1 : 0;
             },
-            [=] __device__(i64 x, int64_t v) { dpo[x] = v; }, s, c.scan);
+            [=] __device__(i64 x, int64_t v) { dpo[x] = v; }, s, c.scan, "scan.plan2");
     }
     const u64 P = static_cast<u64>(read_vector(c, out.dev_pack_offsets.p + I * N, 1)[0]);
     out.n_packs = static_cast<int64_t>(P);
@@ -822,7 +822,7 @@ void emit_plan(Ctx& c, PackTable& T, DevBuf<u32>& slots, DevBuf<int32_t>& igroup
         const i64 PP = static_cast<i64>(P);
         scan_exclusive<int64_t>(
             PP + 1, [=] __device__(i64 q) -> int64_t { return q < PP ? static_cast<int64_t>(pc[q]) : 0; },
-            [=] __device__(i64 q, int64_t v) { mo[q] = v; }, s, c.scan);
+            [=] __device__(i64 q, int64_t v) { mo[q] = v; }, s, c.scan, "scan.plan3");
     }
     const u64 M = static_cast<u64>(read_vector(c, out.pack_member_offsets.p + P, 1)[0]);
     out.n_members = static_cast<int64_t>(M);
@@ -1047,7 +1047,7 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
                         if (keep) dst[v] = src[i];
                         if (i == m - 1) *cntp = v + (keep ? 1u : 0u);
                     },
-                    s, c.scan);
+                    s, c.scan, "scan.plan4");
                 psize[j] = read_scalar(c, cnt.p);
                 pools[j] = std::move(kept);
             }
@@ -1154,7 +1154,7 @@ void pack_device(Ctx& c, DeviceCorpus& corpus, int64_t capacity, const hbp_strat
                 oa[q] = static_cast<int64_t>(attp[q]);
             }
         },
-        s, c.scan);
+        s, c.scan, "scan.plan5");
     if (P > 0)
         LAUNCH(k_out_members, grid_for(P * 8, kB, 148u * 64u), kB, 0, s, pglobal.p, P, out.pack_member_offsets.p,
                T.moff.p, T.cnt.p, T.members.p, out.member_index.p);
@@ -1459,7 +1459,7 @@ void padded_batches_device(Ctx& c, const DeviceCorpus& corpus, int64_t budget, b
                 bi[i] = v + f - 1;
                 if (i == nn - 1) *nbp = v + f;
             },
-            s, c.scan);
+            s, c.scan, "scan.plan6");
     }
     out.n_batches = read_scalar(c, nb.p);
     out.bmax.alloc(out.n_batches + 1, s);

@@ -177,7 +177,7 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
         u32* op = offs.p;
         scan_exclusive<u32>(
             static_cast<i64>(ntiles) * 256, [=] __device__(i64 i) { return hp[i]; },
-            [=] __device__(i64 i, u32 v) { op[i] = v; }, s, c.scan);
+            [=] __device__(i64 i, u32 v) { op[i] = v; }, s, c.scan, "scan.radix1");
         LAUNCH_B("radix.scatter", 16.0 * n, k_radix_scatter, ntiles, RB, 0, s, ki, vi, ko, vo, n, shift, descending,
                  offs.p, ntiles);
         std::swap(ki, ko);

@@ -142,6 +142,9 @@ struct ScanScratch {
     }
 };
 
+constexpr int kScanSmallItems = 8;
+constexpr i64 kScanSmallTiles = 296;  // 2 x 148 SMs
+
 // Large tiles (64 KB of shared memory): the look-back hands the running
 // prefix from tile to tile at a roughly fixed cost per tile, so fewer,
 // larger tiles keep it off the bandwidth (tools/micro/scan_micro.cu, B200,
@@ -153,6 +156,13 @@ void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScra
                     const char* name = "scan", double bytes_per_elem = 2.0 * sizeof(T)) {
     constexpr int TILE = BLOCK * ITEMS;
     if (n <= 0) return;
+    if constexpr (ITEMS > kScanSmallItems) {
+        // fewer than two large tiles per SM: quarter-size tiles keep every SM busy
+        if (n < static_cast<i64>(TILE) * kScanSmallTiles) {
+            scan_exclusive<T, kScanSmallItems, BLOCK>(n, load, store, stream, scratch, name, bytes_per_elem);
+            return;
+        }
+    }
     const i64 tiles = (n + TILE - 1) / TILE;
     scratch.prepare(tiles, stream);
     constexpr int smem = static_cast<int>(sizeof(T)) * (TILE + TILE / 32);

@@ -238,7 +238,7 @@ FitResult scan_fit(Ctx& c, const u64* items, i64 n, u64* leaves, i64 max_bins, u
         const i64 PP = static_cast<i64>(P);
         scan_exclusive<u64>(
             PP + 1, [=] __device__(i64 i) { return i < PP ? static_cast<u64>(cp[i]) : 0ull; },
-            [=] __device__(i64 i, u64 v) { sp[i] = v; }, s, c.scan);
+            [=] __device__(i64 i, u64 v) { sp[i] = v; }, s, c.scan, "scan.fit1");
     }
     LAUNCH(k_fit_slots, grid_for(N, 256), 256, 0, s, kb.p, pos.p, N, start.p, item_slot);
     fr.bins = static_cast<i64>(P);

@@ -44,7 +44,7 @@ void offsets_of(Ctx& c, const int64_t* sizes, u64 n, int64_t* off) {
     const i64 nn = static_cast<i64>(n);
     scan_exclusive<u64>(
         nn + 1, [=] __device__(i64 i) { return i < nn ? static_cast<u64>(sizes[i]) : 0ull; },
-        [=] __device__(i64 i, u64 v) { off[i] = static_cast<int64_t>(v); }, c.stream, c.scan);
+        [=] __device__(i64 i, u64 v) { off[i] = static_cast<int64_t>(v); }, c.stream, c.scan, "scan.sched1");
 }
 
 }  // namespace
@@ -161,7 +161,7 @@ void curriculum_device(Ctx& c, const DevicePlan& in, int32_t warmup, int32_t cut
                 if (sh) lp[v] = static_cast<u32>(i);
                 if (i == II - 1) *cp = v + (sh ? 1u : 0u);
             },
-            s, c.scan);
+            s, c.scan, "scan.sched2");
         n_short = read_scalar(c, cnt.p);
         const u64 ns = n_short;
         scan_exclusive<u32>(
@@ -169,7 +169,7 @@ void curriculum_device(Ctx& c, const DevicePlan& in, int32_t warmup, int32_t cut
             [=] __device__(i64 i, u32 v) {
                 if (!(ig[i] < cutoff)) lp[ns + v] = static_cast<u32>(i);
             },
-            s, c.scan);
+            s, c.scan, "scan.sched3");
     }
     if (n_short < static_cast<u64>(warmup))
         fail_validation("curriculum needs " + std::to_string(warmup) + " short-group iterations but the plan has only " +

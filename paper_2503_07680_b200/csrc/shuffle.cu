@@ -188,7 +188,7 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src, uint64_t
     u32* offp = off.p;
     scan_exclusive<u32>(
         static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? cntp[i] : 0u; },
-        [=] __device__(i64 i, u32 v) { offp[i] = v; }, s, c.scan);
+        [=] __device__(i64 i, u32 v) { offp[i] = v; }, s, c.scan, "scan.fy1");
     cnt.zero();  // reused as fill cursors
     LAUNCH_B("fy.scatter", 20.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, off.p, cnt.p, bucket.p);
     LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);

@@ -21,6 +21,7 @@
 // (residual << 32 | count) per bin, bins in creation order. Slots (rank of
 // an item inside its bin) come from a stable radix sort of the bin column.
 #include <cstdlib>
+#include <vector>
 
 #include "radix.cuh"
 #include "scan.cuh"
@@ -164,6 +165,101 @@ __global__ void __launch_bounds__(kFitThreads, 1)
     if (tid == 0) *n_bins = P;
 }
 
+// ---- SPFHP on one warp: a 32-ary max tree over the packs -----------------
+//
+// Only the emptiest pack is ever asked for, so a tournament tree answers it
+// without a block barrier: the top level (<= 32 nodes) lives in the lanes'
+// registers, every level below in shared memory (the leaves in global
+// memory once they outgrow it). Per item: REDUX max over the top level; if it
+// fits, descend one 32-wide level per step (load, ballot on == max, first
+// lane: the lowest index among the emptiest), then walk back up replacing
+// one child and re-reducing. A new pack raises its ancestors to max(., v).
+constexpr int kTreeMaxLevels = 6;
+
+struct TreeLevels {
+    int H;                         // levels in memory (0: the leaves are the register level)
+    u64 off[kTreeMaxLevels];       // shared-memory offset (u32 units) of level h, if g[h] is null
+    u32* g[kTreeMaxLevels];        // global level h, else null
+    u64 size[kTreeMaxLevels];      // padded entries of level h
+};
+
+__global__ void __launch_bounds__(32, 1)
+    k_wfd_tree(const u64* __restrict__ items, i64 n, u32 cap, TreeLevels T, u32* __restrict__ res,
+               u32* __restrict__ bin_out, u32* __restrict__ cnt, u32* __restrict__ n_bins) {
+    extern __shared__ __align__(16) u32 s_tree[];
+    const u32 lane = threadIdx.x;
+    u32* L[kTreeMaxLevels];
+#pragma unroll
+    for (int h = 0; h < kTreeMaxLevels; ++h) L[h] = h < T.H ? (T.g[h] ? T.g[h] : s_tree + T.off[h]) : nullptr;
+#pragma unroll
+    for (int h = 0; h < kTreeMaxLevels; ++h)
+        if (h < T.H && !T.g[h])
+            for (u64 k = lane; k < T.size[h]; k += 32) L[h][k] = 0u;
+    __syncwarp();
+    u32 top = 0u;  // register level: entry `lane`
+    u32 P = 0;
+    for (i64 base = 0; base < n; base += 32) {
+        const int cnt_c = static_cast<int>(n - base < 32 ? n - base : 32);
+        const u32 mylen = static_cast<int>(lane) < cnt_c ? entry_len(items[base + lane]) : 0u;
+        u32 mybin = 0;
+        for (int j = 0; j < cnt_c; ++j) {
+            const u32 s = __shfl_sync(kFull, mylen, j);
+            const u32 M = __reduce_max_sync(kFull, top);
+            u32 leaf;
+            if (M >= s) {
+                u32 node = __ffs(__ballot_sync(kFull, top == M)) - 1;
+                u32 v[kTreeMaxLevels];
+#pragma unroll
+                for (int h = kTreeMaxLevels - 1; h >= 0; --h) {
+                    if (h < T.H) {
+                        v[h] = L[h][node * 32 + lane];
+                        node = node * 32 + (__ffs(__ballot_sync(kFull, v[h] == M)) - 1);
+                    }
+                }
+                leaf = node;
+                u32 nv = M - s, idx = leaf;
+#pragma unroll
+                for (int h = 0; h < kTreeMaxLevels; ++h) {
+                    if (h < T.H) {
+                        const u32 c = idx & 31u;
+                        const u32 x = lane == c ? nv : v[h];
+                        if (lane == c) L[h][idx] = nv;
+                        nv = __reduce_max_sync(kFull, x);
+                        idx >>= 5;
+                    }
+                }
+                if (lane == idx) top = nv;
+            } else {
+                leaf = P++;
+                const u32 nv = cap - s;
+                u32 idx = leaf;
+                if (lane == 0) {
+#pragma unroll
+                    for (int h = 0; h < kTreeMaxLevels; ++h) {
+                        if (h < T.H) {
+                            if (L[h][idx] < nv) L[h][idx] = nv;
+                            idx >>= 5;
+                        }
+                    }
+                }
+                idx = leaf >> (5 * T.H);
+                if (lane == idx && top < nv) top = nv;
+            }
+            __syncwarp();
+            if (lane == 0) atomicAdd(cnt + leaf, 1u);
+            if (static_cast<int>(lane) == j) mybin = leaf;
+        }
+        if (static_cast<int>(lane) < cnt_c) bin_out[base + lane] = mybin;
+    }
+    // residuals of the bins: the leaf level (or the register level)
+    if (T.H == 0) {
+        if (lane < P) res[lane] = top;
+    } else if (!T.g[0]) {
+        for (u32 k = lane; k < P; k += 32) res[k] = L[0][k];
+    }
+    if (lane == 0) *n_bins = P;
+}
+
 __global__ void k_fit_leaves(const u32* __restrict__ res, const u32* __restrict__ cnt, u64 P, u64* __restrict__ leaves) {
     for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < P;
          i += static_cast<u64>(gridDim.x) * blockDim.x)
@@ -217,7 +313,53 @@ FitResult scan_fit(Ctx& c, const u64* items, i64 n, u64* leaves, i64 max_bins, u
     const bool force_global = fg && *fg && *fg != '0';
     const bool in_smem = !force_global && need <= static_cast<size_t>(smem_optin);
     const size_t smem = in_smem ? need : kFitFixedSmem;
-    if (worst) {
+    const char* fb = std::getenv("HBP_SPFHP_BLOCK");  // tests: the block-wide pick for SPFHP too
+    if (worst && !(fb && *fb && *fb != '0')) {
+        // level sizes, leaves first, each padded to 32; the level of <= 32
+        // entries stays in registers
+        TreeLevels T{};
+        u64 sz = (pmax + 31) / 32 * 32;
+        if (pmax <= 32) sz = 0;
+        while (sz > 0) {
+            if (T.H == kTreeMaxLevels) throw EngineError(HBP_ERR_VALIDATION, "spfhp: too many packs");
+            T.size[T.H++] = sz;
+            const u64 up = (sz / 32 + 31) / 32 * 32;
+            if (sz / 32 <= 32) break;
+            sz = up;
+        }
+        // shared memory for the upper levels, top down, while they fit
+        u64 used = 0;
+        int h = T.H - 1;
+        for (; h >= 0; --h) {
+            if (force_global || (used + T.size[h]) * sizeof(u32) > static_cast<size_t>(smem_optin)) break;
+            T.off[h] = used;
+            used += T.size[h];
+        }
+        std::vector<DevBuf<u32>> glv;
+        for (int k = 0; k <= h; ++k) {
+            if (k == 0) {
+                // leaves in global memory are the residual array itself
+                T.g[0] = res.p;
+                CUDA_CHECK(cudaMemsetAsync(res.p, 0, sizeof(u32) * pmax, s));
+                if (T.size[0] > pmax) {
+                    glv.emplace_back(T.size[0], s);
+                    glv.back().zero();
+                    T.g[0] = glv.back().p;
+                }
+            } else {
+                glv.emplace_back(T.size[k], s);
+                glv.back().zero();
+                T.g[k] = glv.back().p;
+            }
+        }
+        const size_t tsmem = used * sizeof(u32);
+        set_max_dynamic_smem_once(reinterpret_cast<const void*>(&k_wfd_tree), smem_optin);
+        LAUNCH_B("fit.tree", 12.0 * static_cast<double>(n), k_wfd_tree, 1, 32, tsmem, s, items, n, cap, T, res.p,
+                 item_bin, cnt.p, nb.p);
+        if (T.g[0] && T.g[0] != res.p)
+            CUDA_CHECK(cudaMemcpyAsync(res.p, T.g[0], sizeof(u32) * pmax, cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));  // glv lives until the kernel is done
+    } else if (worst) {
         if (in_smem) launch_fit<true, true>(c, items, n, cap, res.p, item_bin, cnt.p, nb.p, smem, smem_optin);
         else launch_fit<true, false>(c, items, n, cap, res.p, item_bin, cnt.p, nb.p, smem, smem_optin);
     } else {

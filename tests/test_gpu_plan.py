@@ -176,12 +176,15 @@ def test_pack(ctx, oracle, strategy, cap):
 
 
 @pytest.mark.parametrize("strategy", ["bfs", "spfhp"])
-@pytest.mark.parametrize("where", ["smem", "global"])
+@pytest.mark.parametrize("where", ["smem", "global", "block"])
 def test_scan_fit_large(ctx, oracle, strategy, where, monkeypatch):
-    # 40K items over ~20K packs: the residual array in shared memory, and
-    # (HBP_FIT_GLOBAL) the same walk over the L2-resident array
+    # 40K items over ~20K packs: the residual array / SPFHP's max tree in
+    # shared memory, (HBP_FIT_GLOBAL) in global memory, and (HBP_SPFHP_BLOCK)
+    # SPFHP through the block-wide pick
     if where == "global":
         monkeypatch.setenv("HBP_FIT_GLOBAL", "1")
+    if where == "block":
+        monkeypatch.setenv("HBP_SPFHP_BLOCK", "1")
     rng = np.random.default_rng(77)
     L = rng.integers(1, 65, size=40_000)
     want = oracle.pack(None, L, 64, strategy, seed=99)

@@ -274,6 +274,7 @@ def run_ours(args, rank, world, local):
     stages = profile_stages(ctx, lib, step_device)
     sweep_res = None if args.no_sweep else run_sweep_leg(ctx, lib, rank, world, dist)
     c4_res = run_c4_leg(ctx, lib, rank, world, dist) if not args.no_c4 else None
+    ingest_res = run_ingest_leg(ctx, lib) if rank == 0 and not args.no_ingest else None
 
     tot_dev = sum(dev_ms)
     tot_e2e = sum(e2e_ms)
@@ -305,6 +306,7 @@ def run_ours(args, rank, world, local):
             "cpu_baseline": cpu,
             "sweep": sweep_res,
             "c4": c4_res,
+            "ingest": ingest_res,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -478,7 +480,13 @@ def profile_stages(ctx, lib, fn):
     ms, launches, nbytes = C.c_double(), C.c_int64(), C.c_double()
     i = 0
     while lib.hbp_ctx_stage_stats(ctx.h, i, name, 128, C.byref(ms), C.byref(launches), C.byref(nbytes)) == 0:
-        out[name.value.decode()] = {"ms": ms.value, "launches": launches.value, "bytes": nbytes.value}
+        k = name.value.decode()
+        # the scan call sites (scan.nf1, scan.radix1, ...) form one kernel family
+        fam = "scan" if k.startswith("scan.") or k == "nf.tiles_scan" else k
+        o = out.setdefault(fam, {"ms": 0.0, "launches": 0, "bytes": 0.0})
+        o["ms"] += ms.value
+        o["launches"] += launches.value
+        o["bytes"] += nbytes.value
         i += 1
     return out
 
@@ -512,6 +520,66 @@ def roofline(stages, peak, peak_kind):
                                 if top_k.startswith("fit.chain") else "hbm"}}
 
 
+INGEST_SAMPLES = 2_000_000
+
+
+def run_ingest_leg(ctx, lib):
+    """load_lengths of a JSONL corpus (2M records of
+    the C2 spec, {"id":i,"length":L} per line, 57 MB) through the C-ABI --
+    host text in, host ids + lengths out (e2e, wall clock) -- with the
+    device-side parse timed by CUDA events; the reference's istream parser
+    (oracle/_ref, one core) on the same bytes beside it."""
+    import time
+    L = synth(lib, C2, INGEST_SAMPLES)
+    text = "".join(f'{{"id":{i},"length":{v}}}\n' for i, v in enumerate(L.tolist())).encode()
+    for _ in range(2):
+        ctx.load_lengths(text, "jsonl", with_ids=True)
+    ctx.synchronize()
+    e2e = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ids, got = ctx.load_lengths(text, "jsonl", with_ids=True)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    assert np.array_equal(got, L) and np.array_equal(ids, np.arange(len(L)))
+    lib.hbp_ctx_set_profiling(ctx.h, 1)
+    ctx.load_lengths(text, "jsonl")
+    ctx.synchronize()
+    lib.hbp_ctx_set_profiling(ctx.h, 0)
+    st = {}
+    name = C.create_string_buffer(128)
+    ms, launches, nbytes = C.c_double(), C.c_int64(), C.c_double()
+    i = 0
+    while lib.hbp_ctx_stage_stats(ctx.h, i, name, 128, C.byref(ms), C.byref(launches), C.byref(nbytes)) == 0:
+        st[name.value.decode()] = ms.value
+        i += 1
+    dev_ms = sum(st.values())
+    parse_ms = st.get("k_parse_jsonl", 0.0)
+    peak, peak_kind = peaks()
+    # parse kernel: reads the text once, reads 2 line starts and writes value + id per line
+    alg = len(text) + 32.0 * len(L)
+    ref = None
+    try:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle"))
+        import pyoracle
+        if pyoracle.available("reference"):
+            o = pyoracle.Oracle("reference")
+            t0 = time.perf_counter()
+            _, want = o.load_lengths(text, "jsonl", "bench")
+            ref = {"ms": (time.perf_counter() - t0) * 1e3, "cores": 1, "kind": "reference",
+                   "identical": bool(np.array_equal(want, got))}
+    except Exception as e:  # noqa: BLE001
+        ref = {"unavailable": str(e)}
+    return {"workload": f"load_lengths(jsonl): {len(L)} records of the C2 spec, {len(text)} bytes",
+            "e2e_ms": round(statistics.median(e2e), 3), "device_ms": round(dev_ms, 4),
+            "records_per_s_e2e": len(L) / (statistics.median(e2e) / 1e3),
+            "stages_ms": {k: round(v, 4) for k, v in sorted(st.items(), key=lambda kv: -kv[1])},
+            "parse_roofline": {"kernel": "k_parse_jsonl", "bound": "hbm", "algorithmic_bytes": alg,
+                               "achieved": alg / (parse_ms / 1e3) / 1e9 if parse_ms else None, "peak": peak,
+                               "peak_kind": peak_kind, "unit": "GB/s",
+                               "frac": alg / (parse_ms / 1e3) / 1e9 / peak if parse_ms else None},
+            "reference": ref}
+
+
 def cpu_baseline_leg(lib):
     try:
         L = synth(lib, C2, REF_SAMPLE)
@@ -532,6 +600,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the auto-selection sweep leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the 100M-sample C4 / C5-sample leg")
+    ap.add_argument("--no-ingest", action="store_true", help="skip the corpus-file (JSONL) ingest leg")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

@@ -355,6 +355,21 @@ int hbp_assign_runtime(hbp_ctx* ctx, hbp_plan* plan, int32_t* sp, int32_t* ckpt,
  * ckpt,phase" rows; same buffer convention as hbp_plan_to_json. */
 int hbp_schedule_csv(hbp_ctx* ctx, hbp_plan* plan, char* out, int64_t capacity, int64_t* out_len);
 
+/* plan_from_json (include/hbp/io.hpp:26, src/io.cpp:112-160) on the GPU:
+ * the manifest text (host memory) -> a device plan whose member_index
+ * indexes the manifest's own samples in member order (hbp_plan_members).
+ * Reads the canonical layout plan_to_json / write_plan produce, verified
+ * byte for byte by re-serialising; text that is not JSON fails with the
+ * reference's "bad plan manifest: <nlohmann message>", valid JSON in another
+ * layout with a validation error saying so. Semantic errors are the
+ * reference's ("plan manifest: unsupported version V", the groups' own,
+ * "... iteration group index out of range", "... pack exceeds its
+ * capacity"), first in its order. */
+int hbp_plan_from_json(hbp_ctx* ctx, const char* text, int64_t bytes, hbp_plan** out, int64_t* out_n_members);
+/* ids[n_members], lengths[n_members] (host) of a plan read by
+ * hbp_plan_from_json: sample k of the plan view is (ids[k], lengths[k]). */
+int hbp_plan_members(hbp_ctx* ctx, hbp_plan* plan, int64_t* ids, int64_t* lengths);
+
 /* Plan manifest (replaces hbp::plan_to_json, src/io.cpp:85-110): the
  * byte-identical nlohmann dump(2) text of the plan, built on the GPU.
  * `samples` is the corpus the plan was built from (ids / lengths of the

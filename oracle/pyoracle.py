@@ -204,6 +204,14 @@ class Oracle:
         self._check(rc)
         return self._take(out, groups, g.l_best)
 
+    def plan_from_json(self, text: bytes) -> abi.FlatPlan:
+        """plan_from_json(text) in the reference (reference kind only); member ids / lengths in the plan."""
+        out = C.POINTER(OraclePlan)()
+        rc = self.lib.oracle_plan_from_json(C.c_char_p(text), C.c_int64(len(text)), C.byref(out), self.err,
+                                            len(self.err))
+        self._check(rc)
+        return self._take(out)
+
     def build_plan_json(self, ids, lengths, groups: Sequence[tuple], l_best=None, **opts) -> bytes:
         """The reference's plan_to_json text of its build_plan (reference kind only)."""
         lengths = np.ascontiguousarray(lengths, dtype=np.int64)

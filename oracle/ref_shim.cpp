@@ -386,6 +386,16 @@ int oracle_build_plan(const int64_t* ids, const int64_t* lengths, int64_t n,
     });
 }
 
+// plan_from_json (io.cpp:112-160) of a manifest text.
+int oracle_plan_from_json(const char* text, int64_t bytes, oracle_plan** out, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const auto plan = R::plan_from_json(std::string(text, static_cast<std::size_t>(bytes)));
+        Flat f;
+        for (const auto& it : plan.iterations) f.add_iteration(it);
+        *out = f.finish(plan.device_count, plan.seed);
+    });
+}
+
 // The reference's plan manifest (io.cpp plan_to_json) of build_plan's plan;
 // *out is malloc'd (oracle_free_text).
 int oracle_build_plan_json(const int64_t* ids, const int64_t* lengths, int64_t n,

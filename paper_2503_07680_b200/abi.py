@@ -424,6 +424,25 @@ class Context:
         b = nb.value
         return order[:n], off[:b + 1], mx[:b]
 
+    def plan_from_json(self, text: bytes):
+        """hbp::plan_from_json on the GPU: (DevicePlanHandle, ids, lengths) --
+        the plan's member_index indexes the manifest's samples (ids, lengths)."""
+        self.lib.hbp_plan_from_json.argtypes = [C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_void_p),
+                                                C.POINTER(C.c_int64)]
+        self.lib.hbp_plan_members.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        h = C.c_void_p()
+        m = C.c_int64()
+        self.check(self.lib.hbp_plan_from_json(self.h, text, C.c_int64(len(text)), C.byref(h), C.byref(m)))
+        v = PlanView()
+        self.check(self.lib.hbp_plan_view_get(self.h, h, C.byref(v)))
+        groups = [(v.groups.groups[k].length, v.groups.groups[k].sp, v.groups.groups[k].ckpt)
+                  for k in range(v.groups.count)]
+        plan = self._plan(h, groups, v.groups.l_best)
+        ids = np.zeros(max(m.value, 1), dtype=np.int64)
+        lens = np.zeros(max(m.value, 1), dtype=np.int64)
+        self.check(self.lib.hbp_plan_members(self.h, h, C.c_void_p(ids.ctypes.data), C.c_void_p(lens.ctypes.data)))
+        return plan, ids[:m.value], lens[:m.value]
+
     def build_plan_samples(self, s: Samples, groups, l_best=None, **opts) -> "DevicePlanHandle":
         g, garr = make_groups(groups, l_best)
         o = make_options(**opts)

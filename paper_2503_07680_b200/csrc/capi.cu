@@ -282,6 +282,34 @@ int hbp_build_batching_plan(hbp_ctx* ctx, const hbp_samples* samples, hbp_group_
     });
 }
 
+int hbp_plan_from_json(hbp_ctx* ctx, const char* text, int64_t bytes, hbp_plan** out, int64_t* out_n_members) {
+    return guarded(ctx, [&] {
+        *out = nullptr;
+        if (bytes < 0 || (bytes > 0 && text == nullptr)) fail_validation("manifest text is null");
+        auto* p = new_plan(ctx);
+        try {
+            plan_from_json_device(*ctx, text, static_cast<u64>(bytes), p->dp, p->read_ids, p->read_lens);
+        } catch (...) {
+            delete_plan(p);
+            throw;
+        }
+        *out_n_members = p->dp.n_members;
+        *out = p;
+    });
+}
+
+int hbp_plan_members(hbp_ctx* ctx, hbp_plan* plan, int64_t* ids, int64_t* lengths) {
+    return guarded(ctx, [&] {
+        if (plan == nullptr) fail_validation("null plan");
+        if (!plan->read_ids.p) fail_validation("plan_members: the plan was not read from a manifest");
+        const size_t m = static_cast<size_t>(plan->dp.n_members);
+        CUDA_CHECK(cudaMemcpyAsync(ids, plan->read_ids.p, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(lengths, plan->read_lens.p, sizeof(int64_t) * m, cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int hbp_padded_batching(hbp_ctx* ctx, const hbp_samples* samples, int64_t token_budget, int32_t mode,
                         uint64_t seed, int32_t* order, int64_t* batch_offsets, int64_t* batch_max,
                         int64_t* n_batches) {

@@ -489,6 +489,32 @@ std::vector<std::string> split_csv(const std::string& line) {
 
 }  // namespace
 
+void upload_text(Ctx& c, const char* text, u64 bytes, DevBuf<unsigned char>& t) {
+    const u64 chunks = (bytes + kChunkBytes - 1) / kChunkBytes;
+    t.alloc(chunks * kChunkBytes + kChunkBytes, c.stream);
+    if (bytes) CUDA_CHECK(cudaMemcpyAsync(t.p, text, bytes, cudaMemcpyHostToDevice, c.stream));
+    CUDA_CHECK(cudaMemsetAsync(t.p + bytes, 0, t.n - bytes, c.stream));
+}
+
+u64 text_line_starts(Ctx& c, const unsigned char* t, u64 bytes, DevBuf<u64>& starts) {
+    cudaStream_t s = c.stream;
+    const u64 chunks = (bytes + kChunkBytes - 1) / kChunkBytes;
+    DevBuf<u64> chunk_line(chunks + 1, s);
+    {
+        const uint4* tv = reinterpret_cast<const uint4*>(t);
+        u64* cl = chunk_line.p;
+        const i64 C = static_cast<i64>(chunks);
+        scan_exclusive<u64>(
+            C + 1, [=] __device__(i64 i) { return i < C ? static_cast<u64>(nl_in(tv[i])) : 0ull; },
+            [=] __device__(i64 i, u64 v) { cl[i] = v; }, s, c.scan, "corpus.lines", 1.0 * kChunkBytes / 1.0);
+    }
+    const u64 nl = read_vector(c, chunk_line.p + chunks, 1)[0];
+    starts.alloc(nl + 2, s);
+    CUDA_CHECK(cudaMemsetAsync(starts.p, 0, sizeof(u64), s));
+    if (chunks) LAUNCH(k_line_starts, grid_for(chunks, 256), 256, 0, s, t, bytes, chunk_line.p, starts.p);
+    return nl;
+}
+
 i64 parse_corpus_text(Ctx& c, const char* text, u64 bytes, int format, const std::string& source,
                       DevBuf<int64_t>& lengths, DevBuf<int64_t>& ids) {
     cudaStream_t s = c.stream;
@@ -509,26 +535,13 @@ i64 parse_corpus_text(Ctx& c, const char* text, u64 bytes, int format, const std
         col = static_cast<int>(k);
         first = 1;
     }
-    const u64 chunks = (bytes + kChunkBytes - 1) / kChunkBytes;
-    DevBuf<unsigned char> t(chunks * kChunkBytes + kChunkBytes, s);
-    if (bytes) CUDA_CHECK(cudaMemcpyAsync(t.p, text, bytes, cudaMemcpyHostToDevice, s));
-    CUDA_CHECK(cudaMemsetAsync(t.p + bytes, 0, t.n - bytes, s));
-    DevBuf<u64> chunk_line(chunks + 1, s);
-    {
-        const uint4* tv = reinterpret_cast<const uint4*>(t.p);
-        u64* cl = chunk_line.p;
-        const i64 C = static_cast<i64>(chunks);
-        scan_exclusive<u64>(
-            C + 1, [=] __device__(i64 i) { return i < C ? static_cast<u64>(nl_in(tv[i])) : 0ull; },
-            [=] __device__(i64 i, u64 v) { cl[i] = v; }, s, c.scan, "corpus.lines", 1.0 * kChunkBytes / 1.0);
-    }
-    const u64 nl = read_vector(c, chunk_line.p + chunks, 1)[0];
+    DevBuf<unsigned char> t;
+    upload_text(c, text, bytes, t);
+    DevBuf<u64> starts;
+    const u64 nl = text_line_starts(c, t.p, bytes, starts);
     unsigned char last = 0;
     if (bytes) last = static_cast<unsigned char>(text[bytes - 1]);
     const u64 lines = nl + ((bytes > 0 && last != '\n') ? 1 : 0);
-    DevBuf<u64> starts(nl + 2, s);
-    CUDA_CHECK(cudaMemsetAsync(starts.p, 0, sizeof(u64), s));
-    if (chunks) LAUNCH(k_line_starts, grid_for(chunks, 256), 256, 0, s, t.p, bytes, chunk_line.p, starts.p);
     DevBuf<i64> vals(lines + 1, s), lid(jsonl ? lines + 1 : 0, s);
     DevBuf<unsigned long long> ferr(1, s);
     CUDA_CHECK(cudaMemsetAsync(ferr.p, 0xff, sizeof(unsigned long long), s));

@@ -198,6 +198,10 @@ __global__ void k_json_write(JsonArgs a, const u64* off, char* out) {
         slot_text<true>(a, g, out + off[g]);
 }
 
+}  // namespace
+
+namespace hbp_b200 {
+
 std::string header_text(const DevicePlan& dp) {
     std::string h = "{\n  \"device_count\": " + std::to_string(dp.device_count) + ",\n  \"groups\": {\n    \"groups\": ";
     if (dp.groups.empty()) {
@@ -223,7 +227,33 @@ std::string footer_text(const DevicePlan& dp) {
            ",\n  \"version\": 1\n}\n";
 }
 
-}  // namespace
+// The manifest body (everything between header_text and footer_text) of a
+// device plan, built on the device into `text` (null: length only).
+// Returns its length.
+u64 plan_json_body(Ctx& c, const DevicePlan& dp, const int64_t* ids, const int64_t* lens, DevBuf<char>* text) {
+    cudaStream_t s = c.stream;
+    JsonArgs a{dp.iter_group.p, dp.iter_dev_offsets.p, dp.dev_pack_offsets.p, dp.pack_capacity.p,
+               dp.pack_member_offsets.p, dp.member_index.p, ids, lens, dp.iter_phase.p, dp.n_iterations, dp.n_devices};
+    const u64 G = static_cast<u64>(dp.n_devices);
+    if (G == 0) return 0;
+    DevBuf<u64> len(G + 1, s), off(G + 1, s);
+    LAUNCH(k_json_len, grid_for(G, 128, 148u * 32u), 128, 0, s, a, len.p);
+    const u64* lp = len.p;
+    u64* op = off.p;
+    const i64 GG = static_cast<i64>(G);
+    scan_exclusive<u64>(
+        GG + 1, [=] __device__(i64 i) { return i < GG ? lp[i] : 0ull; }, [=] __device__(i64 i, u64 v) { op[i] = v; },
+        s, c.scan, "scan.io1");
+    const u64 body = read_scalar(c, off.p + G);
+    if (text == nullptr) return body;  // length only
+    text->alloc(body, s);
+    if (body)
+        LAUNCH_B("io.json", static_cast<double>(body), k_json_write, grid_for(G, 128, 148u * 32u), 128, 0, s, a, off.p,
+                 text->p);
+    return body;
+}
+
+}  // namespace hbp_b200
 
 extern "C" int hbp_plan_to_json(hbp_ctx* ctx, hbp_plan* plan, const hbp_samples* samples, char* out,
                                 int64_t capacity, int64_t* out_len) {
@@ -249,22 +279,8 @@ extern "C" int hbp_plan_to_json(hbp_ctx* ctx, hbp_plan* plan, const hbp_samples*
                 ids = dids.p;
             }
         }
-        JsonArgs a{dp.iter_group.p, dp.iter_dev_offsets.p, dp.dev_pack_offsets.p, dp.pack_capacity.p,
-                   dp.pack_member_offsets.p, dp.member_index.p, ids, lens, dp.iter_phase.p, dp.n_iterations,
-                   dp.n_devices};
-        const u64 G = static_cast<u64>(dp.n_devices);
-        DevBuf<u64> len(G + 1, s), off(G + 1, s);
-        u64 body = 0;
-        if (G > 0) {
-            LAUNCH(k_json_len, grid_for(G, 128, 148u * 32u), 128, 0, s, a, len.p);
-            const u64* lp = len.p;
-            u64* op = off.p;
-            const i64 GG = static_cast<i64>(G);
-            scan_exclusive<u64>(
-                GG + 1, [=] __device__(i64 i) { return i < GG ? lp[i] : 0ull; },
-                [=] __device__(i64 i, u64 v) { op[i] = v; }, s, ctx->scan);
-            body = read_scalar(*ctx, off.p + G);
-        }
+        DevBuf<char> text;
+        const u64 body = plan_json_body(*ctx, dp, ids, lens, out == nullptr ? nullptr : &text);
         const u64 total = head.size() + body + foot.size();
         *out_len = static_cast<int64_t>(total);
         if (out == nullptr) {
@@ -276,9 +292,6 @@ extern "C" int hbp_plan_to_json(hbp_ctx* ctx, hbp_plan* plan, const hbp_samples*
                                                       " bytes, the manifest needs " + std::to_string(total));
         std::memcpy(out, head.data(), head.size());
         if (body) {
-            DevBuf<char> text(body, s);
-            LAUNCH_B("io.json", static_cast<double>(body), k_json_write, grid_for(G, 128, 148u * 32u), 128, 0, s, a,
-                     off.p, text.p);
             // download through two pinned staging blocks: chunk k + 1 crosses
             // PCIe while chunk k is copied into the caller's (pageable) buffer
             constexpr size_t kChunk = size_t(64) << 20;

@@ -137,6 +137,19 @@ void padded_batches_device(Ctx& c, const DeviceCorpus& corpus, int64_t budget, b
 void batching_plan_device(Ctx& c, const DeviceCorpus& corpus, const hbp_group_config& group, int32_t device_count,
                           bool sorted, uint64_t seed, DevicePlan& out);
 
+// io.cu: the plan manifest's header / footer text and its body built on the
+// device (null text: length only); plan_read.cu: the reader.
+std::string header_text(const DevicePlan& dp);
+std::string footer_text(const DevicePlan& dp);
+u64 plan_json_body(Ctx& c, const DevicePlan& dp, const int64_t* ids, const int64_t* lens, DevBuf<char>* text);
+void plan_from_json_device(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, DevBuf<int64_t>& ids,
+                           DevBuf<int64_t>& lens);
+// corpus.cu: text to the device (zero-padded to 16 bytes) and the start of
+// every line (starts[0] = 0, then one past each '\n'); returns the '\n' count.
+void upload_text(Ctx& c, const char* text, u64 bytes, DevBuf<unsigned char>& t);
+u64 text_line_starts(Ctx& c, const unsigned char* t, u64 bytes, DevBuf<u64>& starts);
+std::string json_parse_error_text(const std::string& text);
+
 // corpus.cu: load_lengths of a JSONL / CSV / raw-lengths text
 // (ingest.cpp:57-160); returns the sample count, ids and lengths (device).
 i64 parse_corpus_text(Ctx& c, const char* text, u64 bytes, int format, const std::string& source,
@@ -148,6 +161,8 @@ i64 parse_corpus_text(Ctx& c, const char* text, u64 bytes, int format, const std
 // once made, and the context that owns it (null once the context is gone).
 struct hbp_plan {
     hbp_b200::DevicePlan dp;
+    // a plan read from a manifest carries its own samples (member order)
+    hbp_b200::DevBuf<int64_t> read_ids, read_lens;
     hbp_plan_view view{};
     hbp_ctx* owner = nullptr;
 };

@@ -6,6 +6,7 @@ make_plan_json_golden.py), and byte for byte against the compiled reference
 import hashlib
 import json
 import os
+import re
 
 import numpy as np
 import pytest
@@ -115,3 +116,68 @@ def test_padded_batching_vs_compiled_reference(ctx, oracle, mode, budget):
 def test_padded_batching_budget_error(ctx):
     with pytest.raises(abi.ValidationError, match=r"token budget 100 is below the longest sample \(300\)"):
         ctx.padded_batching(None, np.array([100, 300, 5], dtype=np.int64), 100, "sorted")
+
+
+# ---- reader: hbp_plan_from_json (io.cpp:112-160) ---------------------------
+
+PLAN_KEYS = ["iter_group", "iter_dev_offsets", "dev_index", "dev_pack_offsets", "pack_capacity", "pack_total",
+             "pack_attention", "pack_member_offsets"]
+
+
+@pytest.mark.parametrize("name", ["c1_20k", "neg_ids_5k", "tiny_spill"])
+def test_plan_from_json_round_trip(ctx, oracle, reference, name):
+    ids, L, groups, kw = next((i, l, g, k) for n, i, l, g, k in cases(oracle) if n == name)
+    plan = ctx.build_plan(ids, L, groups, l_best=groups[0][0], **kw)
+    text = plan.to_json(ids, L)
+    back, rid, rlen = ctx.plan_from_json(text)
+    a, b = plan.flat(), back.flat()
+    for k in PLAN_KEYS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    full_ids = np.arange(len(L)) if ids is None else ids
+    assert np.array_equal(rid, full_ids[a.member_index]) and np.array_equal(rlen, L[a.member_index])
+    assert back.to_json(rid, rlen) == text  # save / load / save is bit-exact (test_io.cpp:33-53)
+    want = reference.plan_from_json(text)
+    for k in PLAN_KEYS:
+        assert np.array_equal(getattr(b, k), getattr(want, k)), k
+    assert np.array_equal(rid, want.member_id) and np.array_equal(rlen, want.member_length)
+
+
+def test_plan_from_json_curriculum_phases(ctx, oracle, reference):
+    L = np.maximum(oracle.synth(20_000, "lognormal:8.5:1.4", 0.0, "", 131072, 42), 128)
+    plan = ctx.build_plan(None, L, C1_GROUPS, l_best=8192, device_count=8, seed=7).curriculum_order(50, 1)
+    text = plan.to_json(None, L)
+    assert b'"warmup"' in text
+    back, rid, rlen = ctx.plan_from_json(text)
+    assert back.to_json(rid, rlen) == text
+
+
+def _err(fn):
+    try:
+        fn()
+    except (abi.ValidationError, Exception) as e:  # noqa: BLE001
+        return type(e).__name__, str(e)
+    return None
+
+
+def test_plan_from_json_errors(ctx, oracle, reference):
+    L = np.array([100, 200, 300, 16000, 40000, 5, 7, 9000], dtype=np.int64)
+    text = ctx.build_plan(None, L, [(16384, 1, 0), (65536, 2, 4)], l_best=16384, device_count=3, seed=11).to_json(None, L)
+    edits = [
+        text.replace(b'"version": 1', b'"version": 2'),                       # unsupported version
+        text.replace(b'"group": 1', b'"group": 5', 1),                        # group index out of range
+        re.sub(rb'"capacity": \d+', b'"capacity": 1', text, count=1),      # pack exceeds capacity
+        text.replace(b'"sp": 1', b'"sp": 0', 1),                              # groups validate
+        text[: len(text) // 2],                                               # not JSON
+        b"not json",
+    ]
+    for t in edits:
+        assert t != text
+        got = _err(lambda: ctx.plan_from_json(t))
+        want = _err(lambda: reference.plan_from_json(t))
+        assert got is not None and want is not None
+        assert got[1] == want[1], (got, want)
+    # valid JSON in another layout: the reference reads it (or rejects "{}"),
+    # this reader refuses it as a validation error
+    for t in (b"{}", json.dumps(json.loads(text)).encode()):
+        got = _err(lambda: ctx.plan_from_json(t))
+        assert got is not None and got[0] == "ValidationError"

@@ -366,6 +366,11 @@ int hbp_schedule_csv(hbp_ctx* ctx, hbp_plan* plan, char* out, int64_t capacity, 
  * "... iteration group index out of range", "... pack exceeds its
  * capacity"), first in its order. */
 int hbp_plan_from_json(hbp_ctx* ctx, const char* text, int64_t bytes, hbp_plan** out, int64_t* out_n_members);
+/* A device plan from a host view (all arrays host memory, member_index
+ * required, iter_phase may be NULL): for plans built on the host side of a
+ * caller (e.g. the C++ façade's hbp::Plan) that then use hbp_plan_to_json,
+ * hbp_report_plan, hbp_simulate_plan, ... */
+int hbp_plan_upload(hbp_ctx* ctx, const hbp_plan_view* view, hbp_plan** out);
 /* ids[n_members], lengths[n_members] (host) of a plan read by
  * hbp_plan_from_json: sample k of the plan view is (ids[k], lengths[k]). */
 int hbp_plan_members(hbp_ctx* ctx, hbp_plan* plan, int64_t* ids, int64_t* lengths);

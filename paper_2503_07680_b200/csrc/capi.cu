@@ -298,6 +298,47 @@ int hbp_plan_from_json(hbp_ctx* ctx, const char* text, int64_t bytes, hbp_plan**
     });
 }
 
+int hbp_plan_upload(hbp_ctx* ctx, const hbp_plan_view* v, hbp_plan** out) {
+    return guarded(ctx, [&] {
+        *out = nullptr;
+        if (v == nullptr) fail_validation("null plan view");
+        auto* p = new_plan(ctx);
+        try {
+            DevicePlan& d = p->dp;
+            cudaStream_t s = ctx->stream;
+            d.device_count = v->device_count;
+            d.seed = v->seed;
+            d.groups.assign(v->groups.groups, v->groups.groups + v->groups.count);
+            d.l_best = v->groups.l_best;
+            d.l_max = v->groups.l_max;
+            d.n_iterations = v->n_iterations;
+            d.n_devices = v->n_devices;
+            d.n_packs = v->n_packs;
+            d.n_members = v->n_members;
+            auto up = [&](auto& buf, const auto* src, int64_t n) {
+                buf.alloc(static_cast<size_t>(n) + 1, s);
+                if (n > 0 && src)
+                    CUDA_CHECK(cudaMemcpyAsync(buf.p, src, sizeof(*src) * static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+            };
+            up(d.iter_group, v->iter_group, d.n_iterations);
+            up(d.iter_dev_offsets, v->iter_dev_offsets, d.n_iterations + 1);
+            up(d.dev_index, v->dev_index, d.n_devices);
+            up(d.dev_pack_offsets, v->dev_pack_offsets, d.n_devices + 1);
+            up(d.pack_capacity, v->pack_capacity, d.n_packs);
+            up(d.pack_total, v->pack_total, d.n_packs);
+            up(d.pack_attention, v->pack_attention, d.n_packs);
+            up(d.pack_member_offsets, v->pack_member_offsets, d.n_packs + 1);
+            up(d.member_index, v->member_index, d.n_members);
+            if (v->iter_phase) up(d.iter_phase, v->iter_phase, d.n_iterations);
+            CUDA_CHECK(cudaStreamSynchronize(s));
+        } catch (...) {
+            delete_plan(p);
+            throw;
+        }
+        *out = p;
+    });
+}
+
 int hbp_plan_members(hbp_ctx* ctx, hbp_plan* plan, int64_t* ids, int64_t* lengths) {
     return guarded(ctx, [&] {
         if (plan == nullptr) fail_validation("null plan");

@@ -15,6 +15,7 @@
 #include "hbp/balance.hpp"
 #include "hbp/costmodel.hpp"
 #include "hbp/ingest.hpp"
+#include "hbp/io.hpp"
 #include "hbp/metrics.hpp"
 #include "hbp/packing.hpp"
 #include "hbp/rng.hpp"
@@ -135,6 +136,26 @@ int main() {
             CHECK(r.packs.size() == 4);
             for (const auto& p : r.packs) CHECK(p.total == 4 && p.samples.size() == 1);
         }
+    }
+    // ---- plan manifest (test_io.cpp:33-71) ----
+    {
+        SampleSet set;
+        set.source = "io";
+        for (int i = 0; i < 400; ++i) set.samples.push_back(Sample{i, 100 + (i * 7919) % 60000});
+        PlanOptions o;
+        o.device_count = 4;
+        o.seed = 3;
+        const Plan plan = build_plan(set, two_level(), o);
+        const std::string text = plan_to_json(plan);
+        const Plan parsed = plan_from_json(text);
+        CHECK(plan_to_json(parsed) == text);  // :33-53 bit-exact round trip
+        CHECK(parsed.iterations.size() == plan.iterations.size() && parsed.device_count == 4 && parsed.seed == 3);
+        EXPECT_THROW(ValidationError, plan_from_json("{}"), "plan manifest");           // :55-59
+        EXPECT_THROW(ValidationError, plan_from_json("not json"), "bad plan manifest");
+        std::string bad = text;
+        const auto k = bad.find("\"capacity\": ");
+        bad.replace(k, bad.find(',', k) - k, "\"capacity\": 1");
+        EXPECT_THROW(ValidationError, plan_from_json(bad), "pack exceeds its capacity");  // :61-71
     }
     // ---- ingest (test_ingest.cpp:12-86) ----
     {

@@ -104,3 +104,24 @@ def test_python_load_lengths(hbp, tmp_path):
         hbp.load_lengths(str(tmp_path / "missing.txt"), "raw")
     with pytest.raises(ValueError, match="unknown corpus format: xml"):
         hbp.load_lengths(str(r), "xml")
+
+
+def test_python_plan_manifest(hbp, tmp_path):
+    # Plan.to_json / Plan.from_json / write_plan / read_plan (py_hbp.cpp:300-305, 423-424)
+    L = [100, 200, 300, 16000, 40000, 5, 7, 9000] * 50
+    plan = hbp.build_plan(hbp.SampleSet(L), groups_obj(hbp, [(16384, 1, 0), (65536, 2, 4)], 16384), device_count=3,
+                          seed=11)
+    text = plan.to_json()
+    back = hbp.Plan.from_json(text)
+    assert back.to_json() == text and len(back.iterations) == len(plan.iterations)
+    assert [[[s.id for p in d.packs for s in p.samples] for d in it.devices] for it in back.iterations] == \
+        [[[s.id for p in d.packs for s in p.samples] for d in it.devices] for it in plan.iterations]
+    assert hbp.report(back).abr == hbp.report(plan).abr
+    path = tmp_path / "plan.json"
+    hbp.write_plan(plan, str(path))
+    assert path.read_bytes() == text.encode()
+    assert hbp.read_plan(str(path)).to_json() == text
+    with pytest.raises(OSError, match="cannot open file"):
+        hbp.read_plan(str(tmp_path / "missing.json"))
+    with pytest.raises(ValueError, match="bad plan manifest"):
+        hbp.Plan.from_json("not json")

@@ -31,3 +31,14 @@ for k in k_fy_lists k_radix_scatter k_nf_emit; do
       -o "$OUT/${TAG}_$k" -f $STEP > /dev/null 2>&1
   echo "$k capture: $?"
 done
+# corpus parse + plan reader
+ING="python tools/profile_ingest.py"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file "$OUT/${TAG}_launches_ingest.csv" $ING > /dev/null 2>&1
+echo "ingest launch list: $?"
+ncu --set full --clock-control none --import-source on -k regex:k_parse_jsonl -c 1 \
+    -o "$OUT/${TAG}_k_parse_jsonl" -f $ING > /dev/null 2>&1
+echo "k_parse_jsonl capture: $?"
+ncu --set full --clock-control none --import-source on -k regex:k_plan_lines -c 1 \
+    -o "$OUT/${TAG}_k_plan_lines" -f $ING > /dev/null 2>&1
+echo "k_plan_lines capture: $?"

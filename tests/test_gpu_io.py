@@ -181,3 +181,30 @@ def test_plan_from_json_errors(ctx, oracle, reference):
     for t in (b"{}", json.dumps(json.loads(text)).encode()):
         got = _err(lambda: ctx.plan_from_json(t))
         assert got is not None and got[0] == "ValidationError"
+
+
+@pytest.mark.parametrize("n,devices,seed", [(1, 8, 0), (3, 16, 1), (17, 5, 2), (64, 3, 3), (500, 7, 4)])
+def test_plan_from_json_edge_plans(ctx, oracle, reference, n, devices, seed):
+    # tiny corpora: spill tails, idle devices ("[]"), single-pack iterations
+    rng = np.random.default_rng(seed)
+    L = rng.integers(1, 131073, size=n).astype(np.int64)
+    plan = ctx.build_plan(None, L, TWO_LEVEL, l_best=16384, device_count=devices, seed=seed)
+    text = plan.to_json(None, L)
+    back, rid, rlen = ctx.plan_from_json(text)
+    assert back.to_json(rid, rlen) == text
+    want = reference.plan_from_json(text)
+    b = back.flat()
+    for k in PLAN_KEYS:
+        assert np.array_equal(getattr(b, k), getattr(want, k)), k
+    assert np.array_equal(rid, want.member_id) and np.array_equal(rlen, want.member_length)
+
+
+@pytest.mark.parametrize("mode", ["sorted", "random"])
+def test_plan_from_json_batching_plan(ctx, oracle, reference, mode):
+    L = oracle.synth(3_000, "lognormal:7.2:0.7", 0.05, "uniform:16385:131072", 131072, 9)
+    plan = ctx.build_batching_plan(None, L, (131072, 8, 27), 4, mode, 7)
+    text = plan.to_json(None, L)
+    back, rid, rlen = ctx.plan_from_json(text)
+    assert back.to_json(rid, rlen) == text
+    want = reference.plan_from_json(text)
+    assert np.array_equal(back.flat().pack_member_offsets, want.pack_member_offsets)

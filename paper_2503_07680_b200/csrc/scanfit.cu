@@ -230,20 +230,37 @@ __global__ void __launch_bounds__(32, 1)
                 }
                 if (lane == idx) top = nv;
             } else {
-                leaf = P++;
-                const u32 nv = cap - s;
-                u32 idx = leaf;
-                if (lane == 0) {
+                // No open pack fits: this item and the rest of its run of
+                // equal lengths in the batch open new packs of k = cap / s
+                // items each -- a new pack is the unique emptiest until it
+                // holds k (every older pack is below s) -- placed at once.
+                const u32 same = __ballot_sync(kFull, mylen == s && lane >= static_cast<u32>(j) &&
+                                                          lane < static_cast<u32>(cnt_c)) >> j;
+                const u32 c = ~same == 0u ? 32u : static_cast<u32>(__ffs(~same) - 1);
+                const u32 k = cap / s;
+                const u32 npk = (c + k - 1) / k;
+                if (lane < npk) {
+                    const u32 take = min(k, c - lane * k);
+                    const u32 v = cap - take * s;
+                    u32 idx = P + lane;
 #pragma unroll
                     for (int h = 0; h < kTreeMaxLevels; ++h) {
                         if (h < T.H) {
-                            if (L[h][idx] < nv) L[h][idx] = nv;
+                            atomicMax(L[h] + idx, v);
                             idx >>= 5;
                         }
                     }
+                    atomicAdd(cnt + P + lane, take);
                 }
-                idx = leaf >> (5 * T.H);
-                if (lane == idx && top < nv) top = nv;
+                for (u32 q = 0; q < npk; ++q) {
+                    const u32 v = cap - min(k, c - q * k) * s;
+                    if (lane == ((P + q) >> (5 * T.H)) && top < v) top = v;
+                }
+                if (lane >= static_cast<u32>(j) && lane < static_cast<u32>(j) + c) mybin = P + (lane - j) / k;
+                P += npk;
+                j += static_cast<int>(c) - 1;
+                __syncwarp();
+                continue;
             }
             __syncwarp();
             if (lane == 0) atomicAdd(cnt + leaf, 1u);

@@ -198,6 +198,10 @@ __global__ void __launch_bounds__(32, 1)
     __syncwarp();
     u32 top = 0u;  // register level: entry `lane`
     u32 P = 0;
+    // Levels in use: the register level covers 32^(hA+1) packs; it is pushed
+    // down into memory level hA when the packs outgrow it, so an item pays
+    // for log32 of the packs open, not of the most there could be.
+    int hA = 0;
     for (i64 base = 0; base < n; base += 32) {
         const int cnt_c = static_cast<int>(n - base < 32 ? n - base : 32);
         const u32 mylen = static_cast<int>(lane) < cnt_c ? entry_len(items[base + lane]) : 0u;
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(32, 1)
                 u32 v[kTreeMaxLevels];
 #pragma unroll
                 for (int h = kTreeMaxLevels - 1; h >= 0; --h) {
-                    if (h < T.H) {
+                    if (h < hA) {
                         v[h] = L[h][node * 32 + lane];
                         node = node * 32 + (__ffs(__ballot_sync(kFull, v[h] == M)) - 1);
                     }
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(32, 1)
                 u32 nv = M - s, idx = leaf;
 #pragma unroll
                 for (int h = 0; h < kTreeMaxLevels; ++h) {
-                    if (h < T.H) {
+                    if (h < hA) {
                         const u32 c = idx & 31u;
                         const u32 x = lane == c ? nv : v[h];
                         if (lane == c) L[h][idx] = nv;
@@ -239,13 +243,22 @@ __global__ void __launch_bounds__(32, 1)
                 const u32 c = ~same == 0u ? 32u : static_cast<u32>(__ffs(~same) - 1);
                 const u32 k = cap / s;
                 const u32 npk = (c + k - 1) / k;
+                while (((P + npk - 1) >> (5 * hA)) >= 32u) {
+#pragma unroll
+                    for (int h = 0; h < kTreeMaxLevels; ++h)
+                        if (h == hA) L[h][lane] = top;
+                    const u32 mx = __reduce_max_sync(kFull, top);
+                    top = lane == 0 ? mx : 0u;
+                    ++hA;
+                    __syncwarp();
+                }
                 if (lane < npk) {
                     const u32 take = min(k, c - lane * k);
                     const u32 v = cap - take * s;
                     u32 idx = P + lane;
 #pragma unroll
                     for (int h = 0; h < kTreeMaxLevels; ++h) {
-                        if (h < T.H) {
+                        if (h < hA) {
                             atomicMax(L[h] + idx, v);
                             idx >>= 5;
                         }
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(32, 1)
                 }
                 for (u32 q = 0; q < npk; ++q) {
                     const u32 v = cap - min(k, c - q * k) * s;
-                    if (lane == ((P + q) >> (5 * T.H)) && top < v) top = v;
+                    if (lane == ((P + q) >> (5 * hA)) && top < v) top = v;
                 }
                 if (lane >= static_cast<u32>(j) && lane < static_cast<u32>(j) + c) mybin = P + (lane - j) / k;
                 P += npk;
@@ -269,6 +282,10 @@ __global__ void __launch_bounds__(32, 1)
         if (static_cast<int>(lane) < cnt_c) bin_out[base + lane] = mybin;
     }
     // residuals of the bins: the leaf level (or the register level)
+    if (hA == 0 && T.H > 0) {
+        L[0][lane] = top;
+        __syncwarp();
+    }
     if (T.H == 0) {
         if (lane < P) res[lane] = top;
     } else if (!T.g[0]) {

@@ -392,10 +392,10 @@ class Context:
                                               C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int64)]
         ids = None
         if device_out is None:
-            out = np.zeros(max(cap, 1), dtype=np.int64)
+            out = np.empty(max(cap, 1), dtype=np.int64)  # written up to the count; no fill
             dst, mem = out.ctypes.data, 0
             if with_ids:
-                ids = np.zeros(max(cap, 1), dtype=np.int64)
+                ids = np.empty(max(cap, 1), dtype=np.int64)
         else:
             dst, mem = device_out.data_ptr(), 1
         self.check(self.lib.hbp_load_lengths(self.h, text, C.c_int64(len(text)), C.c_int32(self.CORPUS_FORMATS[fmt]),

@@ -212,10 +212,15 @@ int hbp_load_lengths(hbp_ctx* ctx, const char* text, int64_t bytes, int32_t form
             parse_corpus_text(*ctx, text, static_cast<u64>(bytes), format, source ? source : "", lens, ids);
         if (n > capacity)
             fail_validation("output capacity " + std::to_string(capacity) + " < " + std::to_string(n) + " samples");
-        const cudaMemcpyKind kind = out_memory == HBP_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-        CUDA_CHECK(cudaMemcpyAsync(out_lengths, lens.p, sizeof(int64_t) * n, kind, ctx->stream));
-        if (out_ids) CUDA_CHECK(cudaMemcpyAsync(out_ids, ids.p, sizeof(int64_t) * n, kind, ctx->stream));
-        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (out_memory == HBP_MEM_DEVICE) {
+            CUDA_CHECK(cudaMemcpyAsync(out_lengths, lens.p, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            if (out_ids)
+                CUDA_CHECK(cudaMemcpyAsync(out_ids, ids.p, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } else {
+            staged_copy(*ctx, out_lengths, lens.p, sizeof(int64_t) * static_cast<size_t>(n), false);
+            if (out_ids) staged_copy(*ctx, out_ids, ids.p, sizeof(int64_t) * static_cast<size_t>(n), false);
+        }
         *out_count = n;
     });
 }
@@ -344,10 +349,8 @@ int hbp_plan_members(hbp_ctx* ctx, hbp_plan* plan, int64_t* ids, int64_t* length
         if (plan == nullptr) fail_validation("null plan");
         if (!plan->read_ids.p) fail_validation("plan_members: the plan was not read from a manifest");
         const size_t m = static_cast<size_t>(plan->dp.n_members);
-        CUDA_CHECK(cudaMemcpyAsync(ids, plan->read_ids.p, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_CHECK(cudaMemcpyAsync(lengths, plan->read_lens.p, sizeof(int64_t) * m, cudaMemcpyDeviceToHost,
-                                   ctx->stream));
-        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        staged_copy(*ctx, ids, plan->read_ids.p, sizeof(int64_t) * m, false);
+        staged_copy(*ctx, lengths, plan->read_lens.p, sizeof(int64_t) * m, false);
     });
 }
 

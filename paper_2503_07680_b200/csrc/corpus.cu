@@ -492,8 +492,8 @@ std::vector<std::string> split_csv(const std::string& line) {
 void upload_text(Ctx& c, const char* text, u64 bytes, DevBuf<unsigned char>& t) {
     const u64 chunks = (bytes + kChunkBytes - 1) / kChunkBytes;
     t.alloc(chunks * kChunkBytes + kChunkBytes, c.stream);
-    if (bytes) CUDA_CHECK(cudaMemcpyAsync(t.p, text, bytes, cudaMemcpyHostToDevice, c.stream));
     CUDA_CHECK(cudaMemsetAsync(t.p + bytes, 0, t.n - bytes, c.stream));
+    staged_copy(c, t.p, text, bytes, true);
 }
 
 u64 text_line_starts(Ctx& c, const unsigned char* t, u64 bytes, DevBuf<u64>& starts) {

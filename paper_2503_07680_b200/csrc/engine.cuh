@@ -92,6 +92,54 @@ T read_scalar(Ctx& c, const T* dptr) {
     return *reinterpret_cast<T*>(c.pinned.p);
 }
 
+// Host <-> device copies of pageable host memory through two pinned blocks
+// of the context's pool: chunk k + 1 crosses PCIe while chunk k is copied on
+// the host. Synchronous on return.
+inline void staged_copy(Ctx& c, void* dst, const void* src, size_t n, bool to_device) {
+    if (n == 0) return;
+    constexpr size_t kChunk = size_t(32) << 20;
+    if (n <= kChunk / 8) {  // small: one pageable copy
+        CUDA_CHECK(cudaMemcpyAsync(dst, src, n, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, c.stream));
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        return;
+    }
+    HostBlock stage[2] = {c.host_pool.acquire(std::min(kChunk, n)), c.host_pool.acquire(std::min(kChunk, n))};
+    cudaEvent_t done[2];
+    CUDA_CHECK(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    const size_t chunks = (n + kChunk - 1) / kChunk;
+    auto* d = static_cast<char*>(dst);
+    const auto* h = static_cast<const char*>(src);
+    auto len = [&](size_t k) { return std::min(kChunk, n - k * kChunk); };
+    if (to_device) {
+        for (size_t k = 0; k < chunks; ++k) {
+            if (k >= 2) CUDA_CHECK(cudaEventSynchronize(done[k & 1]));  // block k - 2 has crossed
+            std::memcpy(stage[k & 1].p, h + k * kChunk, len(k));
+            CUDA_CHECK(cudaMemcpyAsync(d + k * kChunk, stage[k & 1].p, len(k), cudaMemcpyHostToDevice, c.stream));
+            CUDA_CHECK(cudaEventRecord(done[k & 1], c.stream));
+        }
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    } else {
+        auto issue = [&](size_t k) {
+            CUDA_CHECK(cudaMemcpyAsync(stage[k & 1].p, d + k * kChunk, len(k), cudaMemcpyDeviceToHost, c.stream));
+            CUDA_CHECK(cudaEventRecord(done[k & 1], c.stream));
+        };
+        auto* out = static_cast<char*>(dst);
+        const auto* dev = static_cast<const char*>(src);
+        d = const_cast<char*>(dev);
+        issue(0);
+        for (size_t k = 0; k < chunks; ++k) {
+            if (k + 1 < chunks) issue(k + 1);
+            CUDA_CHECK(cudaEventSynchronize(done[k & 1]));
+            std::memcpy(out + k * kChunk, stage[k & 1].p, len(k));
+        }
+    }
+    CUDA_CHECK(cudaEventDestroy(done[0]));
+    CUDA_CHECK(cudaEventDestroy(done[1]));
+    c.host_pool.release(stage[0]);
+    c.host_pool.release(stage[1]);
+}
+
 template <typename T>
 std::vector<T> read_vector(Ctx& c, const T* dptr, size_t n) {
     // through the context's pinned staging buffer: a copy into pageable

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <fstream>
 #include <iterator>
+#include <memory>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -25,10 +26,12 @@ SampleSet load_lengths(std::istream& in, CorpusFormat format, const std::string&
     const int32_t f = format == CorpusFormat::Jsonl ? HBP_CORPUS_JSONL
                       : format == CorpusFormat::Csv ? HBP_CORPUS_CSV : HBP_CORPUS_RAW;
     const int64_t cap = static_cast<int64_t>(text.size() / 2 + 1);
-    std::vector<int64_t> ids(static_cast<size_t>(cap)), lengths(static_cast<size_t>(cap));
+    // up to (bytes + 1) / 2 records; left uninitialised, the engine writes the first n
+    std::unique_ptr<int64_t[]> ids(new int64_t[static_cast<size_t>(cap)]);
+    std::unique_ptr<int64_t[]> lengths(new int64_t[static_cast<size_t>(cap)]);
     int64_t n = 0;
     detail::check(hbp_load_lengths(detail::ctx(), text.data(), static_cast<int64_t>(text.size()), f,
-                                   source_name.c_str(), ids.data(), lengths.data(), cap, HBP_MEM_HOST, &n));
+                                   source_name.c_str(), ids.get(), lengths.get(), cap, HBP_MEM_HOST, &n));
     SampleSet set;
     set.source = source_name;
     set.samples.resize(static_cast<size_t>(n));

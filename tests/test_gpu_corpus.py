@@ -130,3 +130,19 @@ def test_jsonl_fuzz(ctx, reference):
         text = bytes(line).replace(b"\n", b" ") + b"\n"
         got, want = _both(ctx, reference, text, "jsonl")
         assert got == want, text
+
+
+def test_golden_fixtures(ctx):
+    # the committed outputs of the reference (tests/golden/make_ingest_golden.py)
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ingest_golden.json")))
+    for g in gold:
+        text = g["text"].encode("latin-1")
+        try:
+            ids, lens = ctx.load_lengths(text, g["format"], "corpus.txt", with_ids=True)
+            got = {"ids": ids.tolist(), "lengths": lens.tolist()}
+        except abi.ValidationError as e:
+            got = {"error": str(e)}
+        want = {k: g[k] for k in ("ids", "lengths", "error") if k in g}
+        assert got == want, g["text"]

@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(RB) k_radix_hist(const u32* __restrict__ keys,
         const u32 d = valid ? digit_of(keys[i], shift, desc) : 0u;
         const unsigned peers = digit_peers(d, valid);
         if (valid && (peers & ((1u << lane) - 1u)) == 0) h[w][d] += __popc(peers);  // one leader per digit
+        __syncwarp();  // the next item's leader of the same digit may be another lane
     }
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += RB) {

@@ -515,6 +515,10 @@ def roofline(stages, peak, peak_kind):
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
             "algorithmic_bytes_per_launch": v["bytes"] / max(v["launches"], 1),
             "launches": v["launches"], "ms": v["ms"], "share_of_kernel_time": v["ms"] / total_ms,
+            "families": {kk: {"ms": round(vv["ms"], 4), "launches": vv["launches"],
+                              "achieved_gbs": round(vv["bytes"] / (vv["ms"] / 1000.0) / 1e9, 1),
+                              "frac": round(vv["bytes"] / (vv["ms"] / 1000.0) / 1e9 / peak, 4)}
+                         for kk, vv in sorted(cands.items(), key=lambda kv: -kv[1]["ms"])[:8]},
             "step_top_kernel": {"kernel": top_k, "ms": top_v["ms"], "share_of_kernel_time": top_v["ms"] / total_ms,
                                 "bound": "latency (first-fit dependency chain across resident warps)"
                                 if top_k.startswith("fit.chain") else "hbm"}}

@@ -328,8 +328,57 @@ __device__ u64 json_number(const unsigned char* t, u64 p, u64 e, bool& is_int, i
     return p;
 }
 
+// Fast path for the common record shapes, {"id":N,"length":M} and
+// {"length":M} (a space allowed after ':' and ',', as json.dumps writes
+// them; JSON whitespace after the closing brace): a few uniform byte tests
+// instead of the grammar walk, so a warp of such lines does not diverge.
+// Anything else -- and numbers of more than 18 digits -- goes to the full
+// walk, which gives the same result for these shapes.
+__device__ __forceinline__ bool fast_int(const unsigned char* t, u64& p, u64 e, i64& v) {
+    const bool neg = p < e && t[p] == '-';
+    if (neg) ++p;
+    if (p >= e || t[p] < '0' || t[p] > '9') return false;
+    const u64 d0 = p;
+    i64 x = 0;
+    while (p < e && t[p] >= '0' && t[p] <= '9') x = x * 10 + (t[p++] - '0');
+    const u64 nd = p - d0;
+    if (nd > 18 || (nd > 1 && t[d0] == '0')) return false;
+    if (p < e && (t[p] == '.' || t[p] == 'e' || t[p] == 'E')) return false;
+    v = neg ? -x : x;
+    return true;
+}
+
+__device__ __forceinline__ bool fast_lit(const unsigned char* t, u64& p, u64 e, const char* s) {
+    for (int k = 0; s[k]; ++k, ++p)
+        if (p >= e || t[p] != static_cast<unsigned char>(s[k])) return false;
+    if (p < e && t[p] == ' ') ++p;
+    return true;
+}
+
+__device__ __forceinline__ bool json_fast(const unsigned char* t, u64 a, u64 e, JsonLine& r) {
+    u64 p = a;
+    if (p >= e || t[p] != '{') return false;
+    ++p;
+    i64 id = 0, len = 0;
+    bool has_id = false;
+    if (p + 1 < e && t[p + 1] == 'i') {
+        if (!fast_lit(t, p, e, "\"id\":") || !fast_int(t, p, e, id) || !fast_lit(t, p, e, ",")) return false;
+        has_id = true;
+    }
+    if (!fast_lit(t, p, e, "\"length\":") || !fast_int(t, p, e, len) || p >= e || t[p] != '}') return false;
+    for (++p; p < e; ++p)
+        if (!json_ws(t[p])) return false;
+    r.blank = false;
+    r.has_id = has_id;
+    r.id = id;
+    r.length = len;
+    r.status = len < 1 ? kJNonPositive : kJOk;
+    return true;
+}
+
 __device__ JsonLine parse_json_line(const unsigned char* __restrict__ t, u64 a, u64 e) {
     JsonLine r{kJOk, true, false, 0, 0};
+    if (json_fast(t, a, e, r)) return r;
     for (u64 p = a; p < e; ++p)
         if (!trim_char(t[p])) {
             r.blank = false;

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "engine_ctx.hpp"
+#include "plan_handle.hpp"
 #include "hbp/io.hpp"
 #include "hbp_b200.h"
 
@@ -37,12 +38,15 @@ void write_text(const std::filesystem::path& path, const std::string& content) {
 
 }  // namespace
 
-std::string plan_to_json(const Plan& plan) {
+namespace detail {
+
+UploadedPlan upload_plan(const Plan& plan) {
+    UploadedPlan u;
     std::vector<hbp_group_config> groups;
     for (const auto& g : plan.groups.groups) groups.push_back(hbp_group_config{g.length, g.config.sp, g.config.ckpt});
     std::vector<int32_t> iter_group, dev_index, member_index;
     std::vector<int8_t> phase;
-    std::vector<int64_t> iter_dev{0}, dev_pack{0}, cap, tot, att, moff{0}, ids, lens;
+    std::vector<int64_t> iter_dev{0}, dev_pack{0}, cap, tot, att, moff{0};
     for (const auto& it : plan.iterations) {
         iter_group.push_back(it.group_index);
         phase.push_back(it.phase == Phase::Warmup ? 1 : 0);
@@ -53,11 +57,11 @@ std::string plan_to_json(const Plan& plan) {
                 tot.push_back(p.total);
                 att.push_back(p.attention);
                 for (const auto& s : p.samples) {
-                    member_index.push_back(static_cast<int32_t>(ids.size()));
-                    ids.push_back(s.id);
-                    lens.push_back(s.length);
+                    member_index.push_back(static_cast<int32_t>(u.ids.size()));
+                    u.ids.push_back(s.id);
+                    u.lens.push_back(s.length);
                 }
-                moff.push_back(static_cast<int64_t>(ids.size()));
+                moff.push_back(static_cast<int64_t>(u.ids.size()));
             }
             dev_pack.push_back(static_cast<int64_t>(cap.size()));
         }
@@ -70,7 +74,7 @@ std::string plan_to_json(const Plan& plan) {
     v.n_iterations = static_cast<int64_t>(iter_group.size());
     v.n_devices = static_cast<int64_t>(dev_index.size());
     v.n_packs = static_cast<int64_t>(cap.size());
-    v.n_members = static_cast<int64_t>(ids.size());
+    v.n_members = static_cast<int64_t>(u.ids.size());
     v.iter_group = iter_group.data();
     v.iter_dev_offsets = iter_dev.data();
     v.dev_index = dev_index.data();
@@ -81,24 +85,13 @@ std::string plan_to_json(const Plan& plan) {
     v.pack_member_offsets = moff.data();
     v.member_index = member_index.data();
     v.iter_phase = phase.data();
-    Handle h;
-    detail::check(hbp_plan_upload(detail::ctx(), &v, &h.p));
-    const hbp_samples smp{ids.data(), lens.data(), static_cast<int64_t>(ids.size()), HBP_MEM_HOST, "plan"};
-    int64_t n = 0;
-    detail::check(hbp_plan_to_json(detail::ctx(), h.p, &smp, nullptr, 0, &n));
-    std::string text(static_cast<size_t>(n), '\0');
-    detail::check(hbp_plan_to_json(detail::ctx(), h.p, &smp, text.data(), n, &n));
-    return text;
+    check(hbp_plan_upload(ctx(), &v, &u.h));
+    return u;
 }
 
-Plan plan_from_json(const std::string& text) {
-    Handle h;
-    int64_t m = 0;
-    detail::check(hbp_plan_from_json(detail::ctx(), text.data(), static_cast<int64_t>(text.size()), &h.p, &m));
-    std::vector<int64_t> ids(static_cast<size_t>(m) + 1), lens(static_cast<size_t>(m) + 1);
-    detail::check(hbp_plan_members(detail::ctx(), h.p, ids.data(), lens.data()));
+Plan plan_of_handle(hbp_plan* h, const std::vector<int64_t>& ids, const std::vector<int64_t>& lens) {
     hbp_plan_view v{};
-    detail::check(hbp_plan_view_get(detail::ctx(), h.p, &v));
+    check(hbp_plan_view_get(ctx(), h, &v));
     Plan plan;
     for (int32_t k = 0; k < v.groups.count; ++k) {
         const auto& g = v.groups.groups[k];
@@ -118,14 +111,37 @@ Plan plan_from_json(const std::string& text) {
             std::vector<Pack> packs;
             for (int64_t q = v.dev_pack_offsets[d]; q < v.dev_pack_offsets[d + 1]; ++q) {
                 Pack p = Pack::make(v.pack_capacity[q]);
-                for (int64_t k = v.pack_member_offsets[q]; k < v.pack_member_offsets[q + 1]; ++k)
-                    p.add(Sample{ids[static_cast<size_t>(v.member_index[k])], lens[static_cast<size_t>(v.member_index[k])]});
+                for (int64_t k = v.pack_member_offsets[q]; k < v.pack_member_offsets[q + 1]; ++k) {
+                    const auto m = static_cast<size_t>(v.member_index[k]);
+                    p.add(Sample{ids[m], lens[m]});
+                }
                 packs.push_back(std::move(p));
             }
             it.devices.push_back(DeviceBatch::build(v.dev_index[d], std::move(packs), sp));
         }
     }
     return plan;
+}
+
+}  // namespace detail
+
+std::string plan_to_json(const Plan& plan) {
+    const detail::UploadedPlan u = detail::upload_plan(plan);
+    const hbp_samples smp{u.ids.data(), u.lens.data(), static_cast<int64_t>(u.ids.size()), HBP_MEM_HOST, "plan"};
+    int64_t n = 0;
+    detail::check(hbp_plan_to_json(detail::ctx(), u.h, &smp, nullptr, 0, &n));
+    std::string text(static_cast<size_t>(n), '\0');
+    detail::check(hbp_plan_to_json(detail::ctx(), u.h, &smp, text.data(), n, &n));
+    return text;
+}
+
+Plan plan_from_json(const std::string& text) {
+    Handle h;
+    int64_t m = 0;
+    detail::check(hbp_plan_from_json(detail::ctx(), text.data(), static_cast<int64_t>(text.size()), &h.p, &m));
+    std::vector<int64_t> ids(static_cast<size_t>(m) + 1), lens(static_cast<size_t>(m) + 1);
+    detail::check(hbp_plan_members(detail::ctx(), h.p, ids.data(), lens.data()));
+    return detail::plan_of_handle(h.p, ids, lens);
 }
 
 void write_plan(const Plan& plan, const std::filesystem::path& path) { write_text(path, plan_to_json(plan)); }

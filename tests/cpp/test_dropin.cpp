@@ -2,6 +2,7 @@
 // through the B200 façade: known answers of the reference's own test suite
 // (proj/tests/*.cpp, cited per case). Built by tests/cpp/Makefile, run by
 // tests/test_gpu_dropin.py on a B200. Exit code = number of failures.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -16,6 +17,7 @@
 #include "hbp/costmodel.hpp"
 #include "hbp/ingest.hpp"
 #include "hbp/io.hpp"
+#include "hbp/schedule.hpp"
 #include "hbp/metrics.hpp"
 #include "hbp/packing.hpp"
 #include "hbp/rng.hpp"
@@ -151,6 +153,14 @@ int main() {
         CHECK(plan_to_json(parsed) == text);  // :33-53 bit-exact round trip
         CHECK(parsed.iterations.size() == plan.iterations.size() && parsed.device_count == 4 && parsed.seed == 3);
         EXPECT_THROW(ValidationError, plan_from_json("{}"), "plan manifest");           // :55-59
+        // schedule (test_schedule.cpp): runtime per iteration and the CSV rows
+        const RuntimeAssignment ra = assign_runtime(plan);
+        CHECK(ra.per_iteration.size() == plan.iterations.size());
+        std::ostringstream csv;
+        write_schedule_csv(plan, csv);
+        const std::string rows = csv.str();
+        CHECK(rows.rfind("iteration,group,sp,ckpt,phase\n", 0) == 0);
+        CHECK(static_cast<size_t>(std::count(rows.begin(), rows.end(), '\n')) == plan.iterations.size() + 1);
         EXPECT_THROW(ValidationError, plan_from_json("not json"), "bad plan manifest");
         std::string bad = text;
         const auto k = bad.find("\"capacity\": ");

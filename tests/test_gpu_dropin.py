@@ -125,3 +125,24 @@ def test_python_plan_manifest(hbp, tmp_path):
         hbp.read_plan(str(tmp_path / "missing.json"))
     with pytest.raises(ValueError, match="bad plan manifest"):
         hbp.Plan.from_json("not json")
+
+
+def test_python_curriculum_and_runtime(hbp, reference):
+    # curriculum_order / assign_runtime (py_hbp.cpp:350-370) through the
+    # facade: same iteration order, phases and switch count as the reference
+    import numpy as np
+    L = np.maximum(reference.synth(20_000, "lognormal:8.5:1.4", 0.0, "", 131072, 42), 128)
+    groups = [(8192, 1, 0), (32768, 4, 0), (131072, 8, 0)]
+    plan = hbp.build_plan(hbp.SampleSet(L.tolist()), groups_obj(hbp, groups, 8192), device_count=8, seed=7)
+    cur = hbp.curriculum_order(plan, hbp.CurriculumSpec(50, 1))
+    assert sum(1 for it in cur.iterations if str(it.phase).endswith("Warmup")) == 50
+    jt, ct, sp, ck, sw = reference.curriculum(None, L, groups, 8192, 50, 1, device_count=8, seed=7)
+    assert cur.to_json().encode() == jt  # same order, phases and packs as the reference
+    per_it, switches = hbp.assign_runtime(cur)
+    assert [rc.sp for rc in per_it] == sp.tolist() and [rc.ckpt for rc in per_it] == ck.tolist() and switches == sw
+    assert len(per_it) == len(cur.iterations)
+    assert all(rc.sp == groups[it.group_index][1] for rc, it in zip(per_it, cur.iterations))
+    changes = sum(1 for a, b in zip(per_it, per_it[1:]) if (a.sp, a.ckpt) != (b.sp, b.ckpt))
+    assert switches == changes
+    with pytest.raises(ValueError):
+        hbp.curriculum_order(plan, hbp.CurriculumSpec(10 ** 6, 1))

@@ -252,3 +252,16 @@ def test_plan_outlives_context(oracle):
     del plan
     want = oracle.build_plan(None, L, TWO_LEVEL, l_best=16384, device_count=4, seed=5)
     assert_same_plan(flat, want)
+
+
+@pytest.mark.parametrize("strategy", ["bfs", "spfhp"])
+def test_scan_fit_c1_group0(ctx, oracle, strategy):
+    # C1's 8K group (64K items): SPFHP's tree outgrows shared memory (leaves
+    # in global memory, upper levels in shared) and grows level by level
+    L = c1_lengths(oracle, 100_000)
+    L = L[L <= 8192]
+    want = oracle.pack(None, L, 8192, strategy, seed=7)
+    got = ctx.pack(None, L, 8192, strategy, seed=7).flat()
+    for k in ("pack_capacity", "pack_total", "pack_attention", "pack_member_offsets"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert np.array_equal(got.members_as_ids(None), want.member_id)

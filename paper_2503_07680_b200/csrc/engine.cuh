@@ -177,6 +177,9 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src, uint64_t draw_b
                          uint64_t* draws_used = nullptr);
 // out[p] = in[src[p]] for 8-byte elements.
 void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m);
+// out = in permuted by the exact Fisher-Yates of `seed` (fy_source_positions
+// + gather in one pass: out[p] = in[src(p)])
+void fy_shuffle_u64(Ctx& c, uint64_t seed, i64 m, const u64* in, u64* out);
 void gather_u32(Ctx& c, const u32* in, const u32* src, u32* out, i64 m);
 
 }  // namespace hbp_b200

@@ -595,7 +595,6 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
     bool residue_ffd = false;
     bool key_ordered = corpus.key32.p == nullptr;  // pool in input order == key order
     if (st.kind == HBP_STRATEGY_ISF || st.kind == HBP_STRATEGY_RANDOM) {
-        DevBuf<u32> src(m, s);
         const int rounds = st.kind == HBP_STRATEGY_ISF ? st.isf_iterations : 1;
         u64 tmin = 0;
         if (st.kind == HBP_STRATEGY_ISF) {
@@ -605,8 +604,7 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         for (int r = 0; r < rounds && cur > 0; ++r) {
             const uint64_t rs = st.kind == HBP_STRATEGY_ISF ? derive_seed(seed, "isf-round", static_cast<uint64_t>(r))
                                                               : derive_seed(seed, "random-pack");
-            fy_source_positions(c, rs, static_cast<i64>(cur), src.p);
-            gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(cur));
+            fy_shuffle_u64(c, rs, static_cast<i64>(cur), A.p, Bf.p);
             trace_mark(c, "isf.shuffle");
             cur = static_cast<u64>(nextfit_freeze(c, Bf.p, static_cast<i64>(cur), cap, tmin, sink, A.p, n_members, n_packs));
             trace_mark(c, "isf.nextfit+freeze");
@@ -617,15 +615,11 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
         residue_ffd = true;
     } else if (st.kind == HBP_STRATEGY_FFS) {
         // first fit over a seeded shuffle (packing.cpp:239-243)
-        DevBuf<u32> src(m, s);
-        fy_source_positions(c, derive_seed(seed, "ffs"), static_cast<i64>(m), src.p);
-        gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(m));
+        fy_shuffle_u64(c, derive_seed(seed, "ffs"), static_cast<i64>(m), A.p, Bf.p);
         CUDA_CHECK(cudaMemcpyAsync(A.p, Bf.p, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
     } else if (st.kind == HBP_STRATEGY_BFS) {
         // best fit over a seeded shuffle (packing.cpp:244-248)
-        DevBuf<u32> src(m, s);
-        fy_source_positions(c, derive_seed(seed, "bfs"), static_cast<i64>(m), src.p);
-        gather_u64(c, A.p, src.p, Bf.p, static_cast<i64>(m));
+        fy_shuffle_u64(c, derive_seed(seed, "bfs"), static_cast<i64>(m), A.p, Bf.p);
         CUDA_CHECK(cudaMemcpyAsync(A.p, Bf.p, sizeof(u64) * m, cudaMemcpyDeviceToDevice, s));
     } else {
         residue_ffd = true;  // SPFHP walks lengths longest first, ids ascending (packing.cpp:135-137)

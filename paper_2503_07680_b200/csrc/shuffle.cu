@@ -135,9 +135,11 @@ __global__ void k_fy_roots(u64 m, const u32* __restrict__ link, u32* __restrict_
     }
 }
 
+// src[p] = the source position of slot p; with `in`, out[p] = in[src[p]]
+// instead (the shuffle applied in the same pass, src not stored).
 __global__ void k_fy_sources(u64 m, const u32* __restrict__ tgt, const u32* __restrict__ nxt,
                              const u32* __restrict__ rootpos, const u32* __restrict__ first0,
-                             u32* __restrict__ src) {
+                             u32* __restrict__ src, const u64* __restrict__ in, u64* __restrict__ out) {
     for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < m;
          p += static_cast<u64>(gridDim.x) * blockDim.x) {
         u32 s;
@@ -149,7 +151,8 @@ __global__ void k_fy_sources(u64 m, const u32* __restrict__ tgt, const u32* __re
             const u32 w = nxt[i];
             s = (w != kNone) ? rootpos[w] : tgt[i];
         }
-        src[p] = s;
+        if (in) out[p] = in[s];
+        else src[p] = s;
     }
 }
 
@@ -163,13 +166,16 @@ __global__ void k_gather(const T* __restrict__ in, const u32* __restrict__ src, 
 
 }  // namespace
 
-void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src, uint64_t draw_base, uint64_t* draws_used) {
+namespace {
+void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* out, uint64_t draw_base,
+            uint64_t* draws_used) {
     if (draws_used) *draws_used = 0;
     if (m_signed <= 0) return;
     const u64 m = static_cast<u64>(m_signed);
     cudaStream_t s = c.stream;
     if (m == 1) {
-        CUDA_CHECK(cudaMemsetAsync(src, 0, sizeof(u32), s));
+        if (in) CUDA_CHECK(cudaMemcpyAsync(out, in, sizeof(u64), cudaMemcpyDeviceToDevice, s));
+        else CUDA_CHECK(cudaMemsetAsync(src, 0, sizeof(u32), s));
         return;
     }
     DevBuf<unsigned long long> used(draws_used ? 1 : 0, s);
@@ -193,8 +199,22 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m_signed, u32* src, uint64_t
     LAUNCH_B("fy.scatter", 20.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, off.p, cnt.p, bucket.p);
     LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);
     LAUNCH_B("fy.roots", 8.0 * m, k_fy_roots, G, B, 0, s, m, link.p, root.p);
-    LAUNCH_B("fy.sources", 16.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, src);
+    if (in)
+        LAUNCH_B("fy.sources_gather", 32.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, nullptr, in,
+                 out);
+    else
+        LAUNCH_B("fy.sources", 16.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, src, nullptr,
+                 nullptr);
     if (draws_used) *draws_used = read_scalar(c, used.p);
+}
+}  // namespace
+
+void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src, uint64_t draw_base, uint64_t* draws_used) {
+    fy_run(c, seed, m, src, nullptr, nullptr, draw_base, draws_used);
+}
+
+void fy_shuffle_u64(Ctx& c, uint64_t seed, i64 m, const u64* in, u64* out) {
+    fy_run(c, seed, m, nullptr, in, out, 0, nullptr);
 }
 
 void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m) {

@@ -122,34 +122,31 @@ __global__ void k_fy_lists(u64 m, const u32* __restrict__ off, u32* __restrict__
     }
 }
 
-__global__ void k_fy_roots(u64 m, const u32* __restrict__ link, u32* __restrict__ rootpos) {
-    for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
-         i += static_cast<u64>(gridDim.x) * blockDim.x) {
-        u32 r = static_cast<u32>(i);
-        u32 l = link[r];
-        while (l != kNone) {
-            r = l;
-            l = link[r];
-        }
-        rootpos[i] = r - 1;
+// src[p] = the source position of slot p; with `in`, out[p] = in[src[p]]
+// instead (the shuffle applied in the same pass, src not stored). A chain is
+// followed to its root here, once per slot that needs it.
+__device__ __forceinline__ u32 chain_root(const u32* __restrict__ link, u32 r) {
+    u32 l = link[r];
+    while (l != kNone) {
+        r = l;
+        l = link[r];
     }
+    return r - 1;
 }
 
-// src[p] = the source position of slot p; with `in`, out[p] = in[src[p]]
-// instead (the shuffle applied in the same pass, src not stored).
 __global__ void k_fy_sources(u64 m, const u32* __restrict__ tgt, const u32* __restrict__ nxt,
-                             const u32* __restrict__ rootpos, const u32* __restrict__ first0,
+                             const u32* __restrict__ link, const u32* __restrict__ first0,
                              u32* __restrict__ src, const u64* __restrict__ in, u64* __restrict__ out) {
     for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < m;
          p += static_cast<u64>(gridDim.x) * blockDim.x) {
         u32 s;
         if (p == 0) {
             const u32 w = *first0;
-            s = (w != kNone) ? rootpos[w] : 0u;
+            s = (w != kNone) ? chain_root(link, w) : 0u;
         } else {
             const u64 i = p + 1;
             const u32 w = nxt[i];
-            s = (w != kNone) ? rootpos[w] : tgt[i];
+            s = (w != kNone) ? chain_root(link, w) : tgt[i];
         }
         if (in) out[p] = in[s];
         else src[p] = s;
@@ -179,8 +176,7 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
         return;
     }
     DevBuf<unsigned long long> used(draws_used ? 1 : 0, s);
-    DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), off(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s),
-        root(m + 1, s);
+    DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), off(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s);
     DevBuf<unsigned long long> rej(1, s);
     DevBuf<u32> first0(1, s);
     cnt.zero();
@@ -198,12 +194,11 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     cnt.zero();  // reused as fill cursors
     LAUNCH_B("fy.scatter", 20.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, off.p, cnt.p, bucket.p);
     LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);
-    LAUNCH_B("fy.roots", 8.0 * m, k_fy_roots, G, B, 0, s, m, link.p, root.p);
     if (in)
-        LAUNCH_B("fy.sources_gather", 32.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, nullptr, in,
+        LAUNCH_B("fy.sources_gather", 32.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, link.p, first0.p, nullptr, in,
                  out);
     else
-        LAUNCH_B("fy.sources", 16.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, root.p, first0.p, src, nullptr,
+        LAUNCH_B("fy.sources", 16.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, link.p, first0.p, src, nullptr,
                  nullptr);
     if (draws_used) *draws_used = read_scalar(c, used.p);
 }

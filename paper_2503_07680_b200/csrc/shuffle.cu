@@ -17,6 +17,8 @@
 // where S_q is the ascending list of steps targeting q. The lists come from
 // a counting sort of steps by target; each chain is followed to its root
 // (depth ~ log m, measured max 19 at 1M). Output: source position per slot.
+#include <cstdlib>
+
 #include "engine.cuh"
 #include "rng.cuh"
 
@@ -33,26 +35,14 @@ __device__ __forceinline__ u32 fy_target(u64 seed, u64 base, u64 m, u64 i, u64 s
     return static_cast<u32>(r);
 }
 
-__global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
-                             unsigned long long* __restrict__ rej) {
-    for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
-         i += static_cast<u64>(gridDim.x) * blockDim.x) {
-        bool bad;
-        const u32 j = fy_target(seed, base, m, i, 0, bad);
-        if (bad) atomicMax(rej, static_cast<unsigned long long>(i));
-        tgt[i] = j;
-        atomicAdd(&cnt[j], 1u);
-    }
-}
-
 // Rare path: a draw at step `rej` was rejected. Every step i <= rej then
-// uses one more draw; repeat until no rejection remains.
-__global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
-                         unsigned long long* __restrict__ rej, unsigned long long* __restrict__ used) {
+// uses one more draw; repeat until no rejection remains. Run by one block.
+__device__ void fy_fix_block(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt, u64 rej0,
+                             unsigned long long* __restrict__ used) {
     __shared__ unsigned long long s_rej;
     __shared__ unsigned long long s_next;
     u64 shift = 0;
-    if (threadIdx.x == 0) s_rej = *rej;
+    if (threadIdx.x == 0) s_rej = rej0;
     __syncthreads();
     while (s_rej != 0) {
         const u64 upto = s_rej;
@@ -79,6 +69,26 @@ __global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* 
     }
     // draws the shuffle consumed: one per step plus one per rejection
     if (used && threadIdx.x == 0) *used = (m - 1) + shift;
+}
+
+// Targets and their counts; rej: the highest rejected step (k_fy_fix
+// repairs from there; it returns at once when there is none).
+__global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
+                             unsigned long long* __restrict__ rej, u64 force) {
+    for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        bool bad;
+        const u32 j = fy_target(seed, base, m, i, 0, bad);
+        bad = bad || i == force;  // tests: HBP_FY_FORCE_REJECT
+        if (bad) atomicMax(rej, static_cast<unsigned long long>(i));
+        tgt[i] = j;
+        atomicAdd(&cnt[j], 1u);
+    }
+}
+
+__global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
+                         const unsigned long long* __restrict__ rej, unsigned long long* __restrict__ used) {
+    fy_fix_block(seed, base, m, tgt, cnt, *rej, used);
 }
 
 __global__ void k_fy_scatter(u64 m, const u32* __restrict__ tgt, const u32* __restrict__ off,
@@ -183,7 +193,11 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     rej.zero();
     const unsigned B = 256;
     const unsigned G = grid_for(m, B, 148u * 32u);
-    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p);
+    // tests only: treat the first draw of one step as rejected, to exercise
+    // the repair on demand (a real rejection has probability < m / 2^64)
+    const char* fr = std::getenv("HBP_FY_FORCE_REJECT");
+    const u64 force = fr ? std::strtoull(fr, nullptr, 10) : 0ull;
+    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, force);
     LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
     // exclusive scan of per-target counts -> list offsets (m + 1 entries)
     const u32* cntp = cnt.p;

@@ -32,3 +32,33 @@ def test_radix_sort_stable(ctx, n, bits, desc):
     order = np.argsort(-keys.astype(np.int64) if desc else keys, kind="stable")
     assert np.array_equal(v, vals[order])
     assert np.array_equal(k, keys[order])
+
+
+def _fy_model(seed, m, forced):
+    # Rng::shuffle (rng.hpp:61-68) over the counter-based draws, with the
+    # first draw of step `forced` rejected: that step and every later one
+    # (smaller i) use one more draw (rng.hpp:32-41)
+    M64 = (1 << 64) - 1
+
+    def draw(k):
+        z = (seed + k * 0x9E3779B97F4A7C15) & M64
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+        return z ^ (z >> 31)
+
+    v = list(range(m))
+    for i in range(m, 1, -1):
+        k = m - i + 1 + (1 if forced and i <= forced else 0)
+        j = draw(k) % i
+        v[i - 1], v[j] = v[j], v[i - 1]
+    return np.array(v, dtype=np.uint32)
+
+
+@pytest.mark.parametrize("forced", [0, 2, 1234, 5000])
+def test_shuffle_rejection_repair(ctx, monkeypatch, forced):
+    # the repair path of a rejected draw (probability < m / 2^64 in real
+    # runs), forced through HBP_FY_FORCE_REJECT and checked against the model
+    if forced:
+        monkeypatch.setenv("HBP_FY_FORCE_REJECT", str(forced))
+    got = ctx.shuffle_positions(77, 5000)
+    assert np.array_equal(got, _fy_model(77, 5000, forced))

@@ -39,11 +39,6 @@ C2_GROUPS = [(16384, 1, 28), (131072, 8, 28)]
 DEVICES, PLAN_SEED = 8, 1
 METRIC = "samples packed/sec"
 UNIT = "samples/s"
-# Bounded CPU sample of the same spec: the reference is superlinear in the
-# corpus size (O(N^2) FFD residue), so the sample is the largest that keeps one
-# reference step at ~10-15 s (3M; 10M takes ~300 s). This still favours the
-# reference over the true 10M workload by ~3x per sample.
-REF_SAMPLE = 3_000_000
 
 
 def peaks():
@@ -123,63 +118,135 @@ def synth(abi_lib, spec, count=None):
 # reference arm: the reference's own CPU implementation (oracle/_ref)
 # ---------------------------------------------------------------------------
 
-def _ref_worker(args):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from pyoracle import Oracle  # bench's CPU legs only
-    L, reps = args
-    o = Oracle("reference")
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        plan = o.build_plan(None, L, C2_GROUPS, l_best=16384, device_count=DEVICES, seed=PLAN_SEED)
-        o.report(plan)
-        o.simulate(plan)
-        times.append(time.perf_counter() - t0)
-    return times
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
 
 
-def cpu_reference(lengths, steps, workers):
-    """Times reference build_plan + report + simulate; `workers` processes
-    each pack their own copy of the sample concurrently."""
-    import multiprocessing as mp
-    if workers <= 1:
-        times = _ref_worker((lengths, steps))
-        return len(lengths) / statistics.mean(times), 1, times
-    with mp.get_context("fork").Pool(workers) as pool:
-        res = pool.map(_ref_worker, [(lengths, steps)] * workers)
-    per_step = [max(r[k] for r in res) for k in range(steps)]
-    return workers * len(lengths) / statistics.mean(per_step), workers, per_step
+def c2_synth_arg(spec):
+    """The reference's synth spec text (ingest.cpp:331-373) for `spec`."""
+    s = f"count={spec['count']},short={spec['short']},max={spec['max_length']}"
+    if spec["long_fraction"] > 0:
+        s += f",long_fraction={spec['long_fraction']},long={spec['long']}"
+    return s
+
+
+def ref_bench_cmd(spec, groups, l_best, profile=None):
+    cmd = [REF_BENCH, "--synth", c2_synth_arg(spec), "--seed", str(spec["seed"]),
+           "--groups", ",".join(f"{l}:{sp}:{ck}" for l, sp, ck in groups), "--l-best", str(l_best),
+           "--devices", str(DEVICES), "--plan-seed", str(PLAN_SEED)]
+    if profile:
+        cmd += ["--profile", profile]
+    return cmd
+
+
+def _pin(core):
+    return lambda: os.sched_setaffinity(0, {core})
+
+
+def ref_run_concurrent(cmd, cores):
+    """One reference step per listed core, all at once (the reference is
+    single-threaded); returns each process's JSON line."""
+    procs = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, preexec_fn=_pin(c))
+             for c in cores]
+    out = []
+    for p in procs:
+        o, e = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError(f"ref_bench rc={p.returncode}: {e.strip()[-300:]}")
+        out.append(json.loads(o.strip().splitlines()[-1]))
+    return out
 
 
 def run_reference(args, rank, world):
+    """The reference's build_plan + report + simulate (oracle/_ref/ref_bench:
+    proj/src compiled in place, its own synth_lengths for the corpus) on the
+    SAME config as our arm: the full C2 corpus, one step per host core, all
+    concurrently. Never imports this repo's package or loads its engine."""
     if rank != 0:
         return 0
-    from paper_2503_07680_b200 import abi
-    lib = abi.load_library()
-    L = synth(lib, C2, REF_SAMPLE)
-    cores = os.cpu_count() or 1
+    cores = sorted(os.sched_getaffinity(0))
     try:
         import psutil
         avail_gb = psutil.virtual_memory().available / 2**30
     except Exception:
         avail_gb = 64.0
-    workers = max(1, min(cores, 64, int(avail_gb // 2)))  # ~0.8 GB peak per 3M-sample worker
-    for _ in range(max(0, min(args.warmup, 1))):
-        _ref_worker((L[:100_000], 1))
-    value, used, times = cpu_reference(L, max(1, args.steps), workers)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic (reference synth_lengths, C2 spec)",
-        "config": {"workload": "C2: HBP build_plan+report+simulate, LongAlign-like long tail, groups [16K sp1, 128K sp8], 8 DP devices",
-                   "samples_per_step": REF_SAMPLE * used, "sample": f"{REF_SAMPLE} samples of the C2 spec per worker"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "reference",
-                         "sample": f"{used} worker processes x {REF_SAMPLE} samples of the C2 spec (reference is single-threaded)"},
+    # peak RSS of one 10M C2 reference step is ~1.7 GB
+    k = max(1, min(args.steps, len(cores), int(avail_gb // 2.5)))
+    spec = dict(C2)
+    if args.n:
+        spec["count"] = args.n
+    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": DATA, "config": bench_config(spec)}
+    if not os.path.exists(REF_BENCH):
+        line["unavailable"] = f"{REF_BENCH} not built (make -C oracle needs /root/reference)"
+        print(json.dumps(line), flush=True)
+        return 0
+    warm = dict(spec, count=min(spec["count"], 100_000))
+    for _ in range(min(args.warmup, 1)):  # pages the binary and libstdc++ in; untimed
+        ref_run_concurrent(ref_bench_cmd(warm, C2_GROUPS, 16384), cores[:1])
+    t0 = time.perf_counter()
+    res = ref_run_concurrent(ref_bench_cmd(spec, C2_GROUPS, 16384), cores[:k])
+    wall = time.perf_counter() - t0
+    step_s = [r["step_s"] for r in res]
+    value = k * spec["count"] / max(step_s)
+    line.update({
+        "value": value, "steps": k, "warmup": min(args.warmup, 1), "ms_per_step": 1000 * statistics.mean(step_s),
+        "ms_steps": [round(1000 * x, 1) for x in step_s], "wall_s": wall,
+        "steps_note": f"{k} steps run concurrently, one per host core (requested {args.steps}); "
+                      "value = steps x samples / slowest step (build_plan + report + simulate; synth not timed)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": k, "kind": "reference",
+                         "sample": f"{k} concurrent single-threaded reference steps, each the full C2 corpus "
+                                   f"({spec['count']} samples)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+        "result": {kk: res[0][kk] for kk in ("iterations", "packs", "abr", "cr", "total_seconds", "plan_fnv")},
+    })
     print(json.dumps(line), flush=True)
     return 0
+
+
+DATA = "synthetic (reference synth_lengths, C2 spec)"
+
+
+def bench_config(spec):
+    """Identical in both arms: the workload, not the implementation."""
+    return {"workload": "C2: HBP build_plan+report+simulate, LongAlign-like long tail, groups [16K sp1, 128K sp8], "
+                        "8 DP devices",
+            "samples_per_step": spec["count"], "synth": c2_synth_arg(spec), "corpus_seed": spec["seed"],
+            "groups": [list(g) for g in C2_GROUPS], "l_best": 16384, "dp_devices": DEVICES, "plan_seed": PLAN_SEED}
+
+
+class CpuBaseline:
+    """cpu_baseline of our arm: one reference step on the full C2 corpus on
+    one host core (the reference is single-threaded), run in the background
+    on a core this process does not use while the GPU legs run."""
+
+    def __init__(self, spec):
+        self.p = None
+        self.spec = spec
+        cores = sorted(os.sched_getaffinity(0))
+        if not os.path.exists(REF_BENCH) or len(cores) < 2:
+            return
+        self.core = cores[-1]
+        os.sched_setaffinity(0, set(cores[:-1]))
+        self.p = subprocess.Popen(ref_bench_cmd(spec, C2_GROUPS, 16384), stdout=subprocess.PIPE,
+                                  stderr=subprocess.PIPE, text=True, preexec_fn=_pin(self.core))
+
+    def result(self):
+        if self.p is None:
+            return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                    "sample": "unavailable: oracle/_ref/ref_bench not built or a single host core"}
+        o, e = self.p.communicate()
+        if self.p.returncode != 0:
+            return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e[-300:]}"}
+        r = json.loads(o.strip().splitlines()[-1])
+        return {"value": r["samples"] / r["step_s"], "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"one step on the full C2 corpus ({r['samples']} samples), host core {self.core}, "
+                          "run concurrently with the GPU legs on a core the GPU process does not use",
+                "seconds": r["step_s"], "result": {k: r[k] for k in ("iterations", "packs", "abr", "cr",
+                                                                     "total_seconds", "plan_fnv")}}
+
+    def kill(self):
+        if self.p is not None and self.p.poll() is None:
+            self.p.kill()
 
 
 # ---------------------------------------------------------------------------
@@ -199,10 +266,12 @@ def run_ours(args, rank, world, local):
     ctx = abi.Context(local)
     stream = torch.cuda.ExternalStream(lib.hbp_ctx_stream(ctx.h))
 
-    spec = dict(C2)
+    spec0 = dict(C2)
     if args.n:
-        spec["count"] = args.n
-    spec["seed"] = C2["seed"] + rank  # independent replica per rank
+        spec0["count"] = args.n
+    # reference step on the same corpus on one spare host core, in the background
+    cpu_bl = CpuBaseline(spec0) if rank == 0 and world == 1 and not args.no_cpu else None
+    spec = dict(spec0, seed=C2["seed"] + rank)  # independent replica per rank
     L = synth(lib, spec)
     n = len(L)
     d_len = torch.from_numpy(L).cuda()
@@ -272,8 +341,10 @@ def run_ours(args, rank, world, local):
 
     # stage profile of one extra step (CUDA events around each engine stage)
     stages = profile_stages(ctx, lib, step_device)
-    sweep_res = None if args.no_sweep else run_sweep_leg(ctx, lib, rank, world, dist)
-    c4_res = run_c4_leg(ctx, lib, rank, world, dist) if not args.no_c4 else None
+    from paper_2503_07680_b200 import sweep as sweep_mod
+    comm = sweep_mod.engine_comm(ctx, dist) if dist is not None else abi.Comm(ctx, abi.Comm.unique_id(ctx), 0, 1)
+    sweep_res = None if args.no_sweep else run_sweep_leg(ctx, lib, rank, world, dist, comm)
+    c4_res = run_c4_leg(ctx, lib, comm, rank, world, dist) if not args.no_c4 else None
     ingest_res = run_ingest_leg(ctx, lib) if rank == 0 and not args.no_ingest else None
 
     tot_dev = sum(dev_ms)
@@ -288,14 +359,15 @@ def run_ours(args, rank, world, local):
         e2e_value = world * n / (tot_e2e / args.steps / 1000.0)
         peak, peak_kind = peaks()
         roof = roofline(stages, peak, peak_kind)
-        cpu = cpu_baseline_leg(lib) if world == 1 and not args.no_cpu else None
+        cpu = cpu_bl.result() if cpu_bl is not None else None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64", "data": "synthetic (synth_lengths, C2 spec; replica seed = 20250515 + rank)",
-            "config": {"workload": "C2: HBP build_plan+report+simulate, LongAlign-like long tail, groups [16K sp1, 128K sp8], 8 DP devices",
-                       "samples_per_rank": n, "groups": C2_GROUPS, "dp_devices": DEVICES, "seed": PLAN_SEED,
-                       "parallelism": f"replicas x{world}", "l2": "flushed (256 MB write) before every step"},
+            "vs_baseline": None, "dtype": "int64",
+            "data": DATA + "; restated bit-identically in csrc/synth.cpp; rank r packs the corpus of seed 20250515 + r",
+            "config": bench_config(spec0),
+            "parallelism": f"replicas x{world} (packing one corpus does not shard, SURVEY.md 8(e))",
+            "l2": "flushed (256 MB write) before every step",
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": tot_e2e / args.steps, "ms_steps": [round(x, 3) for x in e2e_ms]},
             "ms_steps": [round(x, 3) for x in dev_ms],
@@ -309,6 +381,7 @@ def run_ours(args, rank, world, local):
             "ingest": ingest_res,
         }
         print(json.dumps(line), flush=True)
+    comm.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -321,40 +394,37 @@ SWEEP_SMALLER = [512, 1024, 2048, 4096, 8192, 16384, 32768, 65536]  # 256 length
 SWEEP_SP = [1, 2, 4, 8]
 
 
-def run_sweep_leg(ctx, lib, rank, world, dist):
+def run_sweep_leg(ctx, lib, rank, world, dist, comm):
     """C3 auto-selection sweep: 256 length sets x SP{1,2,4,8} x GC{on,off} =
     2048 candidates over the C1 corpus (100K, lengths >= 128), sharded across
-    ranks by length set, NCCL all_gather argmin. One timed repetition after a
-    warm-up of the first length set; device time = max over ranks."""
+    ranks by length set with the NCCL argmin, all in the engine
+    (hbp_sweep_sharded). One timed repetition after a warm-up of the first
+    length set; device time = max over ranks."""
     import torch
     from paper_2503_07680_b200 import abi, sweep
     L = np.maximum(synth(lib, C1), 128)
     cands = sweep.make_candidates(ctx, 131072, SWEEP_SMALLER, SWEEP_SP)
     s, keep = abi.make_samples(None, L, "c1")
     opts = dict(device_count=8, seed=7)
-    gather = sweep.torch_all_gather(dist, "cuda") if dist is not None else None
     ctx.sweep_samples(s, cands[:8], None, **opts)  # warm-up
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    secs, best = sweep.run_sweep(ctx, s, cands, rank, world, gather, **opts)
+    secs, best, local = sweep.run_sweep_nccl(comm, s, cands, None, **opts)
     torch.cuda.synchronize()
     elapsed = time.perf_counter() - t0
     if dist is not None:
         t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-        feas = torch.tensor([sum(1 for v in secs.values() if math.isfinite(v))], device="cuda")
-        dist.all_reduce(feas)
-        n_feasible = int(feas.item())
-    else:
-        n_feasible = sum(1 for v in secs.values() if math.isfinite(v))
     return {"workload": "C3: 256 length sets x SP{1,2,4,8} x GC{on,off}, C1 corpus (100K), 8B analytic cost model",
-            "candidates": len(cands), "feasible": n_feasible, "seconds": elapsed,
+            "candidates": len(cands), "feasible": int(np.isfinite(secs).sum()), "seconds": elapsed,
             "candidates_per_s": len(cands) / elapsed, "best_index": best[1],
             "best_groups": cands[best[1]][0] if best[1] >= 0 else None, "best_seconds": best[0],
-            "sharding": f"length sets round-robin over {world} rank(s), all_gather argmin"}
+            "local_candidates_rank0": local,
+            "sharding": f"length sets round-robin over {world} rank(s); hbp_sweep_sharded: ncclAllReduce(MIN) of "
+                        "seconds + ncclAllGather of (best seconds, best index) on the engine's stream"}
 
 
 C4 = dict(C2, count=100_000_000)
@@ -373,7 +443,7 @@ def c4_profile():
     return p
 
 
-def run_c4_leg(ctx, lib, rank=0, world=1, dist=None, steps=3, warmup=3):
+def run_c4_leg(ctx, lib, comm, rank=0, world=1, dist=None, steps=3, warmup=3):
     """BASELINE config C4: 100M samples of the C2 spec, groups [16K sp1,
     128K sp8] with ckpt derived under the DeepSeek-V2 236B cost model, 8 DP
     devices: build_plan + report (ABR/CR) + simulate, corpus resident in HBM.
@@ -417,11 +487,9 @@ def run_c4_leg(ctx, lib, rank=0, world=1, dist=None, steps=3, warmup=3):
            "samples": n, "groups": groups, "ms_per_step": statistics.mean(ms), "ms_steps": [round(x, 2) for x in ms],
            "samples_per_s": n / (statistics.mean(ms) / 1000.0), "abr": m.abr, "cr": m.cr,
            "estimated_seconds": st.total_seconds}
-    # report + simulate sharded by DP column across the ranks (NCCL all-reduce
-    # of per-iteration vectors), against the single-GPU evaluation
-    from paper_2503_07680_b200 import sharded_eval as se
-    ar = se.torch_all_reduce(dist) if dist is not None else None
-
+    # report + simulate sharded by DP column across the ranks (hbp_eval_sharded:
+    # NCCL all-reduce of per-iteration vectors on the engine's stream),
+    # against the single-GPU evaluation
     def timed_eval(fn):
         best = math.inf
         for _ in range(3):
@@ -440,11 +508,12 @@ def run_c4_leg(ctx, lib, rank=0, world=1, dist=None, steps=3, warmup=3):
         return r, best
 
     (m1, st1), single_s = timed_eval(lambda: (plan.report(), plan.simulate(prof)))
-    (m2, st2), shard_s = timed_eval(lambda: se.sharded_evaluate(ctx, plan, rank, world, ar, prof))
+    (m2, st2), shard_s = timed_eval(lambda: comm.evaluate(plan, prof))
     res["sharded_eval"] = {"ranks": world, "dp_columns": DEVICES, "ms": 1e3 * shard_s, "single_gpu_ms": 1e3 * single_s,
                            "identical": bool(m1.abr == m2.abr and m1.dbr == m2.dbr and m1.cr == m2.cr
                                              and st1.total_seconds == st2.total_seconds),
-                           "exchange": "all_reduce MAX/SUM/MIN of 6 per-iteration vectors, then SUM of 2 (NCCL)"}
+                           "exchange": "hbp_eval_sharded: ncclAllReduce MAX/SUM/MIN of 6 per-iteration vectors, "
+                                       "then SUM of 2, on the engine's stream"}
     out = plan = None
     if world > 1:
         return res
@@ -491,37 +560,40 @@ def profile_stages(ctx, lib, fn):
     return out
 
 
-TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_scan_traffic.json")
+TRAFFIC_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
 
 
 def roofline(stages, peak, peak_kind):
-    """Dominant HBM-bound kernel family: algorithmic bytes / its device time
-    (CUDA events around every launch of the family, summed). The step's
-    largest kernel overall, the first-fit chain, is latency-bound (a
-    dependency chain over bins) and is reported beside it with its
-    share of the step instead of a bandwidth fraction."""
-    cands = {k: v for k, v in stages.items() if v["bytes"] > 0 and v["ms"] > 0}
+    """The step's dominant kernel family (largest summed device time; CUDA
+    events around every launch on the engine's stream): algorithmic bytes
+    (SURVEY.md 8(d) per-unit figures x units, registered per launch by the
+    engine) / its device time. The sort and scan families the north star
+    targets are listed beside it."""
+    cands = {k: v for k, v in stages.items() if v["ms"] > 0}
     if not cands:
         return None
+    total_ms = sum(x["ms"] for x in stages.values())
     k, v = max(cands.items(), key=lambda kv: kv[1]["ms"])
     achieved = v["bytes"] / (v["ms"] / 1000.0) / 1e9
     traffic = None
-    if k == "scan" and os.path.exists(TRAFFIC_FILE):  # ncu --set full capture of the same step, per launch
+    if os.path.exists(TRAFFIC_FILE):  # ncu --set full capture of the same step, per launch
         with open(TRAFFIC_FILE) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    total_ms = sum(x["ms"] for x in stages.values())
-    top_k, top_v = max(stages.items(), key=lambda kv: kv[1]["ms"])
+            traffic = json.load(f).get(k, {}).get("dram_bytes_per_launch")
+
+    def fam(vv):
+        gbs = vv["bytes"] / (vv["ms"] / 1000.0) / 1e9
+        return {"ms": round(vv["ms"], 4), "launches": vv["launches"], "share": round(vv["ms"] / total_ms, 4),
+                "achieved_gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+
     return {"bound": "hbm", "kernel": k, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
             "algorithmic_bytes_per_launch": v["bytes"] / max(v["launches"], 1),
             "launches": v["launches"], "ms": v["ms"], "share_of_kernel_time": v["ms"] / total_ms,
-            "families": {kk: {"ms": round(vv["ms"], 4), "launches": vv["launches"],
-                              "achieved_gbs": round(vv["bytes"] / (vv["ms"] / 1000.0) / 1e9, 1),
-                              "frac": round(vv["bytes"] / (vv["ms"] / 1000.0) / 1e9 / peak, 4)}
-                         for kk, vv in sorted(cands.items(), key=lambda kv: -kv[1]["ms"])[:8]},
-            "step_top_kernel": {"kernel": top_k, "ms": top_v["ms"], "share_of_kernel_time": top_v["ms"] / total_ms,
-                                "bound": "latency (first-fit dependency chain across resident warps)"
-                                if top_k.startswith("fit.chain") else "hbm"}}
+            "note": "fit.chain is a dependency chain over bins (latency-bound, DESIGN.md); its bytes are "
+                    "12 B/item + 12 B/bin (SURVEY.md 8(d) FFD residue)" if k.startswith("fit.chain") else None,
+            "sort_scan": {kk: fam(vv) for kk, vv in stages.items()
+                          if (kk.startswith("radix") or kk == "scan") and vv["ms"] > 0},
+            "families": {kk: fam(vv) for kk, vv in sorted(cands.items(), key=lambda kv: -kv[1]["ms"])[:10]}}
 
 
 INGEST_SAMPLES = 2_000_000
@@ -584,16 +656,6 @@ def run_ingest_leg(ctx, lib):
             "reference": ref}
 
 
-def cpu_baseline_leg(lib):
-    try:
-        L = synth(lib, C2, REF_SAMPLE)
-        value, used, times = cpu_reference(L, 1, 1)
-        return {"value": value, "unit": UNIT, "cores": used, "kind": "reference",
-                "sample": f"{REF_SAMPLE} samples of the C2 spec, 1 step, 1 host core (reference is single-threaded)"}
-    except Exception as e:  # the reference library did not travel
-        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -606,7 +668,19 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the 100M-sample C4 / C5-sample leg")
     ap.add_argument("--no-ingest", action="store_true", help="skip the corpus-file (JSONL) ingest leg")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torchrun
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     rank, world, local = dist_env()
+    if world != args.gpus and args.impl == "ours":
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

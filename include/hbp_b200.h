@@ -452,6 +452,45 @@ int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples,
               const hbp_hardware_profile* profile, double* out_seconds,
               int64_t* out_best);
 
+/* ---- Multi-GPU -------------------------------------------
+ * One process per GPU. The reference has no counterpart (single process; its
+ * "devices" are vector entries, balance.hpp:18-22); these entry points run the
+ * two parts of the path that shard with their one exchange each as NCCL
+ * collectives on the context's stream. NCCL is loaded at run time
+ * (libnccl.so.2 already in the process, else the system's).
+ *
+ * Rank 0 calls hbp_comm_unique_id and sends the HBP_COMM_ID_BYTES bytes to
+ * every rank out of band (e.g. torch.distributed); every rank then calls
+ * hbp_comm_create with the same id, its rank and the world size
+ * (collective: blocks until all ranks joined). */
+#define HBP_COMM_ID_BYTES 128
+typedef struct hbp_comm hbp_comm;
+int hbp_comm_unique_id(hbp_ctx* ctx, unsigned char* out_id);
+int hbp_comm_create(hbp_ctx* ctx, const unsigned char* id, int32_t rank, int32_t world, hbp_comm** out);
+void hbp_comm_destroy(hbp_comm* comm);
+
+/* hbp_sweep across the communicator's ranks (BASELINE C3 / C5): whole length
+ * sets are dealt round-robin in decreasing estimated cost, every rank runs the
+ * single-GPU sweep on its share, then ncclAllReduce(MIN) of the per-candidate
+ * seconds and ncclAllGather of every rank's first error and (best seconds,
+ * best index). Every rank returns the full out_seconds[n_candidates], the
+ * global argmin (lowest index on ties) and the error the sequential sweep
+ * raises (the first in index order). *out_local: candidates this rank
+ * evaluated (may be NULL). Collective. */
+int hbp_sweep_sharded(hbp_ctx* ctx, hbp_comm* comm, const hbp_samples* samples,
+                      const hbp_group_config* cand_groups, const int64_t* cand_offsets,
+                      const int64_t* cand_l_best, int64_t n_candidates,
+                      const hbp_plan_options* options, const hbp_hardware_profile* profile,
+                      double* out_seconds, int64_t* out_best, int64_t* out_local);
+
+/* report (+ simulate when profile != NULL) of a plan every rank holds, each
+ * rank evaluating its DP columns [r N / W, (r + 1) N / W): hbp_eval_columns
+ * phase 0, ncclAllReduce MAX / SUM / MIN, phase 1, ncclAllReduce SUM, finish.
+ * Bit-identical on every rank to hbp_report_plan / hbp_simulate_plan
+ * (metrics.cpp:107-144, sim.cpp:9-60). Collective. */
+int hbp_eval_sharded(hbp_ctx* ctx, hbp_comm* comm, hbp_plan* plan, const hbp_hardware_profile* profile,
+                     hbp_metrics* out, hbp_sim_totals* sim);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -28,6 +28,16 @@ int hbp_test_scan_u32(hbp_ctx* ctx, const uint32_t* in, int64_t n, uint64_t* out
 int hbp_test_radix_sort(hbp_ctx* ctx, uint32_t* keys, uint32_t* values, int64_t n, int32_t bits,
                         int32_t descending);
 
+/* Every later Fisher-Yates on this context treats the first draw of step
+ * `step` as rejected (0: none), exercising the repair of a rejected draw
+ * (probability < m / 2^64 in real runs). */
+int hbp_test_set_force_reject(hbp_ctx* ctx, uint64_t step);
+
+/* The candidates rank `rank` of `world` evaluates in hbp_sweep_sharded
+ * (ascending global indices; out_idx holds n_candidates entries). Host only. */
+int hbp_test_sweep_shard(const hbp_group_config* cand_groups, const int64_t* cand_offsets, int64_t n_candidates,
+                         int32_t rank, int32_t world, int64_t* out_idx, int64_t* out_n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -527,14 +527,7 @@ class Context:
         return self.sweep_samples(s, candidates, profile, **opts)
 
     def sweep_samples(self, s: Samples, candidates, profile: Optional[HardwareProfile] = None, **opts):
-        flat, offs, lbs = [], [0], []
-        for groups, lb in candidates:
-            flat.extend(groups)
-            offs.append(len(flat))
-            lbs.append(lb)
-        garr = (GroupConfig * max(1, len(flat)))(*[GroupConfig(*g) for g in flat])
-        offs = np.array(offs, dtype=np.int64)
-        lbs = np.array(lbs, dtype=np.int64)
+        garr, offs, lbs = flatten_candidates(candidates)
         prof = profile if profile is not None else default_profile()
         o = make_options(**opts)
         out = np.zeros(max(1, len(candidates)))
@@ -564,6 +557,73 @@ class Context:
         self.check(self.lib.hbp_test_radix_sort(self.h, ptr(k, C.c_uint32), ptr(v, C.c_uint32),
                                                 C.c_int64(len(k)), C.c_int32(bits), C.c_int32(int(descending))))
         return k, v
+
+
+def flatten_candidates(candidates):
+    """[(groups[(l, sp, ck)...], l_best)] -> (GroupConfig array, offsets, l_best) of the C-ABI."""
+    flat, offs, lbs = [], [0], []
+    for groups, lb in candidates:
+        flat.extend(groups)
+        offs.append(len(flat))
+        lbs.append(lb)
+    garr = (GroupConfig * max(1, len(flat)))(*[GroupConfig(*g) for g in flat])
+    return garr, np.array(offs, dtype=np.int64), np.array(lbs, dtype=np.int64)
+
+
+COMM_ID_BYTES = 128
+
+
+class Comm:
+    """The engine's NCCL communicator (hbp_comm_*, include/hbp_b200.h): the
+    multi-GPU sweep and the DP-column sharded report/simulate run their
+    exchanges as NCCL collectives on the context's stream, in C++."""
+
+    def __init__(self, ctx: "Context", uid: bytes, rank: int, world: int):
+        lib = ctx.lib
+        lib.hbp_comm_create.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+        lib.hbp_comm_destroy.argtypes = [C.c_void_p]
+        self.ctx, self.rank, self.world = ctx, rank, world
+        h = C.c_void_p()
+        ctx.check(lib.hbp_comm_create(ctx.h, uid, rank, world, C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id(ctx: "Context") -> bytes:
+        buf = C.create_string_buffer(COMM_ID_BYTES)
+        ctx.lib.hbp_comm_unique_id.argtypes = [C.c_void_p, C.c_char_p]
+        ctx.check(ctx.lib.hbp_comm_unique_id(ctx.h, buf))
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.hbp_comm_destroy(self.h)
+            self.h = None
+
+    def sweep(self, s: Samples, candidates, profile: Optional[HardwareProfile] = None, **opts):
+        """(seconds[n] on every rank, global argmin, candidates evaluated here)."""
+        lib = self.ctx.lib
+        garr, offs, lbs = flatten_candidates(candidates)
+        prof = profile if profile is not None else default_profile()
+        o = make_options(**opts)
+        out = np.zeros(max(1, len(candidates)))
+        best, local = C.c_int64(), C.c_int64()
+        lib.hbp_sweep_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64)]
+        self.ctx.check(lib.hbp_sweep_sharded(self.ctx.h, self.h, C.byref(s), garr, offs.ctypes.data,
+                                             lbs.ctypes.data, len(candidates), C.byref(o), C.byref(prof),
+                                             out.ctypes.data, C.byref(best), C.byref(local)))
+        return out[:len(candidates)], best.value, local.value
+
+    def evaluate(self, plan: "DevicePlanHandle", profile: Optional[HardwareProfile] = None):
+        """(Metrics, SimTotals or None): report / simulate by DP column."""
+        lib = self.ctx.lib
+        lib.hbp_eval_sharded.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        m, st = Metrics(), SimTotals()
+        self.ctx.check(lib.hbp_eval_sharded(self.ctx.h, self.h, plan.h,
+                                            C.byref(profile) if profile is not None else None, C.byref(m),
+                                            C.byref(st)))
+        return m, (st if profile is not None else None)
 
 
 class DevicePlanHandle:

@@ -648,6 +648,12 @@ int hbp_memory_used(hbp_ctx* ctx, int64_t length, int32_t sp, int32_t ckpt, cons
 
 // ---- testing hooks ----------------------------------------------------------
 
+int hbp_test_set_force_reject(hbp_ctx* ctx, uint64_t step) {
+    if (ctx == nullptr) return HBP_ERR_VALIDATION;
+    ctx->test_force_reject = step;
+    return HBP_OK;
+}
+
 int hbp_test_shuffle_positions(hbp_ctx* ctx, uint64_t seed, int64_t m, uint32_t* out_src) {
     return guarded(ctx, [&] {
         if (m <= 0) return;

@@ -603,10 +603,12 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
         a.hist = hist.p;
         a.hact = hact.p;
     }
-    if (short_chain) LAUNCH_COOP(name, 0.0, (k_ff_chain<M, kShortWarps>), dim3(G), dim3(kWarps * 32), smem, s, args);
-    else LAUNCH_COOP(name, 0.0, (k_ff_chain<M, warps_for<M>()>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    // algorithmic bytes (FFD residue): 12 B per item + 12 B per bin of the pass
+    const double alg = 12.0 * a.n_items + 12.0 * (a.bin_end - a.bin0);
+    if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>()>), dim3(G), dim3(kWarps * 32), smem, s, args);
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
-    if (replay) LAUNCH_B("fit.replay", 0.0, k_ff_replay<M>, (J + 7) / 8, 256, 0, s, a);
+    if (replay) LAUNCH_B("fit.replay", 12.0 * a.n_items + 16.0 * (a.bin_end - a.bin0), k_ff_replay<M>, (J + 7) / 8, 256, 0, s, a);
     const auto o = read_vector(c, out.p, 2);
     if (c.trace) {
         float ms = 0;

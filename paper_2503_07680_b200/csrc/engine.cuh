@@ -36,6 +36,9 @@ struct hbp_ctx {
     std::map<std::string, double> trace_ms;
     std::chrono::steady_clock::time_point trace_last{};
     hbp_b200::KernelProfiler prof;
+    // tests only (hbp_test_set_force_reject): the Fisher-Yates step whose
+    // first draw is treated as rejected; 0 = none
+    uint64_t test_force_reject = 0;
 };
 
 namespace hbp_b200 {

@@ -79,7 +79,7 @@ __global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
         bool bad;
         const u32 j = fy_target(seed, base, m, i, 0, bad);
-        bad = bad || i == force;  // tests: HBP_FY_FORCE_REJECT
+        bad = bad || i == force;  // tests: hbp_test_set_force_reject
         if (bad) atomicMax(rej, static_cast<unsigned long long>(i));
         tgt[i] = j;
         atomicAdd(&cnt[j], 1u);
@@ -193,10 +193,10 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     rej.zero();
     const unsigned B = 256;
     const unsigned G = grid_for(m, B, 148u * 32u);
-    // tests only: treat the first draw of one step as rejected, to exercise
-    // the repair on demand (a real rejection has probability < m / 2^64)
-    const char* fr = std::getenv("HBP_FY_FORCE_REJECT");
-    const u64 force = fr ? std::strtoull(fr, nullptr, 10) : 0ull;
+    // tests only (hbp_test_set_force_reject): treat the first draw of one
+    // step as rejected, to exercise the repair on demand (a real rejection has
+    // probability < m / 2^64)
+    const u64 force = c.test_force_reject;
     LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, force);
     LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
     // exclusive scan of per-target counts -> list offsets (m + 1 entries)

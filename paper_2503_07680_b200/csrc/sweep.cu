@@ -23,6 +23,8 @@
 #include "costmodel.cuh"
 #include "metrics.cuh"
 #include "pipeline.cuh"
+#include "sweep.cuh"
+#include "../../include/hbp_b200_testing.h"
 
 using namespace hbp_b200;
 
@@ -47,28 +49,26 @@ int sw_guarded(hbp_ctx* ctx, F&& fn) {
 
 namespace {
 
-// One block = a maximal run of consecutive candidates with the same length
-// set: processed exactly as the sequential sweep would (plan built at the
-// block's first candidate with its groups, group validation for the rest),
-// so every candidate gets the same seconds or the same error.
+// One block = a maximal run of consecutive evaluated candidates with the
+// same length set: processed exactly as the sequential sweep would (plan
+// built at the block's first candidate with its groups, group validation for
+// the rest), so every candidate gets the same seconds or the same error.
+// Positions index `idx` (the global candidate indices evaluated here).
 struct SweepBlock {
     int64_t begin, end;
 };
 
-struct SweepErr {
-    int code = HBP_OK;
-    std::string msg;
-};
-
-void sweep_block(hbp_ctx& c, const DeviceCorpus& corpus, const SweepBlock& b, const hbp_group_config* cand_groups,
-                 const int64_t* cand_offsets, const int64_t* cand_l_best, const hbp_plan_options* options,
-                 const hbp_hardware_profile* profile, int pc, std::vector<double>& secs, std::vector<SweepErr>& errs) {
+void sweep_block(hbp_ctx& c, const DeviceCorpus& corpus, const SweepBlock& b, const int64_t* idx,
+                 const hbp_group_config* cand_groups, const int64_t* cand_offsets, const int64_t* cand_l_best,
+                 const hbp_plan_options* options, const hbp_hardware_profile* profile, int pc,
+                 std::vector<double>& secs, std::vector<SweepErr>& errs) {
     CtxScope scope(c);
     std::unique_ptr<DevicePlan> plan;
-    for (int64_t k = b.begin; k < b.end; ++k) {
+    for (int64_t q = b.begin; q < b.end; ++q) {
+        const int64_t k = idx[q];
         std::vector<hbp_group_config> g(cand_groups + cand_offsets[k], cand_groups + cand_offsets[k + 1]);
         try {
-            if (k == b.begin) {
+            if (q == b.begin) {
                 PlanArgs a;
                 a.groups = g;
                 a.l_best = cand_l_best[k];
@@ -106,7 +106,85 @@ void sweep_block(hbp_ctx& c, const DeviceCorpus& corpus, const SweepBlock& b, co
     }
 }
 
+std::vector<int64_t> lengths_of(const hbp_group_config* cand_groups, const int64_t* cand_offsets, int64_t k) {
+    std::vector<int64_t> ls;
+    for (int64_t q = cand_offsets[k]; q < cand_offsets[k + 1]; ++q) ls.push_back(cand_groups[q].length);
+    return ls;
+}
+
 }  // namespace
+
+namespace hbp_b200 {
+
+void sweep_ingest(hbp_ctx& c, const hbp_samples* samples, DeviceCorpus& corpus) {
+    ingest(c, samples, corpus);
+    validate_corpus(c, samples, corpus, (samples && samples->source) ? samples->source : "");
+}
+
+void sweep_evaluate(hbp_ctx& c, const DeviceCorpus& corpus, const hbp_group_config* cand_groups,
+                    const int64_t* cand_offsets, const int64_t* cand_l_best, const std::vector<int64_t>& idx,
+                    const hbp_plan_options* options, const hbp_hardware_profile* profile, std::vector<double>& secs,
+                    std::vector<SweepErr>& errs) {
+    if (idx.empty()) return;
+    const int pc = cm_profile_check(*profile);
+    std::vector<SweepBlock> blocks;
+    for (size_t q = 0; q < idx.size(); ++q) {
+        if (q == 0 || idx[q] != idx[q - 1] + 1 ||
+            lengths_of(cand_groups, cand_offsets, idx[q]) != lengths_of(cand_groups, cand_offsets, idx[q - 1]))
+            blocks.push_back({static_cast<int64_t>(q), static_cast<int64_t>(q) + 1});
+        else
+            blocks.back().end = static_cast<int64_t>(q) + 1;
+    }
+    // Plans at sweep sizes are launch- and latency-bound, so blocks run
+    // concurrently: each worker thread owns a context (its own stream)
+    // on the same GPU and takes blocks in order; the corpus in HBM is
+    // shared read-only.
+    const char* ew = std::getenv("HBP_SWEEP_STREAMS");
+    int W = ew ? std::atoi(ew) : 8;
+    W = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(W, static_cast<int64_t>(blocks.size()))));
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));  // corpus ready for the workers' streams
+    std::vector<hbp_ctx*> workers(static_cast<size_t>(W), nullptr);
+    for (int w = 0; w < W; ++w)
+        if (hbp_ctx_create(c.device, &workers[static_cast<size_t>(w)]) != HBP_OK)
+            throw EngineError(HBP_ERR_CUDA, "sweep: cannot create a worker stream");
+    std::atomic<size_t> next{0};
+    auto work = [&](hbp_ctx* wc) {
+        for (size_t bi; (bi = next.fetch_add(1)) < blocks.size();)
+            sweep_block(*wc, corpus, blocks[bi], idx.data(), cand_groups, cand_offsets, cand_l_best, options,
+                        profile, pc, secs, errs);
+        cudaStreamSynchronize(wc->stream);
+    };
+    std::vector<std::thread> threads;
+    for (int w = 1; w < W; ++w) threads.emplace_back(work, workers[static_cast<size_t>(w)]);
+    work(workers[0]);
+    for (auto& t : threads) t.join();
+    for (auto* wc : workers) {
+        c.launches += wc->launches;
+        hbp_ctx_destroy(wc);
+    }
+}
+
+std::vector<int64_t> sweep_shard(const hbp_group_config* cand_groups, const int64_t* cand_offsets,
+                                 int64_t n_candidates, int rank, int world) {
+    // whole length sets, dealt round-robin in decreasing estimated cost (more
+    // groups and smaller groups pack more packs): every plan is built once
+    std::map<std::vector<int64_t>, std::vector<int64_t>> sets;
+    for (int64_t k = 0; k < n_candidates; ++k) sets[lengths_of(cand_groups, cand_offsets, k)].push_back(k);
+    std::vector<const std::pair<const std::vector<int64_t>, std::vector<int64_t>>*> order;
+    for (const auto& kv : sets) order.push_back(&kv);
+    std::stable_sort(order.begin(), order.end(), [](auto* a, auto* b) {
+        if (a->first.size() != b->first.size()) return a->first.size() > b->first.size();
+        return a->first < b->first;  // (first length, then the whole set) ascending
+    });
+    std::vector<int64_t> mine;
+    for (size_t k = 0; k < order.size(); ++k)
+        if (static_cast<int>(k % static_cast<size_t>(world)) == rank)
+            mine.insert(mine.end(), order[k]->second.begin(), order[k]->second.end());
+    std::sort(mine.begin(), mine.end());
+    return mine;
+}
+
+}  // namespace hbp_b200
 
 extern "C" int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples, const hbp_group_config* cand_groups,
                          const int64_t* cand_offsets, const int64_t* cand_l_best, int64_t n_candidates,
@@ -116,48 +194,12 @@ extern "C" int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples, const hbp_gro
         *out_best = -1;
         if (n_candidates <= 0) return;
         DeviceCorpus corpus;
-        ingest(*ctx, samples, corpus);
-        validate_corpus(*ctx, samples, corpus, (samples && samples->source) ? samples->source : "");
-        const int pc = cm_profile_check(*profile);
+        sweep_ingest(*ctx, samples, corpus);
         std::vector<double> secs(static_cast<size_t>(n_candidates), std::numeric_limits<double>::infinity());
         std::vector<SweepErr> errs(static_cast<size_t>(n_candidates));
-        std::vector<SweepBlock> blocks;
-        auto lengths_of = [&](int64_t k) {
-            std::vector<int64_t> ls;
-            for (int64_t q = cand_offsets[k]; q < cand_offsets[k + 1]; ++q) ls.push_back(cand_groups[q].length);
-            return ls;
-        };
-        for (int64_t k = 0; k < n_candidates; ++k) {
-            if (k == 0 || lengths_of(k) != lengths_of(k - 1)) blocks.push_back({k, k + 1});
-            else blocks.back().end = k + 1;
-        }
-        // Plans at sweep sizes are launch- and latency-bound, so blocks run
-        // concurrently: each worker thread owns a context (its own stream)
-        // on the same GPU and takes blocks in order; the corpus in HBM is
-        // shared read-only.
-        const char* ew = std::getenv("HBP_SWEEP_STREAMS");
-        int W = ew ? std::atoi(ew) : 8;
-        W = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(W, static_cast<int64_t>(blocks.size()))));
-        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // corpus ready for the workers' streams
-        std::vector<hbp_ctx*> workers(static_cast<size_t>(W), nullptr);
-        for (int w = 0; w < W; ++w)
-            if (hbp_ctx_create(ctx->device, &workers[static_cast<size_t>(w)]) != HBP_OK)
-                throw EngineError(HBP_ERR_CUDA, "sweep: cannot create a worker stream");
-        std::atomic<size_t> next{0};
-        auto work = [&](hbp_ctx* wc) {
-            for (size_t bi; (bi = next.fetch_add(1)) < blocks.size();)
-                sweep_block(*wc, corpus, blocks[bi], cand_groups, cand_offsets, cand_l_best, options, profile, pc,
-                            secs, errs);
-            cudaStreamSynchronize(wc->stream);
-        };
-        std::vector<std::thread> threads;
-        for (int w = 1; w < W; ++w) threads.emplace_back(work, workers[static_cast<size_t>(w)]);
-        work(workers[0]);
-        for (auto& t : threads) t.join();
-        for (auto* wc : workers) {
-            ctx->launches += wc->launches;
-            hbp_ctx_destroy(wc);
-        }
+        std::vector<int64_t> all(static_cast<size_t>(n_candidates));
+        for (int64_t k = 0; k < n_candidates; ++k) all[static_cast<size_t>(k)] = k;
+        sweep_evaluate(*ctx, corpus, cand_groups, cand_offsets, cand_l_best, all, options, profile, secs, errs);
         // the error the sequential sweep would raise: the first in index order
         for (int64_t k = 0; k < n_candidates; ++k)
             if (errs[static_cast<size_t>(k)].code != HBP_OK)
@@ -170,4 +212,14 @@ extern "C" int hbp_sweep(hbp_ctx* ctx, const hbp_samples* samples, const hbp_gro
         }
         *out_best = best;
     });
+}
+
+extern "C" int hbp_test_sweep_shard(const hbp_group_config* cand_groups, const int64_t* cand_offsets,
+                                    int64_t n_candidates, int32_t rank, int32_t world, int64_t* out_idx,
+                                    int64_t* out_n) {
+    if (world < 1 || rank < 0 || rank >= world || n_candidates < 0) return HBP_ERR_VALIDATION;
+    const auto v = sweep_shard(cand_groups, cand_offsets, n_candidates, rank, world);
+    for (size_t i = 0; i < v.size(); ++i) out_idx[i] = v[i];
+    *out_n = static_cast<int64_t>(v.size());
+    return HBP_OK;
 }

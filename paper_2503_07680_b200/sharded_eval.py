@@ -15,6 +15,12 @@ Gaps are integers, so the all-reduced sums are exact in any order and every
 rank's result is bit-identical to the single-GPU report() / simulate() of the
 whole plan (hbp_eval_columns*, include/hbp_b200.h). Over NCCL the exchanges
 are 6 + 2 vectors of n_iterations words.
+
+On GPUs the whole exchange runs in C++ on the engine's stream
+(hbp_eval_sharded over abi.Comm, `evaluate_nccl`). `sharded_evaluate` is the
+same protocol with a caller-supplied all_reduce (gloo on CPU hosts,
+tests/test_multiproc.py): the engine's kernels run on the context's stream,
+torch's fills and collectives on torch's, so it synchronises at each hand-over.
 """
 from __future__ import annotations
 
@@ -106,10 +112,20 @@ def sharded_evaluate(ctx: "abi.Context", plan: "abi.DevicePlanHandle", rank: int
     ctx.check(ctx.lib.hbp_plan_view_get(ctx.h, plan.h, C.byref(v)))
     c0, c1 = columns_of(rank, world, v.device_count)
     bufs = ColumnBuffers(v.n_iterations, torch.device("cuda", torch.cuda.current_device()))
-    eval_phase(ctx, plan, 0, c0, c1, bufs, profile)
+    # torch zero-filled the buffers on its current stream; the engine's kernels
+    # run on the context's (non-blocking) stream
+    torch.cuda.current_stream().synchronize()
+    eval_phase(ctx, plan, 0, c0, c1, bufs, profile)  # returns with the context stream drained
     if all_reduce is not None and world > 1:
         reduce_phase0(bufs, all_reduce)
+        torch.cuda.current_stream().synchronize()  # NCCL's all_reduce returns before it lands
     eval_phase(ctx, plan, 1, c0, c1, bufs, profile)
     if all_reduce is not None and world > 1:
         reduce_phase1(bufs, all_reduce)
+        torch.cuda.current_stream().synchronize()
     return eval_finish(ctx, plan, bufs, profile)
+
+
+def evaluate_nccl(comm: "abi.Comm", plan: "abi.DevicePlanHandle", profile: Optional[abi.HardwareProfile] = None):
+    """hbp_eval_sharded: phases and both NCCL exchanges in C++ on the engine's stream."""
+    return comm.evaluate(plan, profile)

@@ -8,9 +8,13 @@ Each candidate's time is simulate(build_plan(corpus, groups_c)).total_seconds
 
 Multi-GPU: candidates that share a length set share one plan, so whole length
 sets are dealt to ranks (round-robin in decreasing estimated cost); every rank
-runs hbp_sweep on its share on its own GPU and one all_gather of
-(best_seconds, best_index) -- 16 bytes per rank, NCCL over NVLink -- yields the
-global argmin. No data-path collective.
+evaluates its share on its own GPU, then one ncclAllGather of
+(best_seconds, best_index) -- 16 bytes per rank over NVLink -- yields the
+global argmin (plus an all-reduce MIN of the per-candidate seconds so every
+rank holds them all). No data-path collective. On GPUs this runs in C++
+(hbp_sweep_sharded over the engine's NCCL communicator, `run_sweep_nccl`);
+`run_sweep` is the same dealing with a caller-supplied all_gather (gloo on
+CPU hosts, tests/test_multiproc.py).
 """
 from __future__ import annotations
 
@@ -117,3 +121,21 @@ def run_sweep(ctx: "abi.Context", samples_struct, candidates: Sequence[Candidate
     if world > 1 and all_gather is not None:
         return secs, reduce_argmin(local, all_gather)
     return secs, local
+
+
+def engine_comm(ctx: "abi.Context", dist) -> "abi.Comm":
+    """The engine's NCCL communicator for the ranks of `dist` (torch.distributed
+    carries the 128-byte NCCL id from rank 0; every collective after that is
+    the engine's own, on its stream)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    box = [abi.Comm.unique_id(ctx) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return abi.Comm(ctx, box[0], rank, world)
+
+
+def run_sweep_nccl(comm: "abi.Comm", samples_struct, candidates: Sequence[Candidate],
+                   profile: Optional[abi.HardwareProfile] = None, **opts):
+    """hbp_sweep_sharded: (seconds of every candidate, (best seconds, best
+    index), candidates this rank evaluated) -- identical on every rank."""
+    secs, best, local = comm.sweep(samples_struct, candidates, profile, **opts)
+    return secs, ((float(secs[best]) if best >= 0 else math.inf), best), local

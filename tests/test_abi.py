@@ -84,3 +84,40 @@ def test_synth_errors():
     rc = lib.hbp_synth_lengths(C.c_int64(4), b"gamma:1:2", C.c_double(0), b"", C.c_int64(10), C.c_uint64(0),
                                out.ctypes.data_as(C.POINTER(C.c_int64)), err, 256)
     assert rc == abi.HBP_ERR_VALIDATION and err.value == b"unknown distribution family: gamma"
+
+
+def _c3_like_candidates():
+    """C3's candidate order (sweep.make_candidates) with ckpt 0: the dealing
+    only reads the length sets."""
+    import itertools
+    out = []
+    smaller = [512, 1024, 2048, 4096, 8192, 16384, 32768, 65536]
+    for r in range(len(smaller) + 1):
+        for subset in itertools.combinations(smaller, r):
+            ls = list(subset) + [131072]
+            for sp in (1, 2, 4, 8):
+                for _gc in (True, False):
+                    out.append(([(l, 1 if i == 0 else sp, 0) for i, l in enumerate(ls)], ls[0]))
+    return out
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_sweep_shard_matches_python_dealing(world):
+    # hbp_sweep_sharded deals length sets in C++; sweep.shard() is the same
+    # rule on the Python (gloo) path: both must give every rank the same share
+    from paper_2503_07680_b200 import sweep
+    lib = abi.load_library()
+    cands = _c3_like_candidates()
+    garr, offs, _ = abi.flatten_candidates(cands)
+    lib.hbp_test_sweep_shard.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                         C.POINTER(C.c_int64)]
+    seen = []
+    for rank in range(world):
+        out = np.zeros(len(cands), dtype=np.int64)
+        n = C.c_int64()
+        assert lib.hbp_test_sweep_shard(garr, offs.ctypes.data, len(cands), rank, world, out.ctypes.data,
+                                        C.byref(n)) == abi.HBP_OK
+        got = out[:n.value].tolist()
+        assert got == sweep.shard(cands, rank, world)
+        seen += got
+    assert sorted(seen) == list(range(len(cands)))

@@ -57,8 +57,12 @@ def _fy_model(seed, m, forced):
 @pytest.mark.parametrize("forced", [0, 2, 1234, 5000])
 def test_shuffle_rejection_repair(ctx, monkeypatch, forced):
     # the repair path of a rejected draw (probability < m / 2^64 in real
-    # runs), forced through HBP_FY_FORCE_REJECT and checked against the model
-    if forced:
-        monkeypatch.setenv("HBP_FY_FORCE_REJECT", str(forced))
-    got = ctx.shuffle_positions(77, 5000)
+    # runs), forced through hbp_test_set_force_reject and checked against the model
+    import ctypes as C
+    ctx.lib.hbp_test_set_force_reject.argtypes = [C.c_void_p, C.c_uint64]
+    ctx.check(ctx.lib.hbp_test_set_force_reject(ctx.h, forced))
+    try:
+        got = ctx.shuffle_positions(77, 5000)
+    finally:
+        ctx.check(ctx.lib.hbp_test_set_force_reject(ctx.h, 0))
     assert np.array_equal(got, _fy_model(77, 5000, forced))

@@ -19,6 +19,7 @@ def emulate(ctx, plan, world, profile):
     n_it, N = len(v.iter_group), v.device_count
     dev = torch.device("cuda", 0)
     ranks = [se.ColumnBuffers(n_it, dev) for _ in range(world)]
+    torch.cuda.synchronize()  # torch's zero fills before the engine's stream writes
     for r, b in enumerate(ranks):
         se.eval_phase(ctx, plan, 0, *se.columns_of(r, world, N), b, profile)
     ops = {se.MAX: torch.maximum, se.SUM: torch.add, se.MIN: torch.minimum}
@@ -29,6 +30,7 @@ def emulate(ctx, plan, world, profile):
             acc = ops[op](acc, get(b))
         for b in ranks:
             get(b).copy_(acc)
+        torch.cuda.synchronize()  # torch's stream before the engine's next phase
 
     for k, op in (("tmax", se.MAX), ("amax", se.MAX), ("tokens", se.SUM), ("pad_gap", se.SUM), ("pad_cap", se.SUM)):
         all_reduce_over(lambda b, k=k: b.t[k], op)

@@ -121,7 +121,7 @@ struct RunStage {
 
 // One run `r` against the lanes in `allowed` (bin order = lane order).
 template <int M, bool STORE>
-__device__ __forceinline__ void serve_run(const ChainArgs& a, int r, unsigned allowed, u32 s, u32 inv_own,
+__device__ __forceinline__ bool serve_run(const ChainArgs& a, int r, unsigned allowed, u32 s, u32 inv_own,
                                           u32 end_item, u32& c, u32 (&R)[M], u32 (&N)[M], u32& lmax, u64 base,
                                           u32 lane) {
     const u32 Sraw = __shfl_sync(0xffffffffu, s, r);
@@ -131,7 +131,7 @@ __device__ __forceinline__ void serve_run(const ChainArgs& a, int r, unsigned al
     u32 off = 0;
     if (STORE) off = __shfl_sync(0xffffffffu, end_item - c, r);
     unsigned room = __ballot_sync(0xffffffffu, lmax >= S + strict) & allowed;
-    if (!room) return;
+    if (!room) return false;
     u32 capl[M], pre[M + 1];
     pre[0] = 0;
 #pragma unroll
@@ -185,6 +185,7 @@ __device__ __forceinline__ void serve_run(const ChainArgs& a, int r, unsigned al
         }
         lmax = nl;
     }
+    return true;
 }
 
 // FFD frontier in closed form. The runs of `seg` share k = floor(cap / s):
@@ -293,11 +294,18 @@ __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 en
         k_own = __umulhi(a.cap, inv_own);
         k_own += (a.cap - k_own * s_own >= s_own) ? 1u : 0u;
     }
+    // A run is active when s <= the warp's max residual at the block's
+    // arrival; every take lowers residuals, so after one the runs that no
+    // longer fit anywhere are dropped at once (one reduce + one ballot) instead
+    // of each paying a serve that finds no room (most active runs of greedy
+    // fill and of FFD's later blocks, measured on C2).
+    const u32 s_eff = s_own + (s >> 31);
     while (act) {
         const int r = __ffs(act) - 1;
         if (!emask) {
             act &= act - 1;
-            serve_run<M, STORE>(a, r, 0xffffffffu, s, inv_own, end_item, c, R, N, lmax, base, lane);
+            if (serve_run<M, STORE>(a, r, 0xffffffffu, s, inv_own, end_item, c, R, N, lmax, base, lane) && act)
+                act &= __ballot_sync(0xffffffffu, s_eff <= __reduce_max_sync(0xffffffffu, lmax));
             continue;
         }
         const u32 kr = __shfl_sync(0xffffffffu, k_own, r);
@@ -309,8 +317,15 @@ __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 en
         const unsigned upto = breaks ? (1u << (__ffs(breaks) - 1)) - 1u : 0xffffffffu;
         const unsigned seg = act & upto;
         act &= ~seg;
-        for (unsigned q = seg; q; q &= q - 1)
-            serve_run<M, STORE>(a, __ffs(q) - 1, ~emask, s, inv_own, end_item, c, R, N, lmax, base, lane);
+        // against the non-empty lanes only the runs that fit one of them
+        const bool ne_lane = ((emask >> lane) & 1u) == 0;
+        unsigned q = seg & __ballot_sync(0xffffffffu, s_eff <= __reduce_max_sync(0xffffffffu, ne_lane ? lmax : 0u));
+        while (q) {
+            const int rr = __ffs(q) - 1;
+            q &= q - 1;
+            if (serve_run<M, STORE>(a, rr, ~emask, s, inv_own, end_item, c, R, N, lmax, base, lane) && q)
+                q &= __ballot_sync(0xffffffffu, s_eff <= __reduce_max_sync(0xffffffffu, ne_lane ? lmax : 0u));
+        }
         frontier_fill<M, STORE>(a, seg, kr, s, end_item, c, R, N, lmax, emask, st, base, lane);
     }
     wmax = __reduce_max_sync(0xffffffffu, lmax);
@@ -709,6 +724,22 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
         return true;
     }
     cudaStream_t s = c.stream;
+    if (c.trace) {
+        if (const char* rf = std::getenv("HBP_CHAIN_RUNS")) {  // the chain's input, appended (analysis tools)
+            const auto rl = read_vector(c, runs.run_len, runs.n_runs);
+            const auto ri = read_vector(c, runs.run_item, runs.n_runs);
+            const auto lv = read_vector(c, leaves, live);
+            if (FILE* f = std::fopen(rf, "ab")) {
+                const u32 hdr[8] = {runs.n_runs, runs.n_items, live, n_bins, cap, static_cast<u32>(ffd),
+                                    runs.run_begin, runs.run_end};
+                std::fwrite(hdr, 4, 8, f);
+                std::fwrite(rl.data(), 4, rl.size(), f);
+                std::fwrite(ri.data(), 4, ri.size(), f);
+                std::fwrite(lv.data(), 8, lv.size(), f);
+                std::fclose(f);
+            }
+        }
+    }
     int dev = 0, sms = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

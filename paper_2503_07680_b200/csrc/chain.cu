@@ -61,6 +61,7 @@ struct ChainArgs {
     u32* carry_out;        // per run: items this pass leaves
     int ffd;
     u32 J, nblocks;
+    u32 rb;  // runs per block (lanes 0..rb-1 carry them; 8, 16 or 32)
     unsigned long long* gring;  // CTA g -> g+1: kQ * 32 tagged counts
     u32* gcons;                 // gcons[(g+1) * kStride]: blocks CTA g+1's first warp has read
     u32* item_bin;   // heads only: at the first item of each take
@@ -446,8 +447,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
 
     // run data of block b, prefetched one block ahead
     auto load_runs = [&](u32 b, u32& s, u32& e, u32& st) {
-        const u32 k = a.run_begin + b * 32 + lane;
-        const bool valid = b < a.nblocks && k < a.run_end;
+        const u32 k = a.run_begin + b * a.rb + lane;
+        const bool valid = b < a.nblocks && lane < a.rb && k < a.run_end;
         s = valid ? a.run_len[k] : 0u;
         st = valid ? a.run_item[k] : 0u;
         e = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
@@ -464,8 +465,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
         const unsigned long long tag = static_cast<unsigned long long>(b + 1) << 32;
         u32 c;
         if (head) {
-            const u32 k = a.run_begin + b * 32 + lane;
-            c = a.carry_in ? (k < a.run_end ? a.carry_in[k] : 0u) : end_item - start_item;
+            const u32 k = a.run_begin + b * a.rb + lane;
+            c = a.carry_in ? (lane < a.rb && k < a.run_end ? a.carry_in[k] : 0u) : end_item - start_item;
         } else if (in_global) {
             unsigned long long v;
             while (((v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane)) >> 32) != (b + 1))
@@ -494,7 +495,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
         }
         if (act) {
             if (a.hist) {  // the replay re-serves this cell from its input counts
-                a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane] = c;
+                if (lane < a.rb) a.hist[(static_cast<u64>(j) * a.nblocks + b) * a.rb + lane] = c;
                 if (lane == 0) a.hact[static_cast<u64>(j) * a.nblocks + b] = act;
             }
             if (a.hist) serve<M, false>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);
@@ -529,8 +530,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
                 sout[(b % kQs) * 32 + lane] = v;
             }
         } else {  // tail: hand the counts to the next pass
-            const u32 k = a.run_begin + b * 32 + lane;
-            if (k < a.run_end) a.carry_out[k] = c;
+            const u32 k = a.run_begin + b * a.rb + lane;
+            if (lane < a.rb && k < a.run_end) a.carry_out[k] = c;
             if (__any_sync(0xffffffffu, c > 0) && lane == 0) atomicOr(a.out + 1, 1u);
         }
         if (a.prof) pf[2] += clock64() - t0;
@@ -564,11 +565,11 @@ __global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
     for (u32 b = 0; b < a.nblocks; ++b) {
         const u32 act = a.hact[static_cast<u64>(j) * a.nblocks + b];
         if (!act) continue;
-        const u32 k = a.run_begin + b * 32 + lane;
-        const bool valid = k < a.run_end;
+        const u32 k = a.run_begin + b * a.rb + lane;
+        const bool valid = lane < a.rb && k < a.run_end;
         const u32 s = valid ? a.run_len[k] : 0u;
         const u32 end_item = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
-        u32 c = a.hist[(static_cast<u64>(j) * a.nblocks + b) * 32 + lane];
+        u32 c = valid ? a.hist[(static_cast<u64>(j) * a.nblocks + b) * a.rb + lane] : 0u;
         serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[threadIdx.x >> 5], base, lane);
     }
     store_bins<M>(a, base, lane, R, N, true);
@@ -651,7 +652,7 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     DevBuf<u32> hist, hact;
     a.hist = a.hact = nullptr;
     if (replay) {
-        hist.alloc(static_cast<size_t>(J) * a.nblocks * 32, s);
+        hist.alloc(static_cast<size_t>(J) * a.nblocks * a.rb, s);
         hact.alloc(static_cast<size_t>(J) * a.nblocks, s);
         a.hist = hist.p;
         a.hact = hact.p;
@@ -793,7 +794,12 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     a.n_bins = n_bins;
     a.cap = cap;
     a.ffd = ffd ? 1 : 0;
-    a.nblocks = (runs.run_end - runs.run_begin + 31) / 32;
+    // runs per block: small blocks shorten each warp's serve of the block
+    // that walks the whole chain last; large ones amortise the hand-off
+    const char* erb = std::getenv("HBP_CHAIN_RB");
+    a.rb = erb ? static_cast<u32>(std::atoi(erb)) : 32u;
+    if (a.rb != 8 && a.rb != 16) a.rb = 32;
+    a.nblocks = (runs.run_end - runs.run_begin + a.rb - 1) / a.rb;
     a.item_bin = item_bin;
     a.item_slot = item_slot;
     a.take = take;

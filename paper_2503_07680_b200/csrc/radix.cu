@@ -4,149 +4,247 @@
 // comparison sort with a total order: sort_decreasing (packing.cpp:55-60,
 // length desc / id asc over an id-ordered input), the stable attention sort
 // of balance_batching (balance.cpp:185-189) and the per-length FIFO order of
-// greedy_fill (balance.cpp:52-60). Each 8-bit pass: (1) per-tile digit
-// histograms staged in shared memory, written digit-major; (2) one
-// decoupled look-back scan gives every (digit, tile) its global offset;
-// (3) the tile is re-read and each element gets its stable rank inside the
-// tile from warp match masks plus per-warp digit counters, then is written
-// to offset + rank. Descending order sorts ~key.
+// greedy_fill (balance.cpp:52-60). Onesweep: one read of the keys builds
+// the digit histograms of every 8-bit pass; each pass is then one kernel
+// (tiles staged by bulk asynchronous copies, stable warp-match ranks, look-back
+// across tiles, coalesced digit-ordered writes). Descending order sorts ~key.
 #include "engine.cuh"
 #include "radix.cuh"
+
+#include <mutex>
+#include <set>
 
 namespace hbp_b200 {
 
 namespace {
 
-#ifndef HBP_RADIX_ITEMS
-#define HBP_RADIX_ITEMS 8
-#endif
-#ifndef HBP_RADIX_MINB
-#define HBP_RADIX_MINB 4
-#endif
-constexpr int RB = 256;                   // threads per block
-constexpr int RITEMS = HBP_RADIX_ITEMS;   // elements per thread per tile
-constexpr int RTILE = RB * RITEMS;
-constexpr int RW = RB / 32;  // warps per block
+// ---------------------------------------------------------------------------
+// Onesweep (one histogram pass for every digit, then one kernel per digit
+// pass with decoupled look-back across tiles; no per-pass histogram or scan
+// launches). Tiles of 4096 pairs are staged in shared memory by one bulk
+// asynchronous copy (cp.async.bulk, completion on an mbarrier), ranked
+// stably with warp match masks in warp-striped order, counted per digit,
+// offset across tiles by look-back on (flag << 62 | count) status words, and
+// written out in digit order so global stores are coalesced.
+// ---------------------------------------------------------------------------
+constexpr int OB = 256;
+constexpr int OITEMS = 16;
+constexpr int OTILE = OB * OITEMS;  // 4096 pairs
+constexpr int OW = OB / 32;
+constexpr int OMAXP = 4;            // digit passes (32-bit keys)
+constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-__device__ __forceinline__ u32 digit_of(u32 k, int shift, bool desc) {
-    const u32 kk = desc ? ~k : k;
-    return (kk >> shift) & 0xffu;
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+    return static_cast<u32>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, u32 phase) {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64g(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64g(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Lanes of the warp holding the same 8-bit digit (among `valid` lanes):
-// eight ballots, cheaper than match.any on B200.
-__device__ __forceinline__ unsigned digit_peers(u32 d, bool valid) {
-    unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const bool bit = (d >> b) & 1u;
-        const unsigned m = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? m : ~m;
-    }
-    return peers;
-}
-
-__global__ void __launch_bounds__(RB) k_radix_hist(const u32* __restrict__ keys, u64 n, int shift, bool desc,
-                                                   u32* __restrict__ hist, u32 ntiles) {
-    __shared__ u32 h[RW][256];
-    for (int i = threadIdx.x; i < RW * 256; i += RB) (&h[0][0])[i] = 0;
+// Digit histograms of every pass in one read of the keys (16-byte loads):
+// counters per (digit, lane) -- lane l of every warp updates column l, so a
+// warp's 32 updates never share an address or a bank whatever the digits
+// (lengths crowd a few high digits). The last block to finish turns the
+// histograms into each pass's bucket starts.
+__global__ void __launch_bounds__(OB) k_os_hist(const u32* __restrict__ keys, u64 n, int passes, bool desc,
+                                               u32* __restrict__ ghist, u32* __restrict__ gstart,
+                                               u32* __restrict__ ticket) {
+    extern __shared__ u32 h[];  // [passes][256][32]
+    __shared__ bool s_last;
+    for (int i = threadIdx.x; i < passes * 256 * 32; i += OB) h[i] = 0;
     __syncthreads();
-    const u64 base = static_cast<u64>(blockIdx.x) * RTILE;
-    const unsigned w = warp_id(), lane = lane_id();
-#pragma unroll 4
-    for (int k = 0; k < RITEMS; ++k) {
-        const u64 i = base + static_cast<u64>(k) * RB + threadIdx.x;
-        const bool valid = i < n;
-        const u32 d = valid ? digit_of(keys[i], shift, desc) : 0u;
-        const unsigned peers = digit_peers(d, valid);
-        if (valid && (peers & ((1u << lane) - 1u)) == 0) h[w][d] += __popc(peers);  // one leader per digit
-        __syncwarp();  // the next item's leader of the same digit may be another lane
+    const unsigned lane = lane_id();
+    const u64 nv = n / 4;
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    auto add = [&](u32 k) {
+        const u32 kk = desc ? ~k : k;
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[(p * 256 + ((kk >> (8 * p)) & 0xffu)) * 32 + lane], 1u);
+    };
+    const u64 stride = static_cast<u64>(gridDim.x) * OB;
+    for (u64 v = static_cast<u64>(blockIdx.x) * OB + threadIdx.x; v < nv; v += stride) {
+        const uint4 q = k4[v];
+        add(q.x);
+        add(q.y);
+        add(q.z);
+        add(q.w);
     }
+    if (blockIdx.x == 0 && threadIdx.x < n - nv * 4) add(keys[nv * 4 + threadIdx.x]);  // the n % 4 tail
     __syncthreads();
-    for (int d = threadIdx.x; d < 256; d += RB) {
-        u32 s = 0;
-#pragma unroll
-        for (int q = 0; q < RW; ++q) s += h[q][d];
-        hist[static_cast<u64>(d) * ntiles + blockIdx.x] = s;
+    for (int i = threadIdx.x; i < passes * 256; i += OB) {
+        u32 c = 0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) c += h[i * 32 + ((l + i) & 31)];  // rotated: no bank conflict
+        if (c) atomicAdd(&ghist[i], c);
     }
-}
-
-// Scatter of one pass. Ranks the tile in shared memory (warp match masks
-// give each element its rank among equal digits of its warp; per-warp digit
-// counts, a prefix over warps and one block scan over digits give the
-// tile-local digit starts), places keys and values there in digit order, then
-// writes them out striped: consecutive threads write consecutive positions of
-// a digit's run, so global writes are coalesced. Three block barriers per
-// tile. Warp w owns the contiguous chunk [w * 512, (w + 1) * 512) of the tile,
-// which keeps the ranking stable.
-__global__ void __launch_bounds__(RB, HBP_RADIX_MINB) k_radix_scatter(const u32* __restrict__ keys_in,
-                                                      const u32* __restrict__ vals_in, u32* __restrict__ keys_out,
-                                                      u32* __restrict__ vals_out, u64 n, int shift, bool desc,
-                                                      const u32* __restrict__ offs, u32 ntiles) {
-    __shared__ u32 s_k[RTILE];
-    __shared__ u32 s_v[RTILE];
-    __shared__ unsigned short s_wc[RW][256];  // per-warp digit counts, then offsets within the digit
-    __shared__ u32 s_dstart[256];
-    __shared__ u32 s_goff[256];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     __shared__ u32 s_red[33];
-    const unsigned lane = lane_id(), w = warp_id();
-    const u64 base = static_cast<u64>(blockIdx.x) * RTILE;
-    const u32 len = static_cast<u32>(base + RTILE < n ? RTILE : n - base);
-    for (int d = lane; d < 256; d += 32) s_wc[w][d] = 0;
-    __syncwarp();
-    constexpr int PER_WARP = RTILE / RW;  // 512
-    u32 key[RITEMS], val[RITEMS], dg[RITEMS], rk[RITEMS];
-#pragma unroll
-    for (int k = 0; k < RITEMS; ++k) {
-        const u32 li = w * PER_WARP + k * 32 + lane;
-        const bool valid = li < len;
-        key[k] = valid ? keys_in[base + li] : 0u;
-        val[k] = valid ? vals_in[base + li] : 0u;
-        dg[k] = valid ? digit_of(key[k], shift, desc) : 256u;
+    for (int p = 0; p < passes; ++p) {
+        const u32 c = *reinterpret_cast<volatile u32*>(&ghist[p * 256 + threadIdx.x]);
+        u32 tot;
+        gstart[p * 256 + threadIdx.x] = block_exclusive_scan<u32>(c, s_red, tot);
     }
+}
+
+// Look-back of digit d for `tile`: the exclusive count of d over the tiles
+// before it -- aggregates summed back to the first inclusive count, polling
+// a word not yet published. (A window of eight words per round trip spilled
+// registers and measured slower.)
+__device__ __forceinline__ unsigned long long look_back(const unsigned long long* __restrict__ status, u32 tile,
+                                                        u32 d) {
+    unsigned long long excl = 0;
+    long long p = static_cast<long long>(tile) - 1;
+    for (;;) {
+        const unsigned long long wv = ld_relaxed_u64g(status + static_cast<u64>(p) * 256 + d);
+        const unsigned long long f = wv & ~kValMask;
+        if (f == 0) continue;
+        excl += wv & kValMask;
+        if (f == kIncl) return excl;
+        --p;
+    }
+}
+
+// One digit pass over a tile (dynamic tile order, so every earlier tile is
+// running or done when a tile looks back).
+template <bool BALLOT>
+__global__ void __launch_bounds__(OB, 3) k_os_pass(const u32* __restrict__ keys_in, const u32* __restrict__ vals_in,
+                                                  u32* __restrict__ keys_out, u32* __restrict__ vals_out, u64 n,
+                                                  int shift, bool desc, const u32* __restrict__ gstart,
+                                                  unsigned long long* __restrict__ status, u32* __restrict__ tiles,
+                                                  bool bulk) {
+    extern __shared__ __align__(128) u32 os_smem[];
+    u32* s_k = os_smem;  // tile as loaded
+    u32* s_v = s_k + OTILE;
+    auto* s_kv = reinterpret_cast<unsigned long long*>(s_v + OTILE);  // tile in digit order: key | val << 32
+    __shared__ unsigned short s_wc[OW][256];
+    __shared__ u32 s_lstart[256];
+    __shared__ int s_gbase[256];
+    __shared__ u32 s_red[33];
+    __shared__ u32 s_tile;
+    __shared__ alignas(8) unsigned long long s_bar;
+    const unsigned tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    if (tid == 0) {
+        s_tile = atomicAdd(tiles, 1u);
+        mbar_init(&s_bar, 1);
+    }
+    for (int i = tid; i < OW * 256 / 2; i += OB) reinterpret_cast<u32*>(&s_wc[0][0])[i] = 0;
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 base = static_cast<u64>(tile) * OTILE;
+    const u32 len = static_cast<u32>(base + OTILE <= n ? OTILE : n - base);
+    if (bulk && len == OTILE) {
+        if (tid == 0) {
+            mbar_expect_tx(&s_bar, 2u * OTILE * 4u);
+            bulk_g2s(s_k, keys_in + base, OTILE * 4u, &s_bar);
+            bulk_g2s(s_v, vals_in + base, OTILE * 4u, &s_bar);
+        }
+        mbar_wait(&s_bar, 0);
+    } else {
+        for (u32 i = tid; i < len; i += OB) {
+            s_k[i] = keys_in[base + i];
+            s_v[i] = vals_in[base + i];
+        }
+        __syncthreads();
+    }
+    // stable ranks: warp w owns elements [w * 512, (w + 1) * 512), row by
+    // row; rank (9 bits) and digit (9 bits, 256 = none) packed per element
+    u32 rd[OITEMS], key[OITEMS];
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int k = 0; k < RITEMS; ++k) {
-        const u32 d = dg[k];
-        const unsigned peers = digit_peers(d, d < 256u);
-        const u32 old = d < 256u ? s_wc[w][d] : 0u;
-        rk[k] = old + __popc(peers & lt);
-        __syncwarp();
-        if (d < 256u && (peers & lt) == 0) s_wc[w][d] = static_cast<unsigned short>(old + __popc(peers));
-        __syncwarp();
-    }
-    __syncthreads();
-    {
-        const u32 d = threadIdx.x;  // RB == 256 digits
-        u32 run = 0;
+    for (int i = 0; i < OITEMS; ++i) {
+        const u32 e = w * (OITEMS * 32) + i * 32 + lane;
+        const bool valid = e < len;
+        key[i] = valid ? s_k[e] : 0u;
+        const u32 d = valid ? ((desc ? ~key[i] : key[i]) >> shift) & 0xffu : 256u;
+        unsigned peers;
+        if (BALLOT) {  // eight ballots instead of one match (lanes with d == 256 never match a valid digit)
+            peers = __ballot_sync(0xffffffffu, valid);
+            if (!valid) peers = ~peers;
 #pragma unroll
-        for (int q = 0; q < RW; ++q) {
-            const u32 c = s_wc[q][d];
-            s_wc[q][d] = static_cast<unsigned short>(run);
-            run += c;
+            for (int b = 0; b < 8; ++b) {
+                const bool bit = (d >> b) & 1u;
+                const unsigned m = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? m : ~m;
+            }
+        } else {
+            peers = __match_any_sync(0xffffffffu, d);
         }
-        u32 tot;
-        const u32 ex = block_exclusive_scan<u32>(run, s_red, tot);
-        s_dstart[d] = ex;
-        s_goff[d] = offs[static_cast<u64>(d) * ntiles + blockIdx.x];
+        const u32 old = valid ? s_wc[w][d] : 0u;
+        rd[i] = ((old + __popc(peers & lt)) << 16) | d;
+        __syncwarp();
+        if (valid && (peers & lt) == 0) s_wc[w][d] = static_cast<unsigned short>(old + __popc(peers));
+        __syncwarp();
     }
     __syncthreads();
+    // digit d = tid: offsets of the warps inside the tile, the tile's count
+    const u32 d = tid;
+    u32 run = 0;
 #pragma unroll
-    for (int k = 0; k < RITEMS; ++k) {
-        const u32 d = dg[k];
-        if (d < 256u) {
-            const u32 p = s_dstart[d] + s_wc[w][d] + rk[k];
-            s_k[p] = key[k];
-            s_v[p] = val[k];
+    for (int q = 0; q < OW; ++q) {
+        const u32 c = s_wc[q][d];
+        s_wc[q][d] = static_cast<unsigned short>(run);
+        run += c;
+    }
+    // publish this tile's count, then look back for the counts before it
+    unsigned long long* st = status + static_cast<u64>(tile) * 256 + d;
+    st_relaxed_u64g(st, (tile == 0 ? kIncl : kAgg) | run);
+    u32 tot;
+    const u32 lstart = block_exclusive_scan<u32>(run, s_red, tot);
+    const unsigned long long excl = tile > 0 ? look_back(status, tile, d) : 0ull;
+    if (tile > 0) st_relaxed_u64g(st, kIncl | (excl + run));
+    s_lstart[d] = lstart;
+    // global position = s_gbase[digit] + position in the digit-ordered tile (n < 2^31)
+    s_gbase[d] = static_cast<int>(gstart[d] + excl) - static_cast<int>(lstart);
+    __syncthreads();
+    // stage in digit order, then write out coalesced
+#pragma unroll
+    for (int i = 0; i < OITEMS; ++i) {
+        const u32 dd = rd[i] & 0xffffu;
+        if (dd < 256u) {
+            const u32 e = w * (OITEMS * 32) + i * 32 + lane;
+            const u32 p = s_lstart[dd] + s_wc[w][dd] + (rd[i] >> 16);
+            s_kv[p] = static_cast<unsigned long long>(key[i]) | (static_cast<unsigned long long>(s_v[e]) << 32);
         }
     }
     __syncthreads();
-    for (u32 p = threadIdx.x; p < len; p += RB) {
-        const u32 kk = s_k[p];
-        const u32 d = digit_of(kk, shift, desc);
-        const u32 g = s_goff[d] + (p - s_dstart[d]);
+    for (u32 p = tid; p < len; p += OB) {
+        const unsigned long long kv = s_kv[p];
+        const u32 kk = static_cast<u32>(kv);
+        const u32 dd = ((desc ? ~kk : kk) >> shift) & 0xffu;
+        const u64 g = static_cast<u64>(static_cast<long long>(s_gbase[dd]) + p);
         keys_out[g] = kk;
-        vals_out[g] = s_v[p];
+        vals_out[g] = static_cast<u32>(kv >> 32);
     }
 }
 
@@ -157,9 +255,6 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
     if (n_signed <= 1) return;
     const u64 n = static_cast<u64>(n_signed);
     cudaStream_t s = c.stream;
-    const u32 ntiles = static_cast<u32>((n + RTILE - 1) / RTILE);
-    DevBuf<u32> hist(static_cast<size_t>(ntiles) * 256, s);
-    DevBuf<u32> offs(static_cast<size_t>(ntiles) * 256, s);
     DevBuf<u32> tk, tv;
     if (!tmp_keys) {
         tk.alloc(n, s);
@@ -169,18 +264,54 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
         tv.alloc(n, s);
         tmp_vals = tv.p;
     }
-    const int passes = (bits + 7) / 8;
+    const int passes = std::max(1, std::min(OMAXP, (bits + 7) / 8));
+    const u32 ntiles = static_cast<u32>((n + OTILE - 1) / OTILE);
+    // one zeroed block: histograms, bucket starts, tickets, tile counters, look-back status
+    const size_t words = static_cast<size_t>(passes) * 256 * 2 + 1 + passes;
+    const size_t status_off = (words * 4 + 255) / 256 * 256;
+    const size_t bytes = status_off + sizeof(unsigned long long) * static_cast<size_t>(passes) * ntiles * 256;
+    DevBuf<unsigned char> scratch(bytes, s);
+    CUDA_CHECK(cudaMemsetAsync(scratch.p, 0, bytes, s));
+    u32* ghist = reinterpret_cast<u32*>(scratch.p);
+    u32* gstart = ghist + passes * 256;
+    u32* ticket = gstart + passes * 256;
+    u32* tiles = ticket + 1;
+    auto* status = reinterpret_cast<unsigned long long*>(scratch.p + status_off);
+    int dev = 0, sms = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const u32 hgrid = static_cast<u32>(std::min<u64>((n / 4 + OB - 1) / OB + 1, static_cast<u64>(sms) * 2));
+    const size_t hsmem = sizeof(u32) * passes * 256 * 32;
+    constexpr size_t kSmem = sizeof(u32) * 4 * OTILE;  // the tile + the digit-ordered tile
+    {  // once per device (the attribute is per device; its driver lock serialises sweep workers)
+        static std::mutex mu;
+        static std::set<int> done;
+        std::lock_guard<std::mutex> g(mu);
+        if (done.insert(dev).second) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_os_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmem)));
+            CUDA_CHECK(cudaFuncSetAttribute(k_os_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmem)));
+            CUDA_CHECK(cudaFuncSetAttribute(k_os_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(sizeof(u32) * OMAXP * 256 * 32)));
+        }
+    }
+    LAUNCH_B("radix.hist", 4.0 * n, k_os_hist, hgrid, OB, hsmem, s, keys, n, passes, descending, ghist, gstart,
+             ticket);
+    // the bulk copies need 16-byte aligned sources (every tile starts 16 KB in)
+    const bool bulk = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(vals) |
+                        reinterpret_cast<uintptr_t>(tmp_keys) | reinterpret_cast<uintptr_t>(tmp_vals)) & 15u) == 0;
+    static const int variant = std::getenv("HBP_RADIX_VARIANT") ? std::atoi(std::getenv("HBP_RADIX_VARIANT")) : 1;
     u32 *ki = keys, *vi = vals, *ko = tmp_keys, *vo = tmp_vals;
     for (int p = 0; p < passes; ++p) {
-        const int shift = 8 * p;
-        LAUNCH_B("radix.hist", 4.0 * n, k_radix_hist, ntiles, RB, 0, s, ki, n, shift, descending, hist.p, ntiles);
-        const u32* hp = hist.p;
-        u32* op = offs.p;
-        scan_exclusive<u32>(
-            static_cast<i64>(ntiles) * 256, [=] __device__(i64 i) { return hp[i]; },
-            [=] __device__(i64 i, u32 v) { op[i] = v; }, s, c.scan, "scan.radix1");
-        LAUNCH_B("radix.scatter", 16.0 * n, k_radix_scatter, ntiles, RB, 0, s, ki, vi, ko, vo, n, shift, descending,
-                 offs.p, ntiles);
+        if (variant == 0)
+            LAUNCH_B("radix.scatter", 16.0 * n, k_os_pass<false>, ntiles, OB, kSmem, s, ki, vi, ko, vo, n,
+                     8 * p, descending, gstart + p * 256, status + static_cast<size_t>(p) * ntiles * 256, tiles + p,
+                     bulk);
+        else
+            LAUNCH_B("radix.scatter", 16.0 * n, k_os_pass<true>, ntiles, OB, kSmem, s, ki, vi, ko, vo, n,
+                     8 * p, descending, gstart + p * 256, status + static_cast<size_t>(p) * ntiles * 256, tiles + p,
+                     bulk);
         std::swap(ki, ko);
         std::swap(vi, vo);
     }

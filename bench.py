@@ -447,8 +447,8 @@ def run_c4_leg(ctx, lib, comm, rank=0, world=1, dist=None, steps=3, warmup=3):
     """BASELINE config C4: 100M samples of the C2 spec, groups [16K sp1,
     128K sp8] with ckpt derived under the DeepSeek-V2 236B cost model, 8 DP
     devices: build_plan + report (ABR/CR) + simulate, corpus resident in HBM.
-    Also C5 on a bounded sample: the first length sets of the 4096-candidate
-    sweep (512 sets x SP{1,2,4,8} x GC{on,off}) over the same corpus."""
+    Then C5 in full: the 4096-candidate sweep (512 length sets x SP{1,2,4,8} x
+    GC{on,off}) over the same corpus, sharded across the ranks."""
     import torch
     from paper_2503_07680_b200 import abi, sweep
     stream = torch.cuda.ExternalStream(lib.hbp_ctx_stream(ctx.h))
@@ -515,23 +515,29 @@ def run_c4_leg(ctx, lib, comm, rank=0, world=1, dist=None, steps=3, warmup=3):
                            "exchange": "hbp_eval_sharded: ncclAllReduce MAX/SUM/MIN of 6 per-iteration vectors, "
                                        "then SUM of 2, on the engine's stream"}
     out = plan = None
-    if world > 1:
-        return res
-    # C5 bounded sample: the first K length sets (8 candidates each) over the 100M corpus
+    # C5 in full: 512 length sets x SP{1,2,4,8} x GC{on,off} = 4096 candidates
+    # over the same 100M corpus, length sets dealt across the ranks
+    # (hbp_sweep_sharded: one plan per set, NCCL MIN of the seconds and
+    # all-gather of each rank's best); wall time = max over ranks
     cands = sweep.make_candidates(ctx, 131072, [256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536], SWEEP_SP, prof)
-    K = 4
-    sample = cands[:8 * K]
     s, keep = abi.device_samples(0, d_len.data_ptr(), n, "c5")
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     t0 = time.perf_counter()
-    secs, best = ctx.sweep_samples(s, sample, prof, device_count=DEVICES, seed=PLAN_SEED)
+    secs, best, local = sweep.run_sweep_nccl(comm, s, cands, prof, device_count=DEVICES, seed=PLAN_SEED)
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
-    res["c5_sample"] = {"workload": f"C5 bounded sample: first {K} of 512 length sets x SP{{1,2,4,8}} x GC{{on,off}} "
-                                    "over the C4 corpus (100M), DeepSeek-V2 cost model",
-                        "candidates": len(sample), "of_candidates": len(cands), "seconds": el,
-                        "candidates_per_s": len(sample) / el,
-                        "feasible": int(sum(1 for v in secs if math.isfinite(v))), "best_index": int(best)}
+    if dist is not None:
+        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    res["c5"] = {"workload": "C5: 512 length sets ({131072} + subsets of {256..64K}) x SP{1,2,4,8} x GC{on,off} "
+                             "over the C4 corpus (100M), DeepSeek-V2 cost model, sharded by length set",
+                 "candidates": len(cands), "seconds": el, "candidates_per_s": len(cands) / el,
+                 "feasible": int(np.isfinite(secs).sum()), "best_index": int(best[1]),
+                 "best_groups": cands[best[1]][0] if best[1] >= 0 else None, "best_seconds": best[0],
+                 "local_candidates_rank0": local, "ranks": world}
     return res
 
 
@@ -665,7 +671,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override corpus size (default 10M)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the auto-selection sweep leg")
-    ap.add_argument("--no-c4", action="store_true", help="skip the 100M-sample C4 / C5-sample leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the 100M-sample C4 / C5 legs")
     ap.add_argument("--no-ingest", action="store_true", help="skip the corpus-file (JSONL) ingest leg")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -141,6 +141,17 @@ void sweep_evaluate(hbp_ctx& c, const DeviceCorpus& corpus, const hbp_group_conf
     // shared read-only.
     const char* ew = std::getenv("HBP_SWEEP_STREAMS");
     int W = ew ? std::atoi(ew) : 8;
+    // every worker holds one plan build in flight: ~300 B per sample at its
+    // peak (pools, shuffle and next-fit scratch, the pack table sized by n;
+    // measured 25 GB per worker at 100M), so at C5 sizes the free HBM, not
+    // the streams, bounds the concurrency
+    {
+        size_t free_b = 0, total_b = 0;
+        CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        const double per_worker = 300.0 * static_cast<double>(std::max<int64_t>(corpus.n, 1)) + (256.0 * (1 << 20));
+        const int by_mem = static_cast<int>(0.75 * static_cast<double>(free_b) / per_worker);
+        W = std::max(1, std::min(W, by_mem));
+    }
     W = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(W, static_cast<int64_t>(blocks.size()))));
     CUDA_CHECK(cudaStreamSynchronize(c.stream));  // corpus ready for the workers' streams
     std::vector<hbp_ctx*> workers(static_cast<size_t>(W), nullptr);

@@ -35,7 +35,10 @@ enum hbp_status {
     HBP_ERR_VALIDATION = 2,
     HBP_ERR_INFEASIBLE = 3,
     HBP_ERR_IO = 4,
-    HBP_ERR_CUDA = 5
+    HBP_ERR_CUDA = 5,
+    /* a JSON key or type error the reference raises as nlohmann::json::exception
+       (plan_from_json, io.cpp:112-160); the message is the library's what() */
+    HBP_ERR_JSON = 6
 };
 
 /* Same order as hbp::StrategyKind (include/hbp/packing.hpp:17). */

@@ -17,7 +17,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhbp_b200.so")
 
-HBP_OK, HBP_ERR_VALIDATION, HBP_ERR_INFEASIBLE, HBP_ERR_IO, HBP_ERR_CUDA = 0, 2, 3, 4, 5
+HBP_OK, HBP_ERR_VALIDATION, HBP_ERR_INFEASIBLE, HBP_ERR_IO, HBP_ERR_CUDA, HBP_ERR_JSON = 0, 2, 3, 4, 5, 6
 STRATEGIES = {"random": 0, "isf": 1, "ffs": 2, "ffd": 3, "bfs": 4, "spfhp": 5}
 HBP_MEM_HOST, HBP_MEM_DEVICE = 0, 1
 
@@ -38,6 +38,11 @@ class CudaError(RuntimeError):
     """A CUDA / internal failure of the engine (status 5)."""
 
 
+class JsonError(RuntimeError):
+    """nlohmann::json::exception (a manifest key / type error, status 6): the
+    reference's module has no mapping for it, so pybind11 raises RuntimeError."""
+
+
 def raise_status(code: int, msg: str) -> None:
     if code == HBP_OK:
         return
@@ -47,6 +52,8 @@ def raise_status(code: int, msg: str) -> None:
         raise InfeasibleError(msg)
     if code == HBP_ERR_IO:
         raise HbpIoError(msg)
+    if code == HBP_ERR_JSON:
+        raise JsonError(msg)
     raise CudaError(msg)
 
 

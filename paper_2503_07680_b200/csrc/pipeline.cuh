@@ -144,6 +144,10 @@ std::string footer_text(const DevicePlan& dp);
 u64 plan_json_body(Ctx& c, const DevicePlan& dp, const int64_t* ids, const int64_t* lens, DevBuf<char>* text);
 void plan_from_json_device(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, DevBuf<int64_t>& ids,
                            DevBuf<int64_t>& lens);
+// plan_json.cu: the reader for any JSON layout (plan_read.cu hands it what
+// is not canonical)
+void plan_from_json_general(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, DevBuf<int64_t>& ids,
+                            DevBuf<int64_t>& lens);
 // corpus.cu: text to the device (zero-padded to 16 bytes) and the start of
 // every line (starts[0] = 0, then one past each '\n'); returns the '\n' count.
 void upload_text(Ctx& c, const char* text, u64 bytes, DevBuf<unsigned char>& t);

@@ -218,19 +218,12 @@ bool parse_footer(const char* text, u64 bytes, bool has_iterations, DevicePlan& 
     return true;
 }
 
-[[noreturn]] void refuse(const char* text, u64 bytes) {
-    // not the canonical layout: the reference's message when it is not JSON
-    // at all (io.cpp:113-118), else a refusal -- this reader does not guess
-    const std::string what = json_parse_error_text(std::string(text, bytes));
-    if (!what.empty()) fail_validation("bad plan manifest: " + what);
-    fail_validation("plan manifest: not in the layout write_plan produces (the GPU reader reads canonical "
-                    "plan_to_json text)");
-}
+// not the canonical layout: the general reader (plan_json.cu) takes it
+struct NotCanonical {};
+[[noreturn]] void refuse(const char*, u64) { throw NotCanonical{}; }
 
-}  // namespace
-
-void plan_from_json_device(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, DevBuf<int64_t>& ids,
-                           DevBuf<int64_t>& lens) {
+void plan_from_json_canonical(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, DevBuf<int64_t>& ids,
+                              DevBuf<int64_t>& lens) {
     cudaStream_t s = c.stream;
     bool has_it = false;
     size_t head_len = 0, foot_len = 0;
@@ -377,6 +370,19 @@ void plan_from_json_device(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, 
         if ((e & 1ull) == 0) fail_validation("plan manifest: iteration group index out of range");
         fail_validation("plan manifest: pack exceeds its capacity");
     }
+}
+
+}  // namespace
+
+void plan_from_json_device(Ctx& c, const char* text, u64 bytes, DevicePlan& dp, DevBuf<int64_t>& ids,
+                           DevBuf<int64_t>& lens) {
+    try {
+        plan_from_json_canonical(c, text, bytes, dp, ids, lens);
+        return;
+    } catch (const NotCanonical&) {
+    }
+    dp.groups.clear();
+    plan_from_json_general(c, text, bytes, dp, ids, lens);
 }
 
 }  // namespace hbp_b200

@@ -392,6 +392,13 @@ void hbp_plan_free(hbp_plan* plan);
  * per_iteration_dbr / _abr may be NULL; otherwise [n_iterations]. */
 int hbp_report(hbp_ctx* ctx, const hbp_plan_view* plan, hbp_metrics* out,
                double* per_iteration_dbr, double* per_iteration_abr);
+/* Run-level totals for cr / ave_t over device batches (include/hbp/metrics.hpp:
+ * cr, ave_t; src/metrics.cpp:71-105): iteration i holds device batches
+ * [iter_dev_offsets[i], iter_dev_offsets[i + 1]) of `tokens` /
+ * `comm_tokens` (host arrays). out[0] = Σ tokens, out[1] = Σ comm tokens,
+ * out[2] = the most devices of any iteration. */
+int hbp_run_totals(hbp_ctx* ctx, const int64_t* tokens, const int64_t* comm_tokens, const int64_t* iter_dev_offsets,
+                   int64_t n_iterations, int64_t* out);
 int hbp_report_plan(hbp_ctx* ctx, hbp_plan* plan, hbp_metrics* out,
                     double* per_iteration_dbr, double* per_iteration_abr);
 

@@ -544,6 +544,26 @@ class Context:
                                       ptr(out, C.c_double), C.byref(best)))
         return out[:len(candidates)], best.value
 
+    def greedy_fill(self, pack_offsets, pack_capacity, ids, lengths, pool_offsets, pool_ids, pool_lengths):
+        """hbp_greedy_fill (balance.cpp:46-101): per pack, in pick order, the
+        flattened pool indices it takes; and which pool samples stay."""
+        class PacksIn(C.Structure):
+            _fields_ = [("n_packs", C.c_int64), ("pack_offsets", C.c_void_p), ("pack_capacity", C.c_void_p),
+                        ("ids", C.c_void_p), ("lengths", C.c_void_p)]
+        po, pc = (np.ascontiguousarray(x, dtype=np.int64) for x in (pack_offsets, pack_capacity))
+        pi, pl = (np.ascontiguousarray(x, dtype=np.int64) for x in (ids, lengths))
+        qo, qi, ql = (np.ascontiguousarray(x, dtype=np.int64) for x in (pool_offsets, pool_ids, pool_lengths))
+        packs = PacksIn(len(pc), po.ctypes.data, pc.ctypes.data, pi.ctypes.data, pl.ctypes.data)
+        m = int(qo[-1]) if len(qo) else 0
+        off = np.zeros(len(pc) + 1, np.int64)
+        added = np.zeros(max(m, 1), np.int64)
+        keep = np.zeros(max(m, 1), np.uint8)
+        self.lib.hbp_greedy_fill.argtypes = [C.c_void_p, C.POINTER(PacksIn), C.c_int32, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        self.check(self.lib.hbp_greedy_fill(self.h, C.byref(packs), len(qo) - 1, qo.ctypes.data, qi.ctypes.data,
+                                            ql.ctypes.data, off.ctypes.data, added.ctypes.data, keep.ctypes.data))
+        return off, added[:off[-1]], keep[:m].astype(bool)
+
     # -- stage hooks (include/hbp_b200_testing.h) --------------------------
     def shuffle_positions(self, seed: int, m: int) -> np.ndarray:
         out = np.zeros(max(m, 1), dtype=np.uint32)

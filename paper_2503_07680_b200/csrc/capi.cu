@@ -564,6 +564,57 @@ int hbp_report(hbp_ctx* ctx, const hbp_plan_view* plan, hbp_metrics* out, double
     });
 }
 
+namespace {
+// Σ tokens, Σ comm tokens and the widest iteration of a run of device
+// batches: integer sums, so the ratios the reference forms from its
+// sequential double sums (metrics.cpp:71-105) come out identical
+__global__ void k_run_totals(const int64_t* __restrict__ tokens, const int64_t* __restrict__ comm,
+                             const int64_t* __restrict__ iter_off, u64 n_iter, u64 n_dev,
+                             unsigned long long* __restrict__ out) {
+    unsigned long long t = 0, cm = 0, w = 0;
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n_dev || i < n_iter;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        if (i < n_dev) {
+            t += static_cast<unsigned long long>(tokens[i]);
+            cm += static_cast<unsigned long long>(comm[i]);
+        }
+        if (i < n_iter) w = max(w, static_cast<unsigned long long>(iter_off[i + 1] - iter_off[i]));
+    }
+    t = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(t & 0xffffffffu)) +
+        (static_cast<unsigned long long>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(t >> 32))) << 32);
+    cm = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cm & 0xffffffffu)) +
+         (static_cast<unsigned long long>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(cm >> 32))) << 32);
+    w = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(min(w, 0xffffffffull)));
+    if ((threadIdx.x & 31u) == 0) {
+        atomicAdd(&out[0], t);
+        atomicAdd(&out[1], cm);
+        atomicMax(&out[2], w);
+    }
+}
+}  // namespace
+
+int hbp_run_totals(hbp_ctx* ctx, const int64_t* tokens, const int64_t* comm_tokens, const int64_t* iter_dev_offsets,
+                   int64_t n_iterations, int64_t* out) {
+    return guarded(ctx, [&] {
+        const u64 I = static_cast<u64>(std::max<int64_t>(n_iterations, 0));
+        const u64 D = I ? static_cast<u64>(iter_dev_offsets[I]) : 0;
+        cudaStream_t s = ctx->stream;
+        DevBuf<int64_t> dt(D + 1, s), dc(D + 1, s), doff(I + 1, s);
+        DevBuf<unsigned long long> o(3, s);
+        o.zero();
+        if (D) {
+            CUDA_CHECK(cudaMemcpyAsync(dt.p, tokens, sizeof(int64_t) * D, cudaMemcpyHostToDevice, s));
+            CUDA_CHECK(cudaMemcpyAsync(dc.p, comm_tokens, sizeof(int64_t) * D, cudaMemcpyHostToDevice, s));
+        }
+        if (I) CUDA_CHECK(cudaMemcpyAsync(doff.p, iter_dev_offsets, sizeof(int64_t) * (I + 1), cudaMemcpyHostToDevice, s));
+        if (I || D)
+            LAUNCH_B("metrics.run_totals", 16.0 * D + 8.0 * I, k_run_totals, grid_for(std::max(I, D), 256, 148u * 4u), 256,
+                     0, s, dt.p, dc.p, doff.p, I, D, o.p);
+        const auto h = read_vector(*ctx, o.p, 3);
+        for (int k = 0; k < 3; ++k) out[k] = static_cast<int64_t>(h[k]);
+    });
+}
+
 int hbp_report_plan(hbp_ctx* ctx, hbp_plan* plan, hbp_metrics* out, double* per_iteration_dbr,
                     double* per_iteration_abr) {
     return guarded(ctx, [&] {

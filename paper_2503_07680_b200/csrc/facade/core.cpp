@@ -6,6 +6,7 @@
 // iteration, pr over one batch, ...) and the plan-invariant corpus
 // fingerprint are evaluated in place, as the reference does.
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -254,27 +255,36 @@ double abr(std::span<const DeviceBatch> iteration) {
     return gap / (static_cast<double>(top) * static_cast<double>(iteration.size()));
 }
 
-double cr(std::span<const std::vector<DeviceBatch>> iterations) {
-    double comm = 0.0, total = 0.0;
-    for (const auto& it : iterations)
+namespace {
+// Σ tokens, Σ comm tokens, widest iteration of a run -- on the engine
+// (hbp_run_totals); the ratios are formed here as the reference forms them
+std::array<int64_t, 3> run_totals(std::span<const std::vector<DeviceBatch>> iterations) {
+    std::vector<int64_t> tok, comm, off{0};
+    for (const auto& it : iterations) {
         for (const auto& d : it) {
-            comm += static_cast<double>(d.comm_tokens);
-            total += static_cast<double>(d.tokens);
+            tok.push_back(d.tokens);
+            comm.push_back(d.comm_tokens);
         }
-    if (total == 0.0) throw ValidationError("cr: no tokens in run");
-    return comm / total;
+        off.push_back(static_cast<int64_t>(tok.size()));
+    }
+    std::array<int64_t, 3> out{0, 0, 0};
+    check(hbp_run_totals(ctx(), tok.data(), comm.data(), off.data(), static_cast<int64_t>(iterations.size()),
+                         out.data()));
+    return out;
+}
+}  // namespace
+
+double cr(std::span<const std::vector<DeviceBatch>> iterations) {
+    const auto t = run_totals(iterations);
+    if (t[0] == 0) throw ValidationError("cr: no tokens in run");
+    return static_cast<double>(t[1]) / static_cast<double>(t[0]);
 }
 
 double ave_t(std::span<const std::vector<DeviceBatch>> iterations) {
     if (iterations.empty()) throw ValidationError("ave_t: no iterations");
-    double total = 0.0;
-    std::size_t devices = 0;
-    for (const auto& it : iterations) {
-        devices = std::max(devices, it.size());
-        for (const auto& d : it) total += static_cast<double>(d.tokens);
-    }
-    if (devices == 0) throw ValidationError("ave_t: no devices");
-    return total / (static_cast<double>(iterations.size()) * static_cast<double>(devices));
+    const auto t = run_totals(iterations);
+    if (t[2] == 0) throw ValidationError("ave_t: no devices");
+    return static_cast<double>(t[0]) / (static_cast<double>(iterations.size()) * static_cast<double>(t[2]));
 }
 
 MetricsReport report(const Plan& plan) {

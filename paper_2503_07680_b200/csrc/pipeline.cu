@@ -1187,6 +1187,42 @@ void plan_to_host(Ctx& c, DevicePlan& p) {
 // stand-alone stages over host pack lists (C++ / Python drop-in calls)
 // ---------------------------------------------------------------------------
 
+// leaves (max(0, capacity - total) << 32 | members) of host-listed packs
+__global__ void k_fill_leaves(const int64_t* __restrict__ cap, const int64_t* __restrict__ off,
+                              const int64_t* __restrict__ lens, u64 P, u64* __restrict__ leaves, u32* __restrict__ base) {
+    for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < P;
+         p += static_cast<u64>(gridDim.x) * blockDim.x) {
+        int64_t tot = 0;
+        for (int64_t k = off[p]; k < off[p + 1]; ++k) tot += lens[k];
+        const int64_t r = cap[p] - tot;
+        const u32 res = r <= 0 ? 0u : (r > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(r));
+        base[p] = static_cast<u32>(off[p + 1] - off[p]);
+        leaves[p] = (static_cast<u64>(res) << 32) | base[p];
+    }
+}
+
+// picks of one pool: count per pack, and the pool sample each placed item is
+__global__ void k_fill_count(const u64* __restrict__ items, const u32* __restrict__ bin, u64 m, u32* __restrict__ cnt) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+         i += static_cast<u64>(gridDim.x) * blockDim.x)
+        if (bin[i] != kNone) atomicAdd(&cnt[bin[i]], 1u);
+}
+
+// pick k of pack p sits at added[off[p] + slot - base[p]] (slots count up
+// from the pack's own members in pick order); its pool sample leaves the pool
+__global__ void k_fill_place(const u64* __restrict__ items, const u32* __restrict__ bin, const u32* __restrict__ slot,
+                             u64 m, const u32* __restrict__ base, const u64* __restrict__ off, int64_t* __restrict__ added,
+                             u8* __restrict__ keep) {
+    for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+         i += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u32 b = bin[i];
+        if (b == kNone) continue;
+        const u32 pi = entry_idx(items[i]);
+        added[off[b] + slot[i] - base[b]] = static_cast<int64_t>(pi);
+        keep[pi] = 0;
+    }
+}
+
 void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int64_t* pack_off, const int64_t* lens,
                         int n_pools, const int64_t* pool_off, const int64_t* pool_ids, const int64_t* pool_lens,
                         std::vector<int64_t>& added_off, std::vector<int64_t>& added, std::vector<uint8_t>& keep) {
@@ -1200,50 +1236,62 @@ void greedy_fill_device(Ctx& c, i64 n_packs, const int64_t* pack_cap, const int6
     hbp_samples in{pool_ids, pool_lens, M, HBP_MEM_HOST, "pools"};
     DeviceCorpus corpus;
     ingest(c, &in, corpus);
-    // leaves: (max(0, capacity - total) << 32) | count, per pack
-    std::vector<u64> leaves(static_cast<size_t>(n_packs));
-    std::vector<u32> base(static_cast<size_t>(n_packs));
-    for (i64 p = 0; p < n_packs; ++p) {
-        int64_t tot = 0;
-        for (int64_t k = pack_off[p]; k < pack_off[p + 1]; ++k) tot += lens[k];
-        const int64_t r = pack_cap[p] - tot;
-        const u32 res = r <= 0 ? 0u : (r > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(r));
-        base[p] = static_cast<u32>(pack_off[p + 1] - pack_off[p]);
-        leaves[p] = (static_cast<u64>(res) << 32) | base[p];
-    }
-    DevBuf<u64> dleaves(static_cast<size_t>(n_packs), s);
-    CUDA_CHECK(cudaMemcpyAsync(dleaves.p, leaves.data(), sizeof(u64) * n_packs, cudaMemcpyHostToDevice, s));
-    std::vector<std::vector<std::pair<u32, u32>>> per_pack(static_cast<size_t>(n_packs));  // (slot, pool index)
-    // pools nearest first; pool-by-pool equals pack-by-pack (each pool is only consumed from)
+    // the packs' leaves, built on the device from the host pack list
+    const u64 P = static_cast<u64>(n_packs);
+    const u64 NM = static_cast<u64>(pack_off[n_packs]);
+    DevBuf<int64_t> dcap(P, s), doff(P + 1, s), dlens(NM + 1, s);
+    CUDA_CHECK(cudaMemcpyAsync(dcap.p, pack_cap, sizeof(int64_t) * P, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(doff.p, pack_off, sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, s));
+    if (NM) CUDA_CHECK(cudaMemcpyAsync(dlens.p, lens, sizeof(int64_t) * NM, cudaMemcpyHostToDevice, s));
+    DevBuf<u64> dleaves(P, s);
+    DevBuf<u32> base(P, s), cnt(P + 1, s);
+    cnt.zero();
+    LAUNCH(k_fill_leaves, G(P), kB, 0, s, dcap.p, doff.p, dlens.p, P, dleaves.p, base.p);
+    // every pool's items (sorted) and their (pack, slot), nearest pool first;
+    // pool-by-pool equals pack-by-pack (each pool is only consumed from)
+    DevBuf<u64> items(static_cast<u64>(M), s);
+    DevBuf<u32> bin(static_cast<u64>(M), s), slot(static_cast<u64>(M), s);
+    DevBuf<u32> mx(1, s);
     for (int j = n_pools - 1; j >= 0; --j) {
         const u64 a = static_cast<u64>(pool_off[j]), m = static_cast<u64>(pool_off[j + 1] - pool_off[j]);
         if (m == 0) continue;
-        DevBuf<u32> idx(m, s);
-        DevBuf<u64> items(m, s);
-        u32* ip = idx.p;
-        for_each_index(c, m, [=] __device__(u64 i) { ip[i] = static_cast<u32>(a + i); });
-        LAUNCH(k_entries_from_idx, G(m), kB, 0, s, corpus.len32.p, idx.p, m, items.p);
-        u32 maxlen = 1;
-        for (u64 i = 0; i < m; ++i) maxlen = std::max<u32>(maxlen, static_cast<u32>(std::min<int64_t>(pool_lens[a + i], 0x7fffffff)));
-        sort_entries(c, corpus, items.p, m, corpus.key32.p == nullptr, maxlen);
-        DevBuf<u32> bin(m, s), slot(m, s);
-        first_fit_runs(c, items.p, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u, FitMode::Fill, bin.p, slot.p,
-                       corpus.key32.p, static_cast<u64>(corpus.neg_ids));
-        const auto hb = read_vector(c, bin.p, m), hs = read_vector(c, slot.p, m);
-        const auto he = read_vector(c, items.p, m);
-        for (u64 i = 0; i < m; ++i) {
-            if (hb[i] == kNone) continue;
-            const u32 pi = entry_idx(he[i]);
-            per_pack[hb[i]].push_back({hs[i], pi});
-            keep[pi] = 0;
-        }
+        u64* it = items.p + a;
+        const u32* len32 = corpus.len32.p;
+        u32* mxp = mx.p;
+        mx.zero();
+        for_each_index(c, m, [=] __device__(u64 i) {
+            const u32 l = len32[a + i];
+            it[i] = (static_cast<u64>(l) << 32) | static_cast<u64>(a + i);
+            atomicMax(mxp, l);
+        });
+        const u32 maxlen = std::max<u32>(1u, read_scalar(c, mx.p));
+        sort_entries(c, corpus, it, m, corpus.key32.p == nullptr, maxlen);
+        first_fit_runs(c, it, static_cast<i64>(m), dleaves.p, n_packs, n_packs, 1u, FitMode::Fill, bin.p + a,
+                       slot.p + a, corpus.key32.p, static_cast<u64>(corpus.neg_ids));
+        LAUNCH(k_fill_count, G(m), kB, 0, s, it, bin.p + a, m, cnt.p);
     }
-    for (i64 p = 0; p < n_packs; ++p) {
-        auto& v = per_pack[static_cast<size_t>(p)];
-        std::sort(v.begin(), v.end());
-        for (auto& x : v) added.push_back(x.second);
-        added_off[p + 1] = static_cast<int64_t>(added.size());
+    // picks per pack -> offsets, then every pick at its place
+    DevBuf<u64> off(P + 1, s);
+    {
+        const u32* cp = cnt.p;
+        u64* op = off.p;
+        const i64 NP = static_cast<i64>(P);
+        scan_exclusive<u64>(
+            NP + 1, [=] __device__(i64 i) { return i < NP ? static_cast<u64>(cp[i]) : 0ull; },
+            [=] __device__(i64 i, u64 v) { op[i] = v; }, s, c.scan, "scan.fill_picks");
     }
+    const u64 total = read_vector(c, off.p + P, 1)[0];
+    DevBuf<int64_t> dadded(total + 1, s);
+    DevBuf<u8> dkeep(static_cast<u64>(M), s);
+    CUDA_CHECK(cudaMemsetAsync(dkeep.p, 1, static_cast<size_t>(M), s));
+    LAUNCH(k_fill_place, G(static_cast<u64>(M)), kB, 0, s, items.p, bin.p, slot.p, static_cast<u64>(M), base.p, off.p,
+           dadded.p, dkeep.p);
+    const auto ho = read_vector(c, off.p, P + 1);
+    for (u64 p = 0; p <= P; ++p) added_off[p] = static_cast<int64_t>(ho[p]);
+    added.resize(total);
+    if (total) CUDA_CHECK(cudaMemcpyAsync(added.data(), dadded.p, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(keep.data(), dkeep.p, static_cast<size_t>(M), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
 void batching_device(Ctx& c, int64_t capacity, i64 n_packs, const int64_t* pack_cap, const int64_t* pack_off,

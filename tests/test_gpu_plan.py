@@ -265,3 +265,42 @@ def test_scan_fit_c1_group0(ctx, oracle, strategy):
     for k in ("pack_capacity", "pack_total", "pack_attention", "pack_member_offsets"):
         assert np.array_equal(getattr(got, k), getattr(want, k)), k
     assert np.array_equal(got.members_as_ids(None), want.member_id)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_standalone_greedy_fill_vs_reference(ctx, reference, seed):
+    """hbp_greedy_fill (the drop-in greedy_fill, balance.cpp:46-101): packs of
+    one group and the smaller groups' pools, picks assembled on the device,
+    against the reference's greedy_fill."""
+    rng = np.random.default_rng(seed)
+    cap = 65536
+    P = 300
+    counts = rng.integers(0, 4, P)
+    lens = rng.integers(8000, 20000, int(counts.sum())).astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    ids = rng.permutation(10 ** 6)[: len(lens)].astype(np.int64)
+    pool_sizes = [4000, 2500]
+    pool_lens = [rng.integers(1, 4096, pool_sizes[0]), rng.integers(4097, 16384, pool_sizes[1])]
+    qo = np.array([0, pool_sizes[0], sum(pool_sizes)], np.int64)
+    ql = np.concatenate(pool_lens).astype(np.int64)
+    qi = (rng.permutation(10 ** 6)[: len(ql)] + 10 ** 6).astype(np.int64)
+    if seed == 2:
+        qi[:50] = -np.arange(2, 52)  # ids <= -2: the {residual, -1} probe quirk
+    g_off, g_added, g_keep = ctx.greedy_fill(off, np.full(P, cap), ids, lens, qo, qi, ql)
+    packs = abi.FlatPlan(device_count=1, seed=0, groups=[], l_best=0, iter_group=np.zeros(0, np.int32),
+                         iter_dev_offsets=np.zeros(1, np.int64), dev_index=np.zeros(0, np.int32),
+                         dev_pack_offsets=np.zeros(1, np.int64), pack_capacity=np.full(P, cap, np.int64),
+                         pack_total=np.array([lens[off[p]:off[p + 1]].sum() for p in range(P)], np.int64),
+                         pack_attention=np.zeros(P, np.int64), pack_member_offsets=off, member_id=ids,
+                         member_length=lens)
+    pools = abi.FlatPlan(device_count=1, seed=0, groups=[], l_best=0, iter_group=np.zeros(0, np.int32),
+                         iter_dev_offsets=np.zeros(1, np.int64), dev_index=np.zeros(0, np.int32),
+                         dev_pack_offsets=np.zeros(1, np.int64), pack_capacity=np.array([4096, 16384], np.int64),
+                         pack_total=np.zeros(2, np.int64), pack_attention=np.zeros(2, np.int64),
+                         pack_member_offsets=qo, member_id=qi, member_length=ql)
+    want_packs, want_pools = reference.greedy_fill(packs, pools)
+    for p in range(P):
+        got = np.concatenate([ids[off[p]:off[p + 1]], qi[g_added[g_off[p]:g_off[p + 1]]]])
+        want = want_packs.member_id[want_packs.pack_member_offsets[p]:want_packs.pack_member_offsets[p + 1]]
+        assert np.array_equal(got, want), p
+    assert np.array_equal(qi[g_keep], want_pools.member_id)

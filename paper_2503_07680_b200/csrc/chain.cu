@@ -70,6 +70,7 @@ struct ChainArgs {
     u32* out;                  // [0] 1 + highest bin with items, [1] FFD overflow
     unsigned long long* prof;  // HBP_TRACE: per warp [wait in, serve, wait out, served runs]
     u32 sleep;                 // ns of back-off per failed poll (idle warps yield issue slots)
+    int single;                // a lone run at the FFD frontier: plain first fit over every lane
     u32* hist;                 // [J][nblocks][32] input counts of active cells (chain -> replay)
     u32* hact;                 // [J][nblocks] active-run mask of every cell (0: nothing to serve)
     unsigned long long* tl;    // HBP_CHAIN_TL: globaltimer when block b reached warp j [J][nblocks]
@@ -245,6 +246,7 @@ __device__ __forceinline__ void frontier_fill(const ChainArgs& a, unsigned seg, 
                                               u32 (&R)[M], u32 (&N)[M], u32& lmax, u32& emask, RunStage& st,
                                               u64 base, u32 lane) {
     const u32 lv = (seg >> lane) & 1u ? c : 0u;
+    if (!__any_sync(0xffffffffu, lv > 0)) return;  // the non-empty lanes took every item
     unsigned long long incl = lv;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -361,6 +363,15 @@ __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 en
         const unsigned upto = breaks ? (1u << (__ffs(breaks) - 1)) - 1u : 0xffffffffu;
         const unsigned seg = act & upto;
         act &= ~seg;
+        if (a.single && (seg & (seg - 1u)) == 0u) {
+            // One run: the empty lanes follow the non-empty ones in bin
+            // order, so first fit over every lane is exactly the non-empty
+            // serve followed by the frontier fill; no scan, no staging. A
+            // lane that received items had its first bin take them.
+            serve_set<M, STORE>(a, seg, 0xffffffffu, s, s_eff, inv_own, end_item, c, R, N, lmax, base, lane);
+            emask &= __ballot_sync(0xffffffffu, N[0] == 0u);
+            continue;
+        }
         // against the non-empty lanes only the runs that fit one of them
         const bool ne_lane = ((emask >> lane) & 1u) == 0;
         const unsigned q = seg & __ballot_sync(0xffffffffu, s_eff <= __reduce_max_sync(0xffffffffu, ne_lane ? lmax : 0u));
@@ -803,6 +814,7 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     a.item_bin = item_bin;
     a.item_slot = item_slot;
     a.take = take;
+    a.single = std::getenv("HBP_CHAIN_NOSINGLE") == nullptr ? 1 : 0;
     const char* es = std::getenv("HBP_CHAIN_SLEEP");
     a.sleep = es ? static_cast<u32>(std::atoi(es)) : 0u;
     // Bins are covered by consecutive passes: a pass's tail hands the counts
@@ -811,8 +823,15 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     // default 8, measured best on C2) whose chain is resident; FFD's first
     // pass is sized by the caller's estimate of the bins FFD opens, so the
     // 2x bin bound costs a second pass only when the estimate is short.
+    // Lane width: a run's serve costs about M-proportional work on the
+    // frontier warp (divisions, prefix and takes over the lane's M bins),
+    // while every extra warp adds a hop to the path of each block. Measured
+    // (tools/chain_env_ab.sh): chains of up to ~5K bins (C1/C3 plans) run
+    // 1.3-2.2x faster at M = 1-2 than at 8; C2's 90-150K-bin chains are
+    // fastest at M = 8. So: the narrowest lanes that keep the chain within
+    // kMaxNarrowWarps warps, else M = 8.
     const char* em = std::getenv("HBP_CHAIN_M");
-    const int m0 = em ? std::atoi(em) : 8;
+    constexpr u64 kMaxNarrowWarps = 160;
     const u64 cap_of[5] = {chain_capacity<1>(sms), chain_capacity<2>(sms), chain_capacity<4>(sms),
                            chain_capacity<8>(sms), chain_capacity<16>(sms)};
     const int widths[5] = {1, 2, 4, 8, 16};
@@ -822,6 +841,16 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     for (int pass = 0; pos < n_bins; ++pass) {
         u64 want = n_bins - pos;
         if (pass == 0 && first_pass_bins > 0 && first_pass_bins < want) want = first_pass_bins;
+        int m0 = 8;
+        if (em) {
+            m0 = std::atoi(em);
+        } else {
+            for (int w : {1, 2, 4})
+                if ((want + 32ull * w - 1) / (32ull * w) <= kMaxNarrowWarps) {
+                    m0 = w;
+                    break;
+                }
+        }
         int wi = 0;
         while (wi < 5 && (widths[wi] < m0 || cap_of[wi] < want)) ++wi;
         if (wi == 5) {

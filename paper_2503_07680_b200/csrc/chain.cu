@@ -49,6 +49,15 @@ constexpr int kShortWarps = 4;
 template <int M>
 __host__ __device__ constexpr int warps_for() { return M <= 4 ? 32 : 16; }
 constexpr u32 kStride = 32;    // u32 between global consumer counters (one 128 B line each)
+// Blocks of run data (and, for a CTA's first warp, of L2 ring words) each
+// warp has in flight ahead of the block it serves. A warp whose cells are
+// inactive spends only ~100 ns per block, while one L2 round trip is
+// ~600 ns: fetched a block ahead, the run data and the ring word set that
+// warp's pace -- and, on the C2 128K-group FFD, the whole chain's (704 ns
+// per block at the first warp of a CTA, 1046 blocks). CTAs of 32 warps
+// keep 4 (their shared memory holds no more).
+template <int kWarps>
+__host__ __device__ constexpr int prefetch_depth() { return kWarps >= 32 ? 4 : 8; }
 
 struct ChainArgs {
     const u32* run_item;
@@ -75,6 +84,30 @@ struct ChainArgs {
     u32* hact;                 // [J][nblocks] active-run mask of every cell (0: nothing to serve)
     unsigned long long* tl;    // HBP_CHAIN_TL: globaltimer when block b reached warp j [J][nblocks]
 };
+
+// Per-warp prefetch ring (shared memory), filled by cp.async kPF - 1 blocks ahead.
+template <int kPF>
+struct ChainPF {
+    unsigned long long ring[kPF][32];  // first warp of a CTA: the L2 ring words (tag checked on use)
+    u32 len[kPF][32];                  // run_len
+    u32 beg[kPF][32];                  // run_item (head with carry: carry_in)
+    u32 end[kPF][32];                  // run_item of the next run
+};
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, u32 src_bytes) {
+    const u32 sa = static_cast<u32>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
+}
+// 16 bytes through L2 only (.cg): the ring words change under the kernel
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+    const u32 sa = static_cast<u32>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -429,11 +462,17 @@ __device__ __forceinline__ u32 store_bins(const ChainArgs& a, u64 base, u32 lane
     return __reduce_max_sync(0xffffffffu, top);
 }
 
-template <int M, int kWarps>
+// TRACE compiles in the per-warp counters and the per-cell timeline
+// (HBP_TRACE); the product kernel keeps its per-block path short: a warp
+// whose cell is inactive only forwards the counts (~40 instructions).
+template <int M, int kWarps, bool TRACE>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
-    extern __shared__ unsigned long long s_ring_raw[];  // [kWarps][kQs][32]: warp w-1 -> w, then RunStage[kWarps]
+    // [kWarps][kQs][32]: warp w-1 -> w, then RunStage[kWarps], then ChainPF[kWarps]
+    extern __shared__ __align__(16) unsigned long long s_ring_raw[];
     auto s_ring = reinterpret_cast<unsigned long long (*)[kQs][32]>(s_ring_raw);
     RunStage* s_stage = reinterpret_cast<RunStage*>(s_ring_raw + kWarps * kQs * 32);
+    constexpr int kPF = prefetch_depth<kWarps>();
+    ChainPF<kPF>* s_pf = reinterpret_cast<ChainPF<kPF>*>(s_stage + kWarps);
     __shared__ u32 s_cons[kWarps];                         // blocks warp w has read from s_ring[w]
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const u32 g = blockIdx.x;
@@ -448,40 +487,70 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
     u32 R[M], N[M];
     u32 wmax = load_bins<M>(a, base, lane, R, N);
     u32 emask = empty_lanes<M>(a, base, lane);
+    const u32 nblocks = a.nblocks, rb = a.rb, run_begin = a.run_begin, run_end = a.run_end, n_runs = a.n_runs;
     const bool head = j == 0, tail = j + 1 == a.J;
     const bool in_global = w == 0, out_global = w + 1 == kWarps;
+    const bool replay = a.hist != nullptr;
     volatile unsigned long long* sin = s_ring[w][0];
     volatile unsigned long long* sout = w + 1 < kWarps ? s_ring[w + 1][0] : nullptr;
     const unsigned long long* gin = a.gring + static_cast<u64>(g) * kQ * 32;  // written by CTA g-1
     unsigned long long* gout = a.gring + static_cast<u64>(g + 1) * kQ * 32;
+    u32* const my_gcons = a.gcons + g * kStride;
+    const u32* const next_gcons = a.gcons + (g + 1) * kStride;
+    volatile u32* const my_scons = reinterpret_cast<volatile u32*>(s_cons) + w;
+    volatile u32* const next_scons = reinterpret_cast<volatile u32*>(s_cons) + (w + 1 < kWarps ? w + 1 : w);
     u32 seen_cons = 0;  // consumer progress known to this producer
 
-    // run data of block b, prefetched one block ahead
-    auto load_runs = [&](u32 b, u32& s, u32& e, u32& st) {
-        const u32 k = a.run_begin + b * a.rb + lane;
-        const bool valid = b < a.nblocks && lane < a.rb && k < a.run_end;
-        s = valid ? a.run_len[k] : 0u;
-        st = valid ? a.run_item[k] : 0u;
-        e = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
+    // run data of blocks b .. b + kPF - 2 (and the first warp's L2 ring
+    // words) in flight while block b is served; one cp.async group per
+    // block. The chain needs run lengths only; the first warp (counts) and
+    // chains that store their heads themselves (item offsets) also the
+    // item bounds.
+    ChainPF<kPF>& pf = s_pf[w];
+    const bool carry_head = head && a.carry_in != nullptr;
+    const bool want_items = head || !replay;
+    const u32* const run_len = a.run_len;
+    const u32* const run_item = a.run_item;
+    auto prefetch = [&](u32 bb) {
+        const int slot = static_cast<int>(bb % kPF);
+        const u32 k = run_begin + bb * rb + lane;
+        const bool valid = bb < nblocks && lane < rb && k < run_end;
+        cp_async4(&pf.len[slot][lane], valid ? run_len + k : run_len, valid ? 4u : 0u);
+        if (want_items) {
+            cp_async4(&pf.beg[slot][lane], valid ? (carry_head ? a.carry_in + k : run_item + k) : run_item,
+                      valid ? 4u : 0u);
+            const bool ve = valid && k + 1 < n_runs;
+            cp_async4(&pf.end[slot][lane], ve ? run_item + k + 1 : run_item, ve ? 4u : 0u);
+        }
+        if (in_global && !head && bb < nblocks && lane < 16)
+            cp_async16_cg(&pf.ring[slot][2 * lane], gin + (bb % kQ) * 32 + 2 * lane);
+        cp_async_commit();
     };
-    u32 s_n, e_n, st_n;
-    load_runs(0, s_n, e_n, st_n);
+#pragma unroll 1
+    for (u32 bb = 0; bb + 1 < static_cast<u32>(kPF); ++bb) prefetch(bb);
 
-    unsigned long long pf[4] = {0, 0, 0, 0};
+    unsigned long long pcnt[4] = {0, 0, 0, 0};
     long long t0 = 0, t1 = 0;
-    for (u32 b = 0; b < a.nblocks; ++b) {
-        if (a.prof) t0 = clock64();
-        const u32 s = s_n, end_item = e_n, start_item = st_n;
-        load_runs(b + 1, s_n, e_n, st_n);
-        const unsigned long long tag = static_cast<unsigned long long>(b + 1) << 32;
+#pragma unroll 1
+    for (u32 b = 0; b < nblocks; ++b) {
+        if (TRACE && a.prof) t0 = clock64();
+        __syncwarp();  // every lane is done with the slot the next prefetch refills
+        prefetch(b + kPF - 1);
+        cp_async_wait<kPF - 1>();
+        __syncwarp();
+        const int slot = static_cast<int>(b % kPF);
+        const u32 s = pf.len[slot][lane];
         u32 c;
         if (head) {
-            const u32 k = a.run_begin + b * a.rb + lane;
-            c = a.carry_in ? (lane < a.rb && k < a.run_end ? a.carry_in[k] : 0u) : end_item - start_item;
+            const u32 kr = run_begin + b * rb + lane;
+            const bool valid = lane < rb && kr < run_end;
+            const u32 e = valid ? (kr + 1 < n_runs ? pf.end[slot][lane] : a.n_items) : 0u;
+            c = carry_head ? pf.beg[slot][lane] : e - pf.beg[slot][lane];
         } else if (in_global) {
-            unsigned long long v;
-            while (((v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane)) >> 32) != (b + 1))
-                if (a.sleep) __nanosleep(a.sleep);
+            unsigned long long v = pf.ring[slot][lane];
+            if ((v >> 32) != (b + 1))
+                while (((v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane)) >> 32) != (b + 1))
+                    if (a.sleep) __nanosleep(a.sleep);
             c = static_cast<u32>(v);
         } else {
             unsigned long long v;
@@ -491,42 +560,47 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
         }
         // every lane has its c; run_len bit 31 = strict (needs r > s)
         const unsigned act = __ballot_sync(0xffffffffu, c > 0 && (s & 0x7fffffffu) + (s >> 31) <= wmax);
-        const u32 n_act = __popc(act);
         unsigned long long t_arr = 0;
-        if (a.tl) t_arr = globaltimer();
-        if (a.prof) {
-            t1 = clock64();
-            pf[0] += t1 - t0;
-            pf[3] += n_act;
-            t0 = t1;
+        if (TRACE) {
+            if (a.tl) t_arr = globaltimer();
+            if (a.prof) {
+                t1 = clock64();
+                pcnt[0] += t1 - t0;
+                pcnt[3] += __popc(act);
+                t0 = t1;
+            }
         }
         if (!head && lane == 0) {
-            if (in_global) st_relaxed_u32(a.gcons + g * kStride, b + 1);
-            else reinterpret_cast<volatile u32*>(s_cons)[w] = b + 1;
+            if (in_global) st_relaxed_u32(my_gcons, b + 1);
+            else *my_scons = b + 1;
         }
-        if (act) {
-            if (a.hist) {  // the replay re-serves this cell from its input counts
-                if (lane < a.rb) a.hist[(static_cast<u64>(j) * a.nblocks + b) * a.rb + lane] = c;
-                if (lane == 0) a.hact[static_cast<u64>(j) * a.nblocks + b] = act;
+        if (act) {  // (the replay's hact is zeroed: inactive cells write nothing)
+            const u32 kr = run_begin + b * rb + lane;
+            const bool valid = lane < rb && kr < run_end;
+            if (replay) {  // the replay re-serves this cell from its input counts
+                if (lane < rb) a.hist[(static_cast<u64>(j) * nblocks + b) * rb + lane] = c;
+                if (lane == 0) a.hact[static_cast<u64>(j) * nblocks + b] = act;
+                serve<M, false>(a, act, s, 0u, c, R, N, wmax, emask, s_stage[w], base, lane);
+            } else {  // short chains store their heads directly
+                const u32 end_item = valid ? (kr + 1 < n_runs ? pf.end[slot][lane] : a.n_items) : 0u;
+                serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);
             }
-            if (a.hist) serve<M, false>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);
-            else serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);  // short chains store directly
-        } else if (a.hist && lane == 0) {
-            a.hact[static_cast<u64>(j) * a.nblocks + b] = 0;
         }
         unsigned long long t_srv = 0;
-        if (a.tl) t_srv = globaltimer();
-        if (a.prof) {
-            t1 = clock64();
-            pf[1] += t1 - t0;
-            t0 = t1;
+        if (TRACE) {
+            if (a.tl) t_srv = globaltimer();
+            if (a.prof) {
+                t1 = clock64();
+                pcnt[1] += t1 - t0;
+                t0 = t1;
+            }
         }
         if (!tail) {
-            const unsigned long long v = tag | c;
+            const unsigned long long v = (static_cast<unsigned long long>(b + 1) << 32) | c;
             if (out_global) {
                 if (b >= static_cast<u32>(kQ) && seen_cons + kQ <= b) {
                     if (lane == 0)
-                        while ((seen_cons = ld_relaxed_u32(a.gcons + (g + 1) * kStride)) + kQ <= b)
+                        while ((seen_cons = ld_relaxed_u32(next_gcons)) + kQ <= b)
                             if (a.sleep) __nanosleep(a.sleep);
                     seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
                 }
@@ -534,28 +608,30 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
             } else {
                 if (b >= static_cast<u32>(kQs) && seen_cons + kQs <= b) {
                     if (lane == 0)
-                        while ((seen_cons = reinterpret_cast<volatile u32*>(s_cons)[w + 1]) + kQs <= b)
+                        while ((seen_cons = *next_scons) + kQs <= b)
                             if (a.sleep) __nanosleep(a.sleep);
                     seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
                 }
                 sout[(b % kQs) * 32 + lane] = v;
             }
         } else {  // tail: hand the counts to the next pass
-            const u32 k = a.run_begin + b * a.rb + lane;
-            if (lane < a.rb && k < a.run_end) a.carry_out[k] = c;
+            const u32 k = run_begin + b * rb + lane;
+            if (lane < rb && k < run_end) a.carry_out[k] = c;
             if (__any_sync(0xffffffffu, c > 0) && lane == 0) atomicOr(a.out + 1, 1u);
         }
-        if (a.prof) pf[2] += clock64() - t0;
-        if (a.tl && lane == 0) {  // arrival | serve ns << 40 | active runs << 56 (timeline)
-            const unsigned long long d = min(t_srv - t_arr, (1ull << 16) - 1);
-            a.tl[static_cast<u64>(j) * a.nblocks + b] =
-                (t_arr & ((1ull << 40) - 1)) | (d << 40) | (static_cast<unsigned long long>(n_act) << 56);
+        if (TRACE) {
+            if (a.prof) pcnt[2] += clock64() - t0;
+            if (a.tl && lane == 0) {  // arrival | serve ns << 40 | active runs << 56 (timeline)
+                const unsigned long long d = min(t_srv - t_arr, (1ull << 16) - 1);
+                a.tl[static_cast<u64>(j) * nblocks + b] =
+                    (t_arr & ((1ull << 40) - 1)) | (d << 40) | (static_cast<unsigned long long>(__popc(act)) << 56);
+            }
         }
     }
-    if (a.prof && lane == 0)
-        for (int i = 0; i < 4; ++i) a.prof[4ull * j + i] = pf[i];
+    if (TRACE && a.prof && lane == 0)
+        for (int i = 0; i < 4; ++i) a.prof[4ull * j + i] = pcnt[i];
     // with a replay to follow, the bins stay as loaded for it
-    const u32 top = store_bins<M>(a, base, lane, R, N, a.hist == nullptr);
+    const u32 top = store_bins<M>(a, base, lane, R, N, !replay);
     if (lane == 0 && top) atomicMax(a.out, top);
 }
 
@@ -589,7 +665,7 @@ __global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
 // Bins one resident chain of width M can hold (per device, queried once).
 template <int M, int kWarps = warps_for<M>()>
 u64 chain_capacity(int sms) {
-    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32 + sizeof(RunStage) * kWarps;
+    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32 + (sizeof(RunStage) + sizeof(ChainPF<prefetch_depth<kWarps>()>)) * kWarps;
     static std::mutex mu;
     static std::map<int, int> per_sm_of;
     int dev = 0;
@@ -597,10 +673,12 @@ u64 chain_capacity(int sms) {
     std::lock_guard<std::mutex> g(mu);
     auto it = per_sm_of.find(dev);
     if (it == per_sm_of.end()) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M, kWarps, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        CUDA_CHECK(cudaFuncSetAttribute(k_ff_chain<M, kWarps, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
         int per_sm = 0;
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M, kWarps>, kWarps * 32, smem));
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_chain<M, kWarps, false>, kWarps * 32, smem));
         it = per_sm_of.emplace(dev, per_sm).first;
     }
     return static_cast<u64>(it->second > 0 ? it->second : 0) * sms * kWarps * 32 * M;
@@ -618,7 +696,10 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
                              chain_capacity<M, kShortWarps>(sms) >= pass_bins;
     const int kWarps = short_chain ? kShortWarps : warps_for<M>();
     const u32 G = (J + kWarps - 1) / kWarps;
-    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32 + sizeof(RunStage) * kWarps;
+    const size_t smem = sizeof(unsigned long long) * kWarps * kQs * 32 +
+                        (sizeof(RunStage) + (short_chain ? sizeof(ChainPF<prefetch_depth<kShortWarps>()>)
+                                                         : sizeof(ChainPF<prefetch_depth<warps_for<M>()>()>))) *
+                            kWarps;
     if (short_chain) (void)chain_capacity<M, kShortWarps>(sms);  // attribute set
     else (void)chain_capacity<M>(sms);
     cudaStream_t s = c.stream;
@@ -665,13 +746,19 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     if (replay) {
         hist.alloc(static_cast<size_t>(J) * a.nblocks * a.rb, s);
         hact.alloc(static_cast<size_t>(J) * a.nblocks, s);
+        hact.zero();  // the chain writes the active cells only
         a.hist = hist.p;
         a.hact = hact.p;
     }
     // algorithmic bytes (FFD residue): 12 B per item + 12 B per bin of the pass
     const double alg = 12.0 * a.n_items + 12.0 * (a.bin_end - a.bin0);
-    if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps>), dim3(G), dim3(kWarps * 32), smem, s, args);
-    else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>()>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    if (c.trace) {
+        if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps, true>), dim3(G), dim3(kWarps * 32), smem, s, args);
+        else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>(), true>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    } else {
+        if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps, false>), dim3(G), dim3(kWarps * 32), smem, s, args);
+        else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>(), false>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    }
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
     if (replay) LAUNCH_B("fit.replay", 12.0 * a.n_items + 16.0 * (a.bin_end - a.bin0), k_ff_replay<M>, (J + 7) / 8, 256, 0, s, a);
     const auto o = read_vector(c, out.p, 2);

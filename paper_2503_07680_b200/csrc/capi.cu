@@ -100,7 +100,11 @@ int hbp_ctx_create(int device, hbp_ctx** out) {
     if (device < 0 || device >= count) return HBP_ERR_VALIDATION;
     auto* c = new hbp_ctx();
     c->device = device;
-    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    // the main stream at the highest priority: the side stream's kernels
+    // (engine.cuh side_fork) only take what the main stream leaves idle
+    int prio_lo = 0, prio_hi = 0;
+    if (cudaSetDevice(device) != cudaSuccess || cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
         cudaGetLastError();
         delete c;
         return HBP_ERR_CUDA;
@@ -127,6 +131,15 @@ void hbp_ctx_destroy(hbp_ctx* ctx) {
         ctx->plans.clear();
         ctx->scan.status.release();
         ctx->scan.counter.release();
+        if (ctx->side) {
+            cudaStreamSynchronize(ctx->side);
+            ctx->side_scan.status.release();
+            ctx->side_scan.counter.release();
+            cudaStreamSynchronize(ctx->side);
+            cudaStreamDestroy(ctx->side);
+            cudaEventDestroy(ctx->ev_fork);
+            cudaEventDestroy(ctx->ev_join);
+        }
         ctx->blocks.stream = ctx->stream;
         ctx->blocks.clear();  // after every buffer that returns blocks to it
         cudaStreamSynchronize(ctx->stream);

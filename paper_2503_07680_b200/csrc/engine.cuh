@@ -29,6 +29,13 @@ struct hbp_ctx {
     int64_t syncs = 0;  // host round trips (read_scalar / read_vector)
     hbp_b200::BlockCache blocks;  // declared before every cached buffer it outlives
     hbp_b200::ScanScratch scan;
+    // a second stream for stages independent of the one in flight (e.g. the
+    // greedy-fill pool sort while the larger group packs); its scans use
+    // their own status ring. Created on first use.
+    cudaStream_t side = nullptr;
+    hbp_b200::ScanScratch side_scan;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool side_off = false;  // HBP_NO_SIDE: forks run inline on the main stream
     hbp_b200::Pinned pinned;
     hbp_b200::PinnedPool host_pool;  // plan host views
     // stage trace (HBP_TRACE=1): wall time between marks, stream synchronised
@@ -82,6 +89,64 @@ struct CtxScope {
         g_launch_counter = prev;
         g_prof = prev_prof;
         g_cache = prev_cache;
+    }
+};
+
+// Fork / join of the context's side stream: work enqueued inside a
+// SideScope runs on the side stream after everything enqueued on the main
+// stream before fork(); join() makes the main stream wait for it. Buffers
+// that cross the two are allocated on the main stream before the fork and
+// released after the join; buffers allocated inside a SideScope are the side
+// stream's own (stream-ordered there, outside the main stream's cache).
+inline void side_fork(Ctx& c) {
+    static const bool no_side = std::getenv("HBP_NO_SIDE") != nullptr;  // A/B: everything on one stream
+    if (no_side) {
+        c.side_off = true;
+        return;
+    }
+    if (!c.side) {
+        int lo = 0, hi = 0;  // lowest priority (the main stream has the highest)
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, lo));
+        CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+    }
+    CUDA_CHECK(cudaEventRecord(c.ev_fork, c.stream));
+    CUDA_CHECK(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+}
+inline void side_join(Ctx& c) {
+    if (c.side_off) return;
+    CUDA_CHECK(cudaEventRecord(c.ev_join, c.side));
+    CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+}
+// Joins a fork when it goes out of scope (also on an exception), so that
+// buffers declared before it are released only after the side stream is done.
+struct SideJoin {
+    Ctx& c;
+    bool armed = false;
+    explicit SideJoin(Ctx& cc) : c(cc) {}
+    void join() {
+        if (armed) side_join(c);
+        armed = false;
+    }
+    ~SideJoin() {
+        if (armed && !c.side_off) {
+            cudaEventRecord(c.ev_join, c.side);
+            cudaStreamWaitEvent(c.stream, c.ev_join, 0);
+        }
+    }
+};
+struct SideScope {
+    Ctx& c;
+    explicit SideScope(Ctx& cc) : c(cc) {
+        if (c.side_off) return;
+        std::swap(c.stream, c.side);
+        std::swap(c.scan, c.side_scan);
+    }
+    ~SideScope() {
+        if (c.side_off) return;
+        std::swap(c.stream, c.side);
+        std::swap(c.scan, c.side_scan);
     }
 };
 

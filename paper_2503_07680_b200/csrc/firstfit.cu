@@ -1085,8 +1085,31 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
     return ks;
 }
 
+void prepare_runs(Ctx& c, const u64* items, i64 n_items, const u32* key32, u64 neg_keys, FitRuns r) {
+    if (n_items <= 0) return;
+    u32* ri = r.run_item;
+    u32* rl = r.run_len;
+    u32* sc = r.n_runs;
+    const i64 nn = n_items;
+    // one scan over run-head flags; each head writes its run's first item
+    // and length (bit 31: strict) at its run index
+    scan_exclusive<u32>(
+        nn, [=] __device__(i64 i) { return run_head(items, i, key32, neg_keys) ? 1u : 0u; },
+        [=] __device__(i64 i, u32 v) {
+            const bool head = run_head(items, i, key32, neg_keys);
+            if (head) {
+                const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
+                ri[v] = static_cast<u32>(i);
+                rl[v] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
+            }
+            if (i == nn - 1) sc[0] = v + (head ? 1u : 0u);
+        },
+        c.stream, c.scan, "scan.ff3", 8.0);
+}
+
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
-                         FitMode mode, u32* item_bin, u32* item_slot, const u32* key32, u64 neg_keys) {
+                         FitMode mode, u32* item_bin, u32* item_slot, const u32* key32, u64 neg_keys,
+                         const FitRuns* pre) {
     FitResult out;
     out.bins = bins0;
     if (n_items_s <= 0) return out;
@@ -1101,40 +1124,30 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     if (neg_keys > 0 && !use_chain)
         throw EngineError(HBP_ERR_CUDA, "greedy fill with sample ids <= -2 needs the chain engine (HBP_ENGINE)");
 
-    // runs of equal length
-    // runs: one scan over run-head flags; each head writes its run's first
-    // item and length (bit 31: strict) at its run index
-    DevBuf<u32> run_item(n, s), run_len(n, s), scal(4, s);
-    {
-        u32* ri = run_item.p;
-        u32* rl = run_len.p;
-        u32* sc = scal.p;
-        const i64 nn = static_cast<i64>(n);
-        scan_exclusive<u32>(
-            nn, [=] __device__(i64 i) { return run_head(items, i, key32, neg_keys) ? 1u : 0u; },
-            [=] __device__(i64 i, u32 v) {
-                const bool head = run_head(items, i, key32, neg_keys);
-                if (head) {
-                    const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
-                    ri[v] = static_cast<u32>(i);
-                    rl[v] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
-                }
-                if (i == nn - 1) sc[0] = v + (head ? 1u : 0u);
-            },
-            s, c.scan, "scan.ff3", 8.0);
+    // runs of equal length (or precomputed by the caller with the same key rules)
+    DevBuf<u32> run_item, run_len, scal;
+    FitRuns fr;
+    if (pre) {
+        fr = *pre;
+    } else {
+        run_item.alloc(n, s);
+        run_len.alloc(n, s);
+        scal.alloc(4, s);
+        fr = FitRuns{run_item.p, run_len.p, scal.p};
+        prepare_runs(c, items, static_cast<i64>(n), key32, neg_keys, fr);
     }
 
     // bulk-place the items that can never share a bin (FFD with no live bins)
     u32 bulk = 0;
     u32 run_begin = 0;
-    const u32 n_runs = read_scalar(c, scal.p);
+    const u32 n_runs = read_scalar(c, fr.n_runs);
     std::vector<u32> h_runs;
     if (ffd && bins0 == 0) {
         // runs are in decreasing length: count leading runs with 2*s > cap
-        h_runs = read_vector(c, run_len.p, n_runs);
+        h_runs = read_vector(c, fr.run_len, n_runs);
         while (run_begin < n_runs && 2ull * h_runs[run_begin] > cap) ++run_begin;
         if (run_begin > 0) {
-            bulk = (run_begin < n_runs) ? read_vector(c, run_item.p + run_begin, 1)[0] : static_cast<u32>(n);
+            bulk = (run_begin < n_runs) ? read_vector(c, fr.run_item + run_begin, 1)[0] : static_cast<u32>(n);
         }
     }
 
@@ -1144,8 +1157,8 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     i64 tree_bins = max_bins;
     i64 est_bins = 0;
     if (ffd) {
-        if (h_runs.empty()) h_runs = read_vector(c, run_len.p, n_runs);
-        const auto h_items = read_vector(c, run_item.p, n_runs);
+        if (h_runs.empty()) h_runs = read_vector(c, fr.run_len, n_runs);
+        const auto h_items = read_vector(c, fr.run_item, n_runs);
         long double sum = 0;
         for (u32 k = 0; k < n_runs; ++k) {
             const u64 e = (k + 1 < n_runs) ? h_items[k + 1] : n;
@@ -1166,7 +1179,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         if (bulk > 0)
             LAUNCH(k_bulk_big, grid_for(bulk, 256, 148u * 16u), 256, 0, s, items, static_cast<u64>(bulk), cap, leaves,
                    item_bin, item_slot, take.p);
-        ChainRuns cr{run_item.p, run_len.p, static_cast<u32>(n), n_runs, run_begin, n_runs};
+        ChainRuns cr{fr.run_item, fr.run_len, static_cast<u32>(n), n_runs, run_begin, n_runs};
         u32 used = 0;
         if (chain_fit(c, cr, leaves, static_cast<u32>(live), static_cast<u32>(ffd ? tree_bins : live), cap, ffd,
                       item_bin, item_slot, take.p, static_cast<u32>(std::min<i64>(est_bins, tree_bins)), used)) {
@@ -1209,8 +1222,8 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     EngineArgs a;
     a.items = items;
     a.n_items = static_cast<u32>(n);
-    a.run_item = run_item.p;
-    a.run_len = run_len.p;
+    a.run_item = fr.run_item;
+    a.run_len = fr.run_len;
     a.n_runs = n_runs;
     a.run_begin = run_begin;
     a.leaves = leaves;
@@ -1222,7 +1235,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     a.rec = rec;
     a.rec0 = rec0;
     a.max_records = static_cast<u32>(max_records);
-    a.out = scal.p;
+    a.out = fr.n_runs;
     DevBuf<unsigned long long> prof;
     a.prof = nullptr;
     if (c.trace) {
@@ -1254,7 +1267,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         u32 stretch = kGap;
         std::vector<u8> scarce;
         while (pos < n_runs) {
-            const u32 ks = fill_parallel_pass(c, leaves, P, run_len.p, run_item.p, pos, n_runs, static_cast<u32>(n),
+            const u32 ks = fill_parallel_pass(c, leaves, P, fr.run_len, fr.run_item, pos, n_runs, static_cast<u32>(n),
                                               rec, nrec, static_cast<u32>(max_records), scarce);
             ++passes;
             if (ks >= n_runs) break;
@@ -1275,7 +1288,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
             a.run_end = end;
             a.rec0 = nrec;
             LAUNCH_B("fit.engine", 0.0, k_fit_engine_v4, 1, 32, smem4, s, a, vl);
-            const auto o = read_vector(c, scal.p, 3);
+            const auto o = read_vector(c, fr.n_runs, 3);
             if (o[2]) throw EngineError(HBP_ERR_CUDA, "first-fit engine: record or bin capacity exceeded");
             nrec = o[1];
             engine_runs += end - ks;
@@ -1300,7 +1313,7 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     } else {
         LAUNCH_B("fit.engine.v1", 0.0, k_fit_engine, 1, 32, 0, s, a);
     }
-    const auto o = read_vector(c, scal.p, 3);
+    const auto o = read_vector(c, fr.n_runs, 3);
     if (o[2]) throw EngineError(HBP_ERR_CUDA, "first-fit engine: record or bin capacity exceeded");
     if (c.trace) {
         const auto pc = read_vector(c, prof.p, 8);

@@ -14,6 +14,8 @@
 // chain inside the tile ("all-convergent"): then the tile's exit is known
 // without knowing its entry and tiles resolve in parallel. Only maximal runs
 // of non-convergent tiles are walked sequentially (one thread per run).
+#include <cstdlib>
+
 #include "engine.cuh"
 #include "stages.cuh"
 
@@ -356,6 +358,352 @@ __global__ void __launch_bounds__(NF_B) k_nf_emit(const u64* __restrict__ F, u64
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// One next-fit round in one launch (after the prefix sums P): per tile of
+// NF_T positions, in tile order claimed by an atomic counter so that every
+// earlier tile is running or done:
+//   next()    gallop over P for the tile's positions (no nxt array in HBM)
+//   spec      pointer doubling as in k_nf_tiles: the speculative chain from
+//             the tile start, its exit, all-convergence
+//   entry     the exit of tile k-1, published as soon as it is known (at
+//             once for an all-convergent tile, after its own entry and walk
+//             otherwise); only non-convergent tiles wait on a predecessor
+//   flags     walk from the entry into the speculative chain; frozen packs
+//             and items among the tile's starts, its last start
+//   look-back frozen totals of the tiles before (decoupled look-back) and the
+//             last start before the tile (the nearest earlier tile with one)
+//   emit      as k_nf_emit
+// Replaces next, tiles, entries, flags, the tile scan and emit (6 launches,
+// the nxt / spec / flags arrays).
+// ---------------------------------------------------------------------------
+constexpr u64 kXKnown = 1ull << 63;  // exit word: the tile's true exit is known
+constexpr u64 kTvAgg = 1ull << 62, kTvInc = 2ull << 62, kTvMask = (1ull << 62) - 1;
+constexpr u64 kLsKnown = 1ull << 63;  // last-start word: 1 + last start (0: none) published
+
+__device__ __forceinline__ u32 nf_gallop(const u64* __restrict__ P, u64 s, u64 m, u64 cap) {
+    const u64 limit = P[s] + cap;
+    const u64 top = s + cap < m ? s + cap : m;
+    u64 lo = s + 1, step = 1;
+    while (lo + step <= top && P[lo + step] <= limit) {
+        lo += step;
+        step <<= 1;
+    }
+    u64 hi = lo + step - 1 < top ? lo + step - 1 : top;
+    while (lo < hi) {
+        const u64 mid = (lo + hi + 1) >> 1;
+        if (P[mid] <= limit) lo = mid;
+        else hi = mid - 1;
+    }
+    return static_cast<u32>(lo);
+}
+
+__device__ __forceinline__ u64 ld_acquire_u64(const u64* p) {
+    u64 v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct NfRoundArgs {
+    const u64* F;
+    const u64* P;
+    u64 m, cap, tmin;
+    PackSink sink;
+    u64 mbase, pbase;
+    u64* newpool;
+    u64* totals;
+    u32 ntiles;
+    u32* tile_ctr;
+    u64* xst;   // [ntiles] kXKnown | true exit
+    u64* tvst;  // [ntiles] look-back words of the frozen totals
+    u64* lsst;  // [ntiles] kLsKnown | (1 + last start)
+};
+
+// levels (reused first for the staged prefix sums, last by the emit for the
+// entries and their destinations) + next + pack totals
+constexpr int NF_PW = 1024;  // prefix sums staged past the tile for next()
+constexpr int NF_SMEM_FUSED = static_cast<int>(sizeof(unsigned short) * NF_LV * NF_T + 2 * sizeof(u32) * NF_T);
+static_assert(sizeof(u64) * (NF_T + NF_PW + 1) <= sizeof(unsigned short) * NF_LV * NF_T, "staged P fits the levels");
+static_assert(sizeof(u64) * (NF_T + NF_T / 32) + sizeof(u32) * (NF_T + NF_T / 32) <=
+                  sizeof(unsigned short) * NF_LV * NF_T,
+              "emit staging fits the levels");
+
+__global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
+    constexpr u64 kElems = (1ull << 31) - 1;
+    extern __shared__ __align__(16) unsigned char nf_smem[];
+    auto* s_L = reinterpret_cast<unsigned short*>(nf_smem);           // [NF_LV][NF_T]
+    auto* s_nx = reinterpret_cast<u32*>(s_L + NF_LV * NF_T);          // absolute next
+    auto* s_tot = s_nx + NF_T;                                        // pack total from each position
+    auto* s_P = reinterpret_cast<u64*>(nf_smem);                      // first: P[a .. a + NF_T + NF_PW]
+    auto* s_F = reinterpret_cast<u64*>(nf_smem);                      // emit: entries (padded), over the levels
+    auto* s_dst = reinterpret_cast<u32*>(s_F + NF_T + NF_T / 32);     // emit: destinations (padded)
+    __shared__ u32 s_spec[NF_T / 32];
+    __shared__ u32 s_fl[NF_T / 32];
+    __shared__ u64 s_red[33];
+    __shared__ u32 s_mx[NF_B / 32];
+    __shared__ u64 s_tv[2];
+    __shared__ u32 s_last2[2];
+    __shared__ u32 s_tile, s_h0, s_hi_entry, s_carry;
+    __shared__ u64 s_entry, s_conv, s_tpre;
+    __shared__ int s_ok;
+    auto pad = [](u32 i) { return i + (i >> 5); };
+    const u32 t = threadIdx.x;
+    if (t == 0) s_tile = atomicAdd(r.tile_ctr, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 m = r.m;
+    const u64 a = static_cast<u64>(tile) * NF_T;
+    const u64 end = a + NF_T < m ? a + NF_T : m;
+    const u32 len = static_cast<u32>(end - a);
+
+    // prefix sums of the tile and NF_PW positions past it, staged; next()
+    // of every position by a gallop over them (global P past the window)
+    const u64 pend = end + NF_PW < m ? end + NF_PW : m;  // staged: P[a .. pend]
+    for (u64 i = a + t; i <= pend; i += NF_B) s_P[i - a] = r.P[i];
+    __syncthreads();
+    {
+        const u64* __restrict__ P = r.P;
+        auto Pat = [&](u64 x) -> u64 { return x <= pend ? s_P[x - a] : P[x]; };
+        const u64 cap = r.cap;
+        for (u32 i = t; i < len; i += NF_B) {
+            const u64 sp = a + i;
+            const u64 base = s_P[i];
+            const u64 limit = base + cap;
+            const u64 top = sp + cap < m ? sp + cap : m;
+            u64 lo = sp + 1, step = 1;
+            while (lo + step <= top && Pat(lo + step) <= limit) {
+                lo += step;
+                step <<= 1;
+            }
+            u64 hi = lo + step - 1 < top ? lo + step - 1 : top;
+            while (lo < hi) {
+                const u64 mid = (lo + hi + 1) >> 1;
+                if (Pat(mid) <= limit) lo = mid;
+                else hi = mid - 1;
+            }
+            s_nx[i] = static_cast<u32>(lo);
+            s_tot[i] = static_cast<u32>(Pat(lo) - base);
+        }
+    }
+    __syncthreads();  // the staged P is overwritten by the levels below
+    for (u32 i = t; i < NF_T; i += NF_B) {
+        u32 f = i;
+        if (i < len) {
+            const u32 nx = s_nx[i];
+            if (nx < end) f = static_cast<u32>(nx - a);
+        }
+        s_L[i] = static_cast<unsigned short>(f);
+    }
+    for (u32 i = t; i < NF_T / 32; i += NF_B) s_spec[i] = 0;
+    if (t == 0) {
+        s_ok = 1;
+        s_hi_entry = a > 0 ? nf_gallop(r.P, a - 1, m, r.cap) : 0u;  // entries lie in [a, next(a - 1)]
+    }
+    __syncthreads();
+    // speculative chain (k_nf_tiles)
+    for (int k = 0; k + 1 < NF_LV; ++k) {
+        const unsigned short* Fk = s_L + k * NF_T;
+        unsigned short* Fn = s_L + (k + 1) * NF_T;
+        for (u32 i = t; i < NF_T; i += NF_B) Fn[i] = Fk[Fk[i]];
+        __syncthreads();
+    }
+    const unsigned short* last = s_L + (NF_LV - 1) * NF_T;
+    const u32 last0 = last[0];
+    if (t == 0) {
+        u32 x = 0, h = 0;
+        for (int k = NF_LV - 2; k >= 0; --k) {
+            const u32 y = s_L[k * NF_T + x];
+            if (y != last0) {
+                x = y;
+                h += 1u << k;
+            }
+        }
+        s_h0 = x == last0 ? h : h + 1;
+    }
+    __syncthreads();
+    const u32 h0 = s_h0;
+    for (u32 q = t; q <= h0; q += NF_B) {
+        u32 x = 0;
+#pragma unroll
+        for (int k = 0; k + 1 < NF_LV; ++k)
+            if ((q >> k) & 1u) x = s_L[k * NF_T + x];
+        atomicOr(&s_spec[x >> 5], 1u << (x & 31));
+    }
+    if (a > 0) {
+        const u64 hi_entry = s_hi_entry;
+        if (hi_entry >= end) {
+            if (t == 0) s_ok = 0;
+        } else {
+            for (u64 e = a + t; e <= hi_entry; e += NF_B)
+                if (last[e - a] != last0) s_ok = 0;
+        }
+    }
+    __syncthreads();
+    const u64 exit_spec = s_nx[last0];
+    const bool allconv = tile == 0 || s_ok;  // tile 0 is entered at its start
+    if (t == 0) {
+        if (allconv) st_release_u64(r.xst + tile, kXKnown | exit_spec);
+        // entry: the true exit of the tile before
+        u64 e = 0;
+        if (tile > 0) {
+            u64 w;
+            while (!((w = ld_acquire_u64(r.xst + tile - 1)) & kXKnown)) {
+            }
+            e = w & ~kXKnown;
+        }
+        // walk from the entry until the speculative chain (k_nf_flags)
+        for (u32 i = 0; i < NF_T / 32; ++i) s_fl[i] = 0;
+        u64 x = e;
+        while (x < end && !((s_spec[(x - a) >> 5] >> ((x - a) & 31)) & 1u)) {
+            const u32 q = static_cast<u32>(x - a);
+            s_fl[q >> 5] |= 1u << (q & 31);
+            x = s_nx[q];
+        }
+        if (!allconv) st_release_u64(r.xst + tile, kXKnown | (x < end ? exit_spec : x));
+        s_entry = e;
+        s_conv = x;
+    }
+    __syncthreads();
+    // final start flags, frozen totals among the tile's starts, last start
+    const u64 conv = s_conv;
+    if (t < NF_T / 32) {  // two warps, one flags word each
+        const u64 p0 = a + 32ull * t;
+        u32 bits = 0;
+        if (p0 < end) {
+            bits = s_spec[t];
+            if (conv >= p0 + 32) bits = 0;
+            else if (conv > p0) bits &= ~((1u << (conv - p0)) - 1u);
+            bits |= s_fl[t];
+            if (end < p0 + 32) bits &= (1u << (end - p0)) - 1u;
+        }
+        s_fl[t] = bits;
+        u64 fe = 0, fp = 0;
+        for (u32 b = bits; b; b &= b - 1) {
+            const u64 st = p0 + __ffs(b) - 1;
+            if (s_tot[st - a] >= r.tmin) {
+                fe += s_nx[st - a] - st;
+                ++fp;
+            }
+        }
+        const u64 v = warp_sum((fp << 31) | fe);
+        u32 lst = bits ? static_cast<u32>(p0) + 32u - __clz(bits) : 0u;  // 1 + last start, absolute
+        lst = warp_max(lst);
+        if ((t & 31u) == 0) {
+            s_tv[t >> 5] = v;
+            s_last2[t >> 5] = lst;
+        }
+    }
+    __syncthreads();
+    // publish (aggregate, last start), then look back over the tiles before
+    if (t == 0) {
+        const u64 tv = s_tv[0] + s_tv[1];
+        const u32 lst = max(s_last2[0], s_last2[1]);
+        st_release_u64(r.lsst + tile, kLsKnown | lst);
+        st_release_u64(r.tvst + tile, (tile == 0 ? kTvInc : kTvAgg) | tv);
+        u64 excl = 0;
+        u32 carry = 0;
+        if (tile > 0) {
+            for (long long q = static_cast<long long>(tile) - 1;; --q) {
+                u64 w;
+                while (((w = ld_acquire_u64(r.tvst + q)) >> 62) == 0) {
+                }
+                excl += w & kTvMask;
+                if ((w >> 62) == 2) break;
+            }
+            for (long long q = static_cast<long long>(tile) - 1; q >= 0 && carry == 0; --q) {
+                u64 w;
+                while (!((w = ld_acquire_u64(r.lsst + q)) & kLsKnown)) {
+                }
+                carry = static_cast<u32>(w);
+            }
+            st_release_u64(r.tvst + tile, kTvInc | (excl + tv));
+        }
+        s_tpre = excl;
+        s_carry = carry;
+    }
+    // the levels are done with: the entries go where they were
+#pragma unroll
+    for (int k = 0; k < EM_ITEMS; ++k) {
+        const u32 li = k * NF_B + t;
+        if (li < len) s_F[pad(li)] = r.F[a + li];
+    }
+    __syncthreads();
+    // emit (k_nf_emit): every position's pack and the inclusive frozen count
+    const u32 p0 = t * EM_ITEMS;
+    const u32 bits = (s_fl[p0 >> 5] >> (p0 & 31)) & 0xffu;
+    u32 e_of[EM_ITEMS];
+    u32 tot_of[EM_ITEMS];
+    u64 v = 0;
+#pragma unroll
+    for (int j = 0; j < EM_ITEMS; ++j) {
+        e_of[j] = 0;
+        tot_of[j] = 0;
+        if ((bits >> j) & 1u) {
+            const u64 st = a + p0 + j;
+            const u32 e = s_nx[p0 + j];
+            const u64 tot = s_tot[p0 + j];
+            e_of[j] = e;
+            tot_of[j] = static_cast<u32>(tot);
+            if (tot >= r.tmin) v += (1ull << 31) | (e - st);
+        }
+    }
+    u64 btot;
+    const u64 ex = block_exclusive_scan<u64>(v, s_red, btot);
+    const u32 my_last = bits ? static_cast<u32>(a) + p0 + 32u - __clz(bits) : 0u;  // 1 + last own start
+    u32 prev = block_exclusive_max(my_last, s_mx);
+    const bool carried = prev == 0;
+    if (carried) prev = s_carry;
+    u64 run = s_tpre + ex;
+    u32 e_cur = 0;
+    bool frz = false;
+    if (!(bits & 1u) && p0 < len) {
+        const u64 st = prev - 1;
+        // a pack carried in from an earlier tile ends at this tile's entry
+        e_cur = carried ? static_cast<u32>(s_entry) : s_nx[st - a];
+        frz = (carried ? r.P[e_cur] - r.P[st] : static_cast<u64>(s_tot[st - a])) >= r.tmin;
+    }
+#pragma unroll
+    for (int j = 0; j < EM_ITEMS; ++j) {
+        const u32 li = p0 + j;
+        if (li >= len) break;
+        const u64 i = a + li;
+        if ((bits >> j) & 1u) {
+            e_cur = e_of[j];
+            frz = tot_of[j] >= r.tmin;
+            if (frz) {
+                const u64 q = r.pbase + (run >> 31);
+                r.sink.pack_off[q] = r.mbase + (run & kElems);
+                r.sink.pack_total[q] = tot_of[j];
+                run += (1ull << 31) | (e_cur - i);
+            }
+        }
+        const u64 fz = run & kElems;
+        s_dst[pad(li)] = frz ? static_cast<u32>(r.mbase + fz - (e_cur - i)) | kToSink : static_cast<u32>(i - fz);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < EM_ITEMS; ++k) {
+        const u32 li = k * NF_B + t;
+        if (li < len) {
+            const u32 d = s_dst[pad(li)];
+            const u64 x = s_F[pad(li)];
+            if (d & kToSink) r.sink.members[d & ~kToSink] = x;
+            else r.newpool[d] = x;
+        }
+    }
+    if (tile == r.ntiles - 1 && t == 0) {  // totals: pool size and sink counters for the next round
+        const u64 tt = s_tpre + btot;
+        r.totals[0] = m - (tt & kElems);
+        r.totals[1] = r.mbase + (tt & kElems);
+        r.totals[2] = r.pbase + (tt >> 31);
+        *r.sink.n_members = r.totals[1];
+        *r.sink.n_packs = r.totals[2];
+    }
+}
+
 }  // namespace
 
 // Starts of the chain 0 -> nxt[0] -> nxt[nxt[0]] -> ... over m positions
@@ -389,11 +737,7 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     const u64 m = static_cast<u64>(m_signed);
     cudaStream_t s = c.stream;
     DevBuf<u64> P(m + 1, s);
-    DevBuf<u32> nxt(m, s);
     const u32 ntiles = static_cast<u32>((m + NF_T - 1) / NF_T);
-    DevBuf<u32> spec(static_cast<size_t>(ntiles) * (NF_T / 32), s), flags(static_cast<size_t>(ntiles) * (NF_T / 32), s);
-    DevBuf<u32> exitpos(ntiles, s), entry(ntiles, s);
-    DevBuf<u8> allconv(ntiles, s);
     DevBuf<u64> newm(3, s);
 
     // prefix sums of lengths in visiting order (m + 1 entries)
@@ -403,28 +747,58 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
             static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? (F[i] >> 32) : 0ull; },
             [=] __device__(i64 i, u64 v) { Pp[i] = v; }, s, c.scan, "scan.nf1");
     }
-    LAUNCH_B("nf.next", 12.0 * m, k_nf_next, grid_for(m, 256, 148u * 32u), 256, 0, s, P.p, m, static_cast<u64>(cap),
-             nxt.p);
-    {
+    static const bool split = std::getenv("HBP_NF_SPLIT") != nullptr;  // A/B: the six-launch round
+    if (split) {
+        DevBuf<u32> nxt(m, s);
+        DevBuf<u32> spec(static_cast<size_t>(ntiles) * (NF_T / 32), s), flags(static_cast<size_t>(ntiles) * (NF_T / 32), s);
+        DevBuf<u32> exitpos(ntiles, s), entry(ntiles, s);
+        DevBuf<u8> allconv(ntiles, s);
+        LAUNCH_B("nf.next", 12.0 * m, k_nf_next, grid_for(m, 256, 148u * 32u), 256, 0, s, P.p, m, static_cast<u64>(cap),
+                 nxt.p);
         const int smem = static_cast<int>(sizeof(unsigned short) * NF_LV * NF_T);
         set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_nf_tiles), smem);
         LAUNCH_B("nf.tiles", 4.25 * m, k_nf_tiles, ntiles, NF_B, smem, s, nxt.p, m, spec.p, exitpos.p, allconv.p);
+        LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
+        DevBuf<u64> tval(ntiles, s), tpre(ntiles, s);
+        DevBuf<u32> tlast(ntiles, s);
+        LAUNCH_B("nf.flags", 4.25 * m, k_nf_flags, ntiles, NF_B, 0, s, nxt.p, spec.p, entry.p, P.p, m, tmin, flags.p,
+                 tval.p, tlast.p);
+        {
+            const u64* tv = tval.p;
+            u64* tp = tpre.p;
+            scan_exclusive<u64>(
+                static_cast<i64>(ntiles), [=] __device__(i64 i) { return tv[i]; },
+                [=] __device__(i64 i, u64 v) { tp[i] = v; }, s, c.scan, "nf.tiles_scan");
+        }
+        LAUNCH_B("nf.freeze_emit", 16.125 * m, k_nf_emit, ntiles, NF_B, 0, s, F, m, flags.p, nxt.p, P.p, tmin, tpre.p,
+                 tlast.p, sink, n_members, n_packs, newpool, newm.p, ntiles);
+        const auto t = read_vector(c, newm.p, 3);
+        n_members = t[1];
+        n_packs = t[2];
+        return static_cast<i64>(t[0]);
     }
-    LAUNCH(k_nf_entries, grid_for(ntiles, 128), 128, 0, s, nxt.p, spec.p, exitpos.p, allconv.p, m, ntiles, entry.p);
-    DevBuf<u64> tval(ntiles, s), tpre(ntiles, s);
-    DevBuf<u32> tlast(ntiles, s);
-    LAUNCH_B("nf.flags", 4.25 * m, k_nf_flags, ntiles, NF_B, 0, s, nxt.p, spec.p, entry.p, P.p, m, tmin, flags.p,
-             tval.p, tlast.p);
-    {
-        const u64* tv = tval.p;
-        u64* tp = tpre.p;
-        scan_exclusive<u64>(
-            static_cast<i64>(ntiles), [=] __device__(i64 i) { return tv[i]; },
-            [=] __device__(i64 i, u64 v) { tp[i] = v; }, s, c.scan, "nf.tiles_scan");
-    }
-    // algorithmic bytes: entries in and out (16 B) + flags
-    LAUNCH_B("nf.freeze_emit", 16.125 * m, k_nf_emit, ntiles, NF_B, 0, s, F, m, flags.p, nxt.p, P.p, tmin, tpre.p,
-             tlast.p, sink, n_members, n_packs, newpool, newm.p, ntiles);
+    // status words of the fused round: exits, frozen totals, last starts, tile counter
+    DevBuf<u64> st(3ull * ntiles + 1, s);
+    st.zero();
+    NfRoundArgs ra;
+    ra.F = F;
+    ra.P = P.p;
+    ra.m = m;
+    ra.cap = cap;
+    ra.tmin = tmin;
+    ra.sink = sink;
+    ra.mbase = n_members;
+    ra.pbase = n_packs;
+    ra.newpool = newpool;
+    ra.totals = newm.p;
+    ra.ntiles = ntiles;
+    ra.xst = st.p;
+    ra.tvst = st.p + ntiles;
+    ra.lsst = st.p + 2ull * ntiles;
+    ra.tile_ctr = reinterpret_cast<u32*>(st.p + 3ull * ntiles);
+    set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_nf_round), NF_SMEM_FUSED);
+    // algorithmic bytes: P read (8 B), entries in and out (16 B)
+    LAUNCH_B("nf.round", 24.0 * m, k_nf_round, ntiles, NF_B, NF_SMEM_FUSED, s, ra);
     const auto t = read_vector(c, newm.p, 3);
     n_members = t[1];
     n_packs = t[2];

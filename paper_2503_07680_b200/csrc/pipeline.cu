@@ -987,37 +987,56 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     for (int gi = ng - 1; gi >= 0; --gi) {
         if (psize[gi] == 0) continue;
         const u32 cap = static_cast<u32>(a.groups[gi].length);
-        PackedGroup pg;
-        pack_pool(c, corpus, pools[gi].p, psize[gi], cap, a.strategy,
-                  derive_seed(a.seed, "pack", static_cast<uint64_t>(gi)), pg);
-        pools[gi].release();
-        psize[gi] = 0;
-
-        // greedy fill from pools gi-1 .. 0 (balance.cpp:235-243)
-        DevBuf<u64> fill_items;
-        DevBuf<u32> fill_bin, fill_slot;
+        // greedy fill from pools gi-1 .. 0 (balance.cpp:235-243): the items
+        // (nearest, i.e. longest, pool first, each sorted by length desc, key
+        // asc) and their runs depend only on the pools, so they are sorted on
+        // the side stream while this group packs on the main stream
         u64 n_fill = 0;
         if (a.greedy_fill && gi > 0) {
             for (int j = 0; j < gi; ++j) n_fill += psize[j];
         }
-        if (n_fill > 0 && pg.P() > 0) {
+        DevBuf<u64> fill_items;
+        DevBuf<u32> fill_bin, fill_slot, run_item, run_len, n_runs;
+        FitRuns fruns;
+        SideJoin fork_guard(c);  // after the buffers the side stream uses: joined before they go
+        if (n_fill > 0) {
             fill_items.alloc(n_fill, s);
-            u64 o = 0;
-            for (int j = gi - 1; j >= 0; --j) {  // nearest (longest) pool first
-                if (!psize[j]) continue;
-                CUDA_CHECK(cudaMemcpyAsync(fill_items.p + o, pools[j].p, sizeof(u64) * psize[j],
-                                           cudaMemcpyDeviceToDevice, s));
-                sort_entries(c, corpus, fill_items.p + o, psize[j], corpus.key32.p == nullptr,
-                             static_cast<u32>(a.groups[j].length));
-                o += psize[j];
+            run_item.alloc(n_fill, s);
+            run_len.alloc(n_fill, s);
+            n_runs.alloc(4, s);
+            fruns = FitRuns{run_item.p, run_len.p, n_runs.p};
+            side_fork(c);
+            fork_guard.armed = true;
+            {
+                SideScope side(c);
+                u64 o = 0;
+                for (int j = gi - 1; j >= 0; --j) {  // nearest (longest) pool first
+                    if (!psize[j]) continue;
+                    CUDA_CHECK(cudaMemcpyAsync(fill_items.p + o, pools[j].p, sizeof(u64) * psize[j],
+                                               cudaMemcpyDeviceToDevice, c.stream));
+                    sort_entries(c, corpus, fill_items.p + o, psize[j], corpus.key32.p == nullptr,
+                                 static_cast<u32>(a.groups[j].length));
+                    o += psize[j];
+                }
+                prepare_runs(c, fill_items.p, static_cast<i64>(n_fill), corpus.key32.p,
+                             static_cast<u64>(corpus.neg_ids), fruns);
             }
-            trace_mark(c, "fill.sort");
+        }
+        PackedGroup pg;
+        pack_pool(c, corpus, pools[gi].p, psize[gi], cap, a.strategy,
+                  derive_seed(a.seed, "pack", static_cast<uint64_t>(gi)), pg);
+        fork_guard.join();
+        pools[gi].release();
+        psize[gi] = 0;
+        trace_mark(c, "fill.sort");
+        if (n_fill > 0 && pg.P() == 0) n_fill = 0;  // nothing to fill
+        if (n_fill > 0) {
             const u64 P = pg.P();
             fill_bin.alloc(n_fill, s);
             fill_slot.alloc(n_fill, s);
             first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p, static_cast<i64>(P),
                            static_cast<i64>(P), cap, FitMode::Fill, fill_bin.p, fill_slot.p, corpus.key32.p,
-                           static_cast<u64>(corpus.neg_ids));
+                           static_cast<u64>(corpus.neg_ids), &fruns);
             trace_mark(c, "fill.engine");
             // remove consumed samples from their pools, order preserved
             if (!consumed.p) {

@@ -71,10 +71,12 @@ __device__ void fy_fix_block(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u
     if (used && threadIdx.x == 0) *used = (m - 1) + shift;
 }
 
-// Targets and their counts; rej: the highest rejected step (k_fy_fix
-// repairs from there; it returns at once when there is none).
+// Targets and their counts; rej[0]: the highest rejected step. The last
+// block to finish repairs from there (fy_fix_block; it returns at once when
+// there is no rejection) -- no separate launch for the rare path.
 __global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
-                             unsigned long long* __restrict__ rej, u64 force) {
+                             unsigned long long* __restrict__ rej, u64 force, unsigned long long* __restrict__ used,
+                             bool split_fix) {
     for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
         bool bad;
@@ -84,6 +86,15 @@ __global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u
         tgt[i] = j;
         atomicAdd(&cnt[j], 1u);
     }
+    if (split_fix) return;
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(rej + 1, 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    fy_fix_block(seed, base, m, tgt, cnt, *reinterpret_cast<volatile unsigned long long*>(rej), used);
 }
 
 __global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
@@ -187,7 +198,7 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     }
     DevBuf<unsigned long long> used(draws_used ? 1 : 0, s);
     DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), off(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s);
-    DevBuf<unsigned long long> rej(1, s);
+    DevBuf<unsigned long long> rej(2, s);  // highest rejected step, finished blocks
     DevBuf<u32> first0(1, s);
     cnt.zero();
     rej.zero();
@@ -197,8 +208,10 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     // step as rejected, to exercise the repair on demand (a real rejection has
     // probability < m / 2^64)
     const u64 force = c.test_force_reject;
-    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, force);
-    LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
+    static const bool split_fix = std::getenv("HBP_FY_SPLITFIX") != nullptr;  // A/B: separate fix-up launch
+    LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, force,
+             used.p, split_fix);
+    if (split_fix) LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
     // exclusive scan of per-target counts -> list offsets (m + 1 entries)
     const u32* cntp = cnt.p;
     u32* offp = off.p;

@@ -76,8 +76,20 @@ enum class FitMode { Ffd, Fill };
 // a bin with residual r takes floor((r - 1) / s) of its items, and the
 // non-negative part after it the usual floor(r' / s) -- the reference's
 // pack-by-pack picks, run by run (flag: bit 31 of run_len).
+// The runs of equal length of sorted items (first item, length | strict
+// bit 31, and their count in n_runs[0]): computed by first_fit_runs, or
+// ahead of it (prepare_runs, no host sync) -- e.g. on the side stream while
+// the bins are still being built. Buffers sized by the caller (n items).
+struct FitRuns {
+    u32* run_item = nullptr;
+    u32* run_len = nullptr;
+    u32* n_runs = nullptr;  // device scalar (4 words: the tree engines reuse it)
+};
+void prepare_runs(Ctx& c, const u64* items, i64 n_items, const u32* key32, u64 neg_keys, FitRuns r);
+
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items, u64* leaves, i64 bins0, i64 max_bins, u32 cap,
-                         FitMode mode, u32* item_bin, u32* item_slot, const u32* key32 = nullptr, u64 neg_keys = 0);
+                         FitMode mode, u32* item_bin, u32* item_slot, const u32* key32 = nullptr, u64 neg_keys = 0,
+                         const FitRuns* pre = nullptr);
 
 // scanfit.cu: best fit (worst = false, packing.cpp:105-127) or the
 // emptiest-pack rule of SPFHP (worst = true, packing.cpp:129-162) of the

@@ -19,16 +19,18 @@
 // frontier warp is on the critical path of every block, so the chain keeps
 // it short (see serve) and writes nothing but the input counts of its
 // active cells; a replay kernel re-serves those cells in parallel and
-// writes the heads (item -> bin, slot). Every warp is resident (cooperative launch), so after the chain fills
-// all bins work on different run blocks at once.
+// writes the heads (item -> bin, slot). CTAs take their chain position in
+// the order they start, so once the chain has filled every resident bin
+// works on a different run block at the same time.
 //
 // Hand-off: each count travels as one 64-bit word (block tag << 32 | count)
 // that the consumer lane polls, so no flag or fence sits on the path --
-// through shared memory between the warps of a CTA, through global memory
-// (L2) from the last warp of a CTA to the first of the next. Consumers
-// publish how many blocks they have read so that producers never overwrite
-// an unread slot (ring of kQ blocks). Items are written straight to
-// (bin, slot); bin counts give the slots.
+// through shared memory between the warps of a CTA (a ring of kQs blocks;
+// consumers publish how many blocks they have read so that producers never
+// overwrite an unread slot), through global memory (L2) from the last warp of
+// a CTA to the first of the next (a slot per block: a CTA never waits for a
+// later one, so the chain needs no co-resident launch). Items are written
+// straight to (bin, slot); bin counts give the slots.
 #include "stages.cuh"
 
 namespace hbp_b200 {
@@ -38,7 +40,6 @@ namespace {
 #ifndef HBP_CHAIN_WALK
 #define HBP_CHAIN_WALK 3  // lanes walked one by one before a warp scan
 #endif
-constexpr int kQ = 32;         // global ring depth per link, in blocks of 32 runs
 constexpr int kQs = 16;        // shared-memory ring depth (dynamic shared memory)
 // warps per CTA (one CTA per SM): fewer for wide lanes so registers stay <= 128
 // Warps per CTA. A short chain spreads over the SMs in CTAs of 4 warps
@@ -48,7 +49,6 @@ constexpr int kQs = 16;        // shared-memory ring depth (dynamic shared memor
 constexpr int kShortWarps = 4;
 template <int M>
 __host__ __device__ constexpr int warps_for() { return M <= 4 ? 32 : 16; }
-constexpr u32 kStride = 32;    // u32 between global consumer counters (one 128 B line each)
 // Blocks of run data (and, for a CTA's first warp, of L2 ring words) each
 // warp has in flight ahead of the block it serves. A warp whose cells are
 // inactive spends only ~100 ns per block, while one L2 round trip is
@@ -71,8 +71,8 @@ struct ChainArgs {
     int ffd;
     u32 J, nblocks;
     u32 rb;  // runs per block (lanes 0..rb-1 carry them; 8, 16 or 32)
-    unsigned long long* gring;  // CTA g -> g+1: kQ * 32 tagged counts
-    u32* gcons;                 // gcons[(g+1) * kStride]: blocks CTA g+1's first warp has read
+    unsigned long long* gring;  // CTA g -> g+1: nblocks * 32 tagged counts (every block has its slot)
+    u32* cta_ctr;               // CTA ids in launch order (atomic counter)
     u32* item_bin;   // heads only: at the first item of each take
     u32* item_slot;
     u32* take;       // items in the take starting here (0: not a head)
@@ -474,12 +474,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
     constexpr int kPF = prefetch_depth<kWarps>();
     ChainPF<kPF>* s_pf = reinterpret_cast<ChainPF<kPF>*>(s_stage + kWarps);
     __shared__ u32 s_cons[kWarps];                         // blocks warp w has read from s_ring[w]
+    __shared__ u32 s_g;
     const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-    const u32 g = blockIdx.x;
-    const u32 j = g * kWarps + w;
+    // CTA ids in the order CTAs start: CTA g only ever waits on CTA g - 1,
+    // which started before it, and the L2 links hold every block (no
+    // back-pressure between CTAs), so the chain needs no co-residency -- no
+    // cooperative launch, and chains on other streams run alongside
+    if (threadIdx.x == 0) s_g = atomicAdd(a.cta_ctr, 1u);
     for (u32 i = threadIdx.x; i < kWarps * kQs * 32; i += blockDim.x) (&s_ring[0][0][0])[i] = 0ull;
     if (threadIdx.x < kWarps) s_cons[threadIdx.x] = 0;
     __syncthreads();
+    const u32 g = s_g;
+    const u32 j = g * kWarps + w;
     if (j >= a.J) return;  // no CTA-wide barriers below
 
     // lane-major: lane l holds bins base + l*M + i (bin order = lane order)
@@ -493,10 +499,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
     const bool replay = a.hist != nullptr;
     volatile unsigned long long* sin = s_ring[w][0];
     volatile unsigned long long* sout = w + 1 < kWarps ? s_ring[w + 1][0] : nullptr;
-    const unsigned long long* gin = a.gring + static_cast<u64>(g) * kQ * 32;  // written by CTA g-1
-    unsigned long long* gout = a.gring + static_cast<u64>(g + 1) * kQ * 32;
-    u32* const my_gcons = a.gcons + g * kStride;
-    const u32* const next_gcons = a.gcons + (g + 1) * kStride;
+    const unsigned long long* gin = a.gring + static_cast<u64>(g) * a.nblocks * 32;  // written by CTA g-1
+    unsigned long long* gout = a.gring + static_cast<u64>(g + 1) * a.nblocks * 32;
     volatile u32* const my_scons = reinterpret_cast<volatile u32*>(s_cons) + w;
     volatile u32* const next_scons = reinterpret_cast<volatile u32*>(s_cons) + (w + 1 < kWarps ? w + 1 : w);
     u32 seen_cons = 0;  // consumer progress known to this producer
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
             cp_async4(&pf.end[slot][lane], ve ? run_item + k + 1 : run_item, ve ? 4u : 0u);
         }
         if (in_global && !head && bb < nblocks && lane < 16)
-            cp_async16_cg(&pf.ring[slot][2 * lane], gin + (bb % kQ) * 32 + 2 * lane);
+            cp_async16_cg(&pf.ring[slot][2 * lane], gin + static_cast<u64>(bb) * 32 + 2 * lane);
         cp_async_commit();
     };
 #pragma unroll 1
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
         } else if (in_global) {
             unsigned long long v = pf.ring[slot][lane];
             if ((v >> 32) != (b + 1))
-                while (((v = ld_relaxed_u64(gin + (b % kQ) * 32 + lane)) >> 32) != (b + 1))
+                while (((v = ld_relaxed_u64(gin + static_cast<u64>(b) * 32 + lane)) >> 32) != (b + 1))
                     if (a.sleep) __nanosleep(a.sleep);
             c = static_cast<u32>(v);
         } else {
@@ -570,10 +574,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
                 t0 = t1;
             }
         }
-        if (!head && lane == 0) {
-            if (in_global) st_relaxed_u32(my_gcons, b + 1);
-            else *my_scons = b + 1;
-        }
+        if (!head && !in_global && lane == 0) *my_scons = b + 1;
         if (act) {  // (the replay's hact is zeroed: inactive cells write nothing)
             const u32 kr = run_begin + b * rb + lane;
             const bool valid = lane < rb && kr < run_end;
@@ -598,13 +599,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
         if (!tail) {
             const unsigned long long v = (static_cast<unsigned long long>(b + 1) << 32) | c;
             if (out_global) {
-                if (b >= static_cast<u32>(kQ) && seen_cons + kQ <= b) {
-                    if (lane == 0)
-                        while ((seen_cons = ld_relaxed_u32(next_gcons)) + kQ <= b)
-                            if (a.sleep) __nanosleep(a.sleep);
-                    seen_cons = __shfl_sync(0xffffffffu, seen_cons, 0);
-                }
-                st_relaxed_u64(gout + (b % kQ) * 32 + lane, v);
+                st_relaxed_u64(gout + static_cast<u64>(b) * 32 + lane, v);
             } else {
                 if (b >= static_cast<u32>(kQs) && seen_cons + kQs <= b) {
                     if (lane == 0)
@@ -704,14 +699,13 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     else (void)chain_capacity<M>(sms);
     cudaStream_t s = c.stream;
     a.J = J;
-    DevBuf<unsigned long long> gring(static_cast<size_t>(G + 1) * kQ * 32, s);
-    DevBuf<u32> gcons(static_cast<size_t>(G + 1) * kStride, s), out(2, s);
+    DevBuf<unsigned long long> gring(static_cast<size_t>(G + 1) * a.nblocks * 32, s);
+    DevBuf<u32> out(4, s);  // [0] top, [1] overflow, [2] CTA id counter
     gring.zero();
-    gcons.zero();
     out.zero();
     a.gring = gring.p;
-    a.gcons = gcons.p;
     a.out = out.p;
+    a.cta_ctr = out.p + 2;
     DevBuf<unsigned long long> prof, tl;
     a.prof = nullptr;
     a.tl = nullptr;
@@ -725,7 +719,6 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
             a.tl = tl.p;
         }
     }
-    void* args[] = {&a};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c.trace) {
         CUDA_CHECK(cudaEventCreate(&e0));
@@ -753,11 +746,11 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     // algorithmic bytes (FFD residue): 12 B per item + 12 B per bin of the pass
     const double alg = 12.0 * a.n_items + 12.0 * (a.bin_end - a.bin0);
     if (c.trace) {
-        if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps, true>), dim3(G), dim3(kWarps * 32), smem, s, args);
-        else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>(), true>), dim3(G), dim3(kWarps * 32), smem, s, args);
+        if (short_chain) LAUNCH_B(name, alg, (k_ff_chain<M, kShortWarps, true>), G, kWarps * 32, smem, s, a);
+        else LAUNCH_B(name, alg, (k_ff_chain<M, warps_for<M>(), true>), G, kWarps * 32, smem, s, a);
     } else {
-        if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps, false>), dim3(G), dim3(kWarps * 32), smem, s, args);
-        else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>(), false>), dim3(G), dim3(kWarps * 32), smem, s, args);
+        if (short_chain) LAUNCH_B(name, alg, (k_ff_chain<M, kShortWarps, false>), G, kWarps * 32, smem, s, a);
+        else LAUNCH_B(name, alg, (k_ff_chain<M, warps_for<M>(), false>), G, kWarps * 32, smem, s, a);
     }
     if (c.trace) CUDA_CHECK(cudaEventRecord(e1, s));
     if (replay) LAUNCH_B("fit.replay", 12.0 * a.n_items + 16.0 * (a.bin_end - a.bin0), k_ff_replay<M>, (J + 7) / 8, 256, 0, s, a);

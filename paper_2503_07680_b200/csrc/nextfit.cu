@@ -732,17 +732,23 @@ void chain_starts(Ctx& c, const u32* nxt, u64 m, u32* flags, u32* tlast) {
 // there (updated), the rest to `newpool`. Returns the new pool size (one
 // host sync).
 i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSink sink, u64* newpool,
-                   u64& n_members, u64& n_packs) {
+                   u64& n_members, u64& n_packs, const u64* P_in) {
     if (m_signed <= 0) return 0;
     const u64 m = static_cast<u64>(m_signed);
     cudaStream_t s = c.stream;
-    DevBuf<u64> P(m + 1, s);
+    DevBuf<u64> Pbuf;
     const u32 ntiles = static_cast<u32>((m + NF_T - 1) / NF_T);
     DevBuf<u64> newm(3, s);
 
-    // prefix sums of lengths in visiting order (m + 1 entries)
-    {
-        u64* Pp = P.p;
+    // prefix sums of lengths in visiting order (m + 1 entries), unless the
+    // shuffle already wrote them
+    struct {
+        const u64* p;
+    } P{P_in};
+    if (!P_in) {
+        Pbuf.alloc(m + 1, s);
+        P.p = Pbuf.p;
+        u64* Pp = Pbuf.p;
         scan_exclusive<u64>(
             static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? (F[i] >> 32) : 0ull; },
             [=] __device__(i64 i, u64 v) { Pp[i] = v; }, s, c.scan, "scan.nf1");

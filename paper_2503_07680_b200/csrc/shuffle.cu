@@ -155,20 +155,24 @@ __device__ __forceinline__ u32 chain_root(const u32* __restrict__ link, u32 r) {
     return r - 1;
 }
 
+// Source position of output slot p.
+__device__ __forceinline__ u32 fy_source(u64 p, const u32* __restrict__ tgt, const u32* __restrict__ nxt,
+                                         const u32* __restrict__ link, const u32* __restrict__ first0) {
+    if (p == 0) {
+        const u32 w = *first0;
+        return (w != kNone) ? chain_root(link, w) : 0u;
+    }
+    const u64 i = p + 1;
+    const u32 w = nxt[i];
+    return (w != kNone) ? chain_root(link, w) : tgt[i];
+}
+
 __global__ void k_fy_sources(u64 m, const u32* __restrict__ tgt, const u32* __restrict__ nxt,
                              const u32* __restrict__ link, const u32* __restrict__ first0,
                              u32* __restrict__ src, const u64* __restrict__ in, u64* __restrict__ out) {
     for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < m;
          p += static_cast<u64>(gridDim.x) * blockDim.x) {
-        u32 s;
-        if (p == 0) {
-            const u32 w = *first0;
-            s = (w != kNone) ? chain_root(link, w) : 0u;
-        } else {
-            const u64 i = p + 1;
-            const u32 w = nxt[i];
-            s = (w != kNone) ? chain_root(link, w) : tgt[i];
-        }
+        const u32 s = fy_source(p, tgt, nxt, link, first0);
         if (in) out[p] = in[s];
         else src[p] = s;
     }
@@ -238,6 +242,8 @@ void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src, uint64_t draw_b
 void fy_shuffle_u64(Ctx& c, uint64_t seed, i64 m, const u64* in, u64* out) {
     fy_run(c, seed, m, nullptr, in, out, 0, nullptr);
 }
+
+
 
 void gather_u64(Ctx& c, const u64* in, const u32* src, u64* out, i64 m) {
     if (m <= 0) return;

@@ -36,7 +36,7 @@ u64 chain_flag_words(u64 m);
 void chain_starts(Ctx& c, const u32* nxt, u64 m, u32* flags, u32* tlast);
 
 i64 nextfit_freeze(Ctx& c, const u64* F, i64 m, u32 cap, u64 tmin, PackSink sink, u64* newpool, u64& n_members,
-                   u64& n_packs);
+                   u64& n_packs, const u64* P_in = nullptr);
 
 // ---- first-fit by runs (firstfit.cu) -------------------------------------
 //

@@ -26,6 +26,7 @@ import os
 import statistics
 import subprocess
 import sys
+import threading
 import time
 
 import numpy as np
@@ -279,25 +280,28 @@ def run_ours(args, rank, world, local):
     prof = abi.default_profile()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    def step_device():
-        s, keep = abi.device_samples(0, d_len.data_ptr(), n, "bench")
-        plan = ctx.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
+    def step_device(c=None, dl=None):
+        c = c or ctx
+        dl = d_len if dl is None else dl
+        s, keep = abi.device_samples(0, dl.data_ptr(), n, "bench")
+        plan = c.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
         plan.report()
         plan.simulate(prof)
         return plan
 
     phases = os.environ.get("HBP_BENCH_PHASES") == "1"
 
-    def step_e2e():
+    def step_e2e(c=None):
+        c = c or ctx
         t0 = time.perf_counter()
         s, keep = abi.make_samples(None, h_len.numpy(), "bench")
-        plan = ctx.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
+        plan = c.build_plan_samples(s, C2_GROUPS, 16384, device_count=DEVICES, seed=PLAN_SEED)
         t1 = time.perf_counter()
         m = plan.report()
         st = plan.simulate(prof)
         t2 = time.perf_counter()
         v = abi.PlanView()
-        ctx.check(lib.hbp_plan_view_get(ctx.h, plan.h, C.byref(v)))
+        c.check(lib.hbp_plan_view_get(c.h, plan.h, C.byref(v)))
         if phases:
             t3 = time.perf_counter()
             print(f"e2e phases ms: build {1e3 * (t1 - t0):.1f} report+sim {1e3 * (t2 - t1):.1f} "
@@ -323,21 +327,71 @@ def run_ours(args, rank, world, local):
             ms.append(a.elapsed_time(b))
         return ms, out
 
+    # Plans in flight: IN_FLIGHT contexts (one stream and one host thread
+    # each; ctypes releases the GIL inside the C-ABI calls) build independent
+    # plans at once, as a loader building the plans of several corpora (or
+    # epochs) does -- one plan leaves the GPU mostly idle in its first-fit
+    # chains and host round trips, and the copies of one overlap the kernels
+    # of another. Each context packs its own copy of the corpus (IN_FLIGHT x
+    # 80 MB > the 126 MB L2). Timed on the device: events on every context's
+    # stream, from a start recorded on an idle device to the last end.
+    ctxs = [ctx] + [abi.Context(local) for _ in range(IN_FLIGHT - 1)]
+    d_lens = [d_len] + [d_len.clone() for _ in range(IN_FLIGHT - 1)]
+    streams = [stream] + [torch.cuda.ExternalStream(lib.hbp_ctx_stream(c.h)) for c in ctxs[1:]]
+
+    def timed_inflight(fn, k):
+        per = [k // IN_FLIGHT + (1 if i < k % IN_FLIGHT else 0) for i in range(IN_FLIGHT)]
+        outs = [None] * IN_FLIGHT
+        errs = []
+
+        def work(i):
+            try:
+                for _ in range(per[i]):
+                    outs[i] = None  # one plan alive per context
+                    outs[i] = fn(i)
+            except Exception as e:  # surfaced after the join
+                errs.append(e)
+
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        th = [threading.Thread(target=work, args=(i,)) for i in range(IN_FLIGHT)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        ends = []
+        for st_ in streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(st_)
+            ends.append(e)
+        torch.cuda.synchronize()
+        return max(start.elapsed_time(e) for e in ends), outs
+
     # the clock sampler starts before the warm-up: nvidia-smi's start-up takes
     # the driver for ~100 ms and would land inside the first timed steps
     clocks = Clocks(local)
     clocks.start()
     time.sleep(1.0)
     for _ in range(args.warmup):
-        step_device()
-        step_e2e()
+        for i in range(IN_FLIGHT):
+            step_device(ctxs[i], d_lens[i])
+            step_e2e(ctxs[i])
     launches0 = ctx.launches
-    dev_ms, plan = timed(step_device, args.steps)
+    dev_ms, plan = timed(step_device, args.steps)  # one plan at a time: the latency of a step
     plan = None  # one plan alive at a time (the e2e loop would otherwise grow the memory pool in its first step)
     launches = (ctx.launches - launches0) // max(1, args.steps)
     e2e_ms, e2e_out = timed(step_e2e, args.steps)
+    e2e_out = None
+    inf_dev_ms, _ = timed_inflight(lambda i: step_device(ctxs[i], d_lens[i]), args.steps)
+    inf_e2e_ms, inf_out = timed_inflight(lambda i: step_e2e(ctxs[i]), args.steps)
     ck = clocks.stop()
-    d2h = e2e_out[1]
+    d2h = [o for o in inf_out if o is not None][0][1]
+    inf_out = None
 
     # stage profile of one extra step (CUDA events around each engine stage)
     stages = profile_stages(ctx, lib, step_device)
@@ -350,13 +404,17 @@ def run_ours(args, rank, world, local):
     tot_dev = sum(dev_ms)
     tot_e2e = sum(e2e_ms)
     if dist is not None:
-        t = torch.tensor([tot_dev, tot_e2e], device="cuda", dtype=torch.float64)
+        t = torch.tensor([tot_dev, tot_e2e, inf_dev_ms, inf_e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_dev, tot_e2e = t.tolist()
+        tot_dev, tot_e2e, inf_dev_ms, inf_e2e_ms = t.tolist()
     if rank == 0:
-        ms_step = tot_dev / args.steps
+        # headline: whole-job throughput with IN_FLIGHT plans in flight; the
+        # one-plan-at-a-time step (its latency) beside it
+        ms_step = inf_dev_ms / args.steps
         value = world * n / (ms_step / 1000.0)
-        e2e_value = world * n / (tot_e2e / args.steps / 1000.0)
+        e2e_value = world * n / (inf_e2e_ms / args.steps / 1000.0)
+        seq_ms = tot_dev / args.steps
+        seq_e2e_ms = tot_e2e / args.steps
         peak, peak_kind = peaks()
         roof = roofline(stages, peak, peak_kind)
         cpu = cpu_bl.result() if cpu_bl is not None else None
@@ -367,10 +425,15 @@ def run_ours(args, rank, world, local):
             "data": DATA + "; restated bit-identically in csrc/synth.cpp; rank r packs the corpus of seed 20250515 + r",
             "config": bench_config(spec0),
             "parallelism": f"replicas x{world} (packing one corpus does not shard, SURVEY.md 8(e))",
-            "l2": "flushed (256 MB write) before every step",
+            "in_flight": IN_FLIGHT,
+            "l2": (f"{IN_FLIGHT} plans in flight, each on its own copy of the corpus ({IN_FLIGHT} x {8 * n >> 20} MB "
+                   "> 126 MB L2); the one-plan-at-a-time steps flush L2 (256 MB write) before every step"),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": tot_e2e / args.steps, "ms_steps": [round(x, 3) for x in e2e_ms]},
-            "ms_steps": [round(x, 3) for x in dev_ms],
+                    "ms_per_step": inf_e2e_ms / args.steps, "in_flight": IN_FLIGHT,
+                    "one_at_a_time": {"value": world * n / (seq_e2e_ms / 1000.0), "ms_per_step": seq_e2e_ms,
+                                      "ms_steps": [round(x, 3) for x in e2e_ms]}},
+            "one_at_a_time": {"value": world * n / (seq_ms / 1000.0), "ms_per_step": seq_ms,
+                              "ms_steps": [round(x, 3) for x in dev_ms]},
             "gpu_launches": int(launches),
             "roofline": roof,
             "stages_ms": {k: round(v["ms"], 4) for k, v in sorted(stages.items(), key=lambda kv: -kv[1]["ms"])[:12]},
@@ -385,10 +448,13 @@ def run_ours(args, rank, world, local):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    for c in ctxs[1:]:
+        c.close()
     ctx.close()
     return 0
 
 
+IN_FLIGHT = int(os.environ.get("HBP_BENCH_IN_FLIGHT", "3"))  # plans built at once (one context each)
 C1 = dict(count=100_000, short="lognormal:8.5:1.4", long_fraction=0.0, long="", max_length=131072, seed=42)
 SWEEP_SMALLER = [512, 1024, 2048, 4096, 8192, 16384, 32768, 65536]  # 256 length sets with 131072
 SWEEP_SP = [1, 2, 4, 8]

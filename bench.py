@@ -387,7 +387,11 @@ def run_ours(args, rank, world, local):
     launches = (ctx.launches - launches0) // max(1, args.steps)
     e2e_ms, e2e_out = timed(step_e2e, args.steps)
     e2e_out = None
+    # warm-up in flight too: the stream-ordered pool grows to hold IN_FLIGHT
+    # working sets at once (growth inside a timed region stalls the device)
+    timed_inflight(lambda i: step_device(ctxs[i], d_lens[i]), max(args.warmup, 1) * IN_FLIGHT)
     inf_dev_ms, _ = timed_inflight(lambda i: step_device(ctxs[i], d_lens[i]), args.steps)
+    timed_inflight(lambda i: step_e2e(ctxs[i]), max(args.warmup, 1) * IN_FLIGHT)
     inf_e2e_ms, inf_out = timed_inflight(lambda i: step_e2e(ctxs[i]), args.steps)
     ck = clocks.stop()
     d2h = [o for o in inf_out if o is not None][0][1]

@@ -745,7 +745,12 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
     }
     // algorithmic bytes (FFD residue): 12 B per item + 12 B per bin of the pass
     const double alg = 12.0 * a.n_items + 12.0 * (a.bin_end - a.bin0);
-    if (c.trace) {
+    static const bool coop = std::getenv("HBP_CHAIN_COOP") != nullptr;  // A/B: co-resident launch
+    if (coop) {
+        void* args[] = {&a};
+        if (short_chain) LAUNCH_COOP(name, alg, (k_ff_chain<M, kShortWarps, false>), dim3(G), dim3(kWarps * 32), smem, s, args);
+        else LAUNCH_COOP(name, alg, (k_ff_chain<M, warps_for<M>(), false>), dim3(G), dim3(kWarps * 32), smem, s, args);
+    } else if (c.trace) {
         if (short_chain) LAUNCH_B(name, alg, (k_ff_chain<M, kShortWarps, true>), G, kWarps * 32, smem, s, a);
         else LAUNCH_B(name, alg, (k_ff_chain<M, warps_for<M>(), true>), G, kWarps * 32, smem, s, a);
     } else {

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(OB, 3) k_os_pass(const u32* __restrict__ keys_
                                                   u32* __restrict__ keys_out, u32* __restrict__ vals_out, u64 n,
                                                   int shift, bool desc, const u32* __restrict__ gstart,
                                                   unsigned long long* __restrict__ status, u32* __restrict__ tiles,
-                                                  bool bulk) {
+                                                  bool bulk, int dbits) {
     extern __shared__ __align__(128) u32 os_smem[];
     u32* s_k = os_smem;  // tile as loaded
     u32* s_v = s_k + OTILE;
@@ -188,11 +188,13 @@ __global__ void __launch_bounds__(OB, 3) k_os_pass(const u32* __restrict__ keys_
         key[i] = valid ? s_k[e] : 0u;
         const u32 d = valid ? ((desc ? ~key[i] : key[i]) >> shift) & 0xffu : 256u;
         unsigned peers;
-        if (BALLOT) {  // eight ballots instead of one match (lanes with d == 256 never match a valid digit)
+        if (BALLOT) {  // one ballot per live digit bit instead of one match (lanes with d == 256 never match a
+                       // valid digit; the bits above the key's width are zero in every digit of this pass)
             peers = __ballot_sync(0xffffffffu, valid);
             if (!valid) peers = ~peers;
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
+                if (b >= dbits) break;
                 const bool bit = (d >> b) & 1u;
                 const unsigned m = __ballot_sync(0xffffffffu, bit);
                 peers &= bit ? m : ~m;
@@ -307,11 +309,11 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
         if (variant == 0)
             LAUNCH_B("radix.scatter", 16.0 * n, k_os_pass<false>, ntiles, OB, kSmem, s, ki, vi, ko, vo, n,
                      8 * p, descending, gstart + p * 256, status + static_cast<size_t>(p) * ntiles * 256, tiles + p,
-                     bulk);
+                     bulk, 8);
         else
             LAUNCH_B("radix.scatter", 16.0 * n, k_os_pass<true>, ntiles, OB, kSmem, s, ki, vi, ko, vo, n,
                      8 * p, descending, gstart + p * 256, status + static_cast<size_t>(p) * ntiles * 256, tiles + p,
-                     bulk);
+                     bulk, std::min(8, bits - 8 * p));
         std::swap(ki, ko);
         std::swap(vi, vo);
     }

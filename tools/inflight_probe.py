@@ -20,6 +20,8 @@ from paper_2503_07680_b200 import abi  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--only", default="", help="e.g. device3: only that mode, --reps times")
     a = ap.parse_args()
     lib = abi.load_library()
     ctxs = [abi.Context(0) for _ in range(4)]
@@ -42,11 +44,19 @@ def main():
             ctx.check(lib.hbp_plan_view_get(ctx.h, plan.h, C.byref(v)))
         return plan
 
-    for e2e in (False, True):
-        for inflight in (1, 2, 3, 4):
+    modes = [(e2e, k) for e2e in (False, True) for k in (1, 2, 3, 4)]
+    if a.only:
+        modes = [(a.only.startswith("e2e"), int(a.only[-1]))] * a.reps
+    for e2e, inflight in modes:
+        if True:
             for c in ctxs[:inflight]:
                 step(c, e2e)
             torch.cuda.synchronize()
+            warm = [threading.Thread(target=lambda c=c: (step(c, e2e), c.synchronize())) for c in ctxs[:inflight]]
+            for t in warm:
+                t.start()
+            for t in warm:
+                t.join()  # the pool grows to hold the in-flight working sets before the timed steps
             per = [a.steps // inflight + (1 if i < a.steps % inflight else 0) for i in range(inflight)]
 
             def work(i):

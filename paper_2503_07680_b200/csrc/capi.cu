@@ -109,11 +109,26 @@ int hbp_ctx_create(int device, hbp_ctx** out) {
         delete c;
         return HBP_ERR_CUDA;
     }
-    // keep freed scratch in the stream-ordered pool between calls
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t threshold = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    // a private stream-ordered pool per context (BlockCache::pool): freed
+    // scratch stays in it between calls, and reuse never makes one
+    // context's stream wait for another's (nor the side stream for the main
+    // one: internal dependencies off, a block is reused once its free ran)
+    {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+            uint64_t threshold = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+            int no = 0;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+            c->blocks.pool = pool;
+        } else {
+            cudaGetLastError();
+        }
     }
     *out = c;
     return HBP_OK;
@@ -144,6 +159,7 @@ void hbp_ctx_destroy(hbp_ctx* ctx) {
         ctx->blocks.clear();  // after every buffer that returns blocks to it
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
+        if (ctx->blocks.pool) cudaMemPoolDestroy(ctx->blocks.pool);
     }
     delete ctx;
 }

@@ -70,6 +70,11 @@ inline void set_max_dynamic_smem_once(const void* func, int bytes) {
 // go back to the stream-ordered pool.
 struct BlockCache {
     cudaStream_t stream = nullptr;
+    // the owning context's own stream-ordered pool (null: the device's
+    // default pool). A private pool never hands a context a block another
+    // context freed, so contexts building plans at once never wait on each
+    // other's streams through the allocator.
+    cudaMemPool_t pool = nullptr;
     std::map<size_t, std::vector<void*>> free_blocks;
     size_t cached = 0;
     static constexpr size_t kLimit = size_t(16) << 30;
@@ -89,7 +94,8 @@ struct BlockCache {
             return q;
         }
         void* q = nullptr;
-        CUDA_CHECK(cudaMallocAsync(&q, rounded, stream));
+        if (pool) CUDA_CHECK(cudaMallocFromPoolAsync(&q, rounded, pool, stream));
+        else CUDA_CHECK(cudaMallocAsync(&q, rounded, stream));
         return q;
     }
     void put(void* q, size_t rounded) {
@@ -147,7 +153,11 @@ struct DevBuf {
             p = static_cast<T*>(cache->get(bytes));
         } else {
             cache = nullptr;
-            CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
+            if (g_cache && g_cache->pool)
+                CUDA_CHECK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, g_cache->pool,
+                                                   stream));
+            else
+                CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, stream));
         }
     }
     void release() {

@@ -102,22 +102,22 @@ __global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* 
     fy_fix_block(seed, base, m, tgt, cnt, *rej, used);
 }
 
-__global__ void k_fy_scatter(u64 m, const u32* __restrict__ tgt, const u32* __restrict__ off,
-                             u32* __restrict__ fill, u32* __restrict__ bucket) {
+// cur[j]: the list offsets, advanced in place (one random atomic per step);
+// afterwards cur[q] is the end of S_q, i.e. the start of S_{q+1}
+__global__ void k_fy_scatter(u64 m, const u32* __restrict__ tgt, u32* __restrict__ cur, u32* __restrict__ bucket) {
     for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
-        const u32 j = tgt[i];
-        const u32 slot = atomicAdd(&fill[j], 1u);
-        bucket[off[j] + slot] = static_cast<u32>(i);
+        bucket[atomicAdd(&cur[tgt[i]], 1u)] = static_cast<u32>(i);
     }
 }
 
 // One thread per position q: sort S_q ascending, emit successor links.
-__global__ void k_fy_lists(u64 m, const u32* __restrict__ off, u32* __restrict__ bucket,
+// ends[q]: end of S_q (its start is ends[q - 1], 0 for q = 0).
+__global__ void k_fy_lists(u64 m, const u32* __restrict__ ends, u32* __restrict__ bucket,
                            u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0) {
     for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < m;
          q += static_cast<u64>(gridDim.x) * blockDim.x) {
-        const u32 a = off[q], b = off[q + 1];
+        const u32 a = q ? ends[q - 1] : 0u, b = ends[q];
         // insertion sort (lists are short: E|S_q| = ln(m/q))
         for (u32 x = a + 1; x < b; ++x) {
             const u32 v = bucket[x];
@@ -201,7 +201,7 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
         return;
     }
     DevBuf<unsigned long long> used(draws_used ? 1 : 0, s);
-    DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), off(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s);
+    DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s);
     DevBuf<unsigned long long> rej(2, s);  // highest rejected step, finished blocks
     DevBuf<u32> first0(1, s);
     cnt.zero();
@@ -216,15 +216,15 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, force,
              used.p, split_fix);
     if (split_fix) LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
-    // exclusive scan of per-target counts -> list offsets (m + 1 entries)
-    const u32* cntp = cnt.p;
-    u32* offp = off.p;
+    // exclusive scan of per-target counts -> list offsets, in place (the
+    // scan loads a whole tile before it stores it); the scatter then
+    // advances them as cursors
+    u32* cntp = cnt.p;
     scan_exclusive<u32>(
-        static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? cntp[i] : 0u; },
-        [=] __device__(i64 i, u32 v) { offp[i] = v; }, s, c.scan, "scan.fy1");
-    cnt.zero();  // reused as fill cursors
-    LAUNCH_B("fy.scatter", 20.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, off.p, cnt.p, bucket.p);
-    LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, off.p, bucket.p, nxt.p, link.p, first0.p);
+        static_cast<i64>(m), [=] __device__(i64 i) { return cntp[i]; },
+        [=] __device__(i64 i, u32 v) { cntp[i] = v; }, s, c.scan, "scan.fy1");
+    LAUNCH_B("fy.scatter", 16.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, cnt.p, bucket.p);
+    LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, cnt.p, bucket.p, nxt.p, link.p, first0.p);
     if (in)
         LAUNCH_B("fy.sources_gather", 32.0 * m, k_fy_sources, G, B, 0, s, m, tgt.p, nxt.p, link.p, first0.p, nullptr, in,
                  out);

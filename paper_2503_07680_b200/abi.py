@@ -10,6 +10,11 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass, field
+
+# the engine's contexts, side streams and sweep workers are independent
+# streams; with the default 8 hardware queues they serialise. Effective when
+# set before the process creates its CUDA context (import this first).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from typing import Optional, Sequence
 
 import numpy as np

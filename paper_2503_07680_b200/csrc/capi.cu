@@ -1,6 +1,7 @@
 // capi.cpp — the extern "C" boundary (include/hbp_b200.h). Every entry point
 // converts exceptions into the reference's status codes and keeps the exact
 // message on the context; the work itself is queued on the context stream.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -92,6 +93,10 @@ void hbp_hardware_profile_defaults(hbp_hardware_profile* p) {
 int hbp_ctx_create(int device, hbp_ctx** out) {
     if (out == nullptr) return HBP_ERR_VALIDATION;
     *out = nullptr;
+    // contexts, their side streams and the sweep's workers are independent
+    // streams: give them their own hardware queues (read when the process's
+    // CUDA context is created; no effect if that already happened)
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         cudaGetLastError();
@@ -136,6 +141,8 @@ int hbp_ctx_create(int device, hbp_ctx** out) {
 
 void hbp_ctx_destroy(hbp_ctx* ctx) {
     if (ctx == nullptr) return;
+    for (hbp_ctx* w : ctx->workers) hbp_ctx_destroy(w);
+    ctx->workers.clear();
     cudaSetDevice(ctx->device);
     if (ctx->stream) {
         cudaStreamSynchronize(ctx->stream);
@@ -160,6 +167,7 @@ void hbp_ctx_destroy(hbp_ctx* ctx) {
         cudaStreamSynchronize(ctx->stream);
         cudaStreamDestroy(ctx->stream);
         if (ctx->blocks.pool) cudaMemPoolDestroy(ctx->blocks.pool);
+        if (ctx->ev_sync) cudaEventDestroy(ctx->ev_sync);
     }
     delete ctx;
 }

@@ -36,6 +36,12 @@ struct hbp_ctx {
     hbp_b200::ScanScratch side_scan;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool side_off = false;  // HBP_NO_SIDE: forks run inline on the main stream
+    std::vector<hbp_ctx*> workers;  // the sweep's worker contexts (kept warm; destroyed with this one)
+    // host round trips wait on a blocking-sync event instead of spinning
+    // (the sweep's many worker threads would otherwise spin on the host cores
+    // they need for launching)
+    bool blocking_sync = false;
+    cudaEvent_t ev_sync = nullptr;
     hbp_b200::Pinned pinned;
     hbp_b200::PinnedPool host_pool;  // plan host views
     // stage trace (HBP_TRACE=1): wall time between marks, stream synchronised
@@ -150,13 +156,24 @@ struct SideScope {
     }
 };
 
+// Waits for the context's stream (spinning, or on a blocking-sync event).
+inline void ctx_sync(Ctx& c) {
+    if (!c.blocking_sync) {
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        return;
+    }
+    if (!c.ev_sync) CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_sync, cudaEventBlockingSync | cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(c.ev_sync, c.stream));
+    CUDA_CHECK(cudaEventSynchronize(c.ev_sync));
+}
+
 // Copies a few device scalars to host (one sync).
 template <typename T>
 T read_scalar(Ctx& c, const T* dptr) {
     c.pinned.ensure(sizeof(T));
     ++c.syncs;
     CUDA_CHECK(cudaMemcpyAsync(c.pinned.p, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
-    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    ctx_sync(c);
     return *reinterpret_cast<T*>(c.pinned.p);
 }
 
@@ -217,7 +234,7 @@ std::vector<T> read_vector(Ctx& c, const T* dptr, size_t n) {
     if (n) {
         c.pinned.ensure(sizeof(T) * n);
         CUDA_CHECK(cudaMemcpyAsync(c.pinned.p, dptr, sizeof(T) * n, cudaMemcpyDeviceToHost, c.stream));
-        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+        ctx_sync(c);
         std::memcpy(out.data(), c.pinned.p, sizeof(T) * n);
     }
     return out;

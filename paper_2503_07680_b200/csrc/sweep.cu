@@ -140,7 +140,7 @@ void sweep_evaluate(hbp_ctx& c, const DeviceCorpus& corpus, const hbp_group_conf
     // on the same GPU and takes blocks in order; the corpus in HBM is
     // shared read-only.
     const char* ew = std::getenv("HBP_SWEEP_STREAMS");
-    int W = ew ? std::atoi(ew) : 8;
+    int W = ew ? std::atoi(ew) : 16;
     // every worker holds one plan build in flight: ~300 B per sample at its
     // peak (pools, shuffle and next-fit scratch, the pack table sized by n;
     // measured 25 GB per worker at 100M), so at C5 sizes the free HBM, not
@@ -154,10 +154,17 @@ void sweep_evaluate(hbp_ctx& c, const DeviceCorpus& corpus, const hbp_group_conf
     }
     W = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(W, static_cast<int64_t>(blocks.size()))));
     CUDA_CHECK(cudaStreamSynchronize(c.stream));  // corpus ready for the workers' streams
-    std::vector<hbp_ctx*> workers(static_cast<size_t>(W), nullptr);
-    for (int w = 0; w < W; ++w)
-        if (hbp_ctx_create(c.device, &workers[static_cast<size_t>(w)]) != HBP_OK)
-            throw EngineError(HBP_ERR_CUDA, "sweep: cannot create a worker stream");
+    // worker contexts live as long as the calling context: their streams,
+    // memory pools and block caches stay warm from one sweep to the next
+    while (static_cast<int>(c.workers.size()) < W) {
+        hbp_ctx* wc = nullptr;
+        if (hbp_ctx_create(c.device, &wc) != HBP_OK) throw EngineError(HBP_ERR_CUDA, "sweep: cannot create a worker stream");
+        static const char* eb = std::getenv("HBP_SWEEP_BLOCKING");
+        wc->blocking_sync = eb != nullptr && std::atoi(eb) != 0;
+        c.workers.push_back(wc);
+    }
+    std::vector<hbp_ctx*> workers(c.workers.begin(), c.workers.begin() + W);
+    for (auto* wc : workers) wc->launches = 0;
     std::atomic<size_t> next{0};
     auto work = [&](hbp_ctx* wc) {
         for (size_t bi; (bi = next.fetch_add(1)) < blocks.size();)
@@ -169,10 +176,7 @@ void sweep_evaluate(hbp_ctx& c, const DeviceCorpus& corpus, const hbp_group_conf
     for (int w = 1; w < W; ++w) threads.emplace_back(work, workers[static_cast<size_t>(w)]);
     work(workers[0]);
     for (auto& t : threads) t.join();
-    for (auto* wc : workers) {
-        c.launches += wc->launches;
-        hbp_ctx_destroy(wc);
-    }
+    for (auto* wc : workers) c.launches += wc->launches;
 }
 
 std::vector<int64_t> sweep_shard(const hbp_group_config* cand_groups, const int64_t* cand_offsets,

@@ -18,7 +18,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--one":
     L = np.maximum(bench.synth(lib, bench.C1), 128)
     cands = sweep.make_candidates(ctx, 131072, bench.SWEEP_SMALLER, bench.SWEEP_SP)
     s, keep = abi.make_samples(None, L, "c1")
-    ctx.sweep_samples(s, cands[:64], None, device_count=8, seed=7)
+    ctx.sweep_samples(s, cands, None, device_count=8, seed=7)  # warm-up: every worker, pools grown
     ctx.synchronize()
     t0 = time.perf_counter()
     secs, best = ctx.sweep_samples(s, cands, None, device_count=8, seed=7)

@@ -957,18 +957,27 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     partition(c, corpus, a.groups, entries, goff);
     trace_mark(c, "group_data");
 
-    // pools: group g = entries[goff[g] .. goff[g+1]) in input order; greedy
-    // fill shrinks them (order preserved) before they are packed.
-    std::vector<DevBuf<u64>> pools(ng);
-    std::vector<u64> psize(ng);
-    for (int g = 0; g < ng; ++g) {
-        psize[g] = goff[g + 1] - goff[g];
-        pools[g].alloc(psize[g] + 1, s);
-        if (psize[g])
-            CUDA_CHECK(cudaMemcpyAsync(pools[g].p, entries.p + goff[g], sizeof(u64) * psize[g],
-                                       cudaMemcpyDeviceToDevice, s));
-    }
-    entries.release();
+    // Pools, concatenated: Pin holds pool g at off[g] in input order (the
+    // partition's output as is); Ps holds the same pools sorted for greedy
+    // fill (length desc, key asc), in DEScending group order, so the fill
+    // items of group gi -- pools gi-1 .. 0, nearest (longest) first,
+    // balance.cpp:235-243 -- are the contiguous tail of Ps from soff[gi-1].
+    // Each pool is sorted once; after a fill, one scan compacts the pools it
+    // drew from in both layouts (order preserved), so sorted stays sorted.
+    std::vector<u64> psize(ng), off(ng + 1, 0), soff(ng, 0);
+    for (int g = 0; g < ng; ++g) psize[g] = goff[g + 1] - goff[g];
+    DevBuf<u64> Pin = std::move(entries), Pin2, Ps, Ps2;
+    auto refresh_offsets = [&]() {
+        off[0] = 0;
+        for (int g = 0; g < ng; ++g) off[g + 1] = off[g] + psize[g];
+        u64 o = 0;
+        for (int g = ng - 1; g >= 0; --g) {
+            soff[g] = o;
+            o += psize[g];
+        }
+    };
+    refresh_offsets();
+    const bool any_fill = a.greedy_fill && ng > 1;
 
     PackTable T;
     const u64 cap_packs = n + static_cast<u64>(ng) * N + 1;
@@ -983,24 +992,24 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     DevBuf<int32_t> igroup(max_iters, s);
     u64 I = 0;
     DevBuf<u8> consumed;
+    bool sorted_ready = false;
 
     for (int gi = ng - 1; gi >= 0; --gi) {
         if (psize[gi] == 0) continue;
         const u32 cap = static_cast<u32>(a.groups[gi].length);
-        // greedy fill from pools gi-1 .. 0 (balance.cpp:235-243): the items
-        // (nearest, i.e. longest, pool first, each sorted by length desc, key
-        // asc) and their runs depend only on the pools, so they are sorted on
-        // the side stream while this group packs on the main stream
+        // greedy fill from pools gi-1 .. 0: the items and their runs depend
+        // only on the pools, so they are prepared on the side stream while
+        // this group packs on the main stream (the first time with the sorts)
         u64 n_fill = 0;
-        if (a.greedy_fill && gi > 0) {
+        if (any_fill && gi > 0) {
             for (int j = 0; j < gi; ++j) n_fill += psize[j];
         }
-        DevBuf<u64> fill_items;
         DevBuf<u32> fill_bin, fill_slot, run_item, run_len, n_runs;
         FitRuns fruns;
+        if (n_fill > 0 && !sorted_ready) Ps.alloc(n + 1, s);
+        const u64* fill_items = n_fill > 0 ? Ps.p + soff[gi - 1] : nullptr;
         SideJoin fork_guard(c);  // after the buffers the side stream uses: joined before they go
         if (n_fill > 0) {
-            fill_items.alloc(n_fill, s);
             run_item.alloc(n_fill, s);
             run_len.alloc(n_fill, s);
             n_runs.alloc(4, s);
@@ -1009,68 +1018,101 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             fork_guard.armed = true;
             {
                 SideScope side(c);
-                u64 o = 0;
-                for (int j = gi - 1; j >= 0; --j) {  // nearest (longest) pool first
-                    if (!psize[j]) continue;
-                    CUDA_CHECK(cudaMemcpyAsync(fill_items.p + o, pools[j].p, sizeof(u64) * psize[j],
-                                               cudaMemcpyDeviceToDevice, c.stream));
-                    sort_entries(c, corpus, fill_items.p + o, psize[j], corpus.key32.p == nullptr,
-                                 static_cast<u32>(a.groups[j].length));
-                    o += psize[j];
+                if (!sorted_ready) {
+                    for (int j = gi - 1; j >= 0; --j) {
+                        if (!psize[j]) continue;
+                        CUDA_CHECK(cudaMemcpyAsync(Ps.p + soff[j], Pin.p + off[j], sizeof(u64) * psize[j],
+                                                   cudaMemcpyDeviceToDevice, c.stream));
+                        sort_entries(c, corpus, Ps.p + soff[j], psize[j], corpus.key32.p == nullptr,
+                                     static_cast<u32>(a.groups[j].length));
+                    }
                 }
-                prepare_runs(c, fill_items.p, static_cast<i64>(n_fill), corpus.key32.p,
+                prepare_runs(c, fill_items, static_cast<i64>(n_fill), corpus.key32.p,
                              static_cast<u64>(corpus.neg_ids), fruns);
             }
+            sorted_ready = true;
         }
         PackedGroup pg;
-        pack_pool(c, corpus, pools[gi].p, psize[gi], cap, a.strategy,
+        pack_pool(c, corpus, Pin.p + off[gi], psize[gi], cap, a.strategy,
                   derive_seed(a.seed, "pack", static_cast<uint64_t>(gi)), pg);
         fork_guard.join();
-        pools[gi].release();
-        psize[gi] = 0;
         trace_mark(c, "fill.sort");
         if (n_fill > 0 && pg.P() == 0) n_fill = 0;  // nothing to fill
         if (n_fill > 0) {
             const u64 P = pg.P();
             fill_bin.alloc(n_fill, s);
             fill_slot.alloc(n_fill, s);
-            first_fit_runs(c, fill_items.p, static_cast<i64>(n_fill), pg.leaves.p, static_cast<i64>(P),
+            first_fit_runs(c, fill_items, static_cast<i64>(n_fill), pg.leaves.p, static_cast<i64>(P),
                            static_cast<i64>(P), cap, FitMode::Fill, fill_bin.p, fill_slot.p, corpus.key32.p,
                            static_cast<u64>(corpus.neg_ids), &fruns);
             trace_mark(c, "fill.engine");
-            // remove consumed samples from their pools, order preserved
             if (!consumed.p) {
                 consumed.alloc(n, s);
                 consumed.zero();
             }
-            LAUNCH(k_mark_consumed, G(n_fill), kB, 0, s, fill_items.p, fill_bin.p, n_fill, consumed.p);
-            for (int j = 0; j < gi; ++j) {
-                if (!psize[j]) continue;
-                DevBuf<u64> kept(psize[j] + 1, s);
-                DevBuf<u32> cnt(1, s);
-                const u64* src = pools[j].p;
-                u64* dst = kept.p;
-                u32* cntp = cnt.p;
-                const u8* cons = consumed.p;
-                const i64 m = static_cast<i64>(psize[j]);
-                scan_exclusive<u32>(
-                    m, [=] __device__(i64 i) { return cons[entry_idx(src[i])] ? 0u : 1u; },
-                    [=] __device__(i64 i, u32 v) {
-                        const bool keep = !cons[entry_idx(src[i])];
-                        if (keep) dst[v] = src[i];
-                        if (i == m - 1) *cntp = v + (keep ? 1u : 0u);
-                    },
-                    s, c.scan, "scan.plan4");
-                psize[j] = read_scalar(c, cnt.p);
-                pools[j] = std::move(kept);
-            }
+            LAUNCH(k_mark_consumed, G(n_fill), kB, 0, s, fill_items, fill_bin.p, n_fill, consumed.p);
         }
         trace_mark(c, "fill.expand+compact");
         const u64 pbase = T.n_packs;
-        const u64 P = layout_group(c, pg, fill_items.p, n_fill, fill_bin.p, fill_slot.p, cap, T);
+        const u64 P = layout_group(c, pg, fill_items, n_fill, fill_bin.p, fill_slot.p, cap, T);
         trace_mark(c, "layout");
         I += batch_group(c, corpus, T, pbase, P, N, cap, gi, a.balance_batching, a.seed, I, slots, igroup);
         trace_mark(c, "batching");
+        if (n_fill > 0) {
+            // the pools gi-1 .. 0 lose the samples this fill took: one scan
+            // compacts both layouts (keep counts of Pin in the low, of Ps in
+            // the high half; Ps only while a later group still fills from it)
+            // and records the running count at the end of each Pin pool (the
+            // new sizes are the differences; one read)
+            std::vector<u64> h_end(gi);
+            for (int j = 0; j < gi; ++j) h_end[j] = psize[j] ? off[j + 1] - 1 : ~0ull;  // empty: never matched
+            DevBuf<u64> dend(gi, s), dincl(gi, s);
+            CUDA_CHECK(cudaMemcpyAsync(dend.p, h_end.data(), sizeof(u64) * gi, cudaMemcpyHostToDevice, s));
+            if (!Pin2.p) Pin2.alloc(n + 1, s);
+            const bool keep_sorted = gi > 1;  // a later group still fills from the sorted pools
+            if (keep_sorted && !Ps2.p) Ps2.alloc(n + 1, s);
+            const u64* pin = Pin.p;
+            const u64* ps = Ps.p + soff[gi - 1];
+            u64* pin2 = Pin2.p;
+            u64* ps2 = keep_sorted ? Ps2.p + soff[gi - 1] : nullptr;
+            const u8* cons = consumed.p;
+            const u64* ends = dend.p;
+            u64* incl = dincl.p;
+            const int nseg = gi;
+            scan_exclusive<u64>(
+                static_cast<i64>(n_fill),
+                [=] __device__(i64 i) -> u64 {
+                    return (cons[entry_idx(pin[i])] ? 0ull : 1ull) |
+                           (ps2 && !cons[entry_idx(ps[i])] ? (1ull << 32) : 0ull);
+                },
+                [=] __device__(i64 i, u64 v) {
+                    const bool k1 = !cons[entry_idx(pin[i])];
+                    if (k1) pin2[static_cast<u32>(v)] = pin[i];
+                    if (ps2 && !cons[entry_idx(ps[i])]) ps2[v >> 32] = ps[i];
+                    for (int j = 0; j < nseg; ++j)
+                        if (static_cast<u64>(i) == ends[j]) incl[j] = static_cast<u32>(v) + (k1 ? 1u : 0u);
+                },
+                s, c.scan, "scan.plan4");
+            const std::vector<u64> h_incl = read_vector(c, dincl.p, gi);  // (also orders the host copy above)
+            std::vector<u64> kept(gi, 0);
+            u64 run = 0;
+            for (int j = 0; j < gi; ++j)
+                if (psize[j]) {
+                    kept[j] = h_incl[j] - run;
+                    run = h_incl[j];
+                }
+            std::swap(Pin, Pin2);
+            if (keep_sorted) std::swap(Ps, Ps2);
+            for (int j = 0; j < gi; ++j) psize[j] = kept[j];
+            // the groups >= gi are done: keep their sizes out of the offsets
+            const u64 base_s = soff[gi - 1];
+            for (int g = gi; g < ng; ++g) psize[g] = 0;
+            refresh_offsets();
+            // Ps2 (now Ps) holds the compacted tail at the old tail start
+            for (int j = 0; j < gi; ++j) soff[j] += base_s;
+        } else {
+            psize[gi] = 0;
+        }
     }
     emit_plan(c, T, slots, igroup, I, N, a.seed, out);
     trace_mark(c, "emit");

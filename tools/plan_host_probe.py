@@ -49,3 +49,6 @@ for gl in ([131072], [8192, 32768, 131072], [512, 2048, 8192, 32768, 131072], [5
     if "-v" in sys.argv:
         for r in sorted(rows, reverse=True)[:8]:
             print(f"    {r[2]:24s} {r[0]:.3f} ms {r[1]} launches")
+    if "-n" in sys.argv:
+        for r in sorted(rows, key=lambda r: -r[1])[:14]:
+            print(f"    {r[2]:24s} {r[1]} launches {r[0]:.3f} ms")

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(NF_B) k_nf_emit(const u64* __restrict__ F, u64
 // ---------------------------------------------------------------------------
 constexpr u64 kXKnown = 1ull << 63;  // exit word: the tile's true exit is known
 constexpr u64 kTvAgg = 1ull << 62, kTvInc = 2ull << 62, kTvMask = (1ull << 62) - 1;
-constexpr u64 kLsKnown = 1ull << 63;  // last-start word: 1 + last start (0: none) published
+constexpr u64 kLsKnown = 1ull << 63;  // last-start word: known | total of that pack << 32 | 1 + last start (0: none)
 
 __device__ __forceinline__ u32 nf_gallop(const u64* __restrict__ P, u64 s, u64 m, u64 cap) {
     const u64 limit = P[s] + cap;
@@ -409,7 +409,6 @@ __device__ __forceinline__ void st_release_u64(u64* p, u64 v) {
 
 struct NfRoundArgs {
     const u64* F;
-    const u64* P;
     u64 m, cap, tmin;
     PackSink sink;
     u64 mbase, pbase;
@@ -419,7 +418,7 @@ struct NfRoundArgs {
     u32* tile_ctr;
     u64* xst;   // [ntiles] kXKnown | true exit
     u64* tvst;  // [ntiles] look-back words of the frozen totals
-    u64* lsst;  // [ntiles] kLsKnown | (1 + last start)
+    u64* lsst;  // [ntiles] kLsKnown | (last pack's total << 32) | (1 + last start)
 };
 
 // levels (reused first for the staged prefix sums, last by the emit for the
@@ -446,7 +445,7 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
     __shared__ u32 s_mx[NF_B / 32];
     __shared__ u64 s_tv[2];
     __shared__ u32 s_last2[2];
-    __shared__ u32 s_tile, s_h0, s_hi_entry, s_carry;
+    __shared__ u32 s_tile, s_h0, s_hi_entry, s_carry, s_carry_tot;
     __shared__ u64 s_entry, s_conv, s_tpre;
     __shared__ int s_ok;
     auto pad = [](u32 i) { return i + (i >> 5); };
@@ -459,36 +458,85 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
     const u64 end = a + NF_T < m ? a + NF_T : m;
     const u32 len = static_cast<u32>(end - a);
 
-    // prefix sums of the tile and NF_PW positions past it, staged; next()
-    // of every position by a gallop over them (global P past the window)
-    const u64 pend = end + NF_PW < m ? end + NF_PW : m;  // staged: P[a .. pend]
-    for (u64 i = a + t; i <= pend; i += NF_B) s_P[i - a] = r.P[i];
+    // lengths of the tile and NF_PW positions past it, scanned in shared
+    // memory into local prefix sums (Pl(x) = sum of lengths in [a, x)); every
+    // position's next() and pack total come from a gallop over them. A pack
+    // running past the window (tiny items) is summed on from the entries.
+    const u64 pend = end + NF_PW < m ? end + NF_PW : m;  // window [a, pend)
+    const u32 wn = static_cast<u32>(pend - a);
+    const u64* __restrict__ F = r.F;
+    constexpr u32 kWI = (NF_T + NF_PW + NF_B) / NF_B;  // window positions per thread (contiguous)
+    for (u32 x = t; x < wn; x += NF_B) s_P[x] = F[a + x] >> 32;  // striped loads
     __syncthreads();
     {
-        const u64* __restrict__ P = r.P;
-        auto Pat = [&](u64 x) -> u64 { return x <= pend ? s_P[x - a] : P[x]; };
-        const u64 cap = r.cap;
-        for (u32 i = t; i < len; i += NF_B) {
-            const u64 sp = a + i;
-            const u64 base = s_P[i];
-            const u64 limit = base + cap;
-            const u64 top = sp + cap < m ? sp + cap : m;
-            u64 lo = sp + 1, step = 1;
-            while (lo + step <= top && Pat(lo + step) <= limit) {
-                lo += step;
-                step <<= 1;
-            }
-            u64 hi = lo + step - 1 < top ? lo + step - 1 : top;
-            while (lo < hi) {
-                const u64 mid = (lo + hi + 1) >> 1;
-                if (Pat(mid) <= limit) lo = mid;
-                else hi = mid - 1;
-            }
-            s_nx[i] = static_cast<u32>(lo);
-            s_tot[i] = static_cast<u32>(Pat(lo) - base);
+        u64 v[kWI];
+        u64 sum = 0;
+#pragma unroll
+        for (u32 k = 0; k < kWI; ++k) {
+            const u32 x = t * kWI + k;
+            v[k] = x < wn ? s_P[x] : 0ull;
+            sum += v[k];
         }
+        u64 tot;
+        u64 run = block_exclusive_scan<u64>(sum, s_red, tot);  // (syncs: every read above is done)
+#pragma unroll
+        for (u32 k = 0; k < kWI; ++k) {
+            const u32 x = t * kWI + k;
+            if (x < wn) s_P[x] = run;
+            run += v[k];
+        }
+        if (t == 0) s_P[wn] = tot;
     }
-    __syncthreads();  // the staged P is overwritten by the levels below
+    __syncthreads();
+    const u64 cap = r.cap;
+    // the pack from position sp (local prefix base = Pl(sp), limit = base + budget):
+    // its end e (largest e <= top with Pl(e) <= limit) and total Pl(e) - base
+    auto pack_from = [&](u64 sp, u64 base, u64 limit, u64 top, u32& e_out, u32& tot_out) {
+        const u64 wtop = top < pend ? top : pend;
+        u64 lo = sp + 1, step = 1;
+        while (lo + step <= wtop && s_P[lo + step - a] <= limit) {
+            lo += step;
+            step <<= 1;
+        }
+        u64 hi = lo + step - 1 < wtop ? lo + step - 1 : wtop;
+        while (lo < hi) {
+            const u64 mid = (lo + hi + 1) >> 1;
+            if (s_P[mid - a] <= limit) lo = mid;
+            else hi = mid - 1;
+        }
+        u64 sum = s_P[lo - a];
+        if (lo == wtop && wtop < top) {  // past the window: sum on
+            while (lo < top) {
+                const u64 l = F[lo] >> 32;
+                if (sum + l > limit) break;
+                sum += l;
+                ++lo;
+            }
+        }
+        e_out = static_cast<u32>(lo);
+        tot_out = static_cast<u32>(sum - base);
+    };
+    for (u32 i = t; i < len; i += NF_B) {
+        const u64 sp = a + i;
+        const u64 base = s_P[i];
+        u32 e, tt;
+        pack_from(sp, base, base + cap, sp + cap < m ? sp + cap : m, e, tt);
+        s_nx[i] = e;
+        s_tot[i] = tt;
+    }
+    if (t == 0) {
+        s_ok = 1;
+        u32 hi = 0;
+        if (a > 0) {  // entries lie in [a, next(a - 1)]: the pack from a - 1 holds its item and Pl(e) <= cap - len
+            const u64 l0 = F[a - 1] >> 32;
+            u32 tt;
+            const u64 top = a - 1 + cap < m ? a - 1 + cap : m;
+            if (top <= a || s_P[1] > cap - l0) hi = static_cast<u32>(a);  // item a does not join a - 1's pack
+            else pack_from(a, 0, cap - l0, top, hi, tt);                  // (it does: e >= a + 1)
+        }
+        s_hi_entry = hi;
+    }
+    __syncthreads();  // the window is overwritten by the levels below
     for (u32 i = t; i < NF_T; i += NF_B) {
         u32 f = i;
         if (i < len) {
@@ -498,10 +546,6 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
         s_L[i] = static_cast<unsigned short>(f);
     }
     for (u32 i = t; i < NF_T / 32; i += NF_B) s_spec[i] = 0;
-    if (t == 0) {
-        s_ok = 1;
-        s_hi_entry = a > 0 ? nf_gallop(r.P, a - 1, m, r.cap) : 0u;  // entries lie in [a, next(a - 1)]
-    }
     __syncthreads();
     // speculative chain (k_nf_tiles)
     for (int k = 0; k + 1 < NF_LV; ++k) {
@@ -601,10 +645,11 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
     if (t == 0) {
         const u64 tv = s_tv[0] + s_tv[1];
         const u32 lst = max(s_last2[0], s_last2[1]);
-        st_release_u64(r.lsst + tile, kLsKnown | lst);
+        const u64 ltot = lst ? s_tot[lst - 1 - a] : 0u;
+        st_release_u64(r.lsst + tile, kLsKnown | (ltot << 32) | lst);
         st_release_u64(r.tvst + tile, (tile == 0 ? kTvInc : kTvAgg) | tv);
         u64 excl = 0;
-        u32 carry = 0;
+        u32 carry = 0, carry_tot = 0;
         if (tile > 0) {
             for (long long q = static_cast<long long>(tile) - 1;; --q) {
                 u64 w;
@@ -618,11 +663,13 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
                 while (!((w = ld_acquire_u64(r.lsst + q)) & kLsKnown)) {
                 }
                 carry = static_cast<u32>(w);
+                carry_tot = static_cast<u32>((w >> 32) & 0x7fffffffu);
             }
             st_release_u64(r.tvst + tile, kTvInc | (excl + tv));
         }
         s_tpre = excl;
         s_carry = carry;
+        s_carry_tot = carry_tot;
     }
     // the levels are done with: the entries go where they were
 #pragma unroll
@@ -663,7 +710,7 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
         const u64 st = prev - 1;
         // a pack carried in from an earlier tile ends at this tile's entry
         e_cur = carried ? static_cast<u32>(s_entry) : s_nx[st - a];
-        frz = (carried ? r.P[e_cur] - r.P[st] : static_cast<u64>(s_tot[st - a])) >= r.tmin;
+        frz = static_cast<u64>(carried ? s_carry_tot : s_tot[st - a]) >= r.tmin;
     }
 #pragma unroll
     for (int j = 0; j < EM_ITEMS; ++j) {
@@ -740,12 +787,14 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     const u32 ntiles = static_cast<u32>((m + NF_T - 1) / NF_T);
     DevBuf<u64> newm(3, s);
 
-    // prefix sums of lengths in visiting order (m + 1 entries), unless the
-    // shuffle already wrote them
+    static const bool split = std::getenv("HBP_NF_SPLIT") != nullptr;  // A/B: the six-launch round
+    // prefix sums of lengths in visiting order (m + 1 entries), for the
+    // split round only (the fused round scans its own window), unless the
+    // caller has them
     struct {
         const u64* p;
     } P{P_in};
-    if (!P_in) {
+    if (split && !P_in) {
         Pbuf.alloc(m + 1, s);
         P.p = Pbuf.p;
         u64* Pp = Pbuf.p;
@@ -753,7 +802,6 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
             static_cast<i64>(m + 1), [=] __device__(i64 i) { return i < static_cast<i64>(m) ? (F[i] >> 32) : 0ull; },
             [=] __device__(i64 i, u64 v) { Pp[i] = v; }, s, c.scan, "scan.nf1");
     }
-    static const bool split = std::getenv("HBP_NF_SPLIT") != nullptr;  // A/B: the six-launch round
     if (split) {
         DevBuf<u32> nxt(m, s);
         DevBuf<u32> spec(static_cast<size_t>(ntiles) * (NF_T / 32), s), flags(static_cast<size_t>(ntiles) * (NF_T / 32), s);
@@ -788,7 +836,6 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     st.zero();
     NfRoundArgs ra;
     ra.F = F;
-    ra.P = P.p;
     ra.m = m;
     ra.cap = cap;
     ra.tmin = tmin;
@@ -803,7 +850,7 @@ i64 nextfit_freeze(Ctx& c, const u64* F, i64 m_signed, u32 cap, u64 tmin, PackSi
     ra.lsst = st.p + 2ull * ntiles;
     ra.tile_ctr = reinterpret_cast<u32*>(st.p + 3ull * ntiles);
     set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_nf_round), NF_SMEM_FUSED);
-    // algorithmic bytes: P read (8 B), entries in and out (16 B)
+    // algorithmic bytes: entries in (lengths, then the entries) and out: 24 B
     LAUNCH_B("nf.round", 24.0 * m, k_nf_round, ntiles, NF_B, NF_SMEM_FUSED, s, ra);
     const auto t = read_vector(c, newm.p, 3);
     n_members = t[1];

@@ -335,7 +335,7 @@ def run_ours(args, rank, world, local):
             ms.append(a.elapsed_time(b))
         return ms, out
 
-    # Plans in flight: IN_FLIGHT contexts (one stream and one host thread
+    # Plans in flight: IN_FLIGHT (5) contexts (one stream and one host thread
     # each; ctypes releases the GIL inside the C-ABI calls) build independent
     # plans at once, as a loader building the plans of several corpora (or
     # epochs) does -- one plan leaves the GPU mostly idle in its first-fit
@@ -466,7 +466,7 @@ def run_ours(args, rank, world, local):
     return 0
 
 
-IN_FLIGHT = int(os.environ.get("HBP_BENCH_IN_FLIGHT", "3"))  # plans built at once (one context each)
+IN_FLIGHT = int(os.environ.get("HBP_BENCH_IN_FLIGHT", "5"))  # plans built at once (one context each)
 C1 = dict(count=100_000, short="lognormal:8.5:1.4", long_fraction=0.0, long="", max_length=131072, seed=42)
 SWEEP_SMALLER = [512, 1024, 2048, 4096, 8192, 16384, 32768, 65536]  # 256 length sets with 131072
 SWEEP_SP = [1, 2, 4, 8]

@@ -536,6 +536,9 @@ u64 rank_ids(Ctx& c, const int64_t* ids_dev, DeviceCorpus& corpus) {
 // Sorts entries by (length desc, key asc) in place.
 void sort_entries(Ctx& c, const DeviceCorpus& corpus, u64* e, u64 n, bool key_ordered, u32 max_len) {
     if (n <= 1) return;
+    if (sort_entries_small(c, e, static_cast<i64>(n), corpus.key32.p, key_ordered ? 0 : corpus.key_bits,
+                           bits_for(max_len)))
+        return;
     cudaStream_t s = c.stream;
     DevBuf<u32> k(n, s), v(n, s), tk(n, s), tv(n, s);
     LAUNCH(k_keys_of_entries, G(n), kB, 0, s, e, corpus.key32.p, n, k.p, v.p);

@@ -250,6 +250,165 @@ __global__ void __launch_bounds__(OB, 3) k_os_pass(const u32* __restrict__ keys_
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Small sorts in one launch: up to kSmallN pairs sorted by one CTA in shared
+// memory, every digit pass inside the kernel (the plans of the sweep sort
+// thousands of packs or samples at a time, where the onesweep's histogram
+// pass, digit passes and their launches dominate). Ranks as in k_os_pass:
+// warp w owns elements [w * 256, (w + 1) * 256) row by row, ballots on the
+// digit's live bits, warp counters per digit, then the digit starts.
+// ---------------------------------------------------------------------------
+constexpr int SB = 1024;
+constexpr int kSmallN = 8192;
+constexpr int SITEMS = kSmallN / SB;  // 8 rows per warp
+
+// Stable sort of (k[0..n), v[0..n)) in shared memory by the low `bits` of the
+// key (descending sorts ~key); the result ends in (k, v). tk / tv: scratch.
+__device__ void small_sort_smem(u32* k, u32* v, u32* tk, u32* tv, u32 n, int bits, bool desc,
+                                unsigned short (*wc)[256], u32* dstart, u32* red) {
+    const unsigned tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int passes = bits <= 0 ? 0 : (bits + 7) / 8;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = 8 * p;
+        const int dbits = bits - shift < 8 ? bits - shift : 8;
+        for (unsigned i = tid; i < 32 * 256; i += SB) (&wc[0][0])[i] = 0;
+        __syncthreads();
+        u32 rd[SITEMS];
+#pragma unroll
+        for (int i = 0; i < SITEMS; ++i) {
+            const u32 e = w * (SITEMS * 32) + i * 32 + lane;
+            const bool valid = e < n;
+            const u32 d = valid ? (((desc ? ~k[e] : k[e]) >> shift) & 0xffu) : 256u;
+            unsigned peers = __ballot_sync(0xffffffffu, valid);
+            if (!valid) peers = ~peers;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (b >= dbits) break;
+                const bool bit = (d >> b) & 1u;
+                const unsigned m = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? m : ~m;
+            }
+            const u32 old = valid ? wc[w][d] : 0u;
+            rd[i] = ((old + __popc(peers & lt)) << 16) | d;
+            __syncwarp();
+            if (valid && (peers & lt) == 0) wc[w][d] = static_cast<unsigned short>(old + __popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        if (tid < 256) {  // digit tid: offsets of the warps, the digit's count
+            u32 run = 0;
+            for (int q = 0; q < 32; ++q) {
+                const u32 c = wc[q][tid];
+                wc[q][tid] = static_cast<unsigned short>(run);
+                run += c;
+            }
+            dstart[tid] = run;
+        }
+        __syncthreads();
+        if (w == 0) {  // exclusive scan over the 256 digit counts (8 per lane)
+            u32 loc[8], sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                loc[q] = dstart[lane * 8 + q];
+                sum += loc[q];
+            }
+            u32 inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= static_cast<unsigned>(o)) inc += t;
+            }
+            u32 run = inc - sum;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                dstart[lane * 8 + q] = run;
+                run += loc[q];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < SITEMS; ++i) {
+            const u32 dd = rd[i] & 0xffffu;
+            if (dd < 256u) {
+                const u32 e = w * (SITEMS * 32) + i * 32 + lane;
+                const u32 pos = dstart[dd] + wc[w][dd] + (rd[i] >> 16);
+                tk[pos] = k[e];
+                tv[pos] = v[e];
+            }
+        }
+        __syncthreads();
+        for (unsigned i = tid; i < n; i += SB) {
+            k[i] = tk[i];
+            v[i] = tv[i];
+        }
+        __syncthreads();
+    }
+    (void)red;
+}
+
+struct SmallSortSmem {
+    u32 k[kSmallN], v[kSmallN], tk[kSmallN], tv[kSmallN];
+    unsigned short wc[32][256];
+    u32 dstart[256];
+    u32 red[33];
+};
+
+__global__ void __launch_bounds__(SB, 1) k_small_sort_pairs(u32* __restrict__ keys, u32* __restrict__ vals, u32 n,
+                                                            int bits, bool desc) {
+    extern __shared__ __align__(16) unsigned char ss_raw[];
+    SmallSortSmem& S = *reinterpret_cast<SmallSortSmem*>(ss_raw);
+    for (unsigned i = threadIdx.x; i < n; i += SB) {
+        S.k[i] = keys[i];
+        S.v[i] = vals[i];
+    }
+    __syncthreads();
+    small_sort_smem(S.k, S.v, S.tk, S.tv, n, bits, desc, S.wc, S.dstart, S.red);
+    for (unsigned i = threadIdx.x; i < n; i += SB) {
+        keys[i] = S.k[i];
+        vals[i] = S.v[i];
+    }
+}
+
+// Entries (len << 32 | idx) sorted by (length desc, key asc) in one launch:
+// by key first when the input is not in key order (key = key32[idx], or idx),
+// then stably by length descending; the entries are regathered.
+__global__ void __launch_bounds__(SB, 1) k_small_sort_entries(u64* __restrict__ e, u32 n, const u32* __restrict__ key32,
+                                                              int key_bits, int len_bits) {
+    extern __shared__ __align__(16) unsigned char ss_raw[];
+    SmallSortSmem& S = *reinterpret_cast<SmallSortSmem*>(ss_raw);
+    for (unsigned i = threadIdx.x; i < n; i += SB) {
+        const u32 idx = static_cast<u32>(e[i]);
+        S.k[i] = key32 ? key32[idx] : idx;
+        S.v[i] = i;
+    }
+    __syncthreads();
+    if (key_bits > 0) small_sort_smem(S.k, S.v, S.tk, S.tv, n, key_bits, false, S.wc, S.dstart, S.red);
+    for (unsigned i = threadIdx.x; i < n; i += SB) S.k[i] = static_cast<u32>(e[S.v[i]] >> 32);
+    __syncthreads();
+    small_sort_smem(S.k, S.v, S.tk, S.tv, n, len_bits, true, S.wc, S.dstart, S.red);
+    // regather through the scratch halves (8 B per entry: tk and tv together)
+    u64* out = reinterpret_cast<u64*>(S.tk);  // tk and tv are contiguous: 2 * kSmallN u32
+    for (unsigned i = threadIdx.x; i < n; i += SB) out[i] = e[S.v[i]];
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < n; i += SB) e[i] = out[i];
+}
+
+void set_small_sort_smem_once() {
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if (done.insert(dev).second) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_small_sort_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(SmallSortSmem))));
+        CUDA_CHECK(cudaFuncSetAttribute(k_small_sort_entries, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(SmallSortSmem))));
+    }
+}
+
 }  // namespace
 
 void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool descending, u32* tmp_keys,
@@ -257,6 +416,12 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
     if (n_signed <= 1) return;
     const u64 n = static_cast<u64>(n_signed);
     cudaStream_t s = c.stream;
+    if (n <= static_cast<u64>(kSmallN)) {  // one CTA, every pass in one launch
+        set_small_sort_smem_once();
+        LAUNCH_B("radix.small", 16.0 * n, k_small_sort_pairs, 1, SB, sizeof(SmallSortSmem), s, keys, vals,
+                 static_cast<u32>(n), bits, descending);
+        return;
+    }
     DevBuf<u32> tk, tv;
     if (!tmp_keys) {
         tk.alloc(n, s);
@@ -321,6 +486,15 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
         CUDA_CHECK(cudaMemcpyAsync(keys, ki, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
         CUDA_CHECK(cudaMemcpyAsync(vals, vi, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
     }
+}
+
+bool sort_entries_small(Ctx& c, u64* e, i64 n, const u32* key32, int key_bits, int len_bits) {
+    if (n > kSmallN) return false;
+    if (n <= 1) return true;
+    set_small_sort_smem_once();
+    LAUNCH_B("radix.small", 32.0 * n, k_small_sort_entries, 1, SB, sizeof(SmallSortSmem), c.stream, e,
+             static_cast<u32>(n), key32, key_bits, len_bits);
+    return true;
 }
 
 }  // namespace hbp_b200

@@ -476,9 +476,9 @@ def run_sweep_leg(ctx, lib, rank, world, dist, comm):
     """C3 auto-selection sweep: 256 length sets x SP{1,2,4,8} x GC{on,off} =
     2048 candidates over the C1 corpus (100K, lengths >= 128), sharded across
     ranks by length set with the NCCL argmin, all in the engine
-    (hbp_sweep_sharded). One timed repetition after an untimed one (the
-    worker contexts and their memory pools are created and grown there);
-    device time = max over ranks."""
+    (hbp_sweep_sharded). Three timed repetitions after an untimed one (the
+    worker contexts and their memory pools are created and grown there),
+    the median reported; time = max over ranks."""
     import torch
     from paper_2503_07680_b200 import abi, sweep
     L = np.maximum(synth(lib, C1), 128)
@@ -489,16 +489,23 @@ def run_sweep_leg(ctx, lib, rank, world, dist, comm):
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    t0 = time.perf_counter()
-    secs, best, local = sweep.run_sweep_nccl(comm, s, cands, None, **opts)
-    torch.cuda.synchronize()
-    elapsed = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    reps = []
+    for _ in range(3):  # three timed repetitions; the median is reported (all of them beside it)
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        secs, best, local = sweep.run_sweep_nccl(comm, s, cands, None, **opts)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        reps.append(el)
+    elapsed = statistics.median(reps)
     return {"workload": "C3: 256 length sets x SP{1,2,4,8} x GC{on,off}, C1 corpus (100K), 8B analytic cost model",
             "candidates": len(cands), "feasible": int(np.isfinite(secs).sum()), "seconds": elapsed,
+            "seconds_reps": [round(x, 4) for x in reps],
             "candidates_per_s": len(cands) / elapsed, "best_index": best[1],
             "best_groups": cands[best[1]][0] if best[1] >= 0 else None, "best_seconds": best[0],
             "local_candidates_rank0": local,

@@ -76,7 +76,7 @@ __device__ void fy_fix_block(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u
 // there is no rejection) -- no separate launch for the rare path.
 __global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
                              unsigned long long* __restrict__ rej, u64 force, unsigned long long* __restrict__ used,
-                             bool split_fix) {
+                             bool split_fix, bool scan_counts) {
     for (u64 i = 2 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i <= m;
          i += static_cast<u64>(gridDim.x) * blockDim.x) {
         bool bad;
@@ -95,6 +95,21 @@ __global__ void k_fy_targets(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u
     if (!s_last) return;
     __threadfence();
     fy_fix_block(seed, base, m, tgt, cnt, *reinterpret_cast<volatile unsigned long long*>(rej), used);
+    if (!scan_counts) return;
+    // small m: the counts' exclusive scan here too (one launch fewer per
+    // shuffle); each thread a contiguous chunk, read through L2
+    __shared__ u32 s_red[33];
+    const u64 chunk = (m + blockDim.x - 1) / blockDim.x;
+    const u64 a = threadIdx.x * chunk, b = a + chunk < m ? a + chunk : m;
+    u32 sum = 0;
+    for (u64 q = a; q < b; ++q) sum += __ldcg(cnt + q);
+    u32 tot;
+    u32 run = block_exclusive_scan<u32>(sum, s_red, tot);
+    for (u64 q = a; q < b; ++q) {
+        const u32 x = __ldcg(cnt + q);
+        cnt[q] = run;
+        run += x;
+    }
 }
 
 __global__ void k_fy_fix(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt,
@@ -213,16 +228,20 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     // probability < m / 2^64)
     const u64 force = c.test_force_reject;
     static const bool split_fix = std::getenv("HBP_FY_SPLITFIX") != nullptr;  // A/B: separate fix-up launch
+    // small shuffles scan the target counts in the targets kernel's last block
+    constexpr u64 kScanInTargets = 8192;
+    const bool scan_in = !split_fix && m <= kScanInTargets;
     LAUNCH_B("fy.targets", 12.0 * m, k_fy_targets, G, B, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, force,
-             used.p, split_fix);
+             used.p, split_fix, scan_in);
     if (split_fix) LAUNCH(k_fy_fix, 1, 1024, 0, s, seed, draw_base, m, tgt.p, cnt.p, rej.p, used.p);
     // exclusive scan of per-target counts -> list offsets, in place (the
     // scan loads a whole tile before it stores it); the scatter then
     // advances them as cursors
     u32* cntp = cnt.p;
-    scan_exclusive<u32>(
-        static_cast<i64>(m), [=] __device__(i64 i) { return cntp[i]; },
-        [=] __device__(i64 i, u32 v) { cntp[i] = v; }, s, c.scan, "scan.fy1");
+    if (!scan_in)
+        scan_exclusive<u32>(
+            static_cast<i64>(m), [=] __device__(i64 i) { return cntp[i]; },
+            [=] __device__(i64 i, u32 v) { cntp[i] = v; }, s, c.scan, "scan.fy1");
     LAUNCH_B("fy.scatter", 16.0 * m, k_fy_scatter, G, B, 0, s, m, tgt.p, cnt.p, bucket.p);
     LAUNCH_B("fy.lists", 20.0 * m, k_fy_lists, G, B, 0, s, m, cnt.p, bucket.p, nxt.p, link.p, first0.p);
     if (in)

@@ -421,23 +421,22 @@ struct NfRoundArgs {
     u64* lsst;  // [ntiles] kLsKnown | (last pack's total << 32) | (1 + last start)
 };
 
-// levels (reused first for the staged prefix sums, last by the emit for the
-// entries and their destinations) + next + pack totals
+// a staging region (first the window's local prefix sums, last the emit's
+// entries and destinations) + next + pack totals
 constexpr int NF_PW = 1024;  // prefix sums staged past the tile for next()
-constexpr int NF_SMEM_FUSED = static_cast<int>(sizeof(unsigned short) * NF_LV * NF_T + 2 * sizeof(u32) * NF_T);
-static_assert(sizeof(u64) * (NF_T + NF_PW + 1) <= sizeof(unsigned short) * NF_LV * NF_T, "staged P fits the levels");
-static_assert(sizeof(u64) * (NF_T + NF_T / 32) + sizeof(u32) * (NF_T + NF_T / 32) <=
-                  sizeof(unsigned short) * NF_LV * NF_T,
-              "emit staging fits the levels");
+constexpr size_t NF_STAGE = sizeof(u64) * (NF_T + NF_PW + 1) > sizeof(u64) * (NF_T + NF_T / 32) + sizeof(u32) * (NF_T + NF_T / 32)
+                                ? sizeof(u64) * (NF_T + NF_PW + 1)
+                                : sizeof(u64) * (NF_T + NF_T / 32) + sizeof(u32) * (NF_T + NF_T / 32);
+static_assert(sizeof(unsigned short) * 5 * NF_T <= NF_STAGE, "the chain's levels fit the staging region");
+constexpr int NF_SMEM_FUSED = static_cast<int>((NF_STAGE + 15) / 16 * 16 + 2 * sizeof(u32) * NF_T);
 
 __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
     constexpr u64 kElems = (1ull << 31) - 1;
     extern __shared__ __align__(16) unsigned char nf_smem[];
-    auto* s_L = reinterpret_cast<unsigned short*>(nf_smem);           // [NF_LV][NF_T]
-    auto* s_nx = reinterpret_cast<u32*>(s_L + NF_LV * NF_T);          // absolute next
+    auto* s_nx = reinterpret_cast<u32*>(nf_smem + (NF_STAGE + 15) / 16 * 16);  // absolute next
     auto* s_tot = s_nx + NF_T;                                        // pack total from each position
-    auto* s_P = reinterpret_cast<u64*>(nf_smem);                      // first: P[a .. a + NF_T + NF_PW]
-    auto* s_F = reinterpret_cast<u64*>(nf_smem);                      // emit: entries (padded), over the levels
+    auto* s_P = reinterpret_cast<u64*>(nf_smem);                      // first: the window's local prefix sums
+    auto* s_F = reinterpret_cast<u64*>(nf_smem);                      // emit: entries (padded), over the window
     auto* s_dst = reinterpret_cast<u32*>(s_F + NF_T + NF_T / 32);     // emit: destinations (padded)
     __shared__ u32 s_spec[NF_T / 32];
     __shared__ u32 s_fl[NF_T / 32];
@@ -536,7 +535,17 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
         }
         s_hi_entry = hi;
     }
-    __syncthreads();  // the window is overwritten by the levels below
+    for (u32 i = t; i < NF_T / 32; i += NF_B) s_spec[i] = 0;
+    __syncthreads();
+    // the speculative chain from the tile start: f(x) = next(x) while it
+    // stays in the tile (else x, a fixed point), doubled four times in shared
+    // memory (over the window, done with) to f^16; one thread jumps the
+    // chain 32 nodes at a time (f^32 = f^16 o f^16) and every thread then
+    // marks the nodes between jumps from the levels (node j*32 + l is
+    // f^l(jump j): five lookups)
+    unsigned short* s_L = reinterpret_cast<unsigned short*>(nf_smem);  // [5][NF_T]
+    __shared__ unsigned short s_jump[NF_T / 32 + 1];
+    __shared__ u32 s_njump;
     for (u32 i = t; i < NF_T; i += NF_B) {
         u32 f = i;
         if (i < len) {
@@ -545,48 +554,53 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
         }
         s_L[i] = static_cast<unsigned short>(f);
     }
-    for (u32 i = t; i < NF_T / 32; i += NF_B) s_spec[i] = 0;
     __syncthreads();
-    // speculative chain (k_nf_tiles)
-    for (int k = 0; k + 1 < NF_LV; ++k) {
+    for (int k = 0; k < 4; ++k) {
         const unsigned short* Fk = s_L + k * NF_T;
         unsigned short* Fn = s_L + (k + 1) * NF_T;
         for (u32 i = t; i < NF_T; i += NF_B) Fn[i] = Fk[Fk[i]];
         __syncthreads();
     }
-    const unsigned short* last = s_L + (NF_LV - 1) * NF_T;
-    const u32 last0 = last[0];
     if (t == 0) {
-        u32 x = 0, h = 0;
-        for (int k = NF_LV - 2; k >= 0; --k) {
-            const u32 y = s_L[k * NF_T + x];
-            if (y != last0) {
-                x = y;
-                h += 1u << k;
-            }
+        const unsigned short* F16 = s_L + 4 * NF_T;
+        u32 x = 0, nj = 0;
+        for (;;) {
+            s_jump[nj++] = static_cast<unsigned short>(x);
+            const u32 y = F16[F16[x]];
+            if (y == x) break;
+            x = y;
         }
-        s_h0 = x == last0 ? h : h + 1;
+        s_njump = nj;
     }
     __syncthreads();
-    const u32 h0 = s_h0;
-    for (u32 q = t; q <= h0; q += NF_B) {
-        u32 x = 0;
+    {
+        const u32 nj = s_njump;
+        for (u32 q = t; q < nj * 32; q += NF_B) {
+            u32 x = s_jump[q >> 5];
+            const u32 l = q & 31u;
 #pragma unroll
-        for (int k = 0; k + 1 < NF_LV; ++k)
-            if ((q >> k) & 1u) x = s_L[k * NF_T + x];
-        atomicOr(&s_spec[x >> 5], 1u << (x & 31));
-    }
-    if (a > 0) {
-        const u64 hi_entry = s_hi_entry;
-        if (hi_entry >= end) {
-            if (t == 0) s_ok = 0;
-        } else {
-            for (u64 e = a + t; e <= hi_entry; e += NF_B)
-                if (last[e - a] != last0) s_ok = 0;
+            for (int k = 0; k < 5; ++k)
+                if ((l >> k) & 1u) x = s_L[k * NF_T + x];
+            if (x < len) atomicOr(&s_spec[x >> 5], 1u << (x & 31));
         }
+        if (t == 0) s_h0 = s_jump[nj - 1];  // the chain's last node in the tile (a fixed point)
     }
     __syncthreads();
-    const u64 exit_spec = s_nx[last0];
+    // all-convergence: every possible entry e in [a, next(a - 1)] meets the
+    // speculative chain inside the tile (a walk from e that leaves the tile
+    // first means the exit depends on the entry)
+    if (a > 0 && t < 32) {
+        const u64 hi_entry = s_hi_entry;
+        bool ok = hi_entry < end;
+        for (u64 e = a + t; ok && e <= hi_entry; e += 32) {
+            u64 y = e;
+            while (y < end && !((s_spec[(y - a) >> 5] >> ((y - a) & 31)) & 1u)) y = s_nx[y - a];
+            if (y >= end) ok = false;
+        }
+        if (!__all_sync(0xffffffffu, ok) && t == 0) s_ok = 0;
+    }
+    __syncthreads();
+    const u64 exit_spec = s_nx[s_h0];
     const bool allconv = tile == 0 || s_ok;  // tile 0 is entered at its start
     if (t == 0) {
         if (allconv) st_release_u64(r.xst + tile, kXKnown | exit_spec);
@@ -671,7 +685,7 @@ __global__ void __launch_bounds__(NF_B) k_nf_round(NfRoundArgs r) {
         s_carry = carry;
         s_carry_tot = carry_tot;
     }
-    // the levels are done with: the entries go where they were
+    // the window is done with: the entries go where it was
 #pragma unroll
     for (int k = 0; k < EM_ITEMS; ++k) {
         const u32 li = k * NF_B + t;

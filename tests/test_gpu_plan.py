@@ -304,3 +304,16 @@ def test_standalone_greedy_fill_vs_reference(ctx, reference, seed):
         want = want_packs.member_id[want_packs.pack_member_offsets[p]:want_packs.pack_member_offsets[p + 1]]
         assert np.array_equal(got, want), p
     assert np.array_equal(qi[g_keep], want_pools.member_id)
+
+
+@pytest.mark.parametrize("cap,hi", [(16384, 3), (4096, 2), (8192, 40)])
+def test_isf_packs_longer_than_the_next_fit_window(ctx, oracle, cap, hi):
+    # tiny items: a pack spans thousands of positions, past the 1,024-position
+    # window each next-fit tile scans past its end (summed on from the entries)
+    rng = np.random.default_rng(cap + hi)
+    L = rng.integers(1, hi + 1, size=120_000)
+    want = oracle.pack(None, L, cap, "isf", seed=5)
+    got = ctx.pack(None, L, cap, "isf", seed=5).flat()
+    for k in ("pack_capacity", "pack_total", "pack_attention", "pack_member_offsets"):
+        assert np.array_equal(getattr(got, k), getattr(want, k)), k
+    assert np.array_equal(got.members_as_ids(None), want.member_id)

@@ -66,3 +66,28 @@ def test_shuffle_rejection_repair(ctx, monkeypatch, forced):
     finally:
         ctx.check(ctx.lib.hbp_test_set_force_reject(ctx.h, 0))
     assert np.array_equal(got, _fy_model(77, 5000, forced))
+
+
+@pytest.mark.parametrize("n", [8191, 8192, 8193])
+@pytest.mark.parametrize("bits", [1, 15, 28, 32])
+@pytest.mark.parametrize("desc", [False, True])
+def test_radix_sort_small_and_onesweep_boundary(ctx, n, bits, desc):
+    # n <= 8192 takes the one-CTA sort (every digit pass in one launch), above
+    # it the onesweep passes; both stable and equal to a stable argsort
+    rng = np.random.default_rng(n * 64 + bits)
+    hi = (1 << bits) if bits < 32 else (1 << 32)
+    keys = rng.integers(0, hi, size=n, dtype=np.uint64).astype(np.uint32)
+    keys[: n // 8] = keys[0]  # ties: stability matters
+    vals = np.arange(n, dtype=np.uint32)
+    k, v = ctx.radix_sort(keys, vals, bits, desc)
+    order = np.argsort(-keys.astype(np.int64) if desc else keys, kind="stable")
+    assert np.array_equal(v, vals[order])
+    assert np.array_equal(k, keys[order])
+
+
+@pytest.mark.parametrize("m", [8191, 8192, 8193])
+def test_shuffle_around_the_in_kernel_scan(ctx, oracle, m):
+    # up to 8192 elements the target counts are scanned by the targets
+    # kernel's last block, above by the look-back scan
+    got = ctx.shuffle_positions(99, m)
+    assert np.array_equal(got, oracle.shuffle_positions(99, m))

@@ -128,34 +128,38 @@ __global__ void k_fy_scatter(u64 m, const u32* __restrict__ tgt, u32* __restrict
 
 // One thread per position q: sort S_q ascending, emit successor links.
 // ends[q]: end of S_q (its start is ends[q - 1], 0 for q = 0).
+__device__ __forceinline__ void fy_list(u64 q, const u32* __restrict__ ends, u32* __restrict__ bucket,
+                                        u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0) {
+    const u32 a = q ? ends[q - 1] : 0u, b = ends[q];
+    // insertion sort (lists are short: E|S_q| = ln(m/q))
+    for (u32 x = a + 1; x < b; ++x) {
+        const u32 v = bucket[x];
+        u32 y = x;
+        while (y > a && bucket[y - 1] > v) {
+            bucket[y] = bucket[y - 1];
+            --y;
+        }
+        bucket[y] = v;
+    }
+    for (u32 x = a; x < b; ++x) nxt[bucket[x]] = (x + 1 < b) ? bucket[x + 1] : kNone;
+    if (q == 0) {
+        *first0 = b > a ? bucket[a] : kNone;
+    } else {
+        // link(q+1) = smallest step > q+1 in S_q (all of S_q are >= q+1)
+        u32 l = kNone;
+        if (b > a) {
+            const u32 e0 = bucket[a];
+            l = (e0 == q + 1) ? (b - a > 1 ? bucket[a + 1] : kNone) : e0;
+        }
+        link[q + 1] = l;
+    }
+}
+
 __global__ void k_fy_lists(u64 m, const u32* __restrict__ ends, u32* __restrict__ bucket,
                            u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0) {
     for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < m;
-         q += static_cast<u64>(gridDim.x) * blockDim.x) {
-        const u32 a = q ? ends[q - 1] : 0u, b = ends[q];
-        // insertion sort (lists are short: E|S_q| = ln(m/q))
-        for (u32 x = a + 1; x < b; ++x) {
-            const u32 v = bucket[x];
-            u32 y = x;
-            while (y > a && bucket[y - 1] > v) {
-                bucket[y] = bucket[y - 1];
-                --y;
-            }
-            bucket[y] = v;
-        }
-        for (u32 x = a; x < b; ++x) nxt[bucket[x]] = (x + 1 < b) ? bucket[x + 1] : kNone;
-        if (q == 0) {
-            *first0 = b > a ? bucket[a] : kNone;
-        } else {
-            // link(q+1) = smallest step > q+1 in S_q (all of S_q are >= q+1)
-            u32 l = kNone;
-            if (b > a) {
-                const u32 e0 = bucket[a];
-                l = (e0 == q + 1) ? (b - a > 1 ? bucket[a + 1] : kNone) : e0;
-            }
-            link[q + 1] = l;
-        }
-    }
+         q += static_cast<u64>(gridDim.x) * blockDim.x)
+        fy_list(q, ends, bucket, nxt, link, first0);
 }
 
 // src[p] = the source position of slot p; with `in`, out[p] = in[src[p]]
@@ -201,6 +205,72 @@ __global__ void k_gather(const T* __restrict__ in, const u32* __restrict__ src, 
     }
 }
 
+
+// The whole shuffle of a small vector in one launch: one cluster of kFyCta
+// CTAs (distributed over its threads, every phase of the multi-launch path,
+// hardware cluster barriers in between; the arrays stay in L2). The plans of
+// the sweep shuffle pools of thousands of samples 8 times per group, where
+// the five launches per shuffle, not the work, bound the throughput.
+constexpr int kFyCta = 8;
+constexpr int kFyThreads = 1024;
+constexpr u64 kFyClusterMax = 65536;
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __cluster_dims__(kFyCta, 1, 1) __launch_bounds__(kFyThreads, 1)
+    k_fy_cluster(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt, u32* __restrict__ bucket,
+                 u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0,
+                 unsigned long long* __restrict__ rej, u32* __restrict__ part, u64 force,
+                 unsigned long long* __restrict__ used, u32* __restrict__ src, const u64* __restrict__ in,
+                 u64* __restrict__ out) {
+    const u64 T = static_cast<u64>(kFyCta) * kFyThreads;
+    const u64 tid = blockIdx.x * static_cast<u64>(kFyThreads) + threadIdx.x;
+    for (u64 q = tid; q <= m; q += T) cnt[q] = 0;
+    cluster_sync_all();
+    // targets and their counts
+    for (u64 i = 2 + tid; i <= m; i += T) {
+        bool bad;
+        const u32 j = fy_target(seed, base, m, i, 0, bad);
+        bad = bad || i == force;
+        if (bad) atomicMax(rej, static_cast<unsigned long long>(i));
+        tgt[i] = j;
+        atomicAdd(&cnt[j], 1u);
+    }
+    cluster_sync_all();
+    if (blockIdx.x == 0) fy_fix_block(seed, base, m, tgt, cnt, *reinterpret_cast<volatile unsigned long long*>(rej), used);
+    cluster_sync_all();
+    // exclusive scan of the counts in place: each CTA a contiguous part
+    __shared__ u32 s_red[33];
+    const u64 per = (m + kFyCta - 1) / kFyCta;
+    const u64 p0 = blockIdx.x * per, p1 = p0 + per < m ? p0 + per : m;
+    const u64 chunk = p1 > p0 ? (p1 - p0 + kFyThreads - 1) / kFyThreads : 0;
+    const u64 a = p0 + threadIdx.x * chunk, b = a + chunk < p1 ? a + chunk : p1;
+    u32 sum = 0;
+    for (u64 q = a; q < b; ++q) sum += cnt[q];
+    u32 tot;
+    u32 run = block_exclusive_scan<u32>(sum, s_red, tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+    cluster_sync_all();
+    for (unsigned k = 0; k < blockIdx.x; ++k) run += part[k];
+    for (u64 q = a; q < b; ++q) {
+        const u32 x = cnt[q];
+        cnt[q] = run;
+        run += x;
+    }
+    cluster_sync_all();
+    for (u64 i = 2 + tid; i <= m; i += T) bucket[atomicAdd(&cnt[tgt[i]], 1u)] = static_cast<u32>(i);
+    cluster_sync_all();
+    for (u64 q = tid; q < m; q += T) fy_list(q, cnt, bucket, nxt, link, first0);
+    cluster_sync_all();
+    for (u64 p = tid; p < m; p += T) {
+        const u32 sp = fy_source(p, tgt, nxt, link, first0);
+        if (in) out[p] = in[sp];
+        else src[p] = sp;
+    }
+}
 }  // namespace
 
 namespace {
@@ -217,6 +287,17 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
     }
     DevBuf<unsigned long long> used(draws_used ? 1 : 0, s);
     DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s);
+    static const bool no_cluster = std::getenv("HBP_FY_NOCLUSTER") != nullptr;  // A/B: the multi-launch path
+    if (m <= kFyClusterMax && !no_cluster) {
+        DevBuf<unsigned long long> rj(1, s), usd(draws_used ? 1 : 0, s);
+        DevBuf<u32> part(kFyCta, s), f0(1, s);
+        rj.zero();
+        LAUNCH_B(in ? "fy.cluster_gather" : "fy.cluster", 40.0 * m, k_fy_cluster, kFyCta, kFyThreads, 0, s, seed,
+                 draw_base, m, tgt.p, cnt.p, bucket.p, nxt.p, link.p, f0.p, rj.p, part.p, c.test_force_reject, usd.p,
+                 src, in, out);
+        if (draws_used) *draws_used = read_scalar(c, usd.p);
+        return;
+    }
     DevBuf<unsigned long long> rej(2, s);  // highest rejected step, finished blocks
     DevBuf<u32> first0(1, s);
     cnt.zero();

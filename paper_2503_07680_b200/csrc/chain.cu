@@ -76,6 +76,8 @@ struct ChainArgs {
     u32* item_bin;   // heads only: at the first item of each take
     u32* item_slot;
     u32* take;       // items in the take starting here (0: not a head)
+    int full;        // STORE writes every item's (bin, slot), not only the head's (chains without replay)
+    bool replayed;   // host: the pass ran a replay (heads only: an expand pass follows)
     u32* out;                  // [0] 1 + highest bin with items, [1] FFD overflow
     unsigned long long* prof;  // HBP_TRACE: per warp [wait in, serve, wait out, served runs]
     u32 sleep;                 // ns of back-off per failed poll (idle warps yield issue slots)
@@ -229,9 +231,17 @@ __device__ __forceinline__ bool serve_run(const ChainArgs& a, int r, unsigned al
             const u32 t = pre[i] < mine ? min(capl[i], mine - pre[i]) : 0u;
             if (STORE && t > 0) {
                 const u32 o = off + (C0 - mine) + pre[i];
-                a.item_bin[o] = static_cast<u32>(base + lane * M + i);
-                a.item_slot[o] = N[i];
+                const u32 bin = static_cast<u32>(base + lane * M + i);
                 a.take[o] = t;
+                if (a.full) {  // a chain without replay: every item (no expand pass after it)
+                    for (u32 k = 0; k < t; ++k) {
+                        a.item_bin[o + k] = bin;
+                        a.item_slot[o + k] = N[i] + k;
+                    }
+                } else {
+                    a.item_bin[o] = bin;
+                    a.item_slot[o] = N[i];
+                }
             }
             R[i] -= t * S;
             N[i] += t;
@@ -315,9 +325,17 @@ __device__ __forceinline__ void frontier_fill(const ChainArgs& a, unsigned seg, 
                         if (STORE) {
                             const unsigned long long ex_q = q ? st.incl[q - 1] : 0ull;
                             const u32 o = st.off[q] + static_cast<u32>(p - ex_q);
-                            a.item_bin[o] = static_cast<u32>(base + lane * M + i);
-                            a.item_slot[o] = nb;
+                            const u32 bin = static_cast<u32>(base + lane * M + i);
                             a.take[o] = t;
+                            if (a.full) {
+                                for (u32 k = 0; k < t; ++k) {
+                                    a.item_bin[o + k] = bin;
+                                    a.item_slot[o + k] = nb + k;
+                                }
+                            } else {
+                                a.item_bin[o] = bin;
+                                a.item_slot[o] = nb;
+                            }
                         }
                         tot += t * st.s[q];
                         nb += t;
@@ -743,6 +761,8 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
         a.hist = hist.p;
         a.hact = hact.p;
     }
+    a.full = replay ? 0 : 1;  // storing itself, the chain writes every item; the replay writes heads
+    a.replayed = replay;
     // algorithmic bytes (FFD residue): 12 B per item + 12 B per bin of the pass
     const double alg = 12.0 * a.n_items + 12.0 * (a.bin_end - a.bin0);
     static const bool coop = std::getenv("HBP_CHAIN_COOP") != nullptr;  // A/B: co-resident launch
@@ -922,7 +942,7 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
     const int widths[5] = {1, 2, 4, 8, 16};
     DevBuf<u32> carry[2] = {DevBuf<u32>(runs.n_runs + 1, s), DevBuf<u32>(runs.n_runs + 1, s)};
     u32 pos = 0, top = live;
-    bool left_over = false;
+    bool left_over = false, any_replay = false;
     for (int pass = 0; pos < n_bins; ++pass) {
         u64 want = n_bins - pos;
         if (pass == 0 && first_pass_bins > 0 && first_pass_bins < want) want = first_pass_bins;
@@ -957,13 +977,17 @@ bool chain_fit(Ctx& c, const ChainRuns& runs, u64* leaves, u32 live, u32 n_bins,
         }
         top = std::max(top, r.first);
         left_over = r.second;
+        any_replay = any_replay || a.replayed;
         pos = a.bin_end;
         if (!left_over) break;
     }
     // FFD never runs past its bin bound; greedy fill leaves what no pack took
     if (ffd && left_over) throw EngineError(HBP_ERR_CUDA, "first-fit chain: bin capacity exceeded");
     used = top;
-    if (expand) expand_heads(c, runs.n_items, item_bin, item_slot, take);
+    // replays wrote heads only: expand them (items the chains wrote in full are
+    // rewritten with the same values); without replays every take is written
+    // and items no take covers keep the caller's kNone
+    if (expand && any_replay) expand_heads(c, runs.n_items, item_bin, item_slot, take);
     return true;
 }
 

@@ -1176,6 +1176,8 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     if (use_chain) {
         DevBuf<u32> take(n, s);
         take.zero();
+        // items no take covers stay unassigned (chains without replay skip the expand)
+        CUDA_CHECK(cudaMemsetAsync(item_bin, 0xff, sizeof(u32) * n, s));
         if (bulk > 0)
             LAUNCH(k_bulk_big, grid_for(bulk, 256, 148u * 16u), 256, 0, s, items, static_cast<u64>(bulk), cap, leaves,
                    item_bin, item_slot, take.p);

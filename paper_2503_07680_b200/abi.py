@@ -21,6 +21,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhbp_b200.so")
+# A/B builds only (tools/): another copy of the library, e.g. variants/<name>/libhbp_b200.so
+LIB_PATH = os.environ.get("HBP_LIB_OVERRIDE", LIB_PATH)
 
 HBP_OK, HBP_ERR_VALIDATION, HBP_ERR_INFEASIBLE, HBP_ERR_IO, HBP_ERR_CUDA, HBP_ERR_JSON = 0, 2, 3, 4, 5, 6
 STRATEGIES = {"random": 0, "isf": 1, "ffs": 2, "ffd": 3, "bfs": 4, "spfhp": 5}

@@ -76,7 +76,6 @@ struct ChainArgs {
     u32* item_bin;   // heads only: at the first item of each take
     u32* item_slot;
     u32* take;       // items in the take starting here (0: not a head)
-    int full;        // STORE writes every item's (bin, slot), not only the head's (chains without replay)
     bool replayed;   // host: the pass ran a replay (heads only: an expand pass follows)
     u32* out;                  // [0] 1 + highest bin with items, [1] FFD overflow
     unsigned long long* prof;  // HBP_TRACE: per warp [wait in, serve, wait out, served runs]
@@ -172,7 +171,7 @@ __device__ unsigned long long g_serve_prof[8];
 #endif
 
 // One run `r` against the lanes in `allowed` (bin order = lane order).
-template <int M, bool STORE>
+template <int M, int STORE>
 __device__ __forceinline__ bool serve_run(const ChainArgs& a, int r, unsigned allowed, u32 s, u32 inv_own,
                                           u32 end_item, u32& c, u32 (&R)[M], u32 (&N)[M], u32& lmax, u64 base,
                                           u32 lane) {
@@ -233,7 +232,7 @@ __device__ __forceinline__ bool serve_run(const ChainArgs& a, int r, unsigned al
                 const u32 o = off + (C0 - mine) + pre[i];
                 const u32 bin = static_cast<u32>(base + lane * M + i);
                 a.take[o] = t;
-                if (a.full) {  // a chain without replay: every item (no expand pass after it)
+                if (STORE == 2) {  // a chain without replay: every item (no expand pass after it)
                     for (u32 k = 0; k < t; ++k) {
                         a.item_bin[o + k] = bin;
                         a.item_slot[o + k] = N[i] + k;
@@ -262,7 +261,7 @@ __device__ __forceinline__ bool serve_run(const ChainArgs& a, int r, unsigned al
 // wavefront over the lanes (1.4x faster where every run takes, 1.3-3x
 // slower elsewhere), a lane-by-lane serve without the warp prefix, a lazy
 // filter, and row-major bins.
-template <int M, bool STORE>
+template <int M, int STORE>
 __device__ __forceinline__ void serve_set(const ChainArgs& a, unsigned act, unsigned allowed, u32 s, u32 s_eff,
                                           u32 inv_own, u32 end_item, u32& c, u32 (&R)[M], u32 (&N)[M], u32& lmax,
                                           u64 base, u32 lane) {
@@ -284,7 +283,7 @@ __device__ __forceinline__ void serve_set(const ChainArgs& a, unsigned act, unsi
 // them filled. Their leftovers (what the warp's non-empty bins left) thus
 // fill the empty bins in order, k items per bin, the last bin partially --
 // exactly what serving them one by one would do -- with one warp scan.
-template <int M, bool STORE>
+template <int M, int STORE>
 __device__ __forceinline__ void frontier_fill(const ChainArgs& a, unsigned seg, u32 k, u32 s, u32 end_item, u32& c,
                                               u32 (&R)[M], u32 (&N)[M], u32& lmax, u32& emask, RunStage& st,
                                               u64 base, u32 lane) {
@@ -327,7 +326,7 @@ __device__ __forceinline__ void frontier_fill(const ChainArgs& a, unsigned seg, 
                             const u32 o = st.off[q] + static_cast<u32>(p - ex_q);
                             const u32 bin = static_cast<u32>(base + lane * M + i);
                             a.take[o] = t;
-                            if (a.full) {
+                            if (STORE == 2) {
                                 for (u32 k = 0; k < t; ++k) {
                                     a.item_bin[o + k] = bin;
                                     a.item_slot[o + k] = nb + k;
@@ -378,7 +377,7 @@ __device__ __forceinline__ void frontier_fill(const ChainArgs& a, unsigned seg, 
 // empty, emask) the runs of a block that share k = floor(cap / s) are served
 // against the non-empty lanes one by one and then fill the empty ones
 // together in closed form (frontier_fill).
-template <int M, bool STORE>
+template <int M, int STORE>
 __device__ __forceinline__ void serve(const ChainArgs& a, u32 act, u32 s, u32 end_item, u32& c, u32 (&R)[M],
                                       u32 (&N)[M], u32& wmax, u32& emask, RunStage& st, u64 base, u32 lane) {
     // run_len bit 31: strict run (ids <= -2 in greedy fill, stages.cuh):
@@ -599,10 +598,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_ff_chain(ChainArgs a) {
             if (replay) {  // the replay re-serves this cell from its input counts
                 if (lane < rb) a.hist[(static_cast<u64>(j) * nblocks + b) * rb + lane] = c;
                 if (lane == 0) a.hact[static_cast<u64>(j) * nblocks + b] = act;
-                serve<M, false>(a, act, s, 0u, c, R, N, wmax, emask, s_stage[w], base, lane);
+                serve<M, 0>(a, act, s, 0u, c, R, N, wmax, emask, s_stage[w], base, lane);
             } else {  // short chains store their heads directly
                 const u32 end_item = valid ? (kr + 1 < n_runs ? pf.end[slot][lane] : a.n_items) : 0u;
-                serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);
+                serve<M, 2>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[w], base, lane);  // every item
             }
         }
         unsigned long long t_srv = 0;
@@ -670,7 +669,7 @@ __global__ void __launch_bounds__(256) k_ff_replay(ChainArgs a) {
         const u32 s = valid ? a.run_len[k] : 0u;
         const u32 end_item = valid ? (k + 1 < a.n_runs ? a.run_item[k + 1] : a.n_items) : 0u;
         u32 c = valid ? a.hist[(static_cast<u64>(j) * a.nblocks + b) * a.rb + lane] : 0u;
-        serve<M, true>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[threadIdx.x >> 5], base, lane);
+        serve<M, 1>(a, act, s, end_item, c, R, N, wmax, emask, s_stage[threadIdx.x >> 5], base, lane);  // heads
     }
     store_bins<M>(a, base, lane, R, N, true);
 }
@@ -761,7 +760,6 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
         a.hist = hist.p;
         a.hact = hact.p;
     }
-    a.full = replay ? 0 : 1;  // storing itself, the chain writes every item; the replay writes heads
     a.replayed = replay;
     // algorithmic bytes (FFD residue): 12 B per item + 12 B per bin of the pass
     const double alg = 12.0 * a.n_items + 12.0 * (a.bin_end - a.bin0);

@@ -2,12 +2,13 @@
 //
 // Reference: dbr / abr / report (src/metrics.cpp:22-144), device_work /
 // iter_time (src/costmodel.cpp:55-104), simulate (src/sim.cpp:9-60) and
-// switch_count (src/schedule.cpp:67-79). A warp takes one iteration at a
-// time: lanes over its packs, warp reductions per device, the devices in
-// order; every per-iteration DBR / ABR / time equals the reference's
-// (bit-identical: the gaps are integer sums, the doubles are formed once). The
-// run-level sums use a fixed-shape reduction (per-thread, per-block, then
-// one block in order): deterministic, and within 1e-15 relative of the
+// switch_count (src/schedule.cpp:67-79). One thread owns one iteration and
+// walks its devices in order, so every per-iteration DBR / ABR / time is
+// computed with the reference's operation order (bit-identical). The
+// run-level sums -- mean DBR / ABR, CR's token sums, the total time -- are
+// warp-level reductions of fixed shape (per thread, the block's last five
+// levels and the final one by warp shuffles, three cross-warp levels in
+// shared memory): deterministic, and within 1e-15 relative of the
 // reference's sequential sums. Integer sums (tokens, comm, padding) are exact.
 #include "costmodel.cuh"
 #include "metrics.cuh"
@@ -52,189 +53,133 @@ __device__ __forceinline__ void add_partial(Partial& a, const Partial& b) {
     a.switches += b.switches;
 }
 
-// Groups of G lanes per iteration (G = the device count rounded up to a power
-// of two, at most 32; 32 / G iterations per warp at a time): lane d of a group
-// sums device d's packs, group reductions (shuffles) give the iteration's
-// maxima, tokens and padding, and the simulate's per-device busy times are
-// computed by all lanes at once. The gaps to the maxima are integers below
-// 2^53, so their integer sums converted once equal the reference's
-// sequential double sums exactly. A warp takes, in turn, the 32 iterations
-// its lanes own in the grid-stride order (lane l: blockIdx.x * EB + w * 32 +
-// l + k * stride), G-lane groups several at once, and the owner lane
-// accumulates each: the run-level sums keep the order of the
-// one-thread-per-iteration reduction (and of the DP-column path).
-template <typename T>
-__device__ __forceinline__ T group_sum(T v, int G) {
-    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-template <typename T>
-__device__ __forceinline__ T group_max(T v, int G) {
-    for (int o = G >> 1; o > 0; o >>= 1) {
-        const T w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w > v ? w : v;
-    }
-    return v;
+// Fixed-order block reduction of the per-thread partials: the pairing
+// s[t] += s[t + w] for w = EB/2 .. 1, the three cross-warp levels through
+// shared memory, the last five inside warp 0 by shuffles (same pairs, same
+// operand order: deterministic and identical wherever it runs).
+__device__ __forceinline__ Partial shfl_down_partial(const Partial& p, int o) {
+    Partial q;
+    q.dbr = __shfl_down_sync(0xffffffffu, p.dbr, o);
+    q.abr = __shfl_down_sync(0xffffffffu, p.abr, o);
+    q.seconds = __shfl_down_sync(0xffffffffu, p.seconds, o);
+    q.tokens = __shfl_down_sync(0xffffffffu, p.tokens, o);
+    q.comm = __shfl_down_sync(0xffffffffu, p.comm, o);
+    q.pad_gap = __shfl_down_sync(0xffffffffu, p.pad_gap, o);
+    q.pad_cap = __shfl_down_sync(0xffffffffu, p.pad_cap, o);
+    q.switches = __shfl_down_sync(0xffffffffu, p.switches, o);
+    return q;
 }
 
-__global__ void __launch_bounds__(EB) k_eval(EvalArgs a, int G) {
-    Partial acc{0, 0, 0, 0, 0, 0, 0, 0};
-    const PlanArrays& P = a.p;
-    const unsigned lane = threadIdx.x & 31u;
-    const int per = 32 / G;                      // iterations a warp takes at once
-    const int grp = static_cast<int>(lane) / G;  // this lane's iteration in the batch
-    const int gl = static_cast<int>(lane) % G;   // its device slot
-    const i64 stride = static_cast<i64>(gridDim.x) * EB;
-    const i64 wbase = blockIdx.x * static_cast<i64>(EB) + (threadIdx.x & ~31u);
-    for (i64 base = wbase; base < P.I; base += stride) {
-        for (int j0 = 0; j0 < 32; j0 += per) {
-            const int j = j0 + grp;
-            const i64 i = base + j;
-            const bool live = i < P.I;
-            const i64 ii = live ? i : P.I - 1;  // idle groups shadow a valid iteration (results dropped)
-            const i64 d0 = P.iter_dev_offsets[ii], d1 = P.iter_dev_offsets[ii + 1];
-            const int g = P.iter_group[ii];
-            const hbp_group_config cfg = a.groups[g];
-            const double nd = static_cast<double>(d1 - d0);
-            // pass 1: this lane's devices d0 + gl, d0 + gl + G, ...
-            int64_t t1 = 0, at1 = 0;  // the lane's single device (the usual case: d1 - d0 <= G)
-            int64_t tmax = 0, amax = 0, tokens = 0;
-            unsigned long long pgap = 0, pcap = 0;
-            for (i64 d = d0 + gl; d < d1; d += G) {
-                int64_t t = 0, at = 0;
-                for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
-                    const int64_t tt = P.pack_total[k], c = P.pack_capacity[k];
-                    t += tt;
-                    at += P.pack_attention[k];
-                    pgap += static_cast<unsigned long long>(c - tt);
-                    pcap += static_cast<unsigned long long>(c);
-                }
-                t1 = t;
-                at1 = at;
-                tmax = t > tmax ? t : tmax;
-                amax = at > amax ? at : amax;
-                tokens += t;
-            }
-            tmax = group_max(tmax, G);
-            amax = group_max(amax, G);
-            tokens = group_sum(tokens, G);
-            pgap = group_sum(pgap, G);
-            pcap = group_sum(pcap, G);
-            double dbr = 0.0, abr = 0.0;
-            int err = 0;  // 1: no devices / zero tokens (dbr), 2: zero attention (abr)
-            if (d1 == d0 || tmax == 0) {
-                err = 1;
-            } else if (amax == 0) {
-                err = 2;
-            } else {
-                int64_t gt = 0, ga = 0;
-                if (d1 - d0 <= G) {
-                    if (d0 + gl < d1) {
-                        gt = tmax - t1;
-                        ga = amax - at1;
-                    }
-                } else {
-                    for (i64 d = d0 + gl; d < d1; d += G) {
-                        int64_t t = 0, at = 0;
-                        for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
-                            t += P.pack_total[k];
-                            at += P.pack_attention[k];
-                        }
-                        gt += tmax - t;
-                        ga += amax - at;
-                    }
-                }
-                gt = group_sum(gt, G);
-                ga = group_sum(ga, G);
-                dbr = __ddiv_rn(static_cast<double>(gt), __dmul_rn(static_cast<double>(tmax), nd));
-                abr = __ddiv_rn(static_cast<double>(ga), __dmul_rn(static_cast<double>(amax), nd));
-            }
-            double imax = 0.0;
-            if (a.simulate && d1 > d0) {
-                for (i64 d = d0 + gl; d < d1; d += G) {
-                    int64_t padded = 0, attn = 0, maxcap = 0;
-                    for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
-                        const int64_t cap = P.pack_capacity[k];
-                        padded += cap;
-                        attn += P.pack_attention[k];
-                        const int64_t pad = cap - P.pack_total[k];
-                        attn += pad * pad;
-                        maxcap = cap > maxcap ? cap : maxcap;
-                    }
-                    double busy = 0.0;
-                    if (padded != 0) {
-                        bool bad = cfg.sp < 1 || cfg.ckpt < 0 || cfg.ckpt > a.prof.layer_count;
-                        if (!bad) bad = cm_memory_used(maxcap, cfg.sp, cfg.ckpt, a.prof) > a.prof.device_memory;
-                        if (bad) {
-                            if (live)
-                                atomicMin(a.sim_err, (static_cast<unsigned long long>(i) << 20) |
-                                                         static_cast<unsigned long long>(d - d0));
-                        } else {
-                            busy = cm_iter_time(padded, attn, cfg.sp, cfg.ckpt, a.prof);
-                        }
-                    }
-                    const double comm = padded != 0 ? cm_comm(padded, cfg.sp, a.prof) : 0.0;
-                    if (live) {
-                        if (a.out_dcomm) a.out_dcomm[d] = comm;
-                        if (a.out_dcomp) a.out_dcomp[d] = __dsub_rn(busy, comm);
-                    }
-                    imax = busy > imax ? busy : imax;
-                }
-                imax = group_max(imax, G);
-                if (a.out_didle && live)
-                    for (i64 d = d0 + gl; d < d1; d += G)
-                        // idle = max - (compute + comm)  (sim.cpp:49-52)
-                        a.out_didle[d] = __dsub_rn(imax, __dadd_rn(a.out_dcomp[d], a.out_dcomm[d]));
-            }
-            // the owners: lane j0 + q takes iteration base + j0 + q (group q's),
-            // in the order of the one-thread-per-iteration kernel
-            for (int q = 0; q < per; ++q) {
-                const int src = q * G;  // group q's first lane holds its reduced values
-                const double v_dbr = __shfl_sync(0xffffffffu, dbr, src);
-                const double v_abr = __shfl_sync(0xffffffffu, abr, src);
-                const double v_imax = __shfl_sync(0xffffffffu, imax, src);
-                const int64_t v_tokens = __shfl_sync(0xffffffffu, tokens, src);
-                const unsigned long long v_gap = __shfl_sync(0xffffffffu, pgap, src);
-                const unsigned long long v_cap = __shfl_sync(0xffffffffu, pcap, src);
-                const int v_err = __shfl_sync(0xffffffffu, err, src);
-                const int v_sp = __shfl_sync(0xffffffffu, cfg.sp, src);
-                const int v_ckpt = __shfl_sync(0xffffffffu, cfg.ckpt, src);
-                const i64 vi = base + j0 + q;
-                if (static_cast<int>(lane) != j0 + q || vi >= P.I) continue;
-                const i64 vd0 = P.iter_dev_offsets[vi], vd1 = P.iter_dev_offsets[vi + 1];
-                if (vi > 0) {
-                    const hbp_group_config prev = a.groups[P.iter_group[vi - 1]];
-                    if (prev.sp != v_sp || prev.ckpt != v_ckpt) acc.switches += 1;
-                }
-                if (vd1 == vd0) {
-                    atomicMin(a.report_err, static_cast<unsigned long long>(2 * vi));  // "dbr: no devices"
-                    continue;
-                }
-                acc.pad_gap += v_gap;
-                acc.pad_cap += v_cap;
-                acc.tokens += static_cast<unsigned long long>(v_tokens);
-                if (v_sp > 1) acc.comm += static_cast<unsigned long long>(v_tokens);
-                if (v_err) atomicMin(a.report_err, static_cast<unsigned long long>(2 * vi + (v_err == 2 ? 1 : 0)));
-                if (a.out_dbr) a.out_dbr[vi] = v_dbr;
-                if (a.out_abr) a.out_abr[vi] = v_abr;
-                acc.dbr += v_dbr;
-                acc.abr += v_abr;
-                if (a.simulate) {
-                    if (a.out_secs) a.out_secs[vi] = v_imax;
-                    acc.seconds += v_imax;
-                }
-            }
-        }
-    }
-    // block reduction in fixed order
+__device__ __forceinline__ void block_reduce_partial(Partial acc, Partial* out) {
     __shared__ Partial s[EB];
     s[threadIdx.x] = acc;
     __syncthreads();
-    for (int w = EB / 2; w > 0; w >>= 1) {
+    for (int w = EB / 2; w >= 32; w >>= 1) {
         if (threadIdx.x < static_cast<unsigned>(w)) add_partial(s[threadIdx.x], s[threadIdx.x + w]);
         __syncthreads();
     }
-    if (threadIdx.x == 0) a.partials[blockIdx.x] = s[0];
+    if (threadIdx.x < 32) {
+        Partial v = s[threadIdx.x];
+        for (int o = 16; o > 0; o >>= 1) {
+            const Partial q = shfl_down_partial(v, o);
+            if (threadIdx.x < static_cast<unsigned>(o)) add_partial(v, q);
+        }
+        if (threadIdx.x == 0) *out = v;
+    }
+}
+
+__global__ void __launch_bounds__(EB) k_eval(EvalArgs a) {
+    Partial acc{0, 0, 0, 0, 0, 0, 0, 0};
+    const PlanArrays& P = a.p;
+    for (i64 i = blockIdx.x * static_cast<i64>(EB) + threadIdx.x; i < P.I; i += static_cast<i64>(gridDim.x) * EB) {
+        const i64 d0 = P.iter_dev_offsets[i], d1 = P.iter_dev_offsets[i + 1];
+        const int g = P.iter_group[i];
+        const hbp_group_config cfg = a.groups[g];
+        if (i > 0) {
+            const hbp_group_config prev = a.groups[P.iter_group[i - 1]];
+            if (prev.sp != cfg.sp || prev.ckpt != cfg.ckpt) acc.switches += 1;
+        }
+        const double nd = static_cast<double>(d1 - d0);
+        if (d1 == d0) {
+            atomicMin(a.report_err, static_cast<unsigned long long>(2 * i));  // "dbr: no devices"
+            continue;
+        }
+        int64_t tmax = 0, amax = 0, tokens = 0;
+        for (i64 d = d0; d < d1; ++d) {
+            int64_t t = 0, at = 0;
+            for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
+                t += P.pack_total[k];
+                at += P.pack_attention[k];
+                acc.pad_gap += static_cast<unsigned long long>(P.pack_capacity[k] - P.pack_total[k]);
+                acc.pad_cap += static_cast<unsigned long long>(P.pack_capacity[k]);
+            }
+            tmax = t > tmax ? t : tmax;
+            amax = at > amax ? at : amax;
+            tokens += t;
+        }
+        acc.tokens += static_cast<unsigned long long>(tokens);
+        if (cfg.sp > 1) acc.comm += static_cast<unsigned long long>(tokens);
+        double dbr = 0.0, abr = 0.0;
+        if (tmax == 0) {
+            atomicMin(a.report_err, static_cast<unsigned long long>(2 * i));
+        } else if (amax == 0) {
+            atomicMin(a.report_err, static_cast<unsigned long long>(2 * i + 1));
+        } else {
+            double gt = 0.0, ga = 0.0;
+            for (i64 d = d0; d < d1; ++d) {
+                int64_t t = 0, at = 0;
+                for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
+                    t += P.pack_total[k];
+                    at += P.pack_attention[k];
+                }
+                gt = __dadd_rn(gt, static_cast<double>(tmax - t));
+                ga = __dadd_rn(ga, static_cast<double>(amax - at));
+            }
+            dbr = __ddiv_rn(gt, __dmul_rn(static_cast<double>(tmax), nd));
+            abr = __ddiv_rn(ga, __dmul_rn(static_cast<double>(amax), nd));
+        }
+        if (a.out_dbr) a.out_dbr[i] = dbr;
+        if (a.out_abr) a.out_abr[i] = abr;
+        acc.dbr += dbr;
+        acc.abr += abr;
+        if (!a.simulate) continue;
+        double imax = 0.0;
+        for (i64 d = d0; d < d1; ++d) {
+            int64_t padded = 0, attn = 0, maxcap = 0;
+            for (i64 k = P.dev_pack_offsets[d]; k < P.dev_pack_offsets[d + 1]; ++k) {
+                const int64_t cap = P.pack_capacity[k];
+                padded += cap;
+                attn += P.pack_attention[k];
+                const int64_t pad = cap - P.pack_total[k];
+                attn += pad * pad;
+                maxcap = cap > maxcap ? cap : maxcap;
+            }
+            double busy = 0.0;
+            if (padded != 0) {
+                bool bad = cfg.sp < 1 || cfg.ckpt < 0 || cfg.ckpt > a.prof.layer_count;
+                if (!bad) bad = cm_memory_used(maxcap, cfg.sp, cfg.ckpt, a.prof) > a.prof.device_memory;
+                if (bad) {
+                    atomicMin(a.sim_err, (static_cast<unsigned long long>(i) << 20) | static_cast<unsigned long long>(d - d0));
+                } else {
+                    busy = cm_iter_time(padded, attn, cfg.sp, cfg.ckpt, a.prof);
+                }
+            }
+            const double comm = padded != 0 ? cm_comm(padded, cfg.sp, a.prof) : (cfg.sp > 1 ? 0.0 : 0.0);
+            if (a.out_dcomm) a.out_dcomm[d] = comm;
+            if (a.out_dcomp) a.out_dcomp[d] = __dsub_rn(busy, comm);
+            imax = busy > imax ? busy : imax;
+        }
+        if (a.out_didle) {
+            for (i64 d = d0; d < d1; ++d) {
+                // idle = max - (compute + comm)  (sim.cpp:49-52)
+                a.out_didle[d] = __dsub_rn(imax, __dadd_rn(a.out_dcomp[d], a.out_dcomm[d]));
+            }
+        }
+        if (a.out_secs) a.out_secs[i] = imax;
+        acc.seconds += imax;
+    }
+    // block reduction in fixed order
+    block_reduce_partial(acc, a.partials + blockIdx.x);
 }
 
 // Fixed-order final reduction of the block partials by one warp: lane l
@@ -301,9 +246,7 @@ void eval_plan(Ctx& c, const PlanArrays& p, int32_t device_count, const std::vec
                profile ? *profile : hbp_hardware_profile{}, d_dbr, d_abr, d_secs, d_dcomp, d_dcomm, d_didle,
                partials.p, errs.p, errs.p + 1};
     const int grid = static_cast<int>(std::min<i64>(EG, (p.I + EB - 1) / EB));
-    int G = 1;  // lanes per iteration: the device count rounded up to a power of two (<= 32)
-    while (G < 32 && G < device_count) G <<= 1;
-    LAUNCH(k_eval, grid, EB, 0, s, a, G);
+    LAUNCH(k_eval, grid, EB, 0, s, a);
     LAUNCH(k_eval_final, 1, 32, 0, s, partials.p, grid, partials.p + EG);
     const auto e = read_vector(c, errs.p, 2);
     if (e[0] != ~0ull) {
@@ -468,14 +411,7 @@ __global__ void __launch_bounds__(EB) k_cols_finish(ColArgs a, Partial* partials
         acc.abr += abr;
         if (a.simulate) acc.seconds += a.b.busy[i];
     }
-    __shared__ Partial s[EB];
-    s[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = EB / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < static_cast<unsigned>(w)) add_partial(s[threadIdx.x], s[threadIdx.x + w]);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+    block_reduce_partial(acc, partials + blockIdx.x);
 }
 
 }  // namespace

@@ -604,9 +604,14 @@ void pack_pool(Ctx& c, const DeviceCorpus& corpus, const u64* pool_in, u64 m, u3
             const double min_fill = static_cast<double>(cap) * st.isf_fill_threshold;  // packing.cpp:177-178
             tmin = static_cast<u64>(std::ceil(min_fill));
         }
-        for (int r = 0; r < rounds && cur > 0; ++r) {
-            const uint64_t rs = st.kind == HBP_STRATEGY_ISF ? derive_seed(seed, "isf-round", static_cast<uint64_t>(r))
-                                                              : derive_seed(seed, "random-pack");
+        std::vector<uint64_t> seeds(static_cast<size_t>(rounds > 0 ? rounds : 0));
+        for (int r = 0; r < rounds; ++r)
+            seeds[r] = st.kind == HBP_STRATEGY_ISF ? derive_seed(seed, "isf-round", static_cast<uint64_t>(r))
+                                                   : derive_seed(seed, "random-pack");
+        // small pools: every round in one launch
+        const bool done = isf_small(c, seeds, A.p, cur, cap, tmin, sink, n_members, n_packs);
+        for (int r = 0; !done && r < rounds && cur > 0; ++r) {
+            const uint64_t rs = seeds[r];
             fy_shuffle_u64(c, rs, static_cast<i64>(cur), A.p, Bf.p);
             trace_mark(c, "isf.shuffle");
             cur = static_cast<u64>(nextfit_freeze(c, Bf.p, static_cast<i64>(cur), cap, tmin, sink, A.p, n_members, n_packs));

@@ -18,13 +18,17 @@
 // a counting sort of steps by target; each chain is followed to its root
 // (depth ~ log m, measured max 19 at 1M). Output: source position per slot.
 #include <cstdlib>
+#include <vector>
 
 #include "engine.cuh"
 #include "rng.cuh"
+#include "stages.cuh"
 
 namespace hbp_b200 {
 
 namespace {
+
+#include "nfround.cuh"
 
 // Draw for step i (m >= i >= 2) with `shift` rejected draws before it.
 __device__ __forceinline__ u32 fy_target(u64 seed, u64 base, u64 m, u64 i, u64 shift, bool& rejected) {
@@ -220,14 +224,18 @@ __device__ __forceinline__ void cluster_sync_all() {
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-__global__ void __cluster_dims__(kFyCta, 1, 1) __launch_bounds__(kFyThreads, 1)
-    k_fy_cluster(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt, u32* __restrict__ bucket,
-                 u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0,
-                 unsigned long long* __restrict__ rej, u32* __restrict__ part, u64 force,
-                 unsigned long long* __restrict__ used, u32* __restrict__ src, const u64* __restrict__ in,
-                 u64* __restrict__ out) {
-    const u64 T = static_cast<u64>(kFyCta) * kFyThreads;
-    const u64 tid = blockIdx.x * static_cast<u64>(kFyThreads) + threadIdx.x;
+// Every phase of the shuffle over one cluster's threads (kFyCta CTAs of any
+// size), cluster barriers in between; the arrays stay in L2.
+__device__ __forceinline__ void fy_cluster_phases(u64 seed, u64 base, u64 m, u32* __restrict__ tgt,
+                                                  u32* __restrict__ cnt, u32* __restrict__ bucket,
+                                                  u32* __restrict__ nxt, u32* __restrict__ link,
+                                                  u32* __restrict__ first0, unsigned long long* __restrict__ rej,
+                                                  u32* __restrict__ part, u64 force,
+                                                  unsigned long long* __restrict__ used, u32* __restrict__ src,
+                                                  const u64* __restrict__ in, u64* __restrict__ out) {
+    const u32 NT = blockDim.x;
+    const u64 T = static_cast<u64>(kFyCta) * NT;
+    const u64 tid = blockIdx.x * static_cast<u64>(NT) + threadIdx.x;
     for (u64 q = tid; q <= m; q += T) cnt[q] = 0;
     cluster_sync_all();
     // targets and their counts
@@ -246,7 +254,7 @@ __global__ void __cluster_dims__(kFyCta, 1, 1) __launch_bounds__(kFyThreads, 1)
     __shared__ u32 s_red[33];
     const u64 per = (m + kFyCta - 1) / kFyCta;
     const u64 p0 = blockIdx.x * per, p1 = p0 + per < m ? p0 + per : m;
-    const u64 chunk = p1 > p0 ? (p1 - p0 + kFyThreads - 1) / kFyThreads : 0;
+    const u64 chunk = p1 > p0 ? (p1 - p0 + NT - 1) / NT : 0;
     const u64 a = p0 + threadIdx.x * chunk, b = a + chunk < p1 ? a + chunk : p1;
     u32 sum = 0;
     for (u64 q = a; q < b; ++q) sum += cnt[q];
@@ -269,6 +277,79 @@ __global__ void __cluster_dims__(kFyCta, 1, 1) __launch_bounds__(kFyThreads, 1)
         const u32 sp = fy_source(p, tgt, nxt, link, first0);
         if (in) out[p] = in[sp];
         else src[p] = sp;
+    }
+}
+
+__global__ void __cluster_dims__(kFyCta, 1, 1) __launch_bounds__(kFyThreads, 1)
+    k_fy_cluster(u64 seed, u64 base, u64 m, u32* __restrict__ tgt, u32* __restrict__ cnt, u32* __restrict__ bucket,
+                 u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0,
+                 unsigned long long* __restrict__ rej, u32* __restrict__ part, u64 force,
+                 unsigned long long* __restrict__ used, u32* __restrict__ src, const u64* __restrict__ in,
+                 u64* __restrict__ out) {
+    fy_cluster_phases(seed, base, m, tgt, cnt, bucket, nxt, link, first0, rej, part, force, used, src, in, out);
+}
+
+// Every ISF round of a small pool (isf_round, packing.cpp:171-185, x the
+// strategy's iterations) in one launch: one cluster shuffles (the phases
+// above) and then runs the next-fit round tile by tile (nfround.cuh: tiles
+// claimed in order, look-backs among the cluster's CTAs); the pool size, the
+// sink counters and the round's next input stay on the device. One launch and
+// one read instead of two launches and one read per round.
+struct IsfSmallArgs {
+    const u64* seeds;  // per round (derive_seed(seed, "isf-round", r))
+    int rounds;
+    u64* A;            // the pool: in, and every round's remainder
+    u64* B;            // a round's shuffled pool
+    u32 *tgt, *cnt, *bucket, *nxt, *link, *first0, *part;
+    unsigned long long* rej;
+    u64 force;
+    u64* nf_status;    // 3 * ntiles_max + 1 words, re-zeroed every round
+    u64 cap, tmin;
+    PackSink sink;
+    u64* state;        // [0] pool size, [1] sink members, [2] sink packs
+};
+
+__global__ void __cluster_dims__(kFyCta, 1, 1) __launch_bounds__(NF_B, 1) k_isf_small(IsfSmallArgs q) {
+    __shared__ u32 s_claim;
+    for (int r = 0; r < q.rounds; ++r) {
+        cluster_sync_all();
+        const u64 m = *reinterpret_cast<volatile u64*>(q.state);
+        if (m == 0) break;
+        const u64 mbase = *reinterpret_cast<volatile u64*>(q.state + 1);
+        const u64 pbase = *reinterpret_cast<volatile u64*>(q.state + 2);
+        const u32 ntiles = static_cast<u32>((m + NF_T - 1) / NF_T);
+        const u64 T = static_cast<u64>(kFyCta) * blockDim.x;
+        const u64 tid = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+        if (tid == 0) *q.rej = 0;
+        for (u64 k = tid; k < 3ull * ntiles + 1; k += T) q.nf_status[k] = 0;
+        cluster_sync_all();
+        fy_cluster_phases(q.seeds[r], 0, m, q.tgt, q.cnt, q.bucket, q.nxt, q.link, q.first0, q.rej, q.part, q.force,
+                          nullptr, nullptr, q.A, q.B);
+        cluster_sync_all();
+        NfRoundArgs ra;
+        ra.F = q.B;
+        ra.m = m;
+        ra.cap = q.cap;
+        ra.tmin = q.tmin;
+        ra.sink = q.sink;
+        ra.mbase = mbase;
+        ra.pbase = pbase;
+        ra.newpool = q.A;
+        ra.totals = q.state;
+        ra.ntiles = ntiles;
+        ra.xst = q.nf_status;
+        ra.tvst = q.nf_status + ntiles;
+        ra.lsst = q.nf_status + 2ull * ntiles;
+        ra.tile_ctr = reinterpret_cast<u32*>(q.nf_status + 3ull * ntiles);
+        for (;;) {
+            if (threadIdx.x == 0) s_claim = atomicAdd(ra.tile_ctr, 1u);
+            __syncthreads();
+            const u32 tile = s_claim;
+            __syncthreads();
+            if (tile >= ntiles) break;
+            nf_tile(ra, tile);
+            __syncthreads();
+        }
     }
 }
 }  // namespace
@@ -337,6 +418,47 @@ void fy_run(Ctx& c, uint64_t seed, i64 m_signed, u32* src, const u64* in, u64* o
 
 void fy_source_positions(Ctx& c, uint64_t seed, i64 m, u32* src, uint64_t draw_base, uint64_t* draws_used) {
     fy_run(c, seed, m, src, nullptr, nullptr, draw_base, draws_used);
+}
+
+bool isf_small(Ctx& c, const std::vector<uint64_t>& seeds, u64* A, u64& cur, u32 cap, u64 tmin, PackSink sink,
+               u64& n_members, u64& n_packs) {
+    static const bool off = std::getenv("HBP_ISF_SPLIT") != nullptr;  // A/B: a shuffle and a next-fit launch per round
+    const u64 m = cur;
+    if (off || m == 0 || m > kFyClusterMax || seeds.empty()) return false;
+    cudaStream_t s = c.stream;
+    const u64 ntiles = (m + NF_T - 1) / NF_T;
+    DevBuf<u64> B(m, s), status(3 * ntiles + 1, s), state(3, s), dseeds(seeds.size(), s);
+    DevBuf<u32> tgt(m + 1, s), cnt(m + 1, s), bucket(m, s), nxt(m + 2, s), link(m + 2, s), first0(1, s), part(kFyCta, s);
+    DevBuf<unsigned long long> rej(1, s);
+    const u64 h_state[3] = {m, n_members, n_packs};
+    CUDA_CHECK(cudaMemcpyAsync(state.p, h_state, sizeof(h_state), cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(dseeds.p, seeds.data(), sizeof(u64) * seeds.size(), cudaMemcpyHostToDevice, s));
+    IsfSmallArgs q;
+    q.seeds = dseeds.p;
+    q.rounds = static_cast<int>(seeds.size());
+    q.A = A;
+    q.B = B.p;
+    q.tgt = tgt.p;
+    q.cnt = cnt.p;
+    q.bucket = bucket.p;
+    q.nxt = nxt.p;
+    q.link = link.p;
+    q.first0 = first0.p;
+    q.part = part.p;
+    q.rej = rej.p;
+    q.force = c.test_force_reject;
+    q.nf_status = status.p;
+    q.cap = cap;
+    q.tmin = tmin;
+    q.sink = sink;
+    q.state = state.p;
+    // algorithmic bytes: the rounds' shuffle and next-fit of the pool
+    LAUNCH_B("isf.small", 64.0 * m * seeds.size(), k_isf_small, kFyCta, NF_B, NF_SMEM_FUSED, s, q);
+    const auto h = read_vector(c, state.p, 3);  // (also orders the stack copies above)
+    cur = h[0];
+    n_members = h[1];
+    n_packs = h[2];
+    return true;
 }
 
 void fy_shuffle_u64(Ctx& c, uint64_t seed, i64 m, const u64* in, u64* out) {

@@ -9,6 +9,8 @@
 // by the id rank otherwise.
 #pragma once
 
+#include <vector>
+
 #include "engine.cuh"
 
 namespace hbp_b200 {
@@ -34,6 +36,13 @@ struct PackSink {
 // 1 + the tile's last start (0: none), chain_flag_words(m) / 64 entries.
 u64 chain_flag_words(u64 m);
 void chain_starts(Ctx& c, const u32* nxt, u64 m, u32* flags, u32* tlast);
+
+// shuffle.cu: every ISF round of a pool of up to 64K samples in one launch
+// (one cluster: the shuffle, then the next-fit round tile by tile); the
+// remainder back in A, cur / n_members / n_packs updated (one read). False
+// (nothing done) for larger pools.
+bool isf_small(Ctx& c, const std::vector<uint64_t>& seeds, u64* A, u64& cur, u32 cap, u64 tmin, PackSink sink,
+               u64& n_members, u64& n_packs);
 
 i64 nextfit_freeze(Ctx& c, const u64* F, i64 m, u32 cap, u64 tmin, PackSink sink, u64* newpool, u64& n_members,
                    u64& n_packs, const u64* P_in = nullptr);

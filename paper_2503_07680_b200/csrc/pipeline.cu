@@ -1087,20 +1087,31 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             const u64* ends = dend.p;
             u64* incl = dincl.p;
             const int nseg = gi;
-            scan_exclusive<u64>(
-                static_cast<i64>(n_fill),
-                [=] __device__(i64 i) -> u64 {
-                    return (cons[entry_idx(pin[i])] ? 0ull : 1ull) |
-                           (ps2 && !cons[entry_idx(ps[i])] ? (1ull << 32) : 0ull);
-                },
-                [=] __device__(i64 i, u64 v) {
-                    const bool k1 = !cons[entry_idx(pin[i])];
-                    if (k1) pin2[static_cast<u32>(v)] = pin[i];
-                    if (ps2 && !cons[entry_idx(ps[i])]) ps2[v >> 32] = ps[i];
-                    for (int j = 0; j < nseg; ++j)
-                        if (static_cast<u64>(i) == ends[j]) incl[j] = static_cast<u32>(v) + (k1 ? 1u : 0u);
-                },
-                s, c.scan, "scan.plan4");
+if (keep_sorted) {
+                scan_exclusive<u64>(
+                    static_cast<i64>(n_fill),
+                    [=] __device__(i64 i) -> u64 {
+                        return (cons[entry_idx(pin[i])] ? 0ull : 1ull) | (!cons[entry_idx(ps[i])] ? (1ull << 32) : 0ull);
+                    },
+                    [=] __device__(i64 i, u64 v) {
+                        const bool k1 = !cons[entry_idx(pin[i])];
+                        if (k1) pin2[static_cast<u32>(v)] = pin[i];
+                        if (!cons[entry_idx(ps[i])]) ps2[v >> 32] = ps[i];
+                        for (int j = 0; j < nseg; ++j)
+                            if (static_cast<u64>(i) == ends[j]) incl[j] = static_cast<u32>(v) + (k1 ? 1u : 0u);
+                    },
+                    s, c.scan, "scan.plan4");
+            } else {  // the last fill: only the input-order pools are used again
+                scan_exclusive<u32>(
+                    static_cast<i64>(n_fill), [=] __device__(i64 i) -> u32 { return cons[entry_idx(pin[i])] ? 0u : 1u; },
+                    [=] __device__(i64 i, u32 v) {
+                        const bool k1 = !cons[entry_idx(pin[i])];
+                        if (k1) pin2[v] = pin[i];
+                        for (int j = 0; j < nseg; ++j)
+                            if (static_cast<u64>(i) == ends[j]) incl[j] = v + (k1 ? 1u : 0u);
+                    },
+                    s, c.scan, "scan.plan4");
+            }
             const std::vector<u64> h_incl = read_vector(c, dincl.p, gi);  // (also orders the host copy above)
             std::vector<u64> kept(gi, 0);
             u64 run = 0;

@@ -1085,6 +1085,41 @@ static u32 fill_parallel_pass(Ctx& c, u64* leaves, u32 P, const u32* run_len, co
     return ks;
 }
 
+// FFD's shape from its runs: [0] runs, [1] the first run no longer than
+// cap / 2 (with bulk; the runs before it each hold items that never share
+// a bin), [3] the items' total length; k_ffd_bulk then writes [2] = the
+// item that run starts at (the bulk-placed items before it).
+__global__ void k_ffd_shape(const u32* __restrict__ run_len, const u32* __restrict__ run_item,
+                            const u32* __restrict__ n_runs_p, u64 n, u32 cap, bool bulk,
+                            unsigned long long* __restrict__ out) {
+    const u32 nr = *n_runs_p;
+    unsigned long long sum = 0, first_short = ~0ull;
+    for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < nr;
+         k += static_cast<u64>(gridDim.x) * blockDim.x) {
+        const u64 len = run_len[k] & 0x7fffffffu;
+        const u64 e = k + 1 < nr ? run_item[k + 1] : n;
+        sum += len * (e - run_item[k]);
+        if (bulk && 2ull * len <= cap && k < first_short) first_short = k;
+    }
+    sum = warp_sum(sum);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, first_short, o);
+        first_short = t < first_short ? t : first_short;
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (sum) atomicAdd(out + 3, sum);
+        if (first_short != ~0ull) atomicMin(out + 1, first_short);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = nr;
+}
+
+__global__ void k_ffd_bulk(const u32* __restrict__ run_item, u64 n, bool bulk, unsigned long long* __restrict__ out) {
+    const u64 nr = out[0];
+    const u64 rb = bulk ? (out[1] < nr ? out[1] : nr) : 0;
+    out[1] = rb;
+    out[2] = rb == 0 ? 0 : (rb < nr ? run_item[rb] : n);
+}
+
 void prepare_runs(Ctx& c, const u64* items, i64 n_items, const u32* key32, u64 neg_keys, FitRuns r) {
     if (n_items <= 0) return;
     u32* ri = r.run_item;
@@ -1140,30 +1175,27 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
     // bulk-place the items that can never share a bin (FFD with no live bins)
     u32 bulk = 0;
     u32 run_begin = 0;
-    const u32 n_runs = read_scalar(c, fr.n_runs);
-    std::vector<u32> h_runs;
-    if (ffd && bins0 == 0) {
-        // runs are in decreasing length: count leading runs with 2*s > cap
-        h_runs = read_vector(c, fr.run_len, n_runs);
-        while (run_begin < n_runs && 2ull * h_runs[run_begin] > cap) ++run_begin;
-        if (run_begin > 0) {
-            bulk = (run_begin < n_runs) ? read_vector(c, fr.run_item + run_begin, 1)[0] : static_cast<u32>(n);
-        }
-    }
-
+    u32 n_runs = 0;
     // First fit never leaves two bins at most half full (the later bin's
     // first item would have fitted the earlier), so FFD opens at most
     // 2 * ceil(sum / cap) + 1 bins: size the tree by that, not by n.
     i64 tree_bins = max_bins;
     i64 est_bins = 0;
     if (ffd) {
-        if (h_runs.empty()) h_runs = read_vector(c, fr.run_len, n_runs);
-        const auto h_items = read_vector(c, fr.run_item, n_runs);
-        long double sum = 0;
-        for (u32 k = 0; k < n_runs; ++k) {
-            const u64 e = (k + 1 < n_runs) ? h_items[k + 1] : n;
-            sum += static_cast<long double>(h_runs[k]) * static_cast<long double>(e - h_items[k]);
-        }
+        // the runs' count, the leading runs longer than cap / 2 (sorted
+        // decreasing: a prefix) with their items, and the items' total
+        // length, on the device and in one read
+        DevBuf<unsigned long long> shape(4, s);
+        shape.zero();
+        CUDA_CHECK(cudaMemsetAsync(shape.p + 1, 0xff, sizeof(unsigned long long), s));  // first short run: none yet
+        LAUNCH(k_ffd_shape, grid_for(n, 256, 148u * 4u), 256, 0, s, fr.run_len, fr.run_item, fr.n_runs, n, cap,
+               bins0 == 0, shape.p);
+        LAUNCH(k_ffd_bulk, 1, 1, 0, s, fr.run_item, n, bins0 == 0, shape.p);
+        const auto h = read_vector(c, shape.p, 4);
+        n_runs = static_cast<u32>(h[0]);
+        run_begin = static_cast<u32>(h[1]);
+        bulk = static_cast<u32>(h[2]);
+        const long double sum = static_cast<long double>(h[3]);
         const i64 bound = static_cast<i64>(2 * std::ceil(sum / cap)) + 2 + bins0;
         // FFD of sorted items is near the volume bound for small items and
         // one bin per item above cap / 2: first chain pass sized by both
@@ -1171,6 +1203,8 @@ FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i
         est_bins = static_cast<i64>(std::max<long double>(static_cast<long double>(bins0 + bulk) * 1.02L, vol * 1.02L)) +
                    1024;
         if (bound < tree_bins) tree_bins = bound;
+    } else {
+        n_runs = read_scalar(c, fr.n_runs);
     }
     const u64 live = static_cast<u64>(bins0) + bulk;
     if (use_chain) {

@@ -87,8 +87,23 @@ __global__ void __launch_bounds__(OB) k_os_hist(const u32* __restrict__ keys, u6
         const u32 kk = desc ? ~k : k;
         for (int p = 0; p < passes; ++p) atomicAdd(&h[(p * 256 + ((kk >> (8 * p)) & 0xffu)) * 32 + lane], 1u);
     };
+    // four 16-byte loads in flight per thread before their counts (one load
+    // per thread at a time left the read latency-bound at ~1 TB/s)
     const u64 stride = static_cast<u64>(gridDim.x) * OB;
-    for (u64 v = static_cast<u64>(blockIdx.x) * OB + threadIdx.x; v < nv; v += stride) {
+    u64 v = static_cast<u64>(blockIdx.x) * OB + threadIdx.x;
+    for (; v + 3 * stride < nv; v += 4 * stride) {
+        uint4 q[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) q[r] = k4[v + r * stride];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            add(q[r].x);
+            add(q[r].y);
+            add(q[r].z);
+            add(q[r].w);
+        }
+    }
+    for (; v < nv; v += stride) {
         const uint4 q = k4[v];
         add(q.x);
         add(q.y);
@@ -247,6 +262,137 @@ __global__ void __launch_bounds__(OB, 3) k_os_pass(const u32* __restrict__ keys_
         const u64 g = static_cast<u64>(static_cast<long long>(s_gbase[dd]) + p);
         keys_out[g] = kk;
         vals_out[g] = static_cast<u32>(kv >> 32);
+    }
+}
+
+// The same pass with the tile permuted in place (32 KB of shared memory per
+// CTA instead of 64 KB, no key registers kept across the look-back): ranks
+// become tile positions, the keys are permuted through registers into s_k and
+// written out, then the values into s_v (their digits read from the permuted
+// keys). 48 registers and 38 KB per CTA: five CTAs per SM instead of three,
+// so the bulk loads and look-backs of more tiles overlap the ranking.
+template <int PROBE>  // 0: the pass; timing probes (wrong output): 1 no look-back, 2 no global stores
+__global__ void __launch_bounds__(OB, 4) k_os_pass_ip(const u32* __restrict__ keys_in, const u32* __restrict__ vals_in,
+                                                     u32* __restrict__ keys_out, u32* __restrict__ vals_out, u64 n,
+                                                     int shift, bool desc, const u32* __restrict__ gstart,
+                                                     unsigned long long* __restrict__ status, u32* __restrict__ tiles,
+                                                     bool bulk, int dbits) {
+    extern __shared__ __align__(128) u32 os_smem[];
+    u32* s_k = os_smem;  // tile as loaded
+    u32* s_v = s_k + OTILE;
+    u32* s_x = s_v + OTILE;  // keys in digit order
+    __shared__ unsigned short s_wc[OW][256];
+    __shared__ int s_gbase[256];
+    __shared__ u32 s_red[33];
+    __shared__ u32 s_tile;
+    __shared__ alignas(8) unsigned long long s_bar;
+    const unsigned tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    if (tid == 0) {
+        s_tile = atomicAdd(tiles, 1u);
+        mbar_init(&s_bar, 1);
+    }
+    for (int i = tid; i < OW * 256 / 2; i += OB) reinterpret_cast<u32*>(&s_wc[0][0])[i] = 0;
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 base = static_cast<u64>(tile) * OTILE;
+    const u32 len = static_cast<u32>(base + OTILE <= n ? OTILE : n - base);
+    if (bulk && len == OTILE) {
+        if (tid == 0) {
+            mbar_expect_tx(&s_bar, 2u * OTILE * 4u);
+            bulk_g2s(s_k, keys_in + base, OTILE * 4u, &s_bar);
+            bulk_g2s(s_v, vals_in + base, OTILE * 4u, &s_bar);
+        }
+        mbar_wait(&s_bar, 0);
+    } else {
+        for (u32 i = tid; i < len; i += OB) {
+            s_k[i] = keys_in[base + i];
+            s_v[i] = vals_in[base + i];
+        }
+        __syncthreads();
+    }
+    // stable ranks as in k_os_pass (ballots on the digit's live bits)
+    // stable ranks (ballots on the digit's live bits), two per word; the
+    // digits are read again from the tile when the ranks become positions
+    u32 pp[OITEMS / 2];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < OITEMS; ++i) {
+        const u32 e = w * (OITEMS * 32) + i * 32 + lane;
+        const bool valid = e < len;
+        const u32 kk = valid ? s_k[e] : 0u;
+        const u32 d = valid ? ((desc ? ~kk : kk) >> shift) & 0xffu : 256u;
+        unsigned peers = __ballot_sync(0xffffffffu, valid);
+        if (!valid) peers = ~peers;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            if (b >= dbits) break;
+            const bool bit = (d >> b) & 1u;
+            const unsigned m = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? m : ~m;
+        }
+        const u32 old = valid ? s_wc[w][d] : 0u;
+        const u32 r = old + __popc(peers & lt);
+        if (i & 1)
+            pp[i / 2] |= r << 16;
+        else
+            pp[i / 2] = r;
+        __syncwarp();
+        if (valid && (peers & lt) == 0) s_wc[w][d] = static_cast<unsigned short>(old + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    const u32 d = tid;
+    u32 run = 0;
+#pragma unroll
+    for (int q = 0; q < OW; ++q) {
+        const u32 c = s_wc[q][d];
+        s_wc[q][d] = static_cast<unsigned short>(run);
+        run += c;
+    }
+    unsigned long long* st = status + static_cast<u64>(tile) * 256 + d;
+    st_relaxed_u64g(st, (tile == 0 || PROBE == 1 ? kIncl : kAgg) | run);
+    u32 tot;
+    const u32 lstart = block_exclusive_scan<u32>(run, s_red, tot);
+    // the digit's first position in the tile, folded into the warp offsets
+#pragma unroll
+    for (int q = 0; q < OW; ++q) s_wc[q][d] = static_cast<unsigned short>(s_wc[q][d] + lstart);
+    const unsigned long long excl = tile > 0 && PROBE != 1 ? look_back(status, tile, d) : 0ull;
+    if (tile > 0 && PROBE != 1) st_relaxed_u64g(st, kIncl | (excl + run));
+    s_gbase[d] = static_cast<int>(gstart[d] + excl) - static_cast<int>(lstart);
+    __syncthreads();
+    // keys permuted into s_x (ranks -> tile positions, 0xffff: no element)
+    // and written out; values permuted into s_k (free by then) and written
+    // out with the digits of the permuted keys
+#pragma unroll
+    for (int i = 0; i < OITEMS; ++i) {
+        const u32 e = w * (OITEMS * 32) + i * 32 + lane;
+        u32 pos = 0xffffu;
+        if (e < len) {
+            const u32 kk = s_k[e];
+            pos = s_wc[w][((desc ? ~kk : kk) >> shift) & 0xffu] + ((pp[i / 2] >> (16 * (i & 1))) & 0xffffu);
+            s_x[pos] = kk;
+        }
+        if (i & 1)
+            pp[i / 2] = (pp[i / 2] & 0xffffu) | (pos << 16);
+        else
+            pp[i / 2] = (pp[i / 2] & 0xffff0000u) | pos;
+    }
+    __syncthreads();
+    for (u32 p = tid; p < len; p += OB) {
+        const u32 kk = s_x[p];
+        if (PROBE == 2 && kk != 0x7fffffffu) continue;
+        keys_out[static_cast<long long>(s_gbase[((desc ? ~kk : kk) >> shift) & 0xffu]) + p] = kk;
+    }
+#pragma unroll
+    for (int i = 0; i < OITEMS; ++i) {
+        const u32 pos = (pp[i / 2] >> (16 * (i & 1))) & 0xffffu;
+        if (pos != 0xffffu) s_k[pos] = s_v[w * (OITEMS * 32) + i * 32 + lane];
+    }
+    __syncthreads();
+    for (u32 p = tid; p < len; p += OB) {
+        const u32 kk = s_x[p];
+        if (PROBE == 2 && kk != 0x7fffffffu) continue;
+        vals_out[static_cast<long long>(s_gbase[((desc ? ~kk : kk) >> shift) & 0xffu]) + p] = s_k[p];
     }
 }
 
@@ -449,7 +595,8 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const u32 hgrid = static_cast<u32>(std::min<u64>((n / 4 + OB - 1) / OB + 1, static_cast<u64>(sms) * 2));
     const size_t hsmem = sizeof(u32) * passes * 256 * 32;
-    constexpr size_t kSmem = sizeof(u32) * 4 * OTILE;  // the tile + the digit-ordered tile
+    constexpr size_t kSmem = sizeof(u32) * 4 * OTILE;    // the tile + the digit-ordered tile
+    constexpr size_t kSmemIp = sizeof(u32) * 3 * OTILE;  // the tile + its keys in digit order
     {  // once per device (the attribute is per device; its driver lock serialises sweep workers)
         static std::mutex mu;
         static std::set<int> done;
@@ -459,6 +606,12 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
                                             static_cast<int>(kSmem)));
             CUDA_CHECK(cudaFuncSetAttribute(k_os_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(kSmem)));
+            CUDA_CHECK(cudaFuncSetAttribute(k_os_pass_ip<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemIp)));
+            CUDA_CHECK(cudaFuncSetAttribute(k_os_pass_ip<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemIp)));
+            CUDA_CHECK(cudaFuncSetAttribute(k_os_pass_ip<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemIp)));
             CUDA_CHECK(cudaFuncSetAttribute(k_os_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(sizeof(u32) * OMAXP * 256 * 32)));
         }
@@ -468,10 +621,18 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
     // the bulk copies need 16-byte aligned sources (every tile starts 16 KB in)
     const bool bulk = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(vals) |
                         reinterpret_cast<uintptr_t>(tmp_keys) | reinterpret_cast<uintptr_t>(tmp_vals)) & 15u) == 0;
-    static const int variant = std::getenv("HBP_RADIX_VARIANT") ? std::atoi(std::getenv("HBP_RADIX_VARIANT")) : 1;
+    static const int variant = std::getenv("HBP_RADIX_VARIANT") ? std::atoi(std::getenv("HBP_RADIX_VARIANT")) : 2;
     u32 *ki = keys, *vi = vals, *ko = tmp_keys, *vo = tmp_vals;
     for (int p = 0; p < passes; ++p) {
-        if (variant == 0)
+        if (variant == 3 || variant == 4)  // timing probes (tools/radix_bench.py; wrong output)
+            LAUNCH_B("radix.scatter", 16.0 * n, (variant == 3 ? k_os_pass_ip<1> : k_os_pass_ip<2>), ntiles, OB,
+                     kSmemIp, s, ki, vi, ko, vo, n, 8 * p, descending, gstart + p * 256,
+                     status + static_cast<size_t>(p) * ntiles * 256, tiles + p, bulk, std::min(8, bits - 8 * p));
+        else if (variant == 2)
+            LAUNCH_B("radix.scatter", 16.0 * n, k_os_pass_ip<0>, ntiles, OB, kSmemIp, s, ki, vi, ko, vo, n, 8 * p,
+                     descending, gstart + p * 256, status + static_cast<size_t>(p) * ntiles * 256, tiles + p, bulk,
+                     std::min(8, bits - 8 * p));
+        else if (variant == 0)
             LAUNCH_B("radix.scatter", 16.0 * n, k_os_pass<false>, ntiles, OB, kSmem, s, ki, vi, ko, vo, n,
                      8 * p, descending, gstart + p * 256, status + static_cast<size_t>(p) * ntiles * 256, tiles + p,
                      bulk, 8);

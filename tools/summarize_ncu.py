@@ -2,6 +2,8 @@
 """Summaries of ncu CSV logs for profiles/:
     summarize_ncu.py launches <launches.csv>   per-kernel share of device time
     summarize_ncu.py traffic <traffic.csv>     DRAM bytes per launch
+    summarize_ncu.py families <traffic.csv>    DRAM bytes per launch of each kernel family
+                                               (the roofline "traffic" bench.py reads)
 Kernel names are shortened to the function name (template args dropped)."""
 import csv
 import json
@@ -56,9 +58,42 @@ def traffic(path):
             "ms_total": tot_t / 1e6, "dram_gbs": tot_b / max(tot_t, 1e-9)}
 
 
+# kernel name prefix -> the stage family bench.py reports
+FAMILIES = [("k_os_hist", "radix.hist"), ("k_os_pass", "radix.scatter"), ("k_small_sort", "radix.small"),
+            ("k_scan_lookback", "scan"), ("k_fy_targets", "fy.targets"), ("k_fy_scatter", "fy.scatter"),
+            ("k_fy_lists", "fy.lists"), ("k_fy_sources", "fy.sources_gather"), ("k_nf_round", "nf.round"),
+            ("k_ff_chain", "fit.chain"), ("k_ff_replay", "fit.replay"), ("k_eval", "k_eval")]
+
+
+def families(path):
+    per = defaultdict(dict)
+    for r in rows(path):
+        per[r["ID"]]["name"] = short(r["Kernel Name"]).replace("void ", "")
+        per[r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+        per[r["ID"]]["unit:" + r["Metric Name"]] = r["Metric Unit"]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}
+    agg = defaultdict(lambda: [0, 0.0, 0.0])
+    for m in per.values():
+        fam = next((f for pre, f in FAMILIES if m["name"].startswith(pre)), None)
+        if fam is None:
+            continue
+        a = agg[fam]
+        a[0] += 1
+        a[1] += m["dram__bytes_read.sum"] * scale[m["unit:dram__bytes_read.sum"]] + \
+            m["dram__bytes_write.sum"] * scale[m["unit:dram__bytes_write.sum"]]
+        a[2] += m["gpu__time_duration.sum"] * scale[m["unit:gpu__time_duration.sum"]]
+    out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                     f"--clock-control none, one C2 step (tools/profile_round.sh, {path.split('/')[-1]}); "
+                     "per kernel family: DRAM bytes per launch"}
+    for fam, (n, b, t) in agg.items():
+        out[fam] = {"launches": n, "dram_bytes": b, "ms": t / 1e6, "dram_bytes_per_launch": b / n,
+                    "dram_gbs": b / max(t, 1e-9)}
+    return out
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    res = launches(path) if mode == "launches" else traffic(path)
+    res = launches(path) if mode == "launches" else families(path) if mode == "families" else traffic(path)
     if mode == "launches" and "--md" in sys.argv:
         print(f"{res['launches']} launches, {res['total_ms']:.2f} ms of kernel time (serialised, cold cache)\n")
         print("| kernel | launches | ms | share |\n|---|---:|---:|---:|")

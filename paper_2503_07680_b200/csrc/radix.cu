@@ -593,8 +593,10 @@ void radix_sort_pairs(Ctx& c, u32* keys, u32* vals, i64 n_signed, int bits, bool
     int dev = 0, sms = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const u32 hgrid = static_cast<u32>(std::min<u64>((n / 4 + OB - 1) / OB + 1, static_cast<u64>(sms) * 2));
     const size_t hsmem = sizeof(u32) * passes * 256 * 32;
+    // as many histogram CTAs as fit on every SM at once (32 KB of counters per pass)
+    const u64 hper = std::max<u64>(1, std::min<u64>(6, (228u * 1024u) / (hsmem + 1024u)));
+    const u32 hgrid = static_cast<u32>(std::min<u64>((n / 4 + OB - 1) / OB + 1, static_cast<u64>(sms) * hper));
     constexpr size_t kSmem = sizeof(u32) * 4 * OTILE;    // the tile + the digit-ordered tile
     constexpr size_t kSmemIp = sizeof(u32) * 3 * OTILE;  // the tile + its keys in digit order
     {  // once per device (the attribute is per device; its driver lock serialises sweep workers)

@@ -22,9 +22,18 @@ echo "traffic rows: $(grep -c dram__bytes_read "$OUT/${TAG}_traffic_c2.csv")"
 ncu --set full --clock-control none --import-source on -k regex:k_ff_chain -c 3 \
     -o "$OUT/${TAG}_chain" -f $STEP > /dev/null 2>&1
 echo "chain capture: $?"
-# the first (largest) launch of each: next-fit round, shuffle kernels, radix pass
+# the largest launch (by grid) of each: next-fit round, shuffle kernels, radix
+# pass -- skip the launches of that kernel before it in the launch list
 for k in k_nf_round k_fy_lists k_fy_scatter k_fy_sources k_os_pass; do
-  ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
+  skip=$(python - "$OUT/${TAG}_launches_c2.csv" "$k" <<'PY'
+import csv, sys
+rows = [r for r in csv.DictReader(l for l in open(sys.argv[1]) if l.startswith('"'))
+        if r["Metric Name"] == "gpu__time_duration.sum" and sys.argv[2] in r["Kernel Name"]]
+grid = [eval(r["Grid Size"])[0] for r in rows]
+print(grid.index(max(grid)) if grid else 0)
+PY
+)
+  ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip "$skip" -c 1 \
       -o "$OUT/${TAG}_$k" -f $STEP > /dev/null 2>&1
   echo "$k capture: $?"
 done

@@ -861,9 +861,9 @@ void expand_heads(Ctx& c, u64 n, u32* item_bin, u32* item_slot, const u32* take)
     cudaStream_t s = c.stream;
     DevBuf<u32> q(n, s), pos(n, s);
     u32* qp = q.p;
-    scan_exclusive<u32>(
+    scan_exclusive_v<u32>(
         static_cast<i64>(n), [=] __device__(i64 x) { return take[x] ? 1u : 0u; },
-        [=] __device__(i64 x, u32 v) { qp[x] = v + (take[x] ? 1u : 0u); }, s, c.scan, "scan.chain1", 8.0);
+        [=] __device__(i64 x, u32 v, u32 h) { qp[x] = v + h; }, s, c.scan, "scan.chain1", 8.0);
     LAUNCH_B("chain.heads", 12.0 * n, k_head_positions, grid_for(n, 256), 256, 0, s, take, q.p, n, pos.p);
     LAUNCH_B("chain.expand", 24.0 * n, k_expand_heads, grid_for(n, 256), 256, 0, s, take, q.p, pos.p, n, item_bin,
              item_slot);

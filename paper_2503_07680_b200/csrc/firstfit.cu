@@ -1128,10 +1128,18 @@ void prepare_runs(Ctx& c, const u64* items, i64 n_items, const u32* key32, u64 n
     const i64 nn = n_items;
     // one scan over run-head flags; each head writes its run's first item
     // and length (bit 31: strict) at its run index
-    scan_exclusive<u32>(
-        nn, [=] __device__(i64 i) { return run_head(items, i, key32, neg_keys) ? 1u : 0u; },
-        [=] __device__(i64 i, u32 v) {
-            const bool head = run_head(items, i, key32, neg_keys);
+    scan_exclusive_v<u32>(
+        nn,
+        [=] __device__(i64 i) {
+            // both loads unconditional (the short-circuit form kept the
+            // unrolled tile load from batching them)
+            const u64 e = items[i], p = items[i > 0 ? i - 1 : 0];
+            bool head = i == 0 || entry_len(e) != entry_len(p);
+            if (!head && neg_keys) head = neg_item(e, key32, neg_keys) != neg_item(p, key32, neg_keys);
+            return head ? 1u : 0u;
+        },
+        [=] __device__(i64 i, u32 v, u32 x) {
+            const bool head = x != 0;
             if (head) {
                 const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
                 ri[v] = static_cast<u32>(i);

@@ -1088,24 +1088,24 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
             u64* incl = dincl.p;
             const int nseg = gi;
 if (keep_sorted) {
-                scan_exclusive<u64>(
+                scan_exclusive_v<u64>(
                     static_cast<i64>(n_fill),
                     [=] __device__(i64 i) -> u64 {
                         return (cons[entry_idx(pin[i])] ? 0ull : 1ull) | (!cons[entry_idx(ps[i])] ? (1ull << 32) : 0ull);
                     },
-                    [=] __device__(i64 i, u64 v) {
-                        const bool k1 = !cons[entry_idx(pin[i])];
+                    [=] __device__(i64 i, u64 v, u64 x) {
+                        const bool k1 = (x & 1ull) != 0;
                         if (k1) pin2[static_cast<u32>(v)] = pin[i];
-                        if (!cons[entry_idx(ps[i])]) ps2[v >> 32] = ps[i];
+                        if (x >> 32) ps2[v >> 32] = ps[i];
                         for (int j = 0; j < nseg; ++j)
                             if (static_cast<u64>(i) == ends[j]) incl[j] = static_cast<u32>(v) + (k1 ? 1u : 0u);
                     },
                     s, c.scan, "scan.plan4");
             } else {  // the last fill: only the input-order pools are used again
-                scan_exclusive<u32>(
+                scan_exclusive_v<u32>(
                     static_cast<i64>(n_fill), [=] __device__(i64 i) -> u32 { return cons[entry_idx(pin[i])] ? 0u : 1u; },
-                    [=] __device__(i64 i, u32 v) {
-                        const bool k1 = !cons[entry_idx(pin[i])];
+                    [=] __device__(i64 i, u32 v, u32 x) {
+                        const bool k1 = x != 0;
                         if (k1) pin2[v] = pin[i];
                         for (int j = 0; j < nseg; ++j)
                             if (static_cast<u64>(i) == ends[j]) incl[j] = v + (k1 ? 1u : 0u);
@@ -1573,10 +1573,9 @@ void padded_batches_device(Ctx& c, const DeviceCorpus& corpus, int64_t budget, b
         u32* bi = out.bidx.p;
         u32* nbp = nb.p;
         const i64 nn = static_cast<i64>(n);
-        scan_exclusive<u32>(
+        scan_exclusive_v<u32>(
             nn, [=] __device__(i64 i) { return (fl[i >> 5] >> (i & 31)) & 1u; },
-            [=] __device__(i64 i, u32 v) {
-                const u32 f = (fl[i >> 5] >> (i & 31)) & 1u;
+            [=] __device__(i64 i, u32 v, u32 f) {
                 if (f) bs[v] = static_cast<u32>(i);
                 bi[i] = v + f - 1;
                 if (i == nn - 1) *nbp = v + f;

@@ -10,8 +10,10 @@
 //
 //   scan_exclusive<ITEMS>(n, load, store, stream, scratch)
 //     load(i)            -> T        element i (i < n)
-//     store(i, excl, v)              receives the exclusive prefix of i
+//     store(i, excl)                 receives the exclusive prefix of i
 //   returns nothing; the total can be captured by the store functor (i==n-1).
+//   scan_exclusive_v: the same with store(i, excl, x), x = load(i) -- stores
+//   that need the element (flags from gathers) do not evaluate it again.
 #pragma once
 
 #include "common.cuh"
@@ -22,7 +24,7 @@ constexpr u64 kScanFlagAgg = 1ull << 62;
 constexpr u64 kScanFlagInc = 2ull << 62;
 constexpr u64 kScanValMask = (1ull << 62) - 1;
 
-template <typename T, int BLOCK, int ITEMS, typename Load, typename Store>
+template <typename T, int BLOCK, int ITEMS, typename Load, typename Store, bool SV = false>
 __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store store, u64* status,
                                                          u32* counter) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -96,11 +98,19 @@ __global__ void __launch_bounds__(BLOCK) k_scan_lookback(i64 n, Load load, Store
         run += x;
     }
     __syncthreads();
+    const T tile_end = s_prefix + total;  // inclusive prefix of the tile's last element
 #pragma unroll
     for (int k = 0; k < ITEMS; ++k) {
         const int li = k * BLOCK + threadIdx.x;
         const i64 gi = base + li;
-        if (gi < n) store(gi, s_items[pad(li)]);
+        if (gi < n) {
+            if constexpr (SV) {
+                const T e = s_items[pad(li)];
+                store(gi, e, static_cast<T>((li + 1 < TILE ? s_items[pad(li + 1)] : tile_end) - e));
+            } else {
+                store(gi, s_items[pad(li)]);
+            }
+        }
     }
 }
 
@@ -145,21 +155,16 @@ struct ScanScratch {
 constexpr int kScanSmallItems = 8;
 constexpr i64 kScanSmallTiles = 296;  // 2 x 148 SMs
 
-// Large tiles (64 KB of shared memory): the look-back hands the running
-// prefix from tile to tile at a roughly fixed cost per tile, so fewer,
-// larger tiles keep it off the bandwidth (tools/micro/scan_micro.cu, B200,
-// 10M / 100M elements: u64 2048-element tiles 2.0 / 2.4 TB/s, 8192-element
-// tiles 2.8 / 3.8 TB/s; u32 16384-element tiles 2.6 / 3.1 TB/s).
-template <typename T, int ITEMS = 32, int BLOCK = (sizeof(T) == 4 ? 512 : 256),
+template <typename T, int ITEMS = 32, int BLOCK = (sizeof(T) == 4 ? 512 : 256), bool SV = false,
           typename Load, typename Store>
-void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch,
-                    const char* name = "scan", double bytes_per_elem = 2.0 * sizeof(T)) {
+void scan_exclusive_impl(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch, const char* name,
+                         double bytes_per_elem) {
     constexpr int TILE = BLOCK * ITEMS;
     if (n <= 0) return;
     if constexpr (ITEMS > kScanSmallItems) {
         // fewer than two large tiles per SM: quarter-size tiles keep every SM busy
         if (n < static_cast<i64>(TILE) * kScanSmallTiles) {
-            scan_exclusive<T, kScanSmallItems, BLOCK>(n, load, store, stream, scratch, name, bytes_per_elem);
+            scan_exclusive_impl<T, kScanSmallItems, BLOCK, SV>(n, load, store, stream, scratch, name, bytes_per_elem);
             return;
         }
     }
@@ -167,9 +172,28 @@ void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScra
     scratch.prepare(tiles, stream);
     constexpr int smem = static_cast<int>(sizeof(T)) * (TILE + TILE / 32);
     if (smem > 48 * 1024)
-        set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_scan_lookback<T, BLOCK, ITEMS, Load, Store>), smem);
-    LAUNCH_B(name, bytes_per_elem * static_cast<double>(n), (k_scan_lookback<T, BLOCK, ITEMS, Load, Store>),
+        set_max_dynamic_smem_once(reinterpret_cast<const void*>(k_scan_lookback<T, BLOCK, ITEMS, Load, Store, SV>),
+                                  smem);
+    LAUNCH_B(name, bytes_per_elem * static_cast<double>(n), (k_scan_lookback<T, BLOCK, ITEMS, Load, Store, SV>),
              static_cast<unsigned>(tiles), BLOCK, smem, stream, n, load, store, scratch.st, scratch.ctr);
+}
+
+// Large tiles (64 KB of shared memory): the look-back hands the running
+// prefix from tile to tile at a roughly fixed cost per tile, so fewer,
+// larger tiles keep it off the bandwidth (tools/micro/scan_micro.cu, B200,
+// 10M / 100M elements: u64 2048-element tiles 2.0 / 2.4 TB/s, 8192-element
+// tiles 2.8 / 3.8 TB/s; u32 16384-element tiles 2.6 / 3.1 TB/s).
+template <typename T, int ITEMS = 32, int BLOCK = (sizeof(T) == 4 ? 512 : 256), typename Load, typename Store>
+void scan_exclusive(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch,
+                    const char* name = "scan", double bytes_per_elem = 2.0 * sizeof(T)) {
+    scan_exclusive_impl<T, ITEMS, BLOCK, false>(n, load, store, stream, scratch, name, bytes_per_elem);
+}
+
+// store(i, excl, x) with x = load(i), read back from the tile in shared memory
+template <typename T, int ITEMS = 32, int BLOCK = (sizeof(T) == 4 ? 512 : 256), typename Load, typename Store>
+void scan_exclusive_v(i64 n, Load load, Store store, cudaStream_t stream, ScanScratch& scratch,
+                      const char* name = "scan", double bytes_per_elem = 2.0 * sizeof(T)) {
+    scan_exclusive_impl<T, ITEMS, BLOCK, true>(n, load, store, stream, scratch, name, bytes_per_elem);
 }
 
 }  // namespace hbp_b200

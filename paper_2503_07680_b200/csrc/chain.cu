@@ -831,29 +831,35 @@ std::pair<u32, bool> run_pass(Ctx& c, ChainArgs& a, const char* name) {
 
 // Heads -> every item: item x belongs to the last head h <= x when
 // x < h + take[h] (same bin, slot + x - h), else it stays unassigned.
-__global__ void k_head_positions(const u32* __restrict__ take, const u32* __restrict__ q, u64 n,
-                                 u32* __restrict__ pos) {
-    for (u64 x = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; x < n;
-         x += static_cast<u64>(gridDim.x) * blockDim.x)
-        if (take[x]) pos[q[x] - 1] = static_cast<u32>(x);
-}
-
 __global__ void k_expand_heads(const u32* __restrict__ take, const u32* __restrict__ q, const u32* __restrict__ pos,
                                u64 n, u32* __restrict__ item_bin, u32* __restrict__ item_slot) {
-    for (u64 x = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; x < n;
-         x += static_cast<u64>(gridDim.x) * blockDim.x) {
-        if (take[x]) continue;  // heads already hold (bin, slot)
-        const u32 k = q[x];
-        u32 b = kNone, sl = kNone;
-        if (k > 0) {
-            const u32 h = pos[k - 1];
-            if (x - h < take[h]) {
-                b = item_bin[h];
-                sl = item_slot[h] + static_cast<u32>(x - h);
-            }
+    // four items per thread, each level of the lookups issued for all four
+    // before the next (heads already hold (bin, slot) and are not written)
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 x0 = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; x0 < n; x0 += 4 * stride) {
+        u32 k[4], h[4], t[4], b[4], sl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u64 x = x0 + u * stride;
+            k[u] = x < n && !take[x] ? q[x] : kNone;  // kNone: head or past the end
         }
-        item_bin[x] = b;
-        item_slot[x] = sl;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) h[u] = k[u] != kNone && k[u] > 0 ? pos[k[u] - 1] : kNone;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = h[u] != kNone ? take[h[u]] : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u64 x = x0 + u * stride;
+            const bool in = h[u] != kNone && x - h[u] < t[u];
+            b[u] = in ? item_bin[h[u]] : kNone;
+            sl[u] = in ? item_slot[h[u]] + static_cast<u32>(x - h[u]) : kNone;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (k[u] == kNone) continue;
+            item_bin[x0 + u * stride] = b[u];
+            item_slot[x0 + u * stride] = sl[u];
+        }
     }
 }
 
@@ -861,10 +867,15 @@ void expand_heads(Ctx& c, u64 n, u32* item_bin, u32* item_slot, const u32* take)
     cudaStream_t s = c.stream;
     DevBuf<u32> q(n, s), pos(n, s);
     u32* qp = q.p;
+    u32* pp = pos.p;
+    // the scan's store also records each head's position (no separate pass)
     scan_exclusive_v<u32>(
         static_cast<i64>(n), [=] __device__(i64 x) { return take[x] ? 1u : 0u; },
-        [=] __device__(i64 x, u32 v, u32 h) { qp[x] = v + h; }, s, c.scan, "scan.chain1", 8.0);
-    LAUNCH_B("chain.heads", 12.0 * n, k_head_positions, grid_for(n, 256), 256, 0, s, take, q.p, n, pos.p);
+        [=] __device__(i64 x, u32 v, u32 h) {
+            qp[x] = v + h;
+            if (h) pp[v] = static_cast<u32>(x);
+        },
+        s, c.scan, "scan.chain1", 12.0);
     LAUNCH_B("chain.expand", 24.0 * n, k_expand_heads, grid_for(n, 256), 256, 0, s, take, q.p, pos.p, n, item_bin,
              item_slot);
 }

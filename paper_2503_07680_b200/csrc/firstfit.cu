@@ -1128,26 +1128,37 @@ void prepare_runs(Ctx& c, const u64* items, i64 n_items, const u32* key32, u64 n
     const i64 nn = n_items;
     // one scan over run-head flags; each head writes its run's first item
     // and length (bit 31: strict) at its run index
-    scan_exclusive_v<u32>(
-        nn,
-        [=] __device__(i64 i) {
-            // both loads unconditional (the short-circuit form kept the
-            // unrolled tile load from batching them)
-            const u64 e = items[i], p = items[i > 0 ? i - 1 : 0];
-            bool head = i == 0 || entry_len(e) != entry_len(p);
-            if (!head && neg_keys) head = neg_item(e, key32, neg_keys) != neg_item(p, key32, neg_keys);
-            return head ? 1u : 0u;
-        },
-        [=] __device__(i64 i, u32 v, u32 x) {
-            const bool head = x != 0;
-            if (head) {
-                const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
-                ri[v] = static_cast<u32>(i);
-                rl[v] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
-            }
-            if (i == nn - 1) sc[0] = v + (head ? 1u : 0u);
-        },
-        c.stream, c.scan, "scan.ff3", 8.0);
+    auto store = [=] __device__(i64 i, u32 v, u32 x) {
+        const bool head = x != 0;
+        if (head) {
+            const bool strict = neg_keys && neg_item(items[i], key32, neg_keys);
+            ri[v] = static_cast<u32>(i);
+            rl[v] = entry_len(items[i]) | (strict ? 0x80000000u : 0u);
+        }
+        if (i == nn - 1) sc[0] = v + (head ? 1u : 0u);
+    };
+    if (neg_keys == 0) {
+        // lengths only: a branch-free flag, so the tile's loads are issued
+        // together (the id-class test below kept them one item at a time:
+        // 9.8M items 115 us)
+        scan_exclusive_v<u32>(
+            nn,
+            [=] __device__(i64 i) {
+                const u64 e = items[i], p = items[i > 0 ? i - 1 : 0];
+                return (i == 0 || entry_len(e) != entry_len(p)) ? 1u : 0u;
+            },
+            store, c.stream, c.scan, "scan.ff3", 8.0);
+    } else {
+        scan_exclusive_v<u32>(
+            nn,
+            [=] __device__(i64 i) {
+                const u64 e = items[i], p = items[i > 0 ? i - 1 : 0];
+                bool head = i == 0 || entry_len(e) != entry_len(p);
+                if (!head) head = neg_item(e, key32, neg_keys) != neg_item(p, key32, neg_keys);
+                return head ? 1u : 0u;
+            },
+            store, c.stream, c.scan, "scan.ff3", 8.0);
+    }
 }
 
 FitResult first_fit_runs(Ctx& c, const u64* items, i64 n_items_s, u64* leaves, i64 bins0, i64 max_bins, u32 cap,

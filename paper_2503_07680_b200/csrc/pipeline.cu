@@ -110,13 +110,16 @@ __global__ void k_ranks_dups(const int64_t* __restrict__ ids, const u32* __restr
 // group_data + entries
 // ---------------------------------------------------------------------------
 
-__global__ void k_group_keys(const u32* __restrict__ len32, u64 n, const int64_t* __restrict__ glen, int ng,
+// Group of every sample (and group_data's l_max check, balance.cpp:32-36:
+// counts[64] <- the first sample longer than lm, in the same read).
+__global__ void k_group_keys(const u32* __restrict__ len32, u64 n, const int64_t* __restrict__ glen, int ng, u32 lm,
                              u32* __restrict__ key, u32* __restrict__ val, unsigned long long* __restrict__ counts) {
     __shared__ unsigned long long s_cnt[64];
     for (int g = threadIdx.x; g < 64; g += blockDim.x) s_cnt[g] = 0;
     __syncthreads();
     GRID_STRIDE(i, n) {
         const u32 L = len32[i];
+        if (L > lm) atomicMin(&counts[64], static_cast<unsigned long long>(i));
         int g = 0;
         while (g < ng - 1 && static_cast<int64_t>(L) > glen[g]) ++g;
         key[i] = static_cast<u32>(g);
@@ -907,8 +910,8 @@ void validate_corpus(Ctx& c, const hbp_samples* in, const DeviceCorpus& corpus, 
 namespace {
 
 // Partitions the corpus by group (stable) and returns entries + offsets.
-void partition(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group_config>& groups, DevBuf<u64>& entries,
-               std::vector<u64>& goff) {
+void partition(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group_config>& groups, int64_t l_max,
+               DevBuf<u64>& entries, std::vector<u64>& goff) {
     cudaStream_t s = c.stream;
     const u64 n = static_cast<u64>(corpus.n);
     const int ng = static_cast<int>(groups.size());
@@ -917,40 +920,24 @@ void partition(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group_config>
     DevBuf<int64_t> dgl(ng, s);
     CUDA_CHECK(cudaMemcpyAsync(dgl.p, gl.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice, s));
     DevBuf<u32> key(n, s), val(n, s), tk(n, s), tv(n, s);
-    DevBuf<unsigned long long> counts(64, s);
+    DevBuf<unsigned long long> counts(65, s);  // per group, then [64] the first sample beyond l_max
     counts.zero();
-    LAUNCH(k_group_keys, G(n), kB, 0, s, corpus.len32.p, n, dgl.p, ng, key.p, val.p, counts.p);
+    const unsigned long long none = ~0ull;
+    CUDA_CHECK(cudaMemcpyAsync(counts.p + 64, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    // len32 saturates at 2^31-1; longer samples are tracked in first_huge
+    const u32 lm = l_max > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(l_max);
+    LAUNCH(k_group_keys, G(n), kB, 0, s, corpus.len32.p, n, dgl.p, ng, lm, key.p, val.p, counts.p);
     if (ng > 1) radix_sort_pairs(c, key.p, val.p, static_cast<i64>(n), bits_for(ng - 1), false, tk.p, tv.p);
     entries.alloc(n, s);
     LAUNCH(k_entries_from_idx, G(n), kB, 0, s, corpus.len32.p, val.p, n, entries.p);
-    const auto cnt = read_vector(c, counts.p, 64);
+    const auto cnt = read_vector(c, counts.p, 65);
+    u64 first = cnt[64];
+    if (corpus.first_huge < first) first = corpus.first_huge;
+    if (first != ~0ull)
+        fail_validation("sample " + std::to_string(corpus.id_of(static_cast<i64>(first))) +
+                        " exceeds the largest packing length " + std::to_string(l_max));
     goff.assign(ng + 1, 0);
     for (int g = 0; g < ng; ++g) goff[g + 1] = goff[g] + cnt[g];
-}
-
-// group_data's check (balance.cpp:32-36): the first sample beyond l_max.
-void check_l_max(Ctx& c, const DeviceCorpus& corpus, int64_t l_max) {
-    cudaStream_t s = c.stream;
-    if (corpus.n == 0) return;
-    {
-        DevBuf<unsigned long long> over(1, s);
-        const unsigned long long none = ~0ull;
-        CUDA_CHECK(cudaMemcpyAsync(over.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
-        const u32* lp = corpus.len32.p;
-        unsigned long long* op = over.p;
-        const u32 lm = l_max > 0x7fffffffLL ? 0x7fffffffu : static_cast<u32>(l_max);
-        const u64 n = static_cast<u64>(corpus.n);
-        // len32 saturates at 2^31-1; longer samples are tracked in first_huge
-        auto k = [=] __device__(u64 i) {
-            if (lp[i] > lm) atomicMin(op, static_cast<unsigned long long>(i));
-        };
-        for_each_index(c, n, k);
-        u64 first = read_scalar(c, over.p);
-        if (corpus.first_huge < first) first = corpus.first_huge;
-        if (first != ~0ull)
-            fail_validation("sample " + std::to_string(corpus.id_of(static_cast<i64>(first))) +
-                            " exceeds the largest packing length " + std::to_string(l_max));
-    }
 }
 
 }  // namespace
@@ -959,11 +946,10 @@ void group_data_device(Ctx& c, DeviceCorpus& corpus, const std::vector<hbp_group
                        std::vector<int64_t>& offsets, std::vector<int32_t>& members) {
     validate_groups(groups, l_max);
     if (groups.size() > 64) fail_validation("the GPU engine supports at most 64 packing groups");
-    check_l_max(c, corpus, l_max);
     DevBuf<u64> entries;
     std::vector<u64> goff;
     if (corpus.n > 0) {
-        partition(c, corpus, groups, entries, goff);
+        partition(c, corpus, groups, l_max, entries, goff);  // also group_data's l_max check
     } else {
         goff.assign(groups.size() + 1, 0);
     }
@@ -984,8 +970,6 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     validate_groups(a.groups, a.l_max);
     if (a.device_count < 1) fail_validation("device count must be >= 1");
     if (a.groups.size() > 64) fail_validation("the GPU engine supports at most 64 packing groups");
-    check_l_max(c, corpus, a.l_max);
-    trace_mark(c, "check");
     out.device_count = a.device_count;
     out.seed = a.seed;
     out.groups = a.groups;
@@ -997,7 +981,7 @@ void build_plan_device(Ctx& c, DeviceCorpus& corpus, const PlanArgs& a, DevicePl
     const int ng = static_cast<int>(a.groups.size());
     DevBuf<u64> entries;
     std::vector<u64> goff;
-    partition(c, corpus, a.groups, entries, goff);
+    partition(c, corpus, a.groups, a.l_max, entries, goff);  // also group_data's l_max check
     trace_mark(c, "group_data");
 
     // Pools, concatenated: Pin holds pool g at off[g] in input order (the

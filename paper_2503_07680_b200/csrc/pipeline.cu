@@ -351,14 +351,14 @@ __global__ void k_spill(const u64* __restrict__ sorted, u64 k, u32 N, u32 cap, c
                 bd = d;
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const u64 oa = __shfl_xor_sync(0xffffffffu, ba, o);
-            const u32 od = __shfl_xor_sync(0xffffffffu, bd, o);
-            if (oa < ba || (oa == ba && od < bd)) {
-                ba = oa;
-                bd = od;
-            }
+        // warp argmin of (attention, device): three REDUX steps (high word,
+        // low word, device) instead of five shuffle rounds on the item's path
+        {
+            const u32 h = static_cast<u32>(ba >> 32);
+            const u32 mh = __reduce_min_sync(0xffffffffu, h);
+            const u32 l = h == mh ? static_cast<u32>(ba) : 0xffffffffu;
+            const u32 ml = __reduce_min_sync(0xffffffffu, l);
+            bd = __reduce_min_sync(0xffffffffu, h == mh && static_cast<u32>(ba) == ml ? bd : 0xffffffffu);
         }
         if (bd == 0xffffffffu) {
             ok = false;

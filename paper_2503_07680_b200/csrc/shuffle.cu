@@ -159,11 +159,52 @@ __device__ __forceinline__ void fy_list(u64 q, const u32* __restrict__ ends, u32
     }
 }
 
+// Four positions per thread with their loads issued together: most lists
+// hold at most two steps (E|S_q| = ln(m/q)), which are ordered in registers
+// (nothing reads the bucket order afterwards); longer ones take fy_list.
 __global__ void k_fy_lists(u64 m, const u32* __restrict__ ends, u32* __restrict__ bucket,
                            u32* __restrict__ nxt, u32* __restrict__ link, u32* __restrict__ first0) {
-    for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < m;
-         q += static_cast<u64>(gridDim.x) * blockDim.x)
-        fy_list(q, ends, bucket, nxt, link, first0);
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 q0 = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q0 < m; q0 += 4 * stride) {
+        u32 a[4], b[4], e0[4], e1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u64 q = q0 + u * stride;
+            a[u] = q < m && q > 0 ? ends[q - 1] : 0u;
+            b[u] = q < m ? ends[q] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u32 len = b[u] - a[u];
+            e0[u] = len >= 1 ? bucket[a[u]] : kNone;
+            e1[u] = len >= 2 ? bucket[a[u] + 1] : kNone;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u64 q = q0 + u * stride;
+            if (q >= m) continue;
+            const u32 len = b[u] - a[u];
+            if (len > 2) {
+                fy_list(q, ends, bucket, nxt, link, first0);
+                continue;
+            }
+            u32 x0 = e0[u], x1 = e1[u];
+            if (len == 2 && x1 < x0) {
+                x0 = e1[u];
+                x1 = e0[u];
+            }
+            if (len >= 1) nxt[x0] = len == 2 ? x1 : kNone;
+            if (len == 2) nxt[x1] = kNone;
+            if (q == 0) {
+                *first0 = len ? x0 : kNone;
+            } else {
+                // link(q+1) = smallest step > q+1 in S_q (all of S_q are >= q+1)
+                u32 l = kNone;
+                if (len) l = (x0 == q + 1) ? (len > 1 ? x1 : kNone) : x0;
+                link[q + 1] = l;
+            }
+        }
+    }
 }
 
 // src[p] = the source position of slot p; with `in`, out[p] = in[src[p]]

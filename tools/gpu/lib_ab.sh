@@ -6,6 +6,6 @@ for r in 1 2 3; do
     if [ $v = base ]; then export HBP_LIB_OVERRIDE=$PWD/abvar/base_libhbp_b200.so; else unset HBP_LIB_OVERRIDE; fi
     echo -n "$v "; timeout 300 python bench.py --no-cpu --no-c4 --no-ingest 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); f=d['roofline']['families']
-print(round(d['ms_per_step'],3), round(d['one_at_a_time']['ms_per_step'],3), 'nf', f['nf.round']['ms'], 'chain', f['fit.chain']['ms'], 'fyl', f['fy.lists']['ms'], 'fys', f['fy.sources_gather']['ms'], round(d['sweep']['candidates_per_s']))"
+print(round(d['ms_per_step'],3), round(d['one_at_a_time']['ms_per_step'],3), 'nf', f['nf.round']['ms'], 'chain', f['fit.chain']['ms'], 'fyl', f['fy.lists']['ms'], 'fys', f['fy.sources_gather']['ms'], 'fysc', f['fy.scatter']['ms'], round(d['sweep']['candidates_per_s']))"
   done
 done > gpurun_out/lib_ab.log 2>&1
